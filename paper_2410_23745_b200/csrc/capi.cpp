@@ -1,0 +1,263 @@
+// extern "C" boundary (include/syno.h).
+#include "../../include/syno.h"
+
+#include <cuda_runtime.h>
+
+#include <cstring>
+#include <functional>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <sstream>
+
+#include "engine.hpp"
+
+using namespace syno;
+
+struct syno_op {
+  Graph graph;
+  Assignment env;
+  bool staged = false;
+  bool replay_only = false;
+  LoopNest unstaged, staged_nest;
+  Plan plan;
+  std::mutex mu;
+  std::map<int, std::unique_ptr<DevPlan>> dev;
+};
+
+static thread_local std::string g_last_error;
+
+template <typename F>
+static int guarded(F&& f) {
+  try {
+    f();
+    return SYNO_OK;
+  } catch (const Error& e) {
+    g_last_error = e.what();
+    return e.code;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return SYNO_E_INVALID;
+  }
+}
+
+static Assignment parse_assignment(const char* kv) {
+  Assignment a;
+  std::string s(kv);
+  for (char& c : s)
+    if (c == ',' || c == ';') c = ' ';
+  std::istringstream in(s);
+  std::string item;
+  while (in >> item) {
+    size_t eq = item.find('=');
+    if (eq == std::string::npos || eq == 0) fail(SYNO_E_INVALID, "bad assignment item '" + item + "'");
+    try {
+      a[item.substr(0, eq)] = std::stoll(item.substr(eq + 1));
+    } catch (const std::exception&) {
+      fail(SYNO_E_INVALID, "bad assignment value in '" + item + "'");
+    }
+  }
+  return a;
+}
+
+static int put_text(const std::string& s, char* buf, size_t cap, size_t* len) {
+  if (len) *len = s.size();
+  if (buf && cap) {
+    size_t n = std::min(cap - 1, s.size());
+    memcpy(buf, s.data(), n);
+    buf[n] = 0;
+  }
+  return SYNO_OK;
+}
+
+static DevPlan& dev_plan(syno_op* op, cudaStream_t stream) {
+  int dev = 0;
+  cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
+  std::lock_guard<std::mutex> lock(op->mu);
+  auto it = op->dev.find(dev);
+  if (it != op->dev.end()) return *it->second;
+  DevPlan* p = build_dev_plan(op->plan, stream);
+  op->dev[dev].reset(p);
+  return *p;
+}
+
+extern "C" {
+
+int syno_compile(const char* doc, const char* assignment_kv, int flags, syno_op_t* out) {
+  return guarded([&] {
+    if (!doc || !out) fail(SYNO_E_INVALID, "null argument");
+    auto op = std::make_unique<syno_op>();
+    op->graph = parse_operator(doc);
+    op->env = assignment_kv ? parse_assignment(assignment_kv) : op->graph.spec->assignment();
+    op->staged = flags & SYNO_STAGED;
+    op->replay_only = flags & SYNO_REPLAY_ONLY;
+    if (op->replay_only) {
+      *out = op.release();
+      return;
+    }
+    op->unstaged = build_loop_nest(op->graph, op->env);
+    LoopNest st = rfactor(op->unstaged);
+    op->staged_nest = st;
+    op->plan = build_plan(op->unstaged, op->staged ? st : op->unstaged, op->graph.spec->batch_dims, op->env);
+    op->plan.flops_staged = nest_flops(st) * op->plan.batch;
+    *out = op.release();
+  });
+}
+
+static void check_weights(syno_op* op, const void* const* w, int n_w) {
+  if (op->replay_only) fail(SYNO_E_INVALID, "handle was compiled with SYNO_REPLAY_ONLY");
+  if (n_w != (int)op->plan.w_ext.size())
+    fail(SYNO_E_SHAPE, op->graph.spec->name + ": expected " + std::to_string(op->plan.w_ext.size()) +
+                           " weight tensors, got " + std::to_string(n_w));
+  for (int j = 0; j < n_w; ++j)
+    if (!w[j]) fail(SYNO_E_INVALID, "null weight pointer");
+}
+
+int syno_forward(syno_op_t op, int dtype, const void* x, const void* const* w, int n_w, void* y, void* stream) {
+  return guarded([&] {
+    if (!op || !x || !y || (n_w && !w)) fail(SYNO_E_INVALID, "null argument");
+    if (dtype < 0 || dtype > 2) fail(SYNO_E_INVALID, "unknown dtype");
+    check_weights(op, w, n_w);
+    cudaStream_t s = (cudaStream_t)stream;
+    DevPlan& dp = dev_plan(op, s);
+    Bindings b;
+    b.x = x;
+    for (int j = 0; j < n_w; ++j) b.w.push_back(w[j]);
+    b.y = y;
+    run_forward(op->plan, dp, (DType)dtype, b, s);
+  });
+}
+
+int syno_backward(syno_op_t op, int dtype, const void* x, const void* const* w, int n_w, const void* dy, void* dx,
+                  void* const* dw, void* stream) {
+  return guarded([&] {
+    if (!op || !x || !dy || (n_w && !w)) fail(SYNO_E_INVALID, "null argument");
+    if (dtype < 0 || dtype > 2) fail(SYNO_E_INVALID, "unknown dtype");
+    check_weights(op, w, n_w);
+    cudaStream_t s = (cudaStream_t)stream;
+    DevPlan& dp = dev_plan(op, s);
+    Bindings b;
+    b.x = x;
+    for (int j = 0; j < n_w; ++j) b.w.push_back(w[j]);
+    b.dy = dy;
+    b.dx = dx;
+    for (int j = 0; j < n_w; ++j) b.dw.push_back(dw ? dw[j] : nullptr);
+    run_backward(op->plan, dp, (DType)dtype, b, s);
+  });
+}
+
+int syno_query(syno_op_t op, syno_info* info) {
+  return guarded([&] {
+    if (!op || !info) fail(SYNO_E_INVALID, "null argument");
+    memset(info, 0, sizeof(*info));
+    std::vector<int> perm;
+    info->complete = match_input(op->graph, &perm);
+    if (op->replay_only) {
+      info->replay_only = 1;
+      info->n_weights = (int)op->graph.weights.size();
+      return;
+    }
+    const Plan& p = op->plan;
+    if (p.x_ext.size() > SYNO_MAX_RANK || p.y_ext.size() > SYNO_MAX_RANK || p.w_ext.size() > SYNO_MAX_WEIGHTS)
+      fail(SYNO_E_UNSUPPORTED, "operator rank exceeds the query struct");
+    info->n_weights = (int)p.w_ext.size();
+    info->batch_rank = (int)p.batch_ext.size();
+    info->x_rank = (int)p.x_ext.size();
+    info->y_rank = (int)p.y_ext.size();
+    for (size_t k = 0; k < p.x_ext.size(); ++k) info->x_shape[k] = p.x_ext[k];
+    for (size_t k = 0; k < p.y_ext.size(); ++k) info->y_shape[k] = p.y_ext[k];
+    int64_t params = 0;
+    for (size_t j = 0; j < p.w_ext.size(); ++j) {
+      if (p.w_ext[j].size() > SYNO_MAX_RANK) fail(SYNO_E_UNSUPPORTED, "weight rank exceeds the query struct");
+      info->w_rank[j] = (int)p.w_ext[j].size();
+      int64_t n = 1;
+      for (size_t k = 0; k < p.w_ext[j].size(); ++k) {
+        info->w_shape[j][k] = p.w_ext[j][k];
+        n *= p.w_ext[j][k];
+      }
+      params += n;
+      info->grad_w_scatter[j] = p.grad_w.at(j).at(0).scatter;
+    }
+    info->params = params;
+    info->flops_unstaged = p.flops_unstaged;
+    info->flops_staged = p.flops_staged;
+    info->n_forward_stages = (int)p.forward.size();
+    info->grad_x_scatter = p.grad_x.at(0).scatter;
+    double g = 1;
+    for (auto e : p.unstaged.axis_ext) g *= (double)e;
+    for (auto e : op->unstaged.stages[0].reduces) g *= (double)e.extent;
+    info->index_grid = (int64_t)g;
+  });
+}
+
+int syno_emit_loop_nest(syno_op_t op, int staged, char* buf, size_t cap, size_t* len) {
+  int rc = guarded([&] {
+    if (!op) fail(SYNO_E_INVALID, "null argument");
+  });
+  if (rc) return rc;
+  if (op->replay_only) { g_last_error = "handle was compiled with SYNO_REPLAY_ONLY"; return SYNO_E_INVALID; }
+  return put_text(emit_loop_nest(staged ? op->staged_nest : op->unstaged), buf, cap, len);
+}
+
+int syno_print_operator(syno_op_t op, char* buf, size_t cap, size_t* len) {
+  if (!op) { g_last_error = "null argument"; return SYNO_E_INVALID; }
+  return put_text(print_operator(op->graph), buf, cap, len);
+}
+
+int syno_describe_plan(syno_op_t op, char* buf, size_t cap, size_t* len) {
+  if (!op) { g_last_error = "null argument"; return SYNO_E_INVALID; }
+  if (op->replay_only) { g_last_error = "handle was compiled with SYNO_REPLAY_ONLY"; return SYNO_E_INVALID; }
+  std::string s;
+  for (auto& st : op->plan.forward) s += "forward: " + st.describe() + "\n";
+  for (auto& st : op->plan.grad_x) s += "grad_x: " + st.describe() + "\n";
+  for (size_t j = 0; j < op->plan.grad_w.size(); ++j)
+    for (auto& st : op->plan.grad_w[j]) s += "grad_w" + std::to_string(j) + ": " + st.describe() + "\n";
+  return put_text(s, buf, cap, len);
+}
+
+int syno_index_map(syno_op_t op, int term, int coord, int64_t* out_dev, void* stream) {
+  return guarded([&] {
+    if (!op || !out_dev) fail(SYNO_E_INVALID, "null argument");
+    if (op->replay_only) fail(SYNO_E_INVALID, "handle was compiled with SYNO_REPLAY_ONLY");
+    // The unstaged stage keeps every reduce (no folding) for this hook.
+    LoopNest& n = op->unstaged;
+    CStage s;
+    for (auto e : op->plan.batch_ext) s.axis_ext.push_back(e);
+    std::map<std::string, int> loop_of;
+    for (auto& a : n.stages[0].axes) {
+      loop_of[a.name] = (int)s.axis_ext.size();
+      s.axis_ext.push_back(a.extent);
+    }
+    for (auto& r : n.stages[0].reduces) {
+      loop_of[r.name] = (int)(s.axis_ext.size() + s.red_ext.size());
+      s.red_ext.push_back(r.extent);
+    }
+    if (term < 0 || term >= (int)n.stages[0].terms.size()) fail(SYNO_E_INVALID, "term out of range");
+    const Access& acc = n.stages[0].terms[term];
+    if (coord < 0 || coord >= (int)acc.exprs.size()) fail(SYNO_E_INVALID, "coordinate out of range");
+    // Convert the one expression; batch loops are not referenced by it.
+    std::function<CE(const E&)> conv = [&](const E& e) -> CE {
+      switch (e->op) {
+        case Op::Iter: return c_loop(loop_of.at(e->name));
+        case Op::Const: return c_const(e->value);
+        case Op::SizeRef: return c_const(eval_size(e->size, n.env));
+        default: break;
+      }
+      COp o = e->op == Op::Add ? COp::Add : e->op == Op::Sub ? COp::Sub : e->op == Op::Mul ? COp::Mul
+              : e->op == Op::FloorDiv ? COp::FloorDiv : COp::Mod;
+      return c_bin(o, conv(e->lhs), conv(e->rhs));
+    };
+    CTerm t;
+    t.coords.push_back(conv(acc.exprs[coord]));
+    s.terms.push_back(t);
+    eval_coordinate_grid(s, 0, 0, out_dev, (cudaStream_t)stream);
+  });
+}
+
+void syno_destroy(syno_op_t op) { delete op; }
+
+const char* syno_last_error(void) { return g_last_error.c_str(); }
+
+const char* syno_version(void) { return "syno-b200 0.1 (sm_100a)"; }
+
+}  // extern "C"

@@ -1,0 +1,650 @@
+// Universal device engine for synthesized-operator stages.
+//
+//  K1  k1_build_table   integer index tables: coordinate programs evaluated
+//                       with Python floor semantics (symexpr.py:242-245) over
+//                       their iterator grids; -1 marks out-of-range
+//                       (codegen.py:535-541 valid mask).
+//  K2/K3 stage_kernel   gather + product + reduce of one stage
+//                       (codegen.py:515-546), fp32/f64 accumulation,
+//                       optional reduce split across blockIdx.y.
+//  K6/K7 scatter form   the reference's np.add.at gradient (codegen.py:727-742)
+//                       with device atomics, for targets that do not invert.
+#include <cuda_bf16.h>
+
+#include <algorithm>
+#include <cstring>
+#include <set>
+
+#include "engine.hpp"
+#include "tc.hpp"
+
+namespace syno {
+
+void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) fail(SYNO_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+// ---------------------------------------------------------------------------
+// K1: coordinate programs
+// ---------------------------------------------------------------------------
+
+enum : int64_t { BC_LOOP = 0, BC_CONST = 1, BC_ADD = 2, BC_SUB = 3, BC_MUL = 4, BC_FDIV = 5, BC_MOD = 6 };
+constexpr int MAXL = 24;     // loops a table may depend on
+constexpr int MAXPROG = 16;  // programs summed into one table
+constexpr int MAXSTACK = 32;
+
+static void compile_prog(const CE& e, const std::vector<int>& local, std::vector<int64_t>* code) {
+  switch (e->op) {
+    case COp::Loop: {
+      int idx = (int)(std::find(local.begin(), local.end(), e->loop) - local.begin());
+      if (idx >= (int)local.size()) fail(SYNO_E_GRAPH, "coordinate program references a foreign loop");
+      code->push_back(BC_LOOP); code->push_back(idx);
+      return;
+    }
+    case COp::Const: code->push_back(BC_CONST); code->push_back(e->value); return;
+    default: break;
+  }
+  compile_prog(e->lhs, local, code);
+  compile_prog(e->rhs, local, code);
+  int64_t op = e->op == COp::Add ? BC_ADD : e->op == COp::Sub ? BC_SUB : e->op == COp::Mul ? BC_MUL
+               : e->op == COp::FloorDiv ? BC_FDIV : BC_MOD;
+  code->push_back(op); code->push_back(0);
+}
+
+static int prog_depth(const CE& e) {
+  if (e->op == COp::Loop || e->op == COp::Const) return 1;
+  return std::max(prog_depth(e->lhs), prog_depth(e->rhs) + 1);
+}
+
+__host__ __device__ inline int64_t dev_floordiv(int64_t a, int64_t b) {
+  if (b == 0) return 0;
+  int64_t q = a / b;
+  if ((a % b != 0) && ((a < 0) != (b < 0))) --q;
+  return q;
+}
+__host__ __device__ inline int64_t dev_mod(int64_t a, int64_t b) {
+  if (b == 0) return 0;
+  int64_t r = a % b;
+  if (r != 0 && ((r < 0) != (b < 0))) r += b;
+  return r;
+}
+
+__device__ int64_t eval_prog(const int64_t* code, int64_t len, const int64_t* vals) {
+  int64_t st[MAXSTACK];
+  int sp = 0;
+  for (int64_t i = 0; i < len; ++i) {
+    int64_t op = code[2 * i], arg = code[2 * i + 1];
+    if (op == BC_LOOP) { st[sp++] = vals[arg]; continue; }
+    if (op == BC_CONST) { st[sp++] = arg; continue; }
+    int64_t b = st[--sp], a = st[--sp];
+    int64_t r;
+    switch (op) {
+      case BC_ADD: r = a + b; break;
+      case BC_SUB: r = a - b; break;
+      case BC_MUL: r = a * b; break;
+      case BC_FDIV: r = dev_floordiv(a, b); break;
+      default: r = dev_mod(a, b); break;
+    }
+    st[sp++] = r;
+  }
+  return st[0];
+}
+
+struct K1Args {
+  int32_t nprog, ndeps;
+  int64_t dep_ext[MAXL];
+  int64_t count;
+  const int64_t* code;
+  int64_t prog_off[MAXPROG];
+  int64_t prog_len[MAXPROG];
+  int64_t n[MAXPROG];       // extent for the range check, <= 0: no check
+  int64_t stride[MAXPROG];
+  int32_t* out;             // table mode
+  int64_t* out_raw;         // raw mode: the single program's value
+};
+
+__global__ void k1_build_table(const __grid_constant__ K1Args a) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= a.count) return;
+  int64_t vals[MAXL];
+  int64_t rem = i;
+  for (int k = a.ndeps - 1; k >= 0; --k) {
+    vals[k] = rem % a.dep_ext[k];
+    rem /= a.dep_ext[k];
+  }
+  if (a.out_raw) {
+    a.out_raw[i] = eval_prog(a.code + a.prog_off[0], a.prog_len[0], vals);
+    return;
+  }
+  int64_t sum = 0;
+  bool ok = true;
+  for (int p = 0; p < a.nprog; ++p) {
+    int64_t v = eval_prog(a.code + a.prog_off[p], a.prog_len[p], vals);
+    if (a.n[p] > 0 && (v < 0 || v >= a.n[p])) ok = false;
+    sum += v * a.stride[p];
+  }
+  a.out[i] = ok ? (int32_t)sum : -1;
+}
+
+struct ProgSpec {
+  CE e;
+  int64_t n, stride;
+};
+
+struct TabSpec {
+  std::vector<int> deps;
+  std::vector<int64_t> dep_ext;
+  std::vector<ProgSpec> progs;
+  int64_t count = 1;
+  size_t offset = 0;
+};
+
+static void launch_k1(const TabSpec& t, int32_t* out, int64_t* out_raw, cudaStream_t stream) {
+  if ((int)t.deps.size() > MAXL) fail(SYNO_E_UNSUPPORTED, "index table depends on too many loops");
+  if ((int)t.progs.size() > MAXPROG) fail(SYNO_E_UNSUPPORTED, "too many coordinates in one index table");
+  K1Args a{};
+  a.nprog = (int)t.progs.size();
+  a.ndeps = (int)t.deps.size();
+  for (size_t k = 0; k < t.deps.size(); ++k) a.dep_ext[k] = t.dep_ext[k];
+  a.count = t.count;
+  std::vector<int64_t> code;
+  for (size_t p = 0; p < t.progs.size(); ++p) {
+    if (prog_depth(t.progs[p].e) > MAXSTACK) fail(SYNO_E_UNSUPPORTED, "coordinate expression too deep");
+    a.prog_off[p] = (int64_t)code.size();
+    size_t before = code.size();
+    compile_prog(t.progs[p].e, t.deps, &code);
+    a.prog_len[p] = (int64_t)(code.size() - before) / 2;
+    a.n[p] = t.progs[p].n;
+    a.stride[p] = t.progs[p].stride;
+  }
+  if (code.empty()) code.push_back(0);
+  int64_t* dcode = nullptr;
+  cuda_check(cudaMallocAsync((void**)&dcode, code.size() * sizeof(int64_t), stream), "cudaMallocAsync(code)");
+  cuda_check(cudaMemcpyAsync(dcode, code.data(), code.size() * sizeof(int64_t), cudaMemcpyHostToDevice, stream),
+             "cudaMemcpyAsync(code)");
+  a.code = dcode;
+  a.out = out;
+  a.out_raw = out_raw;
+  if (t.count > 0) {
+    int64_t blocks = (t.count + 255) / 256;
+    k1_build_table<<<(unsigned)blocks, 256, 0, stream>>>(a);
+    cuda_check(cudaGetLastError(), "k1_build_table");
+  }
+  // The host copy of `code` must outlive the async memcpy: synchronize the
+  // (rare, compile-time) table build before the vector goes away.
+  cuda_check(cudaStreamSynchronize(stream), "k1 sync");
+  cuda_check(cudaFreeAsync(dcode, stream), "cudaFreeAsync(code)");
+}
+
+void eval_coordinate_grid(const CStage& s, int term, int coord, int64_t* out_dev, cudaStream_t stream) {
+  const CTerm& t = term < (int)s.terms.size() ? s.terms[term] : s.target;
+  TabSpec tab;
+  for (int l = 0; l < s.nloops(); ++l) {
+    tab.deps.push_back(l);
+    tab.dep_ext.push_back(s.ext(l));
+    tab.count *= s.ext(l);
+  }
+  tab.progs.push_back({t.coords.at(coord), 0, 1});
+  launch_k1(tab, nullptr, out_dev, stream);
+}
+
+// ---------------------------------------------------------------------------
+// Stage construction (host)
+// ---------------------------------------------------------------------------
+
+struct Fixup {
+  const int32_t** field;
+  int table;
+};
+
+static std::vector<int64_t> row_major_strides(const std::vector<int64_t>& ext) {
+  std::vector<int64_t> s(ext.size(), 1);
+  for (int k = (int)ext.size() - 2; k >= 0; --k) s[k] = s[k + 1] * ext[k + 1];
+  return s;
+}
+
+static void build_kterm(const CStage& s, const CTerm& t, KTerm* k, std::vector<TabSpec>* tabs,
+                        std::vector<Fixup>* fix, bool* dead) {
+  memset(k, 0, sizeof(KTerm));
+  const int A = (int)s.axis_ext.size();
+  const int L = s.nloops();
+  k->kind = t.t.kind == TK_PHANTOM ? 2 : (t.t.kind == TK_STAGE ? 1 : 0);
+  if (t.t.numel() >= (int64_t)INT32_MAX) fail(SYNO_E_UNSUPPORTED, "tensor has 2^31 or more elements");
+  auto strides = row_major_strides(t.t.extents);
+  if (t.coords.size() != t.t.extents.size()) fail(SYNO_E_SHAPE, "access rank does not match tensor rank");
+  std::vector<ProgSpec> rprogs;
+  std::vector<int> all_red;
+  std::vector<int64_t> red_ext;
+  int64_t R = 1;
+  for (int l = A; l < L; ++l) {
+    all_red.push_back(l);
+    red_ext.push_back(s.ext(l));
+    R *= s.ext(l);
+  }
+  for (size_t d = 0; d < t.coords.size(); ++d) {
+    const CE& c = t.coords[d];
+    int64_t n = t.t.extents[d], st = strides[d];
+    std::vector<int> deps;
+    c_loops(c, &deps);
+    if (deps.empty()) {
+      int64_t v = c_eval(c, nullptr);
+      if (v < 0 || v >= n) *dead = true;
+      else k->base += v * st;
+      continue;
+    }
+    if (c->op == COp::Loop && n >= s.ext(c->loop)) {
+      if (c->loop < A) k->lin[c->loop] += st;
+      else rprogs.push_back({c, 0, st});
+      continue;
+    }
+    bool axis_only = deps.back() < A, red_only = deps.front() >= A;
+    if (red_only) {
+      rprogs.push_back({c, n, st});
+      continue;
+    }
+    TabSpec tab;
+    tab.deps = deps;
+    for (int l : deps) {
+      tab.dep_ext.push_back(s.ext(l));
+      tab.count *= s.ext(l);
+    }
+    tab.progs.push_back({c, n, st});
+    if (tab.count >= (int64_t)1 << 28) fail(SYNO_E_UNSUPPORTED, "index table too large");
+    auto tstr = row_major_strides(tab.dep_ext);
+    int tid = (int)tabs->size();
+    tabs->push_back(tab);
+    if (axis_only) {
+      if (k->n_atab >= MAXTAB) fail(SYNO_E_UNSUPPORTED, "too many axis tables in one term");
+      int m = k->n_atab++;
+      for (size_t q = 0; q < deps.size(); ++q) k->atab_s[m][deps[q]] = (int32_t)tstr[q];
+      fix->push_back({&k->atab[m], tid});
+    } else {
+      if (k->n_mix >= MAXMIX) fail(SYNO_E_UNSUPPORTED, "too many mixed tables in one term");
+      int m = k->n_mix++;
+      CE ri = c_const(0);
+      for (size_t q = 0; q < deps.size(); ++q) {
+        if (deps[q] < A) k->mtab_s[m][deps[q]] = (int32_t)tstr[q];
+        else ri = c_bin(COp::Add, ri, c_bin(COp::Mul, c_loop(deps[q]), c_const(tstr[q])));
+      }
+      fix->push_back({&k->mtab[m], tid});
+      TabSpec rt;
+      rt.deps = all_red;
+      rt.dep_ext = red_ext;
+      rt.count = R;
+      rt.progs.push_back({ri, 0, 1});
+      fix->push_back({&k->mri[m], (int)tabs->size()});
+      tabs->push_back(rt);
+    }
+  }
+  if (!rprogs.empty()) {
+    TabSpec rt;
+    rt.deps = all_red;
+    rt.dep_ext = red_ext;
+    rt.count = R;
+    rt.progs = rprogs;
+    fix->push_back({&k->rtab, (int)tabs->size()});
+    tabs->push_back(rt);
+  }
+}
+
+static void build_dev_stage(const CStage& cs, DevStage* ds, cudaStream_t stream) {
+  ds->cs = cs;
+  KStage& k = ds->k;
+  memset(&k, 0, sizeof(KStage));
+  if ((int)cs.axis_ext.size() > MAXA) fail(SYNO_E_UNSUPPORTED, "stage has too many axes");
+  if ((int)cs.terms.size() > MAXT) fail(SYNO_E_UNSUPPORTED, "stage has too many terms");
+  k.n_axes = (int)cs.axis_ext.size();
+  k.n_terms = (int)cs.terms.size();
+  k.out_count = 1;
+  for (size_t a = 0; a < cs.axis_ext.size(); ++a) {
+    k.axis_ext[a] = cs.axis_ext[a];
+    k.out_count *= cs.axis_ext[a];
+  }
+  k.R = 1;
+  for (auto r : cs.red_ext) k.R *= r;
+  k.scale = cs.scale;
+  std::vector<TabSpec> tabs;
+  std::vector<Fixup> fix;
+  bool dead = false;
+  for (size_t t = 0; t < cs.terms.size(); ++t) build_kterm(cs, cs.terms[t], &k.terms[t], &tabs, &fix, &dead);
+  if (cs.scatter) build_kterm(cs, cs.target, &k.target, &tabs, &fix, &dead);
+  ds->dead = dead || cs.dead;
+  size_t total = 0;
+  for (auto& t : tabs) {
+    t.offset = total;
+    total += (size_t)t.count;
+  }
+  ds->table_entries = total;
+  if (total) {
+    cuda_check(cudaMalloc((void**)&ds->tables, total * sizeof(int32_t)), "cudaMalloc(tables)");
+    for (auto& t : tabs) launch_k1(t, ds->tables + t.offset, nullptr, stream);
+  }
+  for (auto& f : fix) *f.field = ds->tables + tabs[f.table].offset;
+}
+
+DevPlan::~DevPlan() {
+  auto rel = [](std::vector<DevStage>& v) {
+    for (auto& s : v)
+      if (s.tables) cudaFree(s.tables);
+  };
+  rel(forward);
+  rel(grad_x);
+  for (auto& g : grad_w) rel(g);
+}
+
+DevPlan* build_dev_plan(const Plan& plan, cudaStream_t stream) {
+  auto dp = std::make_unique<DevPlan>();
+  cuda_check(cudaGetDevice(&dp->device), "cudaGetDevice");
+  for (auto& s : plan.forward) {
+    dp->forward.emplace_back();
+    build_dev_stage(s, &dp->forward.back(), stream);
+  }
+  for (auto& s : plan.grad_x) {
+    dp->grad_x.emplace_back();
+    build_dev_stage(s, &dp->grad_x.back(), stream);
+  }
+  for (auto& gw : plan.grad_w) {
+    dp->grad_w.emplace_back();
+    for (auto& s : gw) {
+      dp->grad_w.back().emplace_back();
+      build_dev_stage(s, &dp->grad_w.back().back(), stream);
+    }
+  }
+  cuda_check(cudaStreamSynchronize(stream), "build_dev_plan");
+  return dp.release();
+}
+
+// ---------------------------------------------------------------------------
+// Stage kernels
+// ---------------------------------------------------------------------------
+
+template <typename T> struct Acc;
+template <> struct Acc<float> { using type = float; };
+template <> struct Acc<__nv_bfloat16> { using type = float; };
+template <> struct Acc<double> { using type = double; };
+
+template <typename TA> __device__ __forceinline__ TA to_acc(float v) { return (TA)v; }
+__device__ __forceinline__ float cvt(float v) { return v; }
+__device__ __forceinline__ float cvt(__nv_bfloat16 v) { return __bfloat162float(v); }
+__device__ __forceinline__ double cvt(double v) { return v; }
+
+template <typename TO, typename TA> __device__ __forceinline__ TO from_acc(TA v) { return (TO)v; }
+template <> __device__ __forceinline__ __nv_bfloat16 from_acc<__nv_bfloat16, float>(float v) { return __float2bfloat16(v); }
+
+template <typename TI, typename TA>
+__device__ __forceinline__ TA load_term(const KTerm& T, int64_t off) {
+  if (T.kind == 0) return (TA)cvt(__ldg(((const TI*)T.ptr) + off));
+  return ((const TA*)T.ptr)[off];
+}
+
+__device__ __forceinline__ void term_prep(const KTerm& T, int n_axes, const int32_t* av, int64_t* base, bool* ok,
+                                          int32_t* ia) {
+  int64_t b = T.base;
+  bool good = true;
+#pragma unroll
+  for (int k = 0; k < MAXA; ++k)
+    if (k < n_axes) b += T.lin[k] * av[k];
+#pragma unroll
+  for (int m = 0; m < MAXTAB; ++m) {
+    if (m < T.n_atab) {
+      int32_t idx = 0;
+#pragma unroll
+      for (int k = 0; k < MAXA; ++k)
+        if (k < n_axes) idx += T.atab_s[m][k] * av[k];
+      int32_t v = __ldg(T.atab[m] + idx);
+      good = good && v >= 0;
+      b += v;
+    }
+  }
+#pragma unroll
+  for (int m = 0; m < MAXMIX; ++m) {
+    int32_t idx = 0;
+    if (m < T.n_mix) {
+#pragma unroll
+      for (int k = 0; k < MAXA; ++k)
+        if (k < n_axes) idx += T.mtab_s[m][k] * av[k];
+    }
+    ia[m] = idx;
+  }
+  *base = b;
+  *ok = good;
+}
+
+__device__ __forceinline__ bool term_offset(const KTerm& T, int64_t base, bool ok, const int32_t* ia, int64_t r,
+                                            int64_t* off) {
+  int64_t o = base;
+  if (T.rtab) {
+    int32_t v = __ldg(T.rtab + r);
+    ok = ok && v >= 0;
+    o += v;
+  }
+#pragma unroll
+  for (int m = 0; m < MAXMIX; ++m) {
+    if (m < T.n_mix) {
+      int32_t v = __ldg(T.mtab[m] + ia[m] + __ldg(T.mri[m] + r));
+      ok = ok && v >= 0;
+      o += v;
+    }
+  }
+  *off = o;
+  return ok;
+}
+
+template <typename T> __device__ __forceinline__ void atomic_add(T* p, T v) { atomicAdd(p, v); }
+
+template <typename TI, typename TA, bool SCATTER>
+__global__ void __launch_bounds__(256) stage_kernel(const __grid_constant__ KStage S) {
+  const int64_t o = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (o >= S.out_count) return;
+  const int64_t r0 = (int64_t)blockIdx.y * S.r_chunk;
+  const int64_t r1 = min(S.R, r0 + S.r_chunk);
+  int32_t av[MAXA];
+  {
+    int64_t rem = o;
+#pragma unroll
+    for (int k = MAXA - 1; k >= 0; --k) {
+      if (k < S.n_axes) {
+        int64_t e = S.axis_ext[k];
+        av[k] = (int32_t)(rem % e);
+        rem /= e;
+      } else {
+        av[k] = 0;
+      }
+    }
+  }
+  int64_t base[MAXT];
+  bool aok[MAXT];
+  int32_t ia[MAXT][MAXMIX];
+#pragma unroll
+  for (int t = 0; t < MAXT; ++t) {
+    base[t] = 0;
+    aok[t] = false;
+    if (t < S.n_terms) term_prep(S.terms[t], S.n_axes, av, &base[t], &aok[t], ia[t]);
+  }
+  int64_t tbase = 0;
+  bool tok = false;
+  int32_t tia[MAXMIX];
+  if (SCATTER) term_prep(S.target, S.n_axes, av, &tbase, &tok, tia);
+  const TA scale = (TA)S.scale;
+  TA acc = 0;
+  for (int64_t r = r0; r < r1; ++r) {
+    TA prod = 1;
+    bool ok = true;
+#pragma unroll
+    for (int t = 0; t < MAXT; ++t) {
+      if (t < S.n_terms && ok) {
+        const KTerm& T = S.terms[t];
+        int64_t off;
+        if (!term_offset(T, base[t], aok[t], ia[t], r, &off)) ok = false;
+        else if (T.kind != 2) prod *= load_term<TI, TA>(T, off);
+      }
+    }
+    if (SCATTER) {
+      int64_t off;
+      if (ok && term_offset(S.target, tbase, tok, tia, r, &off)) atomic_add((TA*)S.out + off, prod * scale);
+    } else if (ok) {
+      acc += prod;
+    }
+  }
+  if (!SCATTER) {
+    if (S.out_acc) ((TA*)S.out)[(int64_t)blockIdx.y * S.out_count * (gridDim.y > 1) + o] = acc * scale;
+    else ((TI*)S.out)[o] = from_acc<TI, TA>(acc * scale);
+  }
+}
+
+template <typename TO, typename TA>
+__global__ void sum_partials(const TA* part, int64_t count, int nsplit, TO* out) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= count) return;
+  TA s = 0;
+  for (int k = 0; k < nsplit; ++k) s += part[(int64_t)k * count + i];
+  out[i] = from_acc<TO, TA>(s);
+}
+
+template <typename TO, typename TA>
+__global__ void cast_kernel(const TA* in, int64_t count, TO* out) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < count) out[i] = from_acc<TO, TA>(in[i]);
+}
+
+// ---------------------------------------------------------------------------
+// Launch
+// ---------------------------------------------------------------------------
+
+static size_t dtype_size(DType dt) { return dt == DT_F64 ? 8 : dt == DT_F32 ? 4 : 2; }
+static size_t acc_size(DType dt) { return dt == DT_F64 ? 8 : 4; }
+
+static const void* bind_ptr(const CTensor& t, const Bindings& b) {
+  switch (t.kind) {
+    case TK_X: return b.x;
+    case TK_W: return b.w.at(t.index);
+    case TK_STAGE: return b.stages.at(t.index);
+    case TK_Y: return b.y;
+    case TK_DY: return b.dy;
+    case TK_DX: return b.dx;
+    case TK_DW: return b.dw.at(t.index);
+    default: return nullptr;
+  }
+}
+
+template <typename TI>
+static void launch_stage_t(const DevStage& ds, const Bindings& b, void* out, bool out_acc, cudaStream_t stream) {
+  using TA = typename Acc<TI>::type;
+  KStage k = ds.k;
+  for (int t = 0; t < k.n_terms; ++t) {
+    k.terms[t].ptr = bind_ptr(ds.cs.terms[t].t, b);
+    if (!k.terms[t].ptr && k.terms[t].kind != 2) fail(SYNO_E_INVALID, "stage input tensor is not bound");
+  }
+  const int64_t out_bytes = k.out_count * (int64_t)(out_acc ? sizeof(TA) : sizeof(TI));
+  if (ds.dead || k.out_count == 0) {
+    if (!ds.cs.scatter && out_bytes) cuda_check(cudaMemsetAsync(out, 0, out_bytes, stream), "memset(dead)");
+    return;
+  }
+  // Reduce split: enough threads to fill the chip about twice.
+  const int64_t want = 148LL * 2048;
+  int64_t nsplit = 1;
+  if (k.out_count < want && k.R >= 64) {
+    nsplit = std::min<int64_t>((want + k.out_count - 1) / k.out_count, k.R / 32);
+    nsplit = std::max<int64_t>(1, std::min<int64_t>(nsplit, 4096));
+  }
+  k.r_chunk = (k.R + nsplit - 1) / nsplit;
+  nsplit = (k.R + k.r_chunk - 1) / k.r_chunk;
+  if (k.R == 0) { nsplit = 1; k.r_chunk = 0; }
+  dim3 grid((unsigned)((k.out_count + 255) / 256), (unsigned)nsplit);
+  if (ds.cs.scatter) {
+    k.out = out;
+    k.out_acc = 1;
+    stage_kernel<TI, TA, true><<<grid, 256, 0, stream>>>(k);
+    cuda_check(cudaGetLastError(), "stage_kernel<scatter>");
+    return;
+  }
+  if (nsplit == 1) {
+    k.out = out;
+    k.out_acc = out_acc;
+    stage_kernel<TI, TA, false><<<grid, 256, 0, stream>>>(k);
+    cuda_check(cudaGetLastError(), "stage_kernel");
+    return;
+  }
+  TA* part = nullptr;
+  cuda_check(cudaMallocAsync((void**)&part, (size_t)nsplit * k.out_count * sizeof(TA), stream), "alloc partials");
+  k.out = part;
+  k.out_acc = 1;
+  stage_kernel<TI, TA, false><<<grid, 256, 0, stream>>>(k);
+  cuda_check(cudaGetLastError(), "stage_kernel<split>");
+  unsigned blocks = (unsigned)((k.out_count + 255) / 256);
+  if (out_acc) sum_partials<TA, TA><<<blocks, 256, 0, stream>>>(part, k.out_count, (int)nsplit, (TA*)out);
+  else sum_partials<TI, TA><<<blocks, 256, 0, stream>>>(part, k.out_count, (int)nsplit, (TI*)out);
+  cuda_check(cudaGetLastError(), "sum_partials");
+  cuda_check(cudaFreeAsync(part, stream), "free partials");
+}
+
+static void launch_stage(DType dt, const DevStage& ds, const Bindings& b, void* out, bool out_acc,
+                         cudaStream_t stream) {
+  switch (dt) {
+    case DT_F32: launch_stage_t<float>(ds, b, out, out_acc, stream); break;
+    case DT_BF16: launch_stage_t<__nv_bfloat16>(ds, b, out, out_acc, stream); break;
+    case DT_F64: launch_stage_t<double>(ds, b, out, out_acc, stream); break;
+    default: fail(SYNO_E_INVALID, "unknown dtype");
+  }
+}
+
+static void launch_cast(DType dt, const void* acc, int64_t count, void* out, cudaStream_t stream) {
+  unsigned blocks = (unsigned)((count + 255) / 256);
+  if (!count) return;
+  if (dt == DT_BF16) cast_kernel<__nv_bfloat16, float><<<blocks, 256, 0, stream>>>((const float*)acc, count, (__nv_bfloat16*)out);
+  cuda_check(cudaGetLastError(), "cast_kernel");
+}
+
+void run_forward(const Plan& plan, DevPlan& dp, DType dt, const Bindings& b_in, cudaStream_t stream) {
+  Bindings b = b_in;
+  b.stages.assign(plan.stage_ext.size(), nullptr);
+  std::vector<void*> owned;
+  for (size_t k = 0; k < plan.stage_ext.size(); ++k) {
+    int64_t n = 1;
+    for (auto e : plan.stage_ext[k]) n *= e;
+    void* p = nullptr;
+    cuda_check(cudaMallocAsync(&p, std::max<int64_t>(n, 1) * acc_size(dt), stream), "alloc stage buffer");
+    b.stages[k] = p;
+    owned.push_back(p);
+  }
+  for (auto& ds : dp.forward) {
+    bool to_stage = ds.cs.out.kind == TK_STAGE;
+    void* out = to_stage ? b.stages[ds.cs.out.index] : b.y;
+    if (!to_stage && !tc_try_stage(dt, ds, b, out, stream)) launch_stage(dt, ds, b, out, to_stage, stream);
+    else if (to_stage) launch_stage(dt, ds, b, out, true, stream);
+  }
+  for (void* p : owned) cuda_check(cudaFreeAsync(p, stream), "free stage buffer");
+}
+
+static void run_grad(DType dt, const DevStage& ds, const Bindings& b, void* out, int64_t count, cudaStream_t stream) {
+  if (!out) return;
+  if (!ds.cs.scatter) {
+    if (!tc_try_stage(dt, ds, b, out, stream)) launch_stage(dt, ds, b, out, false, stream);
+    return;
+  }
+  const size_t asz = acc_size(dt);
+  if (dt != DT_BF16) {
+    cuda_check(cudaMemsetAsync(out, 0, count * asz, stream), "memset(grad)");
+    if (!ds.dead) launch_stage(dt, ds, b, out, true, stream);
+    return;
+  }
+  void* acc = nullptr;
+  cuda_check(cudaMallocAsync(&acc, std::max<int64_t>(count, 1) * asz, stream), "alloc grad acc");
+  cuda_check(cudaMemsetAsync(acc, 0, count * asz, stream), "memset(grad acc)");
+  if (!ds.dead) launch_stage(dt, ds, b, acc, true, stream);
+  launch_cast(dt, acc, count, out, stream);
+  cuda_check(cudaFreeAsync(acc, stream), "free grad acc");
+}
+
+void run_backward(const Plan& plan, DevPlan& dp, DType dt, const Bindings& b, cudaStream_t stream) {
+  int64_t nx = 1;
+  for (auto e : plan.x_ext) nx *= e;
+  run_grad(dt, dp.grad_x.at(0), b, b.dx, nx, stream);
+  for (size_t j = 0; j < plan.w_ext.size(); ++j) {
+    int64_t nw = 1;
+    for (auto e : plan.w_ext[j]) nw *= e;
+    run_grad(dt, dp.grad_w.at(j).at(0), b, j < b.dw.size() ? b.dw[j] : nullptr, nw, stream);
+  }
+}
+
+}  // namespace syno

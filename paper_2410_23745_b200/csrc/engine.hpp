@@ -1,0 +1,92 @@
+// Device engine: index tables (K1), the universal stage kernels and the
+// per-operator device plan.  Host-visible interface used by the C ABI.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "plan.hpp"
+
+namespace syno {
+
+enum DType : int { DT_F32 = 0, DT_BF16 = 1, DT_F64 = 2 };
+
+constexpr int MAXA = 10;    // axes of a stage
+constexpr int MAXT = 8;     // terms of a stage (phantoms included)
+constexpr int MAXTAB = 4;   // axis-only coordinate tables per term
+constexpr int MAXMIX = 4;   // axis x reduce coordinate tables per term
+
+struct KTerm {
+  const void* ptr;
+  int32_t kind;             // 0 = input dtype, 1 = accumulator dtype, 2 = phantom
+  int32_t n_atab, n_mix;
+  int32_t pad_;
+  int64_t base;
+  int64_t lin[MAXA];        // axis-linear offset coefficients
+  const int32_t* atab[MAXTAB];
+  int32_t atab_s[MAXTAB][MAXA];
+  const int32_t* mtab[MAXMIX];
+  int32_t mtab_s[MAXMIX][MAXA];
+  const int32_t* mri[MAXMIX];  // per flat-reduce index into mtab
+  const int32_t* rtab;         // per flat-reduce offset (-1: out of range), null if none
+};
+
+struct KStage {
+  int32_t n_axes, n_terms;
+  int32_t out_acc;          // output in accumulator dtype (stage buffers, scatter scratch)
+  int32_t pad_;
+  int64_t axis_ext[MAXA];
+  int64_t out_count;        // prod(axis_ext)
+  int64_t R;                // prod(red_ext)
+  int64_t r_chunk;          // reduce iterations per blockIdx.y
+  double scale;
+  void* out;
+  KTerm terms[MAXT];
+  KTerm target;             // scatter form only
+};
+
+// One device-resident stage: tables plus a descriptor with null pointers
+// for the run-time tensors (bound per launch).
+struct DevStage {
+  CStage cs;
+  KStage k;
+  std::vector<int> term_slot;   // CTensor of each term, to bind pointers
+  int32_t* tables = nullptr;    // owned device allocation
+  size_t table_entries = 0;
+  bool dead = false;
+};
+
+struct DevPlan {
+  int device = -1;
+  std::vector<DevStage> forward, grad_x;
+  std::vector<std::vector<DevStage>> grad_w;
+  ~DevPlan();
+};
+
+struct Bindings {
+  const void* x = nullptr;
+  std::vector<const void*> w;
+  void* y = nullptr;
+  const void* dy = nullptr;
+  void* dx = nullptr;
+  std::vector<void*> dw;
+  std::vector<void*> stages;  // t_k buffers
+};
+
+// Builds tables on `stream` (K1) for every stage of the plan.
+DevPlan* build_dev_plan(const Plan& plan, cudaStream_t stream);
+
+// Launches. All pointers are device pointers; tensors are dense row-major.
+void run_forward(const Plan& plan, DevPlan& dp, DType dt, const Bindings& b, cudaStream_t stream);
+void run_backward(const Plan& plan, DevPlan& dp, DType dt, const Bindings& b, cudaStream_t stream);
+
+// K1 debug/parity hook: raw int64 values of one coordinate of one term over
+// the full loop grid of a stage (row-major over axes then reduces).
+void eval_coordinate_grid(const CStage& s, int term, int coord, int64_t* out_dev, cudaStream_t stream);
+
+void cuda_check(cudaError_t e, const char* what);
+
+}  // namespace syno

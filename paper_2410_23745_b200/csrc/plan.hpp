@@ -1,0 +1,103 @@
+// Concrete execution plan: loop nests with every size evaluated, iterators
+// renumbered as loop indices, batch axes made explicit, plus the backward
+// stages derived from the unstaged nest.
+//
+// Every stage, forward or backward, has the one shape the reference's
+// _run_stage evaluates (codegen.py:515-546):
+//     out[axes] = scale * sum_{reduces} prod_terms term[coords(axes, reduces)]
+// where a term reads zero when any coordinate is out of range
+// (codegen.py:535-541).  Backward stages come from two derivations:
+//   * gather form: the target term's coordinates are solved for loop
+//     iterators ("transposed gather"); unsolved coordinates
+//     become equality checks.  No atomics, deterministic.
+//   * scatter form: the reference's own algorithm (codegen.py:727-742,
+//     np.add.at) with device atomics, used when inversion would cost more.
+#pragma once
+
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "nest.hpp"
+
+namespace syno {
+
+enum class COp : uint8_t { Loop, Const, Add, Sub, Mul, FloorDiv, Mod };
+
+struct CNode;
+using CE = std::shared_ptr<const CNode>;
+struct CNode {
+  COp op;
+  int loop = -1;       // Loop
+  int64_t value = 0;   // Const
+  CE lhs, rhs;
+};
+
+CE c_loop(int l);
+CE c_const(int64_t v);
+CE c_bin(COp op, CE a, CE b);
+void c_loops(const CE& e, std::vector<int>* out);  // sorted unique loop ids
+int64_t c_eval(const CE& e, const int64_t* loop_vals);
+std::string c_render(const CE& e);
+
+// Tensor roles bound at run time.
+enum TensorKind : int {
+  TK_X = 0,       // operator input (batch + input dims)
+  TK_W = 1,       // weight j
+  TK_STAGE = 2,   // intermediate t_k (workspace, accumulator precision)
+  TK_Y = 3,       // operator output
+  TK_DY = 4,      // upstream gradient
+  TK_DX = 5,      // input gradient
+  TK_DW = 6,      // weight gradient j
+  TK_PHANTOM = 7, // validity-only term (value 1 when in range)
+};
+
+struct CTensor {
+  int kind = TK_X;
+  int index = 0;
+  std::vector<int64_t> extents;
+  int64_t numel() const {
+    int64_t n = 1;
+    for (auto e : extents) n *= e;
+    return n;
+  }
+  bool operator==(const CTensor& o) const { return kind == o.kind && index == o.index; }
+};
+
+struct CTerm {
+  CTensor t;
+  std::vector<CE> coords;
+};
+
+struct CStage {
+  std::vector<int64_t> axis_ext;  // loops [0, A)
+  std::vector<int64_t> red_ext;   // loops [A, A+R)
+  std::vector<CTerm> terms;
+  CTensor out;                    // written row-major over the axes (gather form)
+  bool scatter = false;           // scatter form: out is indexed by `target` instead
+  CTerm target;
+  double scale = 1.0;             // multiplicity of reduces no term reads
+  bool dead = false;              // some term is never in range: out == 0
+  int nloops() const { return (int)(axis_ext.size() + red_ext.size()); }
+  int64_t ext(int l) const { return l < (int)axis_ext.size() ? axis_ext[l] : red_ext[l - axis_ext.size()]; }
+  double grid_points() const;
+  std::string describe() const;
+};
+
+struct Plan {
+  int64_t batch = 1;
+  std::vector<int64_t> batch_ext;
+  std::vector<int64_t> x_ext, y_ext;              // including batch
+  std::vector<std::vector<int64_t>> w_ext;
+  std::vector<std::vector<int64_t>> stage_ext;    // t_k extents (batch-prefixed when data-dependent)
+  std::vector<CStage> forward;                    // staged or unstaged, in order
+  CStage unstaged;                                // batch-explicit unstaged stage (backward source)
+  std::vector<CStage> grad_x;                     // stages producing dX (one)
+  std::vector<std::vector<CStage>> grad_w;        // per weight
+  int64_t flops_unstaged = 0, flops_staged = 0;   // codegen.flops, batch included
+};
+
+Plan build_plan(const LoopNest& unstaged, const LoopNest& staged_or_same, const std::vector<Size>& batch_dims,
+                const Assignment& env);
+
+}  // namespace syno

@@ -1,0 +1,196 @@
+"""GPU parity: the CUDA path (through the C ABI) against the reference's
+golden outputs and the pinned CPU oracle.
+
+Tolerances (metric rel_err = max|d| / max|want|,
+reference test_codegen.py:95-97): integer index maps bit-exact;
+float64 1e-10; float32 1e-4; bfloat16 2e-2 (oracle fed bf16-rounded inputs).
+"""
+from __future__ import annotations
+
+import os
+
+import numpy as np
+import pytest
+
+from conftest import CASE_IDS, CASES, GOLDEN, case_tensors
+
+from oracle import nest_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+TOL = {"float64": 1e-10, "float32": 1e-4, "bfloat16": 2e-2}
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def _run(case, x, ws, up, dtype, staged=False):
+    from paper_2410_23745_b200 import ops
+    from paper_2410_23745_b200 import pgraph as P
+    torch = _torch()
+    g = P.parse_operator(case["document"])
+    h = P.handle_for(g, case["assignment"], staged)
+    xd = ops.to_device(x, dtype)
+    wd = [ops.to_device(w, dtype) for w in ws]
+    ud = ops.to_device(up, dtype)
+    y = ops.forward(h, xd, wd)
+    dx, dws = ops.backward(h, xd, wd, ud, True, True)
+    torch.cuda.synchronize()
+    f = lambda t: t.double().cpu().numpy()  # noqa: E731
+    return f(y), f(dx), [f(d) for d in dws]
+
+
+def _rounded(a, dtype):
+    torch = _torch()
+    return torch.from_numpy(np.asarray(a)).to(getattr(torch, dtype)).double().numpy()
+
+
+@pytest.mark.parametrize("dtype", ["float64", "float32", "bfloat16"])
+@pytest.mark.parametrize("case", CASES, ids=CASE_IDS)
+def test_golden_forward_backward(cuda, case, dtype):
+    x, ws, up, y, ys, dws = case_tensors(case)
+    env, bs = case["env"], case["batch_shape"]
+    if dtype != "float64":
+        x, up = _rounded(x, dtype), _rounded(up, dtype)
+        ws = [_rounded(w, dtype) for w in ws]
+        y = O.interpret(case["nest"], env, x, ws, bs)
+        dws = O.weight_gradient(case["nest"], env, x, up, ws, bs) if ws else []
+    dx_want = O.input_gradient(case["nest"], env, x, up, ws, bs)
+    gy, gdx, gdw = _run(case, x, ws, up, dtype)
+    tol = TOL[dtype]
+    assert O.rel_err(gy, y) < tol
+    assert O.rel_err(gdx, dx_want) < tol
+    for a, b in zip(gdw, dws):
+        assert O.rel_err(a, b) < tol
+    if dtype == "float64":
+        gys, _, _ = _run(case, x, ws, up, dtype, staged=True)
+        assert O.rel_err(gys, ys) < tol
+
+
+@pytest.mark.parametrize("case", CASES, ids=CASE_IDS)
+def test_index_maps_bit_exact(cuda, case):
+    """K1 tables evaluate every coordinate exactly like codegen._eval_array."""
+    from paper_2410_23745_b200 import ops
+    from paper_2410_23745_b200 import pgraph as P
+    g = P.parse_operator(case["document"])
+    h = P.handle_for(g, case["assignment"])
+    nest = O.parse_nest(case["nest"], case["env"])
+    for t, term in enumerate(nest.stages[0].terms):
+        for c in range(len(term.exprs)):
+            got = ops.index_map(h, t, c).cpu().numpy()
+            want = O.index_values(case["nest"], case["env"], t, c, case["batch_shape"]).reshape(-1)
+            assert np.array_equal(got, want), (t, c)
+
+
+def _corpus():
+    ops_ = [ln.strip() for ln in open(os.path.join(GOLDEN, "corpus_conv64.txt")) if ln.strip()]
+    return ops_
+
+
+CORPUS_SPEC = dict(name="conv64", primaries=("C_out", "C_in", "H", "W", "N"), coeffs=("K", "s"),
+                   reference={"C_out": 64, "C_in": 64, "H": 32, "W": 32, "K": 3, "s": 2, "N": 8},
+                   output=("C_out", "H", "W"), input_=("C_in", "H", "W"), batch=("N",))
+REDUCED = [
+    {"C_out": 4, "C_in": 4, "H": 4, "W": 4, "K": 3, "s": 2, "N": 2},
+    {"C_out": 2, "C_in": 4, "H": 8, "W": 4, "K": 3, "s": 2, "N": 2},
+    {"C_out": 4, "C_in": 2, "H": 4, "W": 8, "K": 3, "s": 2, "N": 2},
+    {"C_out": 2, "C_in": 2, "H": 4, "W": 4, "K": 3, "s": 2, "N": 2},
+]
+
+
+def reduced_case(op):
+    from paper_2410_23745_b200 import codegen as C
+    from paper_2410_23745_b200 import pgraph as P
+    spec = P.build_spec(**CORPUS_SPEC)
+    g = P.parse_steps(op, spec)
+    for red in REDUCED:
+        try:
+            if C.flops(g, red) * 4 > 2e7:
+                continue
+            return g, red
+        except Exception:
+            continue
+    return g, None
+
+
+@pytest.mark.parametrize("chunk", range(8))
+def test_corpus_reduced_fp32(cuda, chunk):
+    """Every 8th corpus operator per chunk, at a reduced assignment, fwd + bwd in fp32."""
+    from paper_2410_23745_b200 import codegen as C
+    from paper_2410_23745_b200 import pgraph as P
+    ops_ = _corpus()[chunk::8]
+    checked = 0
+    for op in ops_:
+        g, red = reduced_case(op)
+        if red is None:
+            continue
+        h = P.handle_for(g, red)
+        text = C.emit_loop_nest(g, red)
+        rng = np.random.default_rng(checked)
+        x = rng.standard_normal(h.x_shape)
+        ws = [rng.standard_normal(s) for s in h.w_shapes]
+        up = rng.standard_normal(h.y_shape)
+        xr, upr = _rounded(x, "float32"), _rounded(up, "float32")
+        wr = [_rounded(w, "float32") for w in ws]
+        case = {"document": g.document, "assignment": red}
+        gy, gdx, gdw = _run(case, xr, wr, upr, "float32")
+        bs = h.x_shape[:1]
+        assert O.rel_err(gy, O.interpret(text, red, xr, wr, bs)) < 1e-4, op
+        assert O.rel_err(gdx, O.input_gradient(text, red, xr, upr, wr, bs)) < 1e-4, op
+        for a, b in zip(gdw, O.weight_gradient(text, red, xr, upr, wr, bs) if wr else []):
+            assert O.rel_err(a, b) < 1e-4, op
+        checked += 1
+    assert checked >= len(ops_) // 2
+
+
+def test_cfg1_full_size_fp32(cuda):
+    """cfg1: conv3x3 N=8 C=64 H=W=32 fp32 forward vs the oracle at full size."""
+    from paper_2410_23745_b200 import codegen as C
+    from paper_2410_23745_b200 import pgraph as P
+    case = next(c for c in CASES if c["name"] == "cfg1_reduced")
+    g = P.parse_operator(case["document"])
+    h = P.handle_for(g)
+    rng = np.random.default_rng(0)
+    x = _rounded(rng.standard_normal(h.x_shape), "float32")
+    w = _rounded(rng.standard_normal(h.w_shapes[0]), "float32")
+    text = C.emit_loop_nest(g)
+    env = dict(g.spec.reference)
+    gy, _, _ = _run({"document": g.document, "assignment": None}, x, [w], np.zeros(h.y_shape), "float32")
+    want = O.interpret(text, env, x, [w], (8,))
+    assert O.rel_err(gy, want) < 1e-4
+
+
+def test_numpy_shims_match_reference_signatures(cuda):
+    """interpret / weight_gradient with numpy in, numpy float64 out (codegen.py:598, 664)."""
+    from paper_2410_23745_b200 import codegen as C
+    from paper_2410_23745_b200 import pgraph as P
+    from paper_2410_23745_b200.errors import ShapeMismatch
+    case = next(c for c in CASES if c["name"] == "conv2d_8")
+    x, ws, up, y, ys, dws = case_tensors(case)
+    g = P.parse_operator(case["document"])
+    out = C.interpret(g, x, ws)
+    assert isinstance(out, np.ndarray) and out.dtype == np.float64
+    assert O.rel_err(out, y) < 1e-12
+    assert O.rel_err(C.interpret(g, x, ws, staged=True), ys) < 1e-12
+    (dw,) = C.weight_gradient(g, x, up, ws)
+    assert O.rel_err(dw, dws[0]) < 1e-12
+    with pytest.raises(ShapeMismatch):
+        C.interpret(g, x.transpose(1, 0, 2).copy()[:, :, :7], ws)
+    with pytest.raises(ShapeMismatch):
+        C.interpret(g, x)
+    with pytest.raises(ShapeMismatch):
+        C.interpret(g, x, [np.zeros((8, 8, 3, 2))])
+
+
+def test_torch_autograd_module(cuda):
+    torch = _torch()
+    from paper_2410_23745_b200 import ops
+    from paper_2410_23745_b200 import pgraph as P
+    case = next(c for c in CASES if c["name"] == "sep_shared")
+    g = P.parse_operator(case["document"])
+    m = ops.SynoOperator(g, dtype=torch.float64)
+    x = torch.randn(m.h.x_shape, dtype=torch.float64, device="cuda", requires_grad=True)
+    assert torch.autograd.gradcheck(lambda a, *w: ops.SynoFunction.apply(m.h, a, *w), (x, *m.weight),
+                                    eps=1e-6, atol=1e-7)
