@@ -79,6 +79,7 @@ typedef struct {
   int64_t index_grid;     /* points of the unstaged batch-explicit loop grid */
   int32_t complete;       /* frontier matches the input (pgraph.match_input) */
   int32_t replay_only;    /* compiled with SYNO_REPLAY_ONLY: shapes/flops not filled */
+  int32_t tc_path;        /* 1: bf16 runs on the tcgen05 implicit-GEMM path */
 } syno_info;
 
 /* Parse an operator document (pgraph.print_operator format), replay its
@@ -111,6 +112,10 @@ int syno_index_map(syno_op_t op, int term, int coord, int64_t* out_dev, void* st
 void syno_destroy(syno_op_t op);
 const char* syno_last_error(void);
 const char* syno_version(void);
+
+/* Kernels this library has launched in this process (all handles, all
+ * devices); bench.py reports the difference across its timed region. */
+uint64_t syno_launch_count(void);
 
 #ifdef __cplusplus
 }

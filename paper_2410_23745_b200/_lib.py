@@ -35,7 +35,7 @@ MAX_WEIGHTS = 16
 EXPORTS = (
     "syno_compile", "syno_forward", "syno_backward", "syno_query",
     "syno_emit_loop_nest", "syno_print_operator", "syno_describe_plan",
-    "syno_index_map", "syno_destroy", "syno_last_error", "syno_version",
+    "syno_index_map", "syno_destroy", "syno_last_error", "syno_version", "syno_launch_count",
 )
 
 
@@ -58,6 +58,7 @@ class SynoInfo(ctypes.Structure):
         ("index_grid", ctypes.c_int64),
         ("complete", ctypes.c_int32),
         ("replay_only", ctypes.c_int32),
+        ("tc_path", ctypes.c_int32),
     ]
 
 
@@ -84,8 +85,9 @@ def _load():
     lib.syno_destroy.restype = None
     lib.syno_last_error.restype = ctypes.c_char_p
     lib.syno_version.restype = ctypes.c_char_p
+    lib.syno_launch_count.restype = ctypes.c_uint64
     for name in EXPORTS:
-        if name not in ("syno_destroy", "syno_last_error", "syno_version"):
+        if name not in ("syno_destroy", "syno_last_error", "syno_version", "syno_launch_count"):
             getattr(lib, name).restype = ctypes.c_int
     return lib
 

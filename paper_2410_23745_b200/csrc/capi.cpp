@@ -11,6 +11,7 @@
 #include <sstream>
 
 #include "engine.hpp"
+#include "tc.hpp"
 
 using namespace syno;
 
@@ -187,6 +188,7 @@ int syno_query(syno_op_t op, syno_info* info) {
     for (auto e : p.unstaged.axis_ext) g *= (double)e;
     for (auto e : op->unstaged.stages[0].reduces) g *= (double)e.extent;
     info->index_grid = (int64_t)g;
+    info->tc_path = tc_matches(p);
   });
 }
 
@@ -259,5 +261,7 @@ void syno_destroy(syno_op_t op) { delete op; }
 const char* syno_last_error(void) { return g_last_error.c_str(); }
 
 const char* syno_version(void) { return "syno-b200 0.1 (sm_100a)"; }
+
+uint64_t syno_launch_count(void) { return launch_count(); }
 
 }  // extern "C"

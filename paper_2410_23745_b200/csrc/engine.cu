@@ -12,6 +12,7 @@
 #include <cuda_bf16.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstring>
 #include <set>
 
@@ -23,6 +24,10 @@ namespace syno {
 void cuda_check(cudaError_t e, const char* what) {
   if (e != cudaSuccess) fail(SYNO_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
 }
+
+static std::atomic<uint64_t> g_launches{0};
+void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+uint64_t launch_count() { return g_launches.load(std::memory_order_relaxed); }
 
 // ---------------------------------------------------------------------------
 // K1: coordinate programs
@@ -167,6 +172,7 @@ static void launch_k1(const TabSpec& t, int32_t* out, int64_t* out_raw, cudaStre
   a.out_raw = out_raw;
   if (t.count > 0) {
     int64_t blocks = (t.count + 255) / 256;
+    note_launch();
     k1_build_table<<<(unsigned)blocks, 256, 0, stream>>>(a);
     cuda_check(cudaGetLastError(), "k1_build_table");
   }
@@ -287,7 +293,12 @@ static void build_kterm(const CStage& s, const CTerm& t, KTerm* k, std::vector<T
   }
 }
 
-static void build_dev_stage(const CStage& cs, DevStage* ds, cudaStream_t stream) {
+void release_dev_stage(DevStage& ds) {
+  if (ds.tables) cudaFree(ds.tables);
+  ds.tables = nullptr;
+}
+
+void build_dev_stage(const CStage& cs, DevStage* ds, cudaStream_t stream) {
   ds->cs = cs;
   KStage& k = ds->k;
   memset(&k, 0, sizeof(KStage));
@@ -324,8 +335,7 @@ static void build_dev_stage(const CStage& cs, DevStage* ds, cudaStream_t stream)
 
 DevPlan::~DevPlan() {
   auto rel = [](std::vector<DevStage>& v) {
-    for (auto& s : v)
-      if (s.tables) cudaFree(s.tables);
+    for (auto& s : v) release_dev_stage(s);
   };
   rel(forward);
   rel(grad_x);
@@ -350,6 +360,7 @@ DevPlan* build_dev_plan(const Plan& plan, cudaStream_t stream) {
       build_dev_stage(s, &dp->grad_w.back().back(), stream);
     }
   }
+  dp->tc = tc_build(plan, stream);
   cuda_check(cudaStreamSynchronize(stream), "build_dev_plan");
   return dp.release();
 }
@@ -554,6 +565,7 @@ static void launch_stage_t(const DevStage& ds, const Bindings& b, void* out, boo
   if (ds.cs.scatter) {
     k.out = out;
     k.out_acc = 1;
+    note_launch();
     stage_kernel<TI, TA, true><<<grid, 256, 0, stream>>>(k);
     cuda_check(cudaGetLastError(), "stage_kernel<scatter>");
     return;
@@ -561,6 +573,7 @@ static void launch_stage_t(const DevStage& ds, const Bindings& b, void* out, boo
   if (nsplit == 1) {
     k.out = out;
     k.out_acc = out_acc;
+    note_launch();
     stage_kernel<TI, TA, false><<<grid, 256, 0, stream>>>(k);
     cuda_check(cudaGetLastError(), "stage_kernel");
     return;
@@ -569,17 +582,18 @@ static void launch_stage_t(const DevStage& ds, const Bindings& b, void* out, boo
   cuda_check(cudaMallocAsync((void**)&part, (size_t)nsplit * k.out_count * sizeof(TA), stream), "alloc partials");
   k.out = part;
   k.out_acc = 1;
+  note_launch();
   stage_kernel<TI, TA, false><<<grid, 256, 0, stream>>>(k);
   cuda_check(cudaGetLastError(), "stage_kernel<split>");
   unsigned blocks = (unsigned)((k.out_count + 255) / 256);
+  note_launch();
   if (out_acc) sum_partials<TA, TA><<<blocks, 256, 0, stream>>>(part, k.out_count, (int)nsplit, (TA*)out);
   else sum_partials<TI, TA><<<blocks, 256, 0, stream>>>(part, k.out_count, (int)nsplit, (TI*)out);
   cuda_check(cudaGetLastError(), "sum_partials");
   cuda_check(cudaFreeAsync(part, stream), "free partials");
 }
 
-static void launch_stage(DType dt, const DevStage& ds, const Bindings& b, void* out, bool out_acc,
-                         cudaStream_t stream) {
+void run_stage(DType dt, const DevStage& ds, const Bindings& b, void* out, bool out_acc, cudaStream_t stream) {
   switch (dt) {
     case DT_F32: launch_stage_t<float>(ds, b, out, out_acc, stream); break;
     case DT_BF16: launch_stage_t<__nv_bfloat16>(ds, b, out, out_acc, stream); break;
@@ -590,12 +604,16 @@ static void launch_stage(DType dt, const DevStage& ds, const Bindings& b, void* 
 
 static void launch_cast(DType dt, const void* acc, int64_t count, void* out, cudaStream_t stream) {
   unsigned blocks = (unsigned)((count + 255) / 256);
-  if (!count) return;
-  if (dt == DT_BF16) cast_kernel<__nv_bfloat16, float><<<blocks, 256, 0, stream>>>((const float*)acc, count, (__nv_bfloat16*)out);
+  if (!count || dt != DT_BF16) return;
+  note_launch();
+  cast_kernel<__nv_bfloat16, float><<<blocks, 256, 0, stream>>>((const float*)acc, count, (__nv_bfloat16*)out);
   cuda_check(cudaGetLastError(), "cast_kernel");
 }
 
 void run_forward(const Plan& plan, DevPlan& dp, DType dt, const Bindings& b_in, cudaStream_t stream) {
+  // Tensor-core path first: it computes the unstaged contraction, which the
+  // staged nest equals by construction (codegen.py:605-608).
+  if (dp.tc && tc_forward(*dp.tc, dt, b_in, stream)) return;
   Bindings b = b_in;
   b.stages.assign(plan.stage_ext.size(), nullptr);
   std::vector<void*> owned;
@@ -610,8 +628,7 @@ void run_forward(const Plan& plan, DevPlan& dp, DType dt, const Bindings& b_in, 
   for (auto& ds : dp.forward) {
     bool to_stage = ds.cs.out.kind == TK_STAGE;
     void* out = to_stage ? b.stages[ds.cs.out.index] : b.y;
-    if (!to_stage && !tc_try_stage(dt, ds, b, out, stream)) launch_stage(dt, ds, b, out, to_stage, stream);
-    else if (to_stage) launch_stage(dt, ds, b, out, true, stream);
+    run_stage(dt, ds, b, out, to_stage, stream);
   }
   for (void* p : owned) cuda_check(cudaFreeAsync(p, stream), "free stage buffer");
 }
@@ -619,24 +636,25 @@ void run_forward(const Plan& plan, DevPlan& dp, DType dt, const Bindings& b_in, 
 static void run_grad(DType dt, const DevStage& ds, const Bindings& b, void* out, int64_t count, cudaStream_t stream) {
   if (!out) return;
   if (!ds.cs.scatter) {
-    if (!tc_try_stage(dt, ds, b, out, stream)) launch_stage(dt, ds, b, out, false, stream);
+    run_stage(dt, ds, b, out, false, stream);
     return;
   }
   const size_t asz = acc_size(dt);
   if (dt != DT_BF16) {
     cuda_check(cudaMemsetAsync(out, 0, count * asz, stream), "memset(grad)");
-    if (!ds.dead) launch_stage(dt, ds, b, out, true, stream);
+    if (!ds.dead) run_stage(dt, ds, b, out, true, stream);
     return;
   }
   void* acc = nullptr;
   cuda_check(cudaMallocAsync(&acc, std::max<int64_t>(count, 1) * asz, stream), "alloc grad acc");
   cuda_check(cudaMemsetAsync(acc, 0, count * asz, stream), "memset(grad acc)");
-  if (!ds.dead) launch_stage(dt, ds, b, acc, true, stream);
+  if (!ds.dead) run_stage(dt, ds, b, acc, true, stream);
   launch_cast(dt, acc, count, out, stream);
   cuda_check(cudaFreeAsync(acc, stream), "free grad acc");
 }
 
 void run_backward(const Plan& plan, DevPlan& dp, DType dt, const Bindings& b, cudaStream_t stream) {
+  if (dp.tc && tc_backward(*dp.tc, dt, b, stream)) return;
   int64_t nx = 1;
   for (auto e : plan.x_ext) nx *= e;
   run_grad(dt, dp.grad_x.at(0), b, b.dx, nx, stream);

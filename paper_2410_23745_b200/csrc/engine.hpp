@@ -4,6 +4,7 @@
 
 #include <cuda_runtime.h>
 
+#include <memory>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -59,12 +60,21 @@ struct DevStage {
   bool dead = false;
 };
 
+struct TcPlan;  // tensor-core path (tc.cu)
+struct TcPlanDeleter {
+  void operator()(TcPlan* p) const;
+};
+using TcPlanPtr = std::unique_ptr<TcPlan, TcPlanDeleter>;
+
 struct DevPlan {
   int device = -1;
   std::vector<DevStage> forward, grad_x;
   std::vector<std::vector<DevStage>> grad_w;
+  TcPlanPtr tc;  // null when the operator is not contraction-shaped
   ~DevPlan();
 };
+
+
 
 struct Bindings {
   const void* x = nullptr;
@@ -75,6 +85,11 @@ struct Bindings {
   std::vector<void*> dw;
   std::vector<void*> stages;  // t_k buffers
 };
+
+// Build one device stage (K1 tables) / launch it through the universal kernel.
+void build_dev_stage(const CStage& cs, DevStage* ds, cudaStream_t stream);
+void release_dev_stage(DevStage& ds);
+void run_stage(DType dt, const DevStage& ds, const Bindings& b, void* out, bool out_acc, cudaStream_t stream);
 
 // Builds tables on `stream` (K1) for every stage of the plan.
 DevPlan* build_dev_plan(const Plan& plan, cudaStream_t stream);
@@ -88,5 +103,9 @@ void run_backward(const Plan& plan, DevPlan& dp, DType dt, const Bindings& b, cu
 void eval_coordinate_grid(const CStage& s, int term, int coord, int64_t* out_dev, cudaStream_t stream);
 
 void cuda_check(cudaError_t e, const char* what);
+
+// Process-wide count of kernels this library launched (syno_launch_count).
+void note_launch();
+uint64_t launch_count();
 
 }  // namespace syno

@@ -190,7 +190,7 @@ static CStage remap_stage_loops(CStage s, const std::map<int, int>& m) {
 }
 
 // Gradient of <dy, out> with respect to term j of the unstaged stage S.
-static CStage derive_gradient(const CStage& S, int j, const CTensor& grad) {
+CStage derive_gradient(const CStage& S, int j, const CTensor& grad) {
   const int L = S.nloops();
   const int A = (int)S.axis_ext.size();
   const CTerm& tj = S.terms[j];

@@ -97,6 +97,10 @@ struct Plan {
   int64_t flops_unstaged = 0, flops_staged = 0;   // codegen.flops, batch included
 };
 
+// Gradient of <dy, out> with respect to term j of stage S (gather form when
+// the target's coordinates invert at acceptable cost, else scatter form).
+CStage derive_gradient(const CStage& S, int j, const CTensor& grad);
+
 Plan build_plan(const LoopNest& unstaged, const LoopNest& staged_or_same, const std::vector<Size>& batch_dims,
                 const Assignment& env);
 

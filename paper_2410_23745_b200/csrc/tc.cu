@@ -1,8 +1,714 @@
-// Tensor-core fast path (placeholder until the tcgen05 kernels land).
+// Tensor-core path: operator matcher, operand packing, weight folding and
+// the three tcgen05 GEMM launches (forward, grad-input, grad-weight).
+//
+// Geometry of one windowed pixel dim (unfold over a strided data dim,
+// pgraph.py:390-403): output index h reads input  S*h + r - c  for window
+// r in [0, K).  Write  r - c = S*delta(r) + phi(r)  (floor division): the
+// input is phase plane phi(r) of x (P_phi[u] = x[S*u + phi]) at u = h +
+// delta(r).  Zero-padding every plane by lo/hi rows puts all windows of
+// all output pixels on ONE flat padded grid, so a window is a constant row
+// shift  delta_h*Wp + delta_w  of a 2-D operand and TMA tiles it directly
+// (its out-of-bounds fill supplies the reference's "out of range reads
+// zero", codegen.py:14-16).
 #include "tc.hpp"
+
+#include <cuda.h>
+#include <cuda_bf16.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <functional>
+#include <map>
+#include <set>
+#include <sstream>
+
+#include "tc_gemm.cuh"
 
 namespace syno {
 
-bool tc_try_stage(DType, const DevStage&, const Bindings&, void*, cudaStream_t) { return false; }
+using namespace tc;
+
+// ---------------------------------------------------------------------------
+// TMA descriptors
+// ---------------------------------------------------------------------------
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    cuda_check(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q),
+               "cudaGetDriverEntryPoint(cuTensorMapEncodeTiled)");
+    if (!p || q != cudaDriverEntryPointSuccess) fail(SYNO_E_CUDA, "cuTensorMapEncodeTiled unavailable");
+    return reinterpret_cast<EncodeTiledFn>(p);
+  }();
+  return fn;
+}
+
+// 3-D bf16 map [d0 (K, contiguous)][d1 (rows)][d2 (planes)], box [64][box1][1], 128B swizzle.
+static CUtensorMap make_map(const void* base, uint64_t d0, uint64_t d1, uint64_t d2, uint64_t pitch1_elems,
+                            uint64_t pitch2_elems, uint32_t box1) {
+  CUtensorMap m;
+  cuuint64_t dims[3] = {d0, d1, d2};
+  cuuint64_t strides[2] = {pitch1_elems * 2, pitch2_elems * 2};
+  cuuint32_t box[3] = {(cuuint32_t)BK, box1, 1};
+  cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, es,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) fail(SYNO_E_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+  return m;
+}
+
+// ---------------------------------------------------------------------------
+// Packing kernels (bandwidth-bound layout transforms)
+// ---------------------------------------------------------------------------
+
+struct PackGeom {
+  int64_t s_img, s_c, s_h, s_w;  // source element strides
+  int32_t C, Hin, Win;           // source extents
+  int32_t Sh, Sw;                // phase counts (strides)
+  int32_t lo_h, lo_w, Hp, Wp;    // padded plane grid
+  int32_t n_img;
+  int32_t Cp;                    // channels-last pitch (multiple of 8)
+  int64_t Fpitch;                // channel-major row pitch (multiple of 8)
+};
+
+// dst[plane][img][hp][wp][cp], planes = Sh*Sw, zero outside the source.
+// A 64-channel x 32-pixel tile transposes through shared memory so both the
+// NCHW reads (along w) and the channels-last writes (16 B per thread) coalesce.
+template <typename TI>
+__global__ void __launch_bounds__(256) pack_cl_kernel(const TI* __restrict__ src, __nv_bfloat16* __restrict__ dst,
+                                                      PackGeom g) {
+  __shared__ __nv_bfloat16 tile[64][34];
+  const int wp0 = blockIdx.x * 32;
+  const int hp = blockIdx.y;
+  const int ncb = (g.Cp + 63) / 64;
+  int z = blockIdx.z;
+  const int cb = z % ncb;
+  z /= ncb;
+  const int img = z % g.n_img;
+  const int plane = z / g.n_img;
+  const int ph = plane / g.Sw, pw = plane % g.Sw;
+  const int hi = g.Sh * (hp - g.lo_h) + ph;
+  const int t = threadIdx.x;
+  {
+    const int c = cb * 64 + t / 4;
+    const int w0 = (t % 4) * 8;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int wp = wp0 + w0 + k;
+      const int wi = g.Sw * (wp - g.lo_w) + pw;
+      float v = 0.f;
+      if (c < g.C && hi >= 0 && hi < g.Hin && wi >= 0 && wi < g.Win && wp < g.Wp)
+        v = (float)src[img * g.s_img + c * g.s_c + (int64_t)hi * g.s_h + (int64_t)wi * g.s_w];
+      tile[t / 4][w0 + k] = __float2bfloat16(v);
+    }
+  }
+  __syncthreads();
+  const int w = t / 8, cc = (t % 8) * 8;
+  const int wp = wp0 + w;
+  const int c0 = cb * 64 + cc;
+  if (wp < g.Wp && c0 < g.Cp) {
+    __align__(16) __nv_bfloat16 v[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) v[k] = tile[cc + k][w];
+    const int64_t o = ((((int64_t)plane * g.n_img + img) * g.Hp + hp) * g.Wp + wp) * g.Cp + c0;
+    *reinterpret_cast<uint4*>(dst + o) = *reinterpret_cast<const uint4*>(v);
+  }
+}
+
+// dst[plane][c][flat] with flat = (img*Hp + hp)*Wp + wp, row pitch Fpitch.
+template <typename TI>
+__global__ void __launch_bounds__(256) pack_cm_kernel(const TI* __restrict__ src, __nv_bfloat16* __restrict__ dst,
+                                                      PackGeom g, int64_t total) {
+  const int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 8;  // 8 flat positions per thread
+  if (i >= total) return;
+  const int64_t F = (int64_t)g.n_img * g.Hp * g.Wp;
+  const int64_t row = i / g.Fpitch;
+  const int64_t f0 = i % g.Fpitch;
+  const int c = (int)(row % g.C);
+  const int plane = (int)(row / g.C);
+  const int ph = plane / g.Sw, pw = plane % g.Sw;
+  __align__(16) __nv_bfloat16 v[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const int64_t f = f0 + k;
+    float val = 0.f;
+    if (f < F) {
+      const int wp = (int)(f % g.Wp);
+      const int64_t t = f / g.Wp;
+      const int hp = (int)(t % g.Hp);
+      const int img = (int)(t / g.Hp);
+      const int hi = g.Sh * (hp - g.lo_h) + ph, wi = g.Sw * (wp - g.lo_w) + pw;
+      if (hi >= 0 && hi < g.Hin && wi >= 0 && wi < g.Win)
+        val = (float)src[img * g.s_img + c * g.s_c + (int64_t)hi * g.s_h + (int64_t)wi * g.s_w];
+    }
+    v[k] = __float2bfloat16(val);
+  }
+  *reinterpret_cast<uint4*>(dst + i) = *reinterpret_cast<const uint4*>(v);
+}
+
+// ---------------------------------------------------------------------------
+// Plan
+// ---------------------------------------------------------------------------
+
+struct PixDim {
+  int axis = -1;       // stage loop (output axis)
+  int win = -1;        // window reduce loop, -1 none
+  int S = 1, K = 1;
+  int64_t c = 0;       // offset constant
+  int64_t E = 1;       // output extent
+  int64_t Ein = 1;     // input extent
+  int64_t xs = 0, ys = 0;  // element strides of the coordinate in x and y
+  int lo = 0, hi = 0;  // forward padding of the phase planes
+  int dlo = 0, dhi = 0;  // grad-input padding of dy
+  int64_t Ep() const { return E + lo + hi; }
+  int64_t dEp() const { return E + dlo + dhi; }
+  int delta(int r) const { return (int)std::floor((double)(r - c) / S); }
+  int phi(int r) const { return (int)(((r - c) % S + S) % S); }
+};
+
+struct TcPlan {
+  int n_img = 1;
+  int64_t x_img = 0, y_img = 0;   // element strides of the flattened image index
+  int64_t x_c = 0, y_n = 0;       // channel / output-channel strides
+  int C = 0, N = 0, Cp = 0, Np = 0;
+  PixDim dh, dw;
+  double scale = 1;
+  bool dgrad_ok = false;
+  DevStage fold_fwd, fold_dgrad;
+  std::vector<DevStage> chain;    // dW_j from the folded gradient
+  std::vector<int64_t> w_numel;
+  int nwin() const { return dh.K * dw.K; }
+};
+
+void TcPlanDeleter::operator()(TcPlan* p) const {
+  if (!p) return;
+  release_dev_stage(p->fold_fwd);
+  release_dev_stage(p->fold_dgrad);
+  for (auto& s : p->chain) release_dev_stage(s);
+  delete p;
+}
+
+static std::vector<int64_t> rm_strides(const std::vector<int64_t>& ext) {
+  std::vector<int64_t> s(ext.size(), 1);
+  for (int k = (int)ext.size() - 2; k >= 0; --k) s[k] = s[k + 1] * ext[k + 1];
+  return s;
+}
+
+// S*i + r - c  /  i + r - c  (unfold over a [strided] data dim)
+static bool match_window(const CE& e, int A, int* axis, int* red, int* S, int64_t* c) {
+  if (e->op != COp::Sub || e->rhs->op != COp::Const) return false;
+  const CE& add = e->lhs;
+  if (add->op != COp::Add || add->rhs->op != COp::Loop || add->rhs->loop < A) return false;
+  const CE& data = add->lhs;
+  if (data->op == COp::Loop && data->loop < A) {
+    *S = 1;
+    *axis = data->loop;
+  } else if (data->op == COp::Mul && data->lhs->op == COp::Const && data->rhs->op == COp::Loop &&
+             data->rhs->loop < A) {
+    *S = (int)data->lhs->value;
+    *axis = data->rhs->loop;
+  } else {
+    return false;
+  }
+  *red = add->rhs->loop;
+  *c = e->rhs->value;
+  return *S >= 1;
+}
+
+static TcPlan* try_match(const Plan& plan) {
+  const CStage& S = plan.unstaged;
+  const int A = (int)S.axis_ext.size();
+  const int L = S.nloops();
+  if (S.terms.empty() || S.terms[0].t.kind != TK_X || S.terms.size() < 2) return nullptr;
+  const CTerm& x = S.terms[0];
+  for (size_t t = 1; t < S.terms.size(); ++t)
+    if (S.terms[t].t.kind != TK_W) return nullptr;
+  auto xs = rm_strides(x.t.extents);
+  auto ys = rm_strides(S.axis_ext);  // y is row-major over the stage axes
+  int chan = -1, chan_coord = -1;
+  std::vector<PixDim> pix;
+  std::set<int> used_axes, used_red;
+  for (size_t d = 0; d < x.coords.size(); ++d) {
+    const CE& e = x.coords[d];
+    PixDim p;
+    if (e->op == COp::Loop) {
+      if (e->loop >= A) {
+        if (chan >= 0) return nullptr;
+        chan = e->loop;
+        chan_coord = (int)d;
+        if (x.t.extents[d] != S.ext(chan)) return nullptr;
+        continue;
+      }
+      p.axis = e->loop;
+      p.E = S.ext(p.axis);
+      p.Ein = x.t.extents[d];
+      if (p.Ein != p.E) return nullptr;
+    } else {
+      int axis, red, st;
+      int64_t c;
+      if (!match_window(e, A, &axis, &red, &st, &c)) return nullptr;
+      p.axis = axis;
+      p.win = red;
+      p.S = st;
+      p.K = (int)S.ext(red);
+      p.c = c;
+      p.E = S.ext(axis);
+      p.Ein = x.t.extents[d];
+      if (!used_red.insert(red).second) return nullptr;
+    }
+    if (!used_axes.insert(p.axis).second) return nullptr;
+    p.xs = xs[d];
+    p.ys = ys[p.axis];
+    pix.push_back(p);
+  }
+  if (chan < 0) return nullptr;
+  used_red.insert(chan);
+  // exactly one axis is read only by weights
+  int naxis = -1;
+  for (int a = 0; a < A; ++a)
+    if (!used_axes.count(a)) {
+      if (naxis >= 0) return nullptr;
+      naxis = a;
+    }
+  if (naxis < 0) return nullptr;
+  // weights: bare loops only
+  bool n_in_w = false;
+  for (size_t t = 1; t < S.terms.size(); ++t)
+    for (auto& e : S.terms[t].coords) {
+      if (e->op != COp::Loop) return nullptr;
+      if (e->loop == naxis) n_in_w = true;
+      if (e->loop < A && e->loop != naxis) return nullptr;
+    }
+  if (!n_in_w) return nullptr;
+  // image dims: all pixel dims but the last two, window-free and row-major-contiguous
+  auto tp = std::make_unique<TcPlan>();
+  while (pix.size() < 2) pix.insert(pix.begin(), PixDim());  // unit dims
+  const size_t nimg = pix.size() - 2;
+  for (size_t k = 0; k < nimg; ++k) {
+    if (pix[k].win >= 0) return nullptr;
+    if (k + 1 < nimg && (pix[k].xs != pix[k + 1].xs * pix[k + 1].E || pix[k].ys != pix[k + 1].ys * pix[k + 1].E))
+      return nullptr;
+  }
+  tp->n_img = 1;
+  for (size_t k = 0; k < nimg; ++k) tp->n_img *= (int)pix[k].E;
+  tp->x_img = nimg ? pix[nimg - 1].xs : 0;
+  tp->y_img = nimg ? pix[nimg - 1].ys : 0;
+  tp->dh = pix[nimg];
+  tp->dw = pix[nimg + 1];
+  tp->x_c = xs[chan_coord];
+  tp->y_n = ys[naxis];
+  tp->C = (int)S.ext(chan);
+  tp->N = (int)S.ext(naxis);
+  tp->Cp = (tp->C + 7) / 8 * 8;
+  tp->Np = (tp->N + 7) / 8 * 8;
+  tp->scale = S.scale;
+  for (PixDim* p : {&tp->dh, &tp->dw}) {
+    int dmin = 0, dmax = 0;
+    for (int r = 0; r < p->K; ++r) {
+      dmin = std::min(dmin, p->delta(r));
+      dmax = std::max(dmax, p->delta(r));
+    }
+    p->lo = -dmin;
+    p->hi = dmax;
+    // grad-input reads dy at u - delta(r)
+    p->dlo = dmax;
+    p->dhi = -dmin;
+    if (p->S > 2 || p->E * p->S < 1) return nullptr;
+  }
+  if (tp->nwin() > MAXWIN) return nullptr;
+  if (tp->dh.S * tp->dw.S > 8) return nullptr;
+  tp->dgrad_ok = tp->dh.Ein == (int64_t)tp->dh.S * tp->dh.E && tp->dw.Ein == (int64_t)tp->dw.S * tp->dw.E;
+  // loop ids of the fold stages: rh, rw, then two channel axes, then weight-only reduces
+  std::vector<int> wonly;
+  for (int l = A; l < L; ++l)
+    if (!used_red.count(l)) wonly.push_back(l);
+  (void)wonly;
+  return tp.release();
+}
+
+// Fold stage: Wf[rh][rw][a][b] = sum_{weight-only reduces} prod_j w_j, with (a, b) = (n, ci)
+// for the forward operand and (ci, n) for the grad-input operand.  Channel extents
+// are padded (the weight's own range check zero-fills the pad).
+static CStage fold_stage(const Plan& plan, const TcPlan& tp, bool dgrad, bool padded) {
+  const CStage& S = plan.unstaged;
+  const int A = (int)S.axis_ext.size();
+  int naxis = -1, chan = -1;
+  for (int a = 0; a < A; ++a) {
+    bool in_x = false;
+    for (auto& e : S.terms[0].coords) {
+      std::vector<int> ls;
+      c_loops(e, &ls);
+      in_x = in_x || std::count(ls.begin(), ls.end(), a);
+    }
+    if (!in_x) naxis = a;
+  }
+  for (auto& e : S.terms[0].coords)
+    if (e->op == COp::Loop && e->loop >= A) chan = e->loop;
+  std::map<int, int> m;
+  CStage f;
+  f.axis_ext = {tp.dh.K, tp.dw.K};
+  if (tp.dh.win >= 0) m[tp.dh.win] = 0;
+  if (tp.dw.win >= 0) m[tp.dw.win] = 1;
+  if (!dgrad) {
+    m[naxis] = 2;
+    m[chan] = 3;
+    f.axis_ext.push_back(tp.N);
+    f.axis_ext.push_back(padded ? tp.Cp : tp.C);
+  } else {
+    m[chan] = 2;
+    m[naxis] = 3;
+    f.axis_ext.push_back(tp.C);
+    f.axis_ext.push_back(padded ? tp.Np : tp.N);
+  }
+  for (int l = A; l < S.nloops(); ++l)
+    if (!m.count(l)) {
+      m[l] = 4 + (int)f.red_ext.size();
+      f.red_ext.push_back(S.ext(l));
+    }
+  std::function<CE(const CE&)> rn = [&](const CE& e) -> CE {
+    if (e->op == COp::Loop) return c_loop(m.at(e->loop));
+    if (e->op == COp::Const) return e;
+    return c_bin(e->op, rn(e->lhs), rn(e->rhs));
+  };
+  for (size_t t = 1; t < S.terms.size(); ++t) {
+    CTerm ct = S.terms[t];
+    for (auto& c : ct.coords) c = rn(c);
+    f.terms.push_back(ct);
+  }
+  f.out.kind = TK_STAGE;
+  f.out.index = 0;
+  f.out.extents = f.axis_ext;
+  return f;
+}
+
+bool tc_matches(const Plan& plan) {
+  TcPlan* raw = try_match(plan);
+  delete raw;
+  if (!raw) return false;
+  // the chain rule through the fold must invert (bare weight coordinates always do)
+  return true;
+}
+
+TcPlanPtr tc_build(const Plan& plan, cudaStream_t stream) {
+  TcPlan* raw = try_match(plan);
+  if (!raw) return TcPlanPtr();
+  TcPlanPtr tp(raw);
+  build_dev_stage(fold_stage(plan, *tp, false, true), &tp->fold_fwd, stream);
+  if (tp->dgrad_ok) build_dev_stage(fold_stage(plan, *tp, true, true), &tp->fold_dgrad, stream);
+  // chain rule through the fold: dW_j from dWf[rh][rw][n][ci] (fp32)
+  CStage ref = fold_stage(plan, *tp, false, false);
+  for (size_t j = 0; j < plan.w_ext.size(); ++j) {
+    CTensor gw;
+    gw.kind = TK_DW;
+    gw.index = (int)j;
+    gw.extents = plan.w_ext[j];
+    CStage g = derive_gradient(ref, (int)j, gw);
+    if (g.scatter) return TcPlanPtr();
+    for (auto& t : g.terms)
+      if (t.t.kind == TK_DY) {
+        t.t.kind = TK_STAGE;  // dWf is fp32: read in accumulator precision
+        t.t.index = 0;
+      }
+    tp->chain.emplace_back();
+    build_dev_stage(g, &tp->chain.back(), stream);
+    int64_t n = 1;
+    for (auto e : plan.w_ext[j]) n *= e;
+    tp->w_numel.push_back(n);
+  }
+  return tp;
+}
+
+std::string tc_describe(const TcPlan* tp) {
+  if (!tp) return "tc: none\n";
+  std::ostringstream o;
+  o << "tc: img=" << tp->n_img << " C=" << tp->C << " N=" << tp->N << " H=" << tp->dh.E << "(S" << tp->dh.S << ",K"
+    << tp->dh.K << ",lo" << tp->dh.lo << ",hi" << tp->dh.hi << ") W=" << tp->dw.E << "(S" << tp->dw.S << ",K"
+    << tp->dw.K << ",lo" << tp->dw.lo << ",hi" << tp->dw.hi << ") dgrad=" << tp->dgrad_ok << "\n";
+  return o.str();
+}
+
+// ---------------------------------------------------------------------------
+// Launch helpers
+// ---------------------------------------------------------------------------
+
+template <int BN>
+static void launch_gemm(const TcGemmParams& p, dim3 grid, cudaStream_t stream) {
+  static bool configured = false;
+  constexpr int smem = smem_bytes<BN>();
+  if (!configured) {
+    cuda_check(cudaFuncSetAttribute(tc_gemm_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
+               "cudaFuncSetAttribute(tc_gemm)");
+    configured = true;
+  }
+  note_launch();
+  tc_gemm_kernel<BN><<<grid, THREADS, smem, stream>>>(p);
+  cuda_check(cudaGetLastError(), "tc_gemm_kernel");
+}
+
+static void gemm(TcGemmParams& p, int bn, dim3 grid, cudaStream_t stream) {
+  if (bn == 64) launch_gemm<64>(p, grid, stream);
+  else if (bn == 128) launch_gemm<128>(p, grid, stream);
+  else launch_gemm<256>(p, grid, stream);
+}
+
+static int pick_bn(int n) { return n <= 64 ? 64 : n <= 128 ? 128 : 256; }
+
+template <typename T>
+static T* ws_alloc(size_t count, cudaStream_t stream, std::vector<void*>* owned) {
+  void* p = nullptr;
+  cuda_check(cudaMallocAsync(&p, std::max<size_t>(count, 1) * sizeof(T), stream), "cudaMallocAsync(tc workspace)");
+  owned->push_back(p);
+  return static_cast<T*>(p);
+}
+
+static void pack_cl(const void* src, DType dt, const PackGeom& g, __nv_bfloat16* dst, cudaStream_t stream) {
+  dim3 grid((unsigned)((g.Wp + 31) / 32), (unsigned)g.Hp, (unsigned)(((g.Cp + 63) / 64) * g.n_img * g.Sh * g.Sw));
+  note_launch();
+  if (dt == DT_BF16) pack_cl_kernel<__nv_bfloat16><<<grid, 256, 0, stream>>>((const __nv_bfloat16*)src, dst, g);
+  else pack_cl_kernel<float><<<grid, 256, 0, stream>>>((const float*)src, dst, g);
+  cuda_check(cudaGetLastError(), "pack_cl_kernel");
+}
+
+static void pack_cm(const void* src, DType dt, const PackGeom& g, __nv_bfloat16* dst, cudaStream_t stream) {
+  const int64_t total = (int64_t)g.Sh * g.Sw * g.C * g.Fpitch;
+  const int64_t threads = total / 8;
+  note_launch();
+  if (dt == DT_BF16)
+    pack_cm_kernel<__nv_bfloat16><<<(unsigned)((threads + 255) / 256), 256, 0, stream>>>(
+        (const __nv_bfloat16*)src, dst, g, total);
+  else
+    pack_cm_kernel<float><<<(unsigned)((threads + 255) / 256), 256, 0, stream>>>((const float*)src, dst, g, total);
+  cuda_check(cudaGetLastError(), "pack_cm_kernel");
+}
+
+static PackGeom geom(const TcPlan& tp, bool dy_side, bool grad_pad) {
+  PackGeom g{};
+  g.n_img = tp.n_img;
+  if (!dy_side) {
+    g.s_img = tp.x_img;
+    g.s_c = tp.x_c;
+    g.s_h = tp.dh.xs;
+    g.s_w = tp.dw.xs;
+    g.C = tp.C;
+    g.Hin = (int)tp.dh.Ein;
+    g.Win = (int)tp.dw.Ein;
+    g.Sh = tp.dh.S;
+    g.Sw = tp.dw.S;
+    g.Cp = tp.Cp;
+  } else {
+    g.s_img = tp.y_img;
+    g.s_c = tp.y_n;
+    g.s_h = tp.dh.ys;
+    g.s_w = tp.dw.ys;
+    g.C = tp.N;
+    g.Hin = (int)tp.dh.E;
+    g.Win = (int)tp.dw.E;
+    g.Sh = g.Sw = 1;
+    g.Cp = tp.Np;
+  }
+  g.lo_h = grad_pad ? tp.dh.dlo : tp.dh.lo;
+  g.lo_w = grad_pad ? tp.dw.dlo : tp.dw.lo;
+  g.Hp = (int)(grad_pad ? tp.dh.dEp() : tp.dh.Ep());
+  g.Wp = (int)(grad_pad ? tp.dw.dEp() : tp.dw.Ep());
+  const int64_t F = (int64_t)g.n_img * g.Hp * g.Wp;
+  g.Fpitch = (F + 7) / 8 * 8;
+  return g;
+}
+
+// ---------------------------------------------------------------------------
+// Forward: y[img, n, h, w] = scale * sum_win sum_ci Xcl[plane][flat + shift] Wf[win][n][ci]
+// ---------------------------------------------------------------------------
+
+bool tc_forward(TcPlan& tp, DType dt, const Bindings& b, cudaStream_t stream) {
+  if (dt != DT_BF16) return false;
+  std::vector<void*> owned;
+  const PackGeom g = geom(tp, false, false);
+  const int planes = g.Sh * g.Sw;
+  const int64_t F = (int64_t)g.n_img * g.Hp * g.Wp;
+  auto* xcl = ws_alloc<__nv_bfloat16>((size_t)planes * F * tp.Cp, stream, &owned);
+  pack_cl(b.x, dt, g, xcl, stream);
+  auto* wf = ws_alloc<__nv_bfloat16>((size_t)tp.nwin() * tp.N * tp.Cp, stream, &owned);
+  run_stage(dt, tp.fold_fwd, b, wf, false, stream);
+
+  const int bn = pick_bn(tp.N);
+  TcGemmParams p;
+  memset(&p, 0, sizeof(p));
+  p.tma_a = make_map(xcl, tp.Cp, F, planes, tp.Cp, F * tp.Cp, BM);
+  p.tma_b = make_map(wf, tp.Cp, tp.N, tp.nwin(), tp.Cp, (int64_t)tp.N * tp.Cp, bn);
+  p.mode = MODE_ROWS;
+  p.n_cblocks = (tp.Cp + BK - 1) / BK;
+  p.n_win = tp.nwin();
+  for (int rh = 0; rh < tp.dh.K; ++rh)
+    for (int rw = 0; rw < tp.dw.K; ++rw) {
+      const int w = rh * tp.dw.K + rw;
+      p.a_shift[w] = tp.dh.delta(rh) * g.Wp + tp.dw.delta(rw);
+      p.a_plane[w] = tp.dh.phi(rh) * g.Sw + tp.dw.phi(rw);
+      p.b_plane[w] = w;
+    }
+  p.win_base[0] = 0;
+  p.win_count[0] = tp.nwin();
+  p.g_out_off[0] = 0;
+  p.Hp = g.Hp;
+  p.Wp = g.Wp;
+  p.lo_h = g.lo_h;
+  p.lo_w = g.lo_w;
+  p.H = (int)tp.dh.E;
+  p.W = (int)tp.dw.E;
+  p.n_img = tp.n_img;
+  p.o_img = tp.y_img;
+  p.o_h = tp.dh.ys;
+  p.o_w = tp.dw.ys;
+  p.o_n = tp.y_n;
+  p.n_ext = tp.N;
+  p.out_kind = OUT_BF16;
+  p.scale = (float)tp.scale;
+  p.out = b.y;
+  p.tx_bytes = (uint32_t)((BM + bn) * BK * 2);
+  dim3 grid((unsigned)((F + BM - 1) / BM), (unsigned)((tp.N + bn - 1) / bn), 1);
+  gemm(p, bn, grid, stream);
+  for (void* q : owned) cuda_check(cudaFreeAsync(q, stream), "cudaFreeAsync(tc workspace)");
+  return true;
+}
+
+// ---------------------------------------------------------------------------
+// Backward
+// ---------------------------------------------------------------------------
+
+static void grad_input(TcPlan& tp, DType dt, const Bindings& b, cudaStream_t stream, std::vector<void*>* owned) {
+  const PackGeom g = geom(tp, true, true);
+  const int64_t F = (int64_t)g.n_img * g.Hp * g.Wp;
+  auto* dycl = ws_alloc<__nv_bfloat16>((size_t)F * tp.Np, stream, owned);
+  pack_cl(b.dy, dt, g, dycl, stream);
+  auto* wt = ws_alloc<__nv_bfloat16>((size_t)tp.nwin() * tp.C * tp.Np, stream, owned);
+  run_stage(dt, tp.fold_dgrad, b, wt, false, stream);
+
+  const int bn = pick_bn(tp.C);
+  TcGemmParams p;
+  memset(&p, 0, sizeof(p));
+  p.tma_a = make_map(dycl, tp.Np, F, 1, tp.Np, F * tp.Np, BM);
+  p.tma_b = make_map(wt, tp.Np, tp.C, tp.nwin(), tp.Np, (int64_t)tp.C * tp.Np, bn);
+  p.mode = MODE_ROWS;
+  p.n_cblocks = (tp.Np + BK - 1) / BK;
+  // group = output phase (psi_h, psi_w); its windows have phi(r) == psi
+  const int Sh = tp.dh.S, Sw = tp.dw.S;
+  int n = 0;
+  for (int ph = 0; ph < Sh; ++ph)
+    for (int pw = 0; pw < Sw; ++pw) {
+      const int grp = ph * Sw + pw;
+      p.win_base[grp] = n;
+      for (int rh = 0; rh < tp.dh.K; ++rh)
+        for (int rw = 0; rw < tp.dw.K; ++rw) {
+          if (tp.dh.phi(rh) != ph || tp.dw.phi(rw) != pw) continue;
+          p.a_shift[n] = -tp.dh.delta(rh) * g.Wp - tp.dw.delta(rw);
+          p.a_plane[n] = 0;
+          p.b_plane[n] = rh * tp.dw.K + rw;
+          ++n;
+        }
+      p.win_count[grp] = n - p.win_base[grp];
+      p.g_out_off[grp] = ph * tp.dh.xs + pw * tp.dw.xs;
+    }
+  p.n_win = n;
+  p.Hp = g.Hp;
+  p.Wp = g.Wp;
+  p.lo_h = g.lo_h;
+  p.lo_w = g.lo_w;
+  p.H = (int)tp.dh.E;
+  p.W = (int)tp.dw.E;
+  p.n_img = tp.n_img;
+  p.o_img = tp.x_img;
+  p.o_h = tp.dh.xs * Sh;
+  p.o_w = tp.dw.xs * Sw;
+  p.o_n = tp.x_c;
+  p.n_ext = tp.C;
+  p.out_kind = OUT_BF16;
+  p.scale = (float)tp.scale;
+  p.out = b.dx;
+  p.tx_bytes = (uint32_t)((BM + bn) * BK * 2);
+  dim3 grid((unsigned)((F + BM - 1) / BM), (unsigned)((tp.C + bn - 1) / bn), (unsigned)(Sh * Sw));
+  gemm(p, bn, grid, stream);
+}
+
+static void grad_weight(TcPlan& tp, DType dt, const Bindings& b, cudaStream_t stream, std::vector<void*>* owned) {
+  // both operands channel-major over the forward's flat padded grid
+  const PackGeom gx = geom(tp, false, false);
+  PackGeom gy = geom(tp, true, false);
+  gy.Fpitch = gx.Fpitch;
+  const int planes = gx.Sh * gx.Sw;
+  const int64_t F = (int64_t)gx.n_img * gx.Hp * gx.Wp;
+  auto* xcm = ws_alloc<__nv_bfloat16>((size_t)planes * tp.C * gx.Fpitch, stream, owned);
+  auto* dycm = ws_alloc<__nv_bfloat16>((size_t)tp.N * gx.Fpitch, stream, owned);
+  pack_cm(b.x, dt, gx, xcm, stream);
+  pack_cm(b.dy, dt, gy, dycm, stream);
+  const size_t nwf = (size_t)tp.nwin() * tp.N * tp.C;
+  float* dwf = ws_alloc<float>(nwf, stream, owned);
+  cuda_check(cudaMemsetAsync(dwf, 0, nwf * sizeof(float), stream), "memset(dWf)");
+
+  const int bn = pick_bn(tp.C);
+  TcGemmParams p;
+  memset(&p, 0, sizeof(p));
+  p.tma_a = make_map(dycm, F, tp.N, 1, gx.Fpitch, (int64_t)tp.N * gx.Fpitch, BM);
+  p.tma_b = make_map(xcm, F, tp.C, planes, gx.Fpitch, (int64_t)tp.C * gx.Fpitch, bn);
+  p.mode = MODE_WGRAD;
+  p.n_cblocks = (int)((F + BK - 1) / BK);
+  p.n_win = tp.nwin();
+  for (int rh = 0; rh < tp.dh.K; ++rh)
+    for (int rw = 0; rw < tp.dw.K; ++rw) {
+      const int w = rh * tp.dw.K + rw;
+      p.a_shift[w] = tp.dh.delta(rh) * gx.Wp + tp.dw.delta(rw);
+      p.a_plane[w] = tp.dh.phi(rh) * gx.Sw + tp.dw.phi(rw);
+    }
+  const int gx_tiles = (tp.N + BM - 1) / BM, gy_tiles = (tp.C + bn - 1) / bn;
+  int ksplit = std::max(1, (2 * 148) / std::max(1, gx_tiles * gy_tiles * tp.nwin()));
+  ksplit = std::min(ksplit, std::max(1, p.n_cblocks / 4));
+  p.ksplit = ksplit;
+  p.m_ext = tp.N;
+  p.n_ext = tp.C;
+  p.o_m = tp.C;
+  p.o_n = 1;
+  for (int w = 0; w < 8; ++w) p.g_out_off[w] = 0;
+  p.out_kind = OUT_F32_ATOMIC;
+  p.scale = (float)tp.scale;
+  p.out = dwf;
+  p.tx_bytes = (uint32_t)((BM + bn) * BK * 2);
+  // per-window output offset: the kernel adds g_out_off[g] only for g < 8, so
+  // wgrad launches one grid per block of 8 windows
+  for (int w0 = 0; w0 < tp.nwin(); w0 += 8) {
+    TcGemmParams q = p;
+    const int nw = std::min(8, tp.nwin() - w0);
+    for (int k = 0; k < nw; ++k) {
+      q.a_shift[k] = p.a_shift[w0 + k];
+      q.a_plane[k] = p.a_plane[w0 + k];
+      q.g_out_off[k] = (int64_t)(w0 + k) * tp.N * tp.C;
+    }
+    dim3 grid((unsigned)gx_tiles, (unsigned)gy_tiles, (unsigned)(nw * ksplit));
+    gemm(q, bn, grid, stream);
+  }
+  // chain rule through the fold, into each requested weight gradient
+  Bindings cb = b;
+  cb.stages = {dwf};
+  for (size_t j = 0; j < tp.chain.size(); ++j) {
+    if (j >= b.dw.size() || !b.dw[j]) continue;
+    run_stage(dt, tp.chain[j], cb, b.dw[j], false, stream);
+  }
+}
+
+bool tc_backward(TcPlan& tp, DType dt, const Bindings& b, cudaStream_t stream) {
+  if (dt != DT_BF16) return false;
+  if (b.dx && !tp.dgrad_ok) return false;
+  std::vector<void*> owned;
+  if (b.dx) grad_input(tp, dt, b, stream, &owned);
+  bool any_w = false;
+  for (auto* p : b.dw) any_w = any_w || p;
+  if (any_w) grad_weight(tp, dt, b, stream, &owned);
+  for (void* q : owned) cuda_check(cudaFreeAsync(q, stream), "cudaFreeAsync(tc workspace)");
+  return true;
+}
 
 }  // namespace syno

@@ -77,3 +77,15 @@ def test_bad_arguments_report_status_and_message():
     assert "output and input" in _lib.last_error()
     rc = _lib.lib.syno_compile(None, None, 0, ctypes.byref(ptr))
     assert rc == _lib.SYNO_E_INVALID
+
+
+def test_config_operators_take_the_tensor_core_path():
+    """Host-side matcher: every Appendix-A contraction operator qualifies
+    for the tcgen05 path; pooling (no weights) stays on the universal engine."""
+    from paper_2410_23745_b200 import workloads as WL
+    for L in WL.resnet18_cifar(8) + [WL.qkv(2, 64), WL.cfg1_conv(2)]:
+        assert P.handle_for(L.graph).info.tc_path == 1, L.name
+    pool = P.parse_steps(WL.SUMPOOL3X3, P.build_spec("pool", ("C", "H", "W", "N"), ("K",),
+                                                     {"C": 8, "H": 8, "W": 8, "N": 2, "K": 3},
+                                                     ("C", "H", "W"), ("C", "H", "W"), ("N",)))
+    assert P.handle_for(pool).info.tc_path == 0
