@@ -19,6 +19,17 @@ CE c_const(int64_t v) {
   return n;
 }
 CE c_bin(COp op, CE a, CE b) {
+  if (a->op == COp::Const && b->op == COp::Const) {  // constant folding (Python semantics)
+    int64_t x = a->value, y = b->value;
+    switch (op) {
+      case COp::Add: return c_const(x + y);
+      case COp::Sub: return c_const(x - y);
+      case COp::Mul: return c_const(x * y);
+      case COp::FloorDiv: return c_const(py_floordiv(x, y));
+      case COp::Mod: return c_const(py_mod(x, y));
+      default: break;
+    }
+  }
   auto n = std::make_shared<CNode>();
   n->op = op; n->lhs = std::move(a); n->rhs = std::move(b);
   return n;

@@ -636,16 +636,16 @@ static void grad_input(TcPlan& tp, DType dt, const Bindings& b, cudaStream_t str
 }
 
 static void grad_weight(TcPlan& tp, DType dt, const Bindings& b, cudaStream_t stream, std::vector<void*>* owned) {
-  // both operands channel-major over the forward's flat padded grid
+  // both operands channels-last over the forward's flat padded grid; the
+  // GEMM reads them MN-major (K = pixel rows), so a window is a row shift
   const PackGeom gx = geom(tp, false, false);
-  PackGeom gy = geom(tp, true, false);
-  gy.Fpitch = gx.Fpitch;
+  const PackGeom gy = geom(tp, true, false);
   const int planes = gx.Sh * gx.Sw;
   const int64_t F = (int64_t)gx.n_img * gx.Hp * gx.Wp;
-  auto* xcm = ws_alloc<__nv_bfloat16>((size_t)planes * tp.C * gx.Fpitch, stream, owned);
-  auto* dycm = ws_alloc<__nv_bfloat16>((size_t)tp.N * gx.Fpitch, stream, owned);
-  pack_cm(b.x, dt, gx, xcm, stream);
-  pack_cm(b.dy, dt, gy, dycm, stream);
+  auto* xcl = ws_alloc<__nv_bfloat16>((size_t)planes * F * tp.Cp, stream, owned);
+  auto* dycl = ws_alloc<__nv_bfloat16>((size_t)F * tp.Np, stream, owned);
+  pack_cl(b.x, dt, gx, xcl, stream);
+  pack_cl(b.dy, dt, gy, dycl, stream);
   const size_t nwf = (size_t)tp.nwin() * tp.N * tp.C;
   float* dwf = ws_alloc<float>(nwf, stream, owned);
   cuda_check(cudaMemsetAsync(dwf, 0, nwf * sizeof(float), stream), "memset(dWf)");
@@ -653,8 +653,8 @@ static void grad_weight(TcPlan& tp, DType dt, const Bindings& b, cudaStream_t st
   const int bn = pick_bn(tp.C);
   TcGemmParams p;
   memset(&p, 0, sizeof(p));
-  p.tma_a = make_map(dycm, F, tp.N, 1, gx.Fpitch, (int64_t)tp.N * gx.Fpitch, BM);
-  p.tma_b = make_map(xcm, F, tp.C, planes, gx.Fpitch, (int64_t)tp.C * gx.Fpitch, bn);
+  p.tma_a = make_map(dycl, tp.Np, F, 1, tp.Np, F * tp.Np, 64);
+  p.tma_b = make_map(xcl, tp.Cp, F, planes, tp.Cp, F * tp.Cp, 64);
   p.mode = MODE_WGRAD;
   p.n_cblocks = (int)((F + BK - 1) / BK);
   p.n_win = tp.nwin();

@@ -26,7 +26,7 @@ constexpr int THREADS = 192;
 
 enum Mode : int32_t {
   MODE_ROWS = 0,   // A rows = flat padded pixels (+ window shift); k = (cblock, window)
-  MODE_WGRAD = 1,  // A rows = C_out, B rows = C_in, k = pixel blocks; window = group
+  MODE_WGRAD = 1,  // M = C_out, N = C_in, k = pixel rows (MN-major channels-last tiles); window = group
 };
 
 enum OutKind : int32_t { OUT_BF16 = 0, OUT_F32 = 1, OUT_F32_ATOMIC = 2 };
@@ -105,11 +105,26 @@ __device__ __forceinline__ uint64_t sw128_desc(const void* smem) {
   return d;
 }
 
-// kind::f16 instruction descriptor: bf16 x bf16 -> f32, both K-major.
-__host__ __device__ constexpr uint32_t idesc_bf16(int m, int n) {
+// MN-major, 128-byte swizzle descriptor (canonical ((8,n),(8,k)) : ((1,LBO),(8,SBO)) in
+// 16-byte units): 64 MN elements per 128 B row, one row per k; MN atoms of
+// 64 elements are `lbo` bytes apart, 8-row k groups 1024 B apart.
+__device__ __forceinline__ uint64_t sw128_mn_desc(const void* smem, uint32_t lbo) {
+  uint64_t addr = smem_u32(smem);
+  uint64_t d = 0;
+  d |= (addr >> 4) & 0x3FFF;
+  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)(1024 >> 4) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)2 << 61;
+  return d;
+}
+
+// kind::f16 instruction descriptor: bf16 x bf16 -> f32; majors 0 = K, 1 = MN.
+__host__ __device__ constexpr uint32_t idesc_bf16(int m, int n, int a_mn = 0, int b_mn = 0) {
   return (1u << 4)            // D format f32
          | (1u << 7)          // A bf16
          | (1u << 10)         // B bf16
+         | ((uint32_t)a_mn << 15) | ((uint32_t)b_mn << 16)
          | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(m >> 4) << 24);
 }
 
@@ -205,42 +220,44 @@ __global__ void __launch_bounds__(THREADS, 1) tc_gemm_kernel(const __grid_consta
         const uint32_t ph = (uint32_t)(i / STAGES) & 1u;
         mbar_wait(&empty[s], ph ^ 1u);
         const int kb = kb0 + i;
-        int a0, a1, a2, b0, b1, b2;
+        mbar_expect_tx(&full[s], p.tx_bytes);
         if (p.mode == MODE_ROWS) {
+          // K-major tiles: A = 128 pixel rows x 64 channels, B = BN rows x 64 channels
           const int cb = kb % p.n_cblocks;
           const int w = win0 + kb / p.n_cblocks;
-          a0 = cb * BK;
-          a1 = p.a_row_base + mt * BM + p.a_shift[w];
-          a2 = p.a_plane[w];
-          b0 = cb * BK;
-          b1 = nt * BN;
-          b2 = p.b_plane[w];
+          tma_load_3d(sa + s * A_BYTES, &p.tma_a, &full[s], cb * BK, p.a_row_base + mt * BM + p.a_shift[w],
+                      p.a_plane[w]);
+          tma_load_3d(sb + s * B_BYTES, &p.tma_b, &full[s], cb * BK, nt * BN, p.b_plane[w]);
         } else {
-          a0 = kb * BK;  // pixel block (dy, no shift)
-          a1 = mt * BM;
-          a2 = 0;
-          b0 = kb * BK + p.a_shift[g];
-          b1 = nt * BN;
-          b2 = p.a_plane[g];
+          // MN-major tiles from channels-last operands: 64 pixel rows (k) x 64 channels per box;
+          // the window is a pixel-row shift of the x operand.
+#pragma unroll
+          for (int h = 0; h < BM / 64; ++h)
+            tma_load_3d(sa + s * A_BYTES + h * 8192, &p.tma_a, &full[s], mt * BM + h * 64, kb * BK, 0);
+#pragma unroll
+          for (int h = 0; h < BN / 64; ++h)
+            tma_load_3d(sb + s * B_BYTES + h * 8192, &p.tma_b, &full[s], nt * BN + h * 64, kb * BK + p.a_shift[g],
+                        p.a_plane[g]);
         }
-        mbar_expect_tx(&full[s], p.tx_bytes);
-        tma_load_3d(sa + s * A_BYTES, &p.tma_a, &full[s], a0, a1, a2);
-        tma_load_3d(sb + s * B_BYTES, &p.tma_b, &full[s], b0, b1, b2);
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {
-      const uint32_t idesc = idesc_bf16(BM, BN);
+      const bool mn = p.mode == MODE_WGRAD;
+      const uint32_t idesc = mn ? idesc_bf16(BM, BN, 1, 1) : idesc_bf16(BM, BN);
+      // per UMMA_K = 16 step: K-major advances 32 B inside the swizzled row,
+      // MN-major advances two 8-row k groups (2 x 1024 B)
+      const uint64_t kstep = mn ? (2048 >> 4) : (32 >> 4);
       for (int i = 0; i < nkb; ++i) {
         const int s = i % STAGES;
         const uint32_t ph = (uint32_t)(i / STAGES) & 1u;
         mbar_wait(&full[s], ph);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const uint64_t da = sw128_desc(sa + s * A_BYTES);
-        const uint64_t db = sw128_desc(sb + s * B_BYTES);
+        const uint64_t da = mn ? sw128_mn_desc(sa + s * A_BYTES, 8192) : sw128_desc(sa + s * A_BYTES);
+        const uint64_t db = mn ? sw128_mn_desc(sb + s * B_BYTES, 8192) : sw128_desc(sb + s * B_BYTES);
 #pragma unroll
         for (int k = 0; k < BK / 16; ++k)
-          mma_bf16(tmem, da + (uint64_t)(k * 2), db + (uint64_t)(k * 2), idesc, (i > 0 || k > 0) ? 1u : 0u);
+          mma_bf16(tmem, da + (uint64_t)k * kstep, db + (uint64_t)k * kstep, idesc, (i > 0 || k > 0) ? 1u : 0u);
         mma_commit(&empty[s]);
       }
       if (nkb > 0) mma_commit(tfull);
