@@ -158,7 +158,9 @@ def run_layers(args, rank, world, device, peaks):
         state.append(dict(L=L, h=h, x=x, ws=ws, dy=dy, y=y, dx=dx, dws=dws,
                           work=layer_work(h, len(ws), esize)))
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=device)  # > 126 MB L2
-    stream = torch.cuda.current_stream(device)
+    # a dedicated stream: CUDA-graph capture needs a non-default stream, and the
+    # library keeps one workspace per (device, stream)
+    stream = torch.cuda.Stream(device)
     import ctypes
     sp = ctypes.c_void_p(stream.cuda_stream)
     code = ops._DT[dtype]
@@ -194,10 +196,25 @@ def run_layers(args, rank, world, device, peaks):
                 k += 1
         return evs
 
-    for _ in range(args.warmup):
-        flush.zero_()
-        one_step(False)
+    with torch.cuda.stream(stream):
+        for _ in range(args.warmup):
+            flush.zero_()
+            one_step(False)
     torch.cuda.synchronize(device)
+
+    # The step is captured once as a CUDA graph (kernel launches only: the
+    # library allocates nothing and never synchronises in steady state).
+    graph = None
+    launches_per_step = None
+    if args.graph:
+        c0 = _lib.lib.syno_launch_count()
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=stream):
+            one_step(False)
+        launches_per_step = _lib.lib.syno_launch_count() - c0
+        with torch.cuda.stream(stream):
+            graph.replay()
+        torch.cuda.synchronize(device)
 
     sampler = ClockSampler(torch.cuda.current_device() if device.index is None else device.index)
     if rank == 0:
@@ -206,21 +223,39 @@ def run_layers(args, rank, world, device, peaks):
     torch.cuda.synchronize(device)
     launches0 = _lib.lib.syno_launch_count()
     step_ms = []
-    all_evs = []
+    evs = []
     for _ in range(args.steps):
-        flush.zero_()  # L2 flush between timed steps, outside the step's events
-        all_evs.append(one_step(True))
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(stream):
+            flush.zero_()  # L2 flush between timed steps, outside the step's events
+        with torch.cuda.stream(stream):
+            e0.record(stream)
+            if graph is not None:
+                graph.replay()
+            else:
+                one_step(False)
+            e1.record(stream)
+        evs.append((e0, e1))
     torch.cuda.synchronize(device)
     barrier(world)
     launches = _lib.lib.syno_launch_count() - launches0
+    if graph is not None:
+        launches = launches_per_step * args.steps
     if rank == 0:
         sampler.stop()
-    for evs in all_evs:
-        step_ms.append(evs[0].elapsed_time(evs[-1]))
+    step_ms = [a.elapsed_time(b) for a, b in evs]
+
+    # per-(layer, phase) breakdown: a separate eager pass with events between calls
+    for _ in range(2):
+        with torch.cuda.stream(stream):
+            flush.zero_()
+            all_evs = one_step(True)
+        torch.cuda.synchronize(device)
         k = 0
         for i in range(len(state)):
             for p, _ in phases:
-                times[(i, p)].append(evs[k].elapsed_time(evs[k + 1]))
+                times[(i, p)].append(all_evs[k].elapsed_time(all_evs[k + 1]))
                 k += 1
     ms = statistics.mean(step_ms)
     ms_max = allreduce_max(ms, world, device)
@@ -244,7 +279,8 @@ def run_layers(args, rank, world, device, peaks):
         achieved = B / (dms / 1e3) / 1e9
         roof = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                 "frac": achieved / peaks["hbm_gbs"]}
-    roof.update({"traffic": load_traffic(state[di]["L"].name, dp), "kernel": f"{state[di]['L'].name}:{dp}",
+    roof.update({"traffic": load_traffic(state[di]["L"].name, dp),
+                 "kernel": f"{state[di]['L'].name}:{dp} (one library call: pack + fold + tcgen05 GEMMs)",
                  "kernel_ms": dms, "share_of_step": dms / ms, "peak_source": peaks["source"]})
     # whole-step roofline: sum of per-call roofline times over the measured step time
     t_roof = 0.0
@@ -253,7 +289,8 @@ def run_layers(args, rank, world, device, peaks):
             t_roof += max(s["work"][f"{p}_flops"] / (tflops_peak * 1e12), s["work"][f"{p}_bytes"] / (peaks["hbm_gbs"] * 1e9))
     step_flops = sum(s["work"]["fwd_flops"] + (0 if fwd_only else s["work"]["bwd_flops"]) for s in state)
 
-    e2e = measure_e2e(state, phases, args, device, dtype, world)
+    with torch.cuda.stream(stream):
+        e2e = measure_e2e(state, phases, args, device, dtype, world)
     breakdown = {f"{state[i]['L'].name}:{p}": round(avg[(i, p)], 4) for (i, p) in avg}
     return {
         "value": value, "ms_per_step": ms_max, "roofline": roof,
@@ -464,6 +501,7 @@ def main():
     ap.add_argument("--batch", type=int, default=0)
     ap.add_argument("--impl", default="syno", choices=["syno", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-graph", dest="graph", action="store_false", help="eager launches instead of a CUDA graph")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
 

@@ -304,6 +304,11 @@ void build_dev_stage(const CStage& cs, DevStage* ds, cudaStream_t stream) {
   memset(&k, 0, sizeof(KStage));
   if ((int)cs.axis_ext.size() > MAXA) fail(SYNO_E_UNSUPPORTED, "stage has too many axes");
   if ((int)cs.terms.size() > MAXT) fail(SYNO_E_UNSUPPORTED, "stage has too many terms");
+  {
+    double n = 1;
+    for (auto e : cs.axis_ext) n *= (double)e;
+    if (n >= 2147483647.0) fail(SYNO_E_UNSUPPORTED, "stage has 2^31 or more outputs");
+  }
   k.n_axes = (int)cs.axis_ext.size();
   k.n_terms = (int)cs.terms.size();
   k.out_count = 1;
@@ -342,24 +347,36 @@ DevPlan::~DevPlan() {
   for (auto& g : grad_w) rel(g);
 }
 
+static void ensure_forward(const Plan& plan, DevPlan& dp, cudaStream_t stream) {
+  std::lock_guard<std::mutex> lock(dp.mu);
+  if (dp.have_forward) return;
+  for (auto& s : plan.forward) {
+    dp.forward.emplace_back();
+    build_dev_stage(s, &dp.forward.back(), stream);
+  }
+  dp.have_forward = true;
+}
+
+static void ensure_backward(const Plan& plan, DevPlan& dp, cudaStream_t stream) {
+  std::lock_guard<std::mutex> lock(dp.mu);
+  if (dp.have_backward) return;
+  for (auto& s : plan.grad_x) {
+    dp.grad_x.emplace_back();
+    build_dev_stage(s, &dp.grad_x.back(), stream);
+  }
+  for (auto& gw : plan.grad_w) {
+    dp.grad_w.emplace_back();
+    for (auto& s : gw) {
+      dp.grad_w.back().emplace_back();
+      build_dev_stage(s, &dp.grad_w.back().back(), stream);
+    }
+  }
+  dp.have_backward = true;
+}
+
 DevPlan* build_dev_plan(const Plan& plan, cudaStream_t stream) {
   auto dp = std::make_unique<DevPlan>();
   cuda_check(cudaGetDevice(&dp->device), "cudaGetDevice");
-  for (auto& s : plan.forward) {
-    dp->forward.emplace_back();
-    build_dev_stage(s, &dp->forward.back(), stream);
-  }
-  for (auto& s : plan.grad_x) {
-    dp->grad_x.emplace_back();
-    build_dev_stage(s, &dp->grad_x.back(), stream);
-  }
-  for (auto& gw : plan.grad_w) {
-    dp->grad_w.emplace_back();
-    for (auto& s : gw) {
-      dp->grad_w.back().emplace_back();
-      build_dev_stage(s, &dp->grad_w.back().back(), stream);
-    }
-  }
   dp->tc = tc_build(plan, stream);
   cuda_check(cudaStreamSynchronize(stream), "build_dev_plan");
   return dp.release();
@@ -443,10 +460,104 @@ __device__ __forceinline__ bool term_offset(const KTerm& T, int64_t base, bool o
 
 template <typename T> __device__ __forceinline__ void atomic_add(T* p, T v) { atomicAdd(p, v); }
 
-template <typename TI, typename TA, bool SCATTER>
-__global__ void __launch_bounds__(256) stage_kernel(const __grid_constant__ KStage S) {
+// NT = compile-time bound on the number of terms: fewer live registers and
+// higher occupancy for the common 1-3 term stages.
+template <typename TI, typename TA, bool SCATTER, int NT>
+__global__ void __launch_bounds__(256, NT <= 2 ? 4 : 2) stage_kernel(const __grid_constant__ KStage S) {
   const int64_t o = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (o >= S.out_count) return;
+  const int64_t r0 = (int64_t)blockIdx.y * S.r_chunk;
+  const int64_t r1 = min(S.R, r0 + S.r_chunk);
+  int32_t av[MAXA];
+  {
+    uint32_t rem = (uint32_t)o;  // out_count < 2^31 (checked on the host)
+#pragma unroll
+    for (int k = MAXA - 1; k >= 0; --k) {
+      if (k < S.n_axes) {
+        const uint32_t e = (uint32_t)S.axis_ext[k];
+        av[k] = (int32_t)(rem % e);
+        rem /= e;
+      } else {
+        av[k] = 0;
+      }
+    }
+  }
+  int64_t base[NT];
+  bool aok[NT];
+  int32_t ia[NT][MAXMIX];
+#pragma unroll
+  for (int t = 0; t < NT; ++t) {
+    base[t] = 0;
+    aok[t] = false;
+    if (t < S.n_terms) term_prep(S.terms[t], S.n_axes, av, &base[t], &aok[t], ia[t]);
+  }
+  int64_t tbase = 0;
+  bool tok = false;
+  int32_t tia[MAXMIX];
+  if (SCATTER) term_prep(S.target, S.n_axes, av, &tbase, &tok, tia);
+  const TA scale = (TA)S.scale;
+  TA acc = 0;
+  for (int64_t r = r0; r < r1; ++r) {
+    TA prod = 1;
+    bool ok = true;
+#pragma unroll
+    for (int t = 0; t < NT; ++t) {
+      if (t < S.n_terms && ok) {
+        const KTerm& T = S.terms[t];
+        int64_t off;
+        if (!term_offset(T, base[t], aok[t], ia[t], r, &off)) ok = false;
+        else if (T.kind != 2) prod *= load_term<TI, TA>(T, off);
+      }
+    }
+    if (SCATTER) {
+      int64_t off;
+      if (ok && term_offset(S.target, tbase, tok, tia, r, &off)) atomic_add((TA*)S.out + off, prod * scale);
+    } else if (ok) {
+      acc += prod;
+    }
+  }
+  if (!SCATTER) {
+    if (S.out_acc) ((TA*)S.out)[(int64_t)blockIdx.y * S.out_count * (gridDim.y > 1) + o] = acc * scale;
+    else ((TI*)S.out)[o] = from_acc<TI, TA>(acc * scale);
+  }
+}
+
+// Affine form: no reduction and every coordinate a bare iterator (weight
+// folds and re-layouts, identity-like gathers): offsets are linear in the
+// output digits, so the kernel is a plain strided gather-product.
+template <typename TI, typename TA, int NT>
+__global__ void __launch_bounds__(256) affine_kernel(const __grid_constant__ KStage S) {
+  const int64_t o = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (o >= S.out_count) return;
+  int64_t off[NT];
+#pragma unroll
+  for (int t = 0; t < NT; ++t) off[t] = t < S.n_terms ? S.terms[t].base : 0;
+  uint32_t rem = (uint32_t)o;
+#pragma unroll
+  for (int k = MAXA - 1; k >= 0; --k) {
+    if (k < S.n_axes) {
+      const uint32_t e = (uint32_t)S.axis_ext[k];
+      const uint32_t d = rem % e;
+      rem /= e;
+#pragma unroll
+      for (int t = 0; t < NT; ++t)
+        if (t < S.n_terms) off[t] += S.terms[t].lin[k] * (int64_t)d;
+    }
+  }
+  TA prod = (TA)S.scale;
+#pragma unroll
+  for (int t = 0; t < NT; ++t)
+    if (t < S.n_terms) prod *= load_term<TI, TA>(S.terms[t], off[t]);
+  if (S.out_acc) ((TA*)S.out)[o] = prod;
+  else ((TI*)S.out)[o] = from_acc<TI, TA>(prod);
+}
+
+// K3: block-cooperative form for stages with few outputs and long reductions
+// (weight gradients of small weights, pooling to a point): one block per
+// output, threads stride the reduce range, warp-shuffle + smem tree reduce.
+template <typename TI, typename TA>
+__global__ void __launch_bounds__(256) stage_block_kernel(const __grid_constant__ KStage S) {
+  const int64_t o = blockIdx.x;
   const int64_t r0 = (int64_t)blockIdx.y * S.r_chunk;
   const int64_t r1 = min(S.R, r0 + S.r_chunk);
   int32_t av[MAXA];
@@ -472,13 +583,8 @@ __global__ void __launch_bounds__(256) stage_kernel(const __grid_constant__ KSta
     aok[t] = false;
     if (t < S.n_terms) term_prep(S.terms[t], S.n_axes, av, &base[t], &aok[t], ia[t]);
   }
-  int64_t tbase = 0;
-  bool tok = false;
-  int32_t tia[MAXMIX];
-  if (SCATTER) term_prep(S.target, S.n_axes, av, &tbase, &tok, tia);
-  const TA scale = (TA)S.scale;
   TA acc = 0;
-  for (int64_t r = r0; r < r1; ++r) {
+  for (int64_t r = r0 + threadIdx.x; r < r1; r += blockDim.x) {
     TA prod = 1;
     bool ok = true;
 #pragma unroll
@@ -490,16 +596,23 @@ __global__ void __launch_bounds__(256) stage_kernel(const __grid_constant__ KSta
         else if (T.kind != 2) prod *= load_term<TI, TA>(T, off);
       }
     }
-    if (SCATTER) {
-      int64_t off;
-      if (ok && term_offset(S.target, tbase, tok, tia, r, &off)) atomic_add((TA*)S.out + off, prod * scale);
-    } else if (ok) {
-      acc += prod;
-    }
+    if (ok) acc += prod;
   }
-  if (!SCATTER) {
-    if (S.out_acc) ((TA*)S.out)[(int64_t)blockIdx.y * S.out_count * (gridDim.y > 1) + o] = acc * scale;
-    else ((TI*)S.out)[o] = from_acc<TI, TA>(acc * scale);
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, d);
+  __shared__ TA part[32];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) part[warp] = acc;
+  __syncthreads();
+  if (warp == 0) {
+    acc = lane < (int)(blockDim.x >> 5) ? part[lane] : (TA)0;
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, d);
+    if (lane == 0) {
+      const TA v = acc * (TA)S.scale;
+      if (S.out_acc) ((TA*)S.out)[(int64_t)blockIdx.y * S.out_count * (gridDim.y > 1) + o] = v;
+      else ((TI*)S.out)[o] = from_acc<TI, TA>(v);
+    }
   }
 }
 
@@ -538,6 +651,13 @@ static const void* bind_ptr(const CTensor& t, const Bindings& b) {
   }
 }
 
+template <typename TI, typename TA, bool SCATTER>
+static void launch_nt(const KStage& k, dim3 grid, cudaStream_t stream) {
+  if (k.n_terms <= 2) stage_kernel<TI, TA, SCATTER, 2><<<grid, 256, 0, stream>>>(k);
+  else if (k.n_terms <= 4) stage_kernel<TI, TA, SCATTER, 4><<<grid, 256, 0, stream>>>(k);
+  else stage_kernel<TI, TA, SCATTER, MAXT><<<grid, 256, 0, stream>>>(k);
+}
+
 template <typename TI>
 static void launch_stage_t(const DevStage& ds, const Bindings& b, void* out, bool out_acc, cudaStream_t stream) {
   using TA = typename Acc<TI>::type;
@@ -551,10 +671,26 @@ static void launch_stage_t(const DevStage& ds, const Bindings& b, void* out, boo
     if (!ds.cs.scatter && out_bytes) cuda_check(cudaMemsetAsync(out, 0, out_bytes, stream), "memset(dead)");
     return;
   }
+  bool affine = !ds.cs.scatter && k.R == 1;
+  for (int t = 0; t < k.n_terms && affine; ++t)
+    affine = k.terms[t].kind != 2 && k.terms[t].n_atab == 0 && k.terms[t].n_mix == 0 && k.terms[t].rtab == nullptr;
+  if (affine) {
+    k.out = out;
+    k.out_acc = out_acc;
+    const unsigned blocks = (unsigned)((k.out_count + 255) / 256);
+    note_launch();
+    if (k.n_terms <= 2) affine_kernel<TI, TA, 2><<<blocks, 256, 0, stream>>>(k);
+    else affine_kernel<TI, TA, MAXT><<<blocks, 256, 0, stream>>>(k);
+    cuda_check(cudaGetLastError(), "affine_kernel");
+    return;
+  }
+  const bool block_mode = !ds.cs.scatter && k.out_count <= 16384 && k.R >= 2048;
   // Reduce split: enough threads to fill the chip about twice.
   const int64_t want = 148LL * 2048;
   int64_t nsplit = 1;
-  if (k.out_count < want && k.R >= 64) {
+  if (block_mode) {
+    nsplit = std::max<int64_t>(1, std::min<int64_t>({(4 * 148 + k.out_count - 1) / k.out_count, k.R / 2048, 1024}));
+  } else if (k.out_count < want && k.R >= 64) {
     nsplit = std::min<int64_t>((want + k.out_count - 1) / k.out_count, k.R / 32);
     nsplit = std::max<int64_t>(1, std::min<int64_t>(nsplit, 4096));
   }
@@ -562,11 +698,31 @@ static void launch_stage_t(const DevStage& ds, const Bindings& b, void* out, boo
   nsplit = (k.R + k.r_chunk - 1) / k.r_chunk;
   if (k.R == 0) { nsplit = 1; k.r_chunk = 0; }
   dim3 grid((unsigned)((k.out_count + 255) / 256), (unsigned)nsplit);
+  if (block_mode) {
+    dim3 bgrid((unsigned)k.out_count, (unsigned)nsplit);
+    TA* part = nullptr;
+    if (nsplit > 1)
+      cuda_check(cudaMallocAsync((void**)&part, (size_t)nsplit * k.out_count * sizeof(TA), stream), "alloc partials");
+    k.out = nsplit > 1 ? (void*)part : out;
+    k.out_acc = nsplit > 1 ? 1 : out_acc;
+    note_launch();
+    stage_block_kernel<TI, TA><<<bgrid, 256, 0, stream>>>(k);
+    cuda_check(cudaGetLastError(), "stage_block_kernel");
+    if (nsplit > 1) {
+      unsigned blocks = (unsigned)((k.out_count + 255) / 256);
+      note_launch();
+      if (out_acc) sum_partials<TA, TA><<<blocks, 256, 0, stream>>>(part, k.out_count, (int)nsplit, (TA*)out);
+      else sum_partials<TI, TA><<<blocks, 256, 0, stream>>>(part, k.out_count, (int)nsplit, (TI*)out);
+      cuda_check(cudaGetLastError(), "sum_partials");
+      cuda_check(cudaFreeAsync(part, stream), "free partials");
+    }
+    return;
+  }
   if (ds.cs.scatter) {
     k.out = out;
     k.out_acc = 1;
     note_launch();
-    stage_kernel<TI, TA, true><<<grid, 256, 0, stream>>>(k);
+    launch_nt<TI, TA, true>(k, grid, stream);
     cuda_check(cudaGetLastError(), "stage_kernel<scatter>");
     return;
   }
@@ -574,7 +730,7 @@ static void launch_stage_t(const DevStage& ds, const Bindings& b, void* out, boo
     k.out = out;
     k.out_acc = out_acc;
     note_launch();
-    stage_kernel<TI, TA, false><<<grid, 256, 0, stream>>>(k);
+    launch_nt<TI, TA, false>(k, grid, stream);
     cuda_check(cudaGetLastError(), "stage_kernel");
     return;
   }
@@ -583,7 +739,7 @@ static void launch_stage_t(const DevStage& ds, const Bindings& b, void* out, boo
   k.out = part;
   k.out_acc = 1;
   note_launch();
-  stage_kernel<TI, TA, false><<<grid, 256, 0, stream>>>(k);
+  launch_nt<TI, TA, false>(k, grid, stream);
   cuda_check(cudaGetLastError(), "stage_kernel<split>");
   unsigned blocks = (unsigned)((k.out_count + 255) / 256);
   note_launch();
@@ -614,6 +770,7 @@ void run_forward(const Plan& plan, DevPlan& dp, DType dt, const Bindings& b_in, 
   // Tensor-core path first: it computes the unstaged contraction, which the
   // staged nest equals by construction (codegen.py:605-608).
   if (dp.tc && tc_forward(*dp.tc, dt, b_in, stream)) return;
+  ensure_forward(plan, dp, stream);
   Bindings b = b_in;
   b.stages.assign(plan.stage_ext.size(), nullptr);
   std::vector<void*> owned;
@@ -655,6 +812,7 @@ static void run_grad(DType dt, const DevStage& ds, const Bindings& b, void* out,
 
 void run_backward(const Plan& plan, DevPlan& dp, DType dt, const Bindings& b, cudaStream_t stream) {
   if (dp.tc && tc_backward(*dp.tc, dt, b, stream)) return;
+  ensure_backward(plan, dp, stream);
   int64_t nx = 1;
   for (auto e : plan.x_ext) nx *= e;
   run_grad(dt, dp.grad_x.at(0), b, b.dx, nx, stream);

@@ -68,6 +68,10 @@ using TcPlanPtr = std::unique_ptr<TcPlan, TcPlanDeleter>;
 
 struct DevPlan {
   int device = -1;
+  // Universal-engine stages are built on first use (the tensor-core path
+  // usually makes them unnecessary); guarded by `mu`.
+  std::mutex mu;
+  bool have_forward = false, have_backward = false;
   std::vector<DevStage> forward, grad_x;
   std::vector<std::vector<DevStage>> grad_w;
   TcPlanPtr tc;  // null when the operator is not contraction-shaped

@@ -16,10 +16,13 @@
 #include <cuda_bf16.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstring>
 #include <functional>
 #include <map>
+#include <memory>
+#include <mutex>
 #include <set>
 #include <sstream>
 
@@ -78,79 +81,53 @@ struct PackGeom {
   int64_t Fpitch;                // channel-major row pitch (multiple of 8)
 };
 
-// dst[plane][img][hp][wp][cp], planes = Sh*Sw, zero outside the source.
-// A 64-channel x 32-pixel tile transposes through shared memory so both the
-// NCHW reads (along w) and the channels-last writes (16 B per thread) coalesce.
+// dst[plane][img][hp][wp][cp] (flat pixel f = ((plane*n_img + img)*Hp + hp)*Wp + wp),
+// zero outside the source.  A block moves 32 consecutive flat pixels x 64
+// channels through shared memory: lanes walk pixels for the NCHW reads
+// (coalesced along w), 8 threads per pixel write 16-byte channel chunks.
 template <typename TI>
 __global__ void __launch_bounds__(256) pack_cl_kernel(const TI* __restrict__ src, __nv_bfloat16* __restrict__ dst,
-                                                      PackGeom g) {
+                                                      PackGeom g, int64_t total_pix) {
   __shared__ __nv_bfloat16 tile[64][34];
-  const int wp0 = blockIdx.x * 32;
-  const int hp = blockIdx.y;
-  const int ncb = (g.Cp + 63) / 64;
-  int z = blockIdx.z;
-  const int cb = z % ncb;
-  z /= ncb;
-  const int img = z % g.n_img;
-  const int plane = z / g.n_img;
-  const int ph = plane / g.Sw, pw = plane % g.Sw;
-  const int hi = g.Sh * (hp - g.lo_h) + ph;
+  const int64_t f0 = (int64_t)blockIdx.x * 32;
+  const int cb = blockIdx.y;
   const int t = threadIdx.x;
   {
-    const int c = cb * 64 + t / 4;
-    const int w0 = (t % 4) * 8;
+    const int lane = t & 31, warp = t >> 5;
+    const int64_t f = f0 + lane;
+    bool inb = f < total_pix;
+    const TI* row = src;
+    if (inb) {
+      const int wp = (int)(f % g.Wp);
+      int64_t q = f / g.Wp;
+      const int hp = (int)(q % g.Hp);
+      q /= g.Hp;
+      const int img = (int)(q % g.n_img);
+      const int plane = (int)(q / g.n_img);
+      const int hi = g.Sh * (hp - g.lo_h) + plane / g.Sw;
+      const int wi = g.Sw * (wp - g.lo_w) + plane % g.Sw;
+      inb = hi >= 0 && hi < g.Hin && wi >= 0 && wi < g.Win;
+      row = src + img * g.s_img + (int64_t)hi * g.s_h + (int64_t)wi * g.s_w;
+    }
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
-      const int wp = wp0 + w0 + k;
-      const int wi = g.Sw * (wp - g.lo_w) + pw;
+      const int cl = warp * 8 + k;
+      const int c = cb * 64 + cl;
       float v = 0.f;
-      if (c < g.C && hi >= 0 && hi < g.Hin && wi >= 0 && wi < g.Win && wp < g.Wp)
-        v = (float)src[img * g.s_img + c * g.s_c + (int64_t)hi * g.s_h + (int64_t)wi * g.s_w];
-      tile[t / 4][w0 + k] = __float2bfloat16(v);
+      if (inb && c < g.C) v = (float)row[c * g.s_c];
+      tile[cl][lane] = __float2bfloat16(v);
     }
   }
   __syncthreads();
   const int w = t / 8, cc = (t % 8) * 8;
-  const int wp = wp0 + w;
+  const int64_t f = f0 + w;
   const int c0 = cb * 64 + cc;
-  if (wp < g.Wp && c0 < g.Cp) {
+  if (f < total_pix && c0 < g.Cp) {
     __align__(16) __nv_bfloat16 v[8];
 #pragma unroll
     for (int k = 0; k < 8; ++k) v[k] = tile[cc + k][w];
-    const int64_t o = ((((int64_t)plane * g.n_img + img) * g.Hp + hp) * g.Wp + wp) * g.Cp + c0;
-    *reinterpret_cast<uint4*>(dst + o) = *reinterpret_cast<const uint4*>(v);
+    *reinterpret_cast<uint4*>(dst + f * g.Cp + c0) = *reinterpret_cast<const uint4*>(v);
   }
-}
-
-// dst[plane][c][flat] with flat = (img*Hp + hp)*Wp + wp, row pitch Fpitch.
-template <typename TI>
-__global__ void __launch_bounds__(256) pack_cm_kernel(const TI* __restrict__ src, __nv_bfloat16* __restrict__ dst,
-                                                      PackGeom g, int64_t total) {
-  const int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 8;  // 8 flat positions per thread
-  if (i >= total) return;
-  const int64_t F = (int64_t)g.n_img * g.Hp * g.Wp;
-  const int64_t row = i / g.Fpitch;
-  const int64_t f0 = i % g.Fpitch;
-  const int c = (int)(row % g.C);
-  const int plane = (int)(row / g.C);
-  const int ph = plane / g.Sw, pw = plane % g.Sw;
-  __align__(16) __nv_bfloat16 v[8];
-#pragma unroll
-  for (int k = 0; k < 8; ++k) {
-    const int64_t f = f0 + k;
-    float val = 0.f;
-    if (f < F) {
-      const int wp = (int)(f % g.Wp);
-      const int64_t t = f / g.Wp;
-      const int hp = (int)(t % g.Hp);
-      const int img = (int)(t / g.Hp);
-      const int hi = g.Sh * (hp - g.lo_h) + ph, wi = g.Sw * (wp - g.lo_w) + pw;
-      if (hi >= 0 && hi < g.Hin && wi >= 0 && wi < g.Win)
-        val = (float)src[img * g.s_img + c * g.s_c + (int64_t)hi * g.s_h + (int64_t)wi * g.s_w];
-    }
-    v[k] = __float2bfloat16(val);
-  }
-  *reinterpret_cast<uint4*>(dst + i) = *reinterpret_cast<const uint4*>(v);
 }
 
 // ---------------------------------------------------------------------------
@@ -184,16 +161,10 @@ struct TcPlan {
   DevStage fold_fwd, fold_dgrad;
   std::vector<DevStage> chain;    // dW_j from the folded gradient
   std::vector<int64_t> w_numel;
+  std::mutex mu;                  // guards ws
+  std::map<std::pair<int, void*>, std::unique_ptr<struct TcWs>> ws;  // per (device, stream)
   int nwin() const { return dh.K * dw.K; }
 };
-
-void TcPlanDeleter::operator()(TcPlan* p) const {
-  if (!p) return;
-  release_dev_stage(p->fold_fwd);
-  release_dev_stage(p->fold_dgrad);
-  for (auto& s : p->chain) release_dev_stage(s);
-  delete p;
-}
 
 static std::vector<int64_t> rm_strides(const std::vector<int64_t>& ext) {
   std::vector<int64_t> s(ext.size(), 1);
@@ -439,20 +410,39 @@ std::string tc_describe(const TcPlan* tp) {
 // ---------------------------------------------------------------------------
 
 template <int BN>
-static void launch_gemm(const TcGemmParams& p, dim3 grid, cudaStream_t stream) {
-  static bool configured = false;
+static void launch_gemm(const TcGemmParams& p, unsigned grid, cudaStream_t stream) {
+  static std::atomic<uint64_t> configured{0};  // per-device bit
   constexpr int smem = smem_bytes<BN>();
-  if (!configured) {
+  int dev = 0;
+  cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
+  const uint64_t bit = 1ull << (dev & 63);
+  if (!(configured.load() & bit)) {
     cuda_check(cudaFuncSetAttribute(tc_gemm_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
                "cudaFuncSetAttribute(tc_gemm)");
-    configured = true;
+    configured.fetch_or(bit);
   }
   note_launch();
   tc_gemm_kernel<BN><<<grid, THREADS, smem, stream>>>(p);
   cuda_check(cudaGetLastError(), "tc_gemm_kernel");
 }
 
-static void gemm(TcGemmParams& p, int bn, dim3 grid, cudaStream_t stream) {
+static int sm_count() {
+  int dev = 0, n = 148;
+  cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
+  cuda_check(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev), "cudaDeviceGetAttribute");
+  return n;
+}
+
+// Persistent launch: one CTA per SM walks the (n fastest, m, z) tile grid.
+static void gemm(TcGemmParams& p, int bn, int m_tiles, int n_tiles, int z_tiles, cudaStream_t stream) {
+  p.m_tiles = m_tiles;
+  p.n_tiles = n_tiles;
+  p.z_tiles = z_tiles;
+  const int a_region = bn == 64 ? a_region_bytes<64>() : bn == 128 ? a_region_bytes<128>() : a_region_bytes<256>();
+  p.a_stages = std::max(1, std::min(8, a_region / p.a_stage_bytes));
+  const int64_t tiles = (int64_t)m_tiles * n_tiles * z_tiles;
+  if (tiles <= 0) return;
+  const unsigned grid = (unsigned)std::min<int64_t>(tiles, sm_count());
   if (bn == 64) launch_gemm<64>(p, grid, stream);
   else if (bn == 128) launch_gemm<128>(p, grid, stream);
   else launch_gemm<256>(p, grid, stream);
@@ -460,32 +450,13 @@ static void gemm(TcGemmParams& p, int bn, dim3 grid, cudaStream_t stream) {
 
 static int pick_bn(int n) { return n <= 64 ? 64 : n <= 128 ? 128 : 256; }
 
-template <typename T>
-static T* ws_alloc(size_t count, cudaStream_t stream, std::vector<void*>* owned) {
-  void* p = nullptr;
-  cuda_check(cudaMallocAsync(&p, std::max<size_t>(count, 1) * sizeof(T), stream), "cudaMallocAsync(tc workspace)");
-  owned->push_back(p);
-  return static_cast<T*>(p);
-}
-
 static void pack_cl(const void* src, DType dt, const PackGeom& g, __nv_bfloat16* dst, cudaStream_t stream) {
-  dim3 grid((unsigned)((g.Wp + 31) / 32), (unsigned)g.Hp, (unsigned)(((g.Cp + 63) / 64) * g.n_img * g.Sh * g.Sw));
+  const int64_t pix = (int64_t)g.Sh * g.Sw * g.n_img * g.Hp * g.Wp;
+  dim3 grid((unsigned)((pix + 31) / 32), (unsigned)((g.Cp + 63) / 64));
   note_launch();
-  if (dt == DT_BF16) pack_cl_kernel<__nv_bfloat16><<<grid, 256, 0, stream>>>((const __nv_bfloat16*)src, dst, g);
-  else pack_cl_kernel<float><<<grid, 256, 0, stream>>>((const float*)src, dst, g);
+  if (dt == DT_BF16) pack_cl_kernel<__nv_bfloat16><<<grid, 256, 0, stream>>>((const __nv_bfloat16*)src, dst, g, pix);
+  else pack_cl_kernel<float><<<grid, 256, 0, stream>>>((const float*)src, dst, g, pix);
   cuda_check(cudaGetLastError(), "pack_cl_kernel");
-}
-
-static void pack_cm(const void* src, DType dt, const PackGeom& g, __nv_bfloat16* dst, cudaStream_t stream) {
-  const int64_t total = (int64_t)g.Sh * g.Sw * g.C * g.Fpitch;
-  const int64_t threads = total / 8;
-  note_launch();
-  if (dt == DT_BF16)
-    pack_cm_kernel<__nv_bfloat16><<<(unsigned)((threads + 255) / 256), 256, 0, stream>>>(
-        (const __nv_bfloat16*)src, dst, g, total);
-  else
-    pack_cm_kernel<float><<<(unsigned)((threads + 255) / 256), 256, 0, stream>>>((const float*)src, dst, g, total);
-  cuda_check(cudaGetLastError(), "pack_cm_kernel");
 }
 
 static PackGeom geom(const TcPlan& tp, bool dy_side, bool grad_pad) {
@@ -522,192 +493,294 @@ static PackGeom geom(const TcPlan& tp, bool dy_side, bool grad_pad) {
   return g;
 }
 
-// ---------------------------------------------------------------------------
-// Forward: y[img, n, h, w] = scale * sum_win sum_ci Xcl[plane][flat + shift] Wf[win][n][ci]
-// ---------------------------------------------------------------------------
+// MODE_ROWS schedule.  Windows of each group are sorted by (plane, row
+// shift) and cut into chunks whose shift span fits one TMA box (<= 128 extra
+// rows): one A halo tile serves every window of a chunk.
+struct Win {
+  int shift, plane, bplane;
+};
+
+static int base_mode() {
+  static int m = [] {
+    // measured on B200: the swizzle follows absolute smem address bits, so a
+    // row-shifted view needs base offset 0 (mode 1 fails the parity tests)
+    const char* e = getenv("SYNO_TC_BASEMODE");
+    return e ? atoi(e) : 0;
+  }();
+  return m;
+}
+
+static void rows_schedule(TcGemmParams& p, std::vector<std::vector<Win>> groups, int bn) {
+  int n = 0, nc = 0, span = 0;
+  if (groups.size() > 8) fail(SYNO_E_UNSUPPORTED, "too many window groups");
+  for (size_t g = 0; g < groups.size(); ++g) {
+    auto& ws = groups[g];
+    std::sort(ws.begin(), ws.end(), [](const Win& a, const Win& b) {
+      return a.plane != b.plane ? a.plane < b.plane : a.shift < b.shift;
+    });
+    p.g_chunk0[g] = nc;
+    for (size_t i = 0; i < ws.size(); ++i) {
+      const bool fresh = i == 0 || ws[i].plane != ws[i - 1].plane || ws[i].shift - p.chunk_pmin[nc - 1] > 128;
+      if (fresh) {
+        if (nc >= MAXCHUNK) fail(SYNO_E_UNSUPPORTED, "too many window chunks");
+        p.chunk_plane[nc] = ws[i].plane;
+        p.chunk_pmin[nc] = ws[i].shift;
+        p.chunk_w0[nc] = n;
+        ++nc;
+      }
+      if (n >= MAXWIN) fail(SYNO_E_UNSUPPORTED, "too many windows");
+      p.a_shift[n] = ws[i].shift;
+      p.b_plane[n] = ws[i].bplane;
+      span = std::max(span, ws[i].shift - p.chunk_pmin[nc - 1]);
+      ++n;
+      p.chunk_w1[nc - 1] = n;
+    }
+    p.g_chunk1[g] = nc;
+  }
+  p.n_win = n;
+  p.a_rows = BM + span;
+  p.a_tx = (uint32_t)p.a_rows * BK * 2;
+  p.a_stage_bytes = (int)((p.a_tx + 1023) / 1024 * 1024);
+  p.b_tx = (uint32_t)bn * BK * 2;
+  p.base_mode = base_mode();
+}
+
+// Per (device, stream) workspace of an operator: packed operands, folded
+// weights, the fp32 grad-weight accumulator and the fully built GEMM
+// parameters (their TMA maps point into the workspace, so they are encoded
+// once).  Steady-state calls only launch kernels: no allocation, no host
+// synchronisation, CUDA-graph capturable.
+struct TcWs {
+  __nv_bfloat16 *xcl = nullptr, *wf = nullptr, *dycl_g = nullptr, *dycl_w = nullptr, *wt = nullptr;
+  float* dwf = nullptr;
+  PackGeom gx{}, gdy_g{}, gdy_w{};
+  bool share_dy = false;
+  TcGemmParams fwd, dg, wg;
+  int bn_fwd = 0, bn_dg = 0, bn_wg = 0;
+  int t_fwd[3] = {0, 0, 0}, t_dg[3] = {0, 0, 0}, t_wg[3] = {0, 0, 0};
+  std::vector<void*> owned;
+  ~TcWs() {
+    for (void* q : owned) cudaFree(q);
+  }
+};
+
+void TcPlanDeleter::operator()(TcPlan* p) const {
+  if (!p) return;
+  release_dev_stage(p->fold_fwd);
+  release_dev_stage(p->fold_dgrad);
+  for (auto& s : p->chain) release_dev_stage(s);
+  delete p;
+}
+
+static bool same_grid(const PackGeom& a, const PackGeom& b) {
+  return a.lo_h == b.lo_h && a.lo_w == b.lo_w && a.Hp == b.Hp && a.Wp == b.Wp;
+}
+
+template <typename T>
+static T* ws_alloc(TcWs& w, size_t count) {
+  void* p = nullptr;
+  cuda_check(cudaMalloc(&p, std::max<size_t>(count, 1) * sizeof(T)), "cudaMalloc(tc workspace)");
+  w.owned.push_back(p);
+  return static_cast<T*>(p);
+}
+
+static void build_ws(TcPlan& tp, TcWs& w) {
+  w.gx = geom(tp, false, false);
+  const int planes = w.gx.Sh * w.gx.Sw;
+  const int64_t F = (int64_t)w.gx.n_img * w.gx.Hp * w.gx.Wp;
+  w.xcl = ws_alloc<__nv_bfloat16>(w, (size_t)planes * F * tp.Cp);
+  w.wf = ws_alloc<__nv_bfloat16>(w, (size_t)tp.nwin() * tp.N * tp.Cp);
+
+  // ---- forward: y = sum_win sum_ci Xcl[plane][flat + shift] Wf[win][n][ci]
+  {
+    const int bn = pick_bn(tp.N);
+    TcGemmParams& p = w.fwd;
+    memset(&p, 0, sizeof(p));
+    p.mode = MODE_ROWS;
+    p.n_cblocks = (tp.Cp + BK - 1) / BK;
+    std::vector<std::vector<Win>> groups(1);
+    for (int rh = 0; rh < tp.dh.K; ++rh)
+      for (int rw = 0; rw < tp.dw.K; ++rw)
+        groups[0].push_back({tp.dh.delta(rh) * w.gx.Wp + tp.dw.delta(rw), tp.dh.phi(rh) * w.gx.Sw + tp.dw.phi(rw),
+                             rh * tp.dw.K + rw});
+    rows_schedule(p, groups, bn);
+    p.tma_a = make_map(w.xcl, tp.Cp, F, planes, tp.Cp, F * tp.Cp, p.a_rows);
+    p.tma_b = make_map(w.wf, tp.Cp, tp.N, tp.nwin(), tp.Cp, (int64_t)tp.N * tp.Cp, bn);
+    p.Hp = w.gx.Hp;
+    p.Wp = w.gx.Wp;
+    p.lo_h = w.gx.lo_h;
+    p.lo_w = w.gx.lo_w;
+    p.H = (int)tp.dh.E;
+    p.W = (int)tp.dw.E;
+    p.n_img = tp.n_img;
+    p.o_img = tp.y_img;
+    p.o_h = tp.dh.ys;
+    p.o_w = tp.dw.ys;
+    p.o_n = tp.y_n;
+    p.n_ext = tp.N;
+    p.out_kind = OUT_BF16;
+    p.scale = (float)tp.scale;
+    w.bn_fwd = bn;
+    w.t_fwd[0] = (int)((F + BM - 1) / BM);
+    w.t_fwd[1] = (tp.N + bn - 1) / bn;
+    w.t_fwd[2] = 1;
+  }
+
+  // ---- backward operands
+  w.gdy_g = geom(tp, true, true);
+  w.gdy_w = geom(tp, true, false);
+  w.share_dy = same_grid(w.gdy_g, w.gdy_w);
+  const int64_t Fg = (int64_t)w.gdy_g.n_img * w.gdy_g.Hp * w.gdy_g.Wp;
+  if (tp.dgrad_ok) {
+    w.dycl_g = ws_alloc<__nv_bfloat16>(w, (size_t)Fg * tp.Np);
+    w.wt = ws_alloc<__nv_bfloat16>(w, (size_t)tp.nwin() * tp.C * tp.Np);
+  }
+  w.dycl_w = (w.share_dy && w.dycl_g) ? w.dycl_g : ws_alloc<__nv_bfloat16>(w, (size_t)F * tp.Np);
+  w.dwf = ws_alloc<float>(w, (size_t)tp.nwin() * tp.N * tp.C);
+
+  // ---- grad-input: one group per output phase (psi_h, psi_w); its windows have phi(r) == psi
+  if (tp.dgrad_ok) {
+    const int bn = pick_bn(tp.C);
+    TcGemmParams& p = w.dg;
+    memset(&p, 0, sizeof(p));
+    p.mode = MODE_ROWS;
+    p.n_cblocks = (tp.Np + BK - 1) / BK;
+    const int Sh = tp.dh.S, Sw = tp.dw.S;
+    std::vector<std::vector<Win>> groups(Sh * Sw);
+    for (int ph = 0; ph < Sh; ++ph)
+      for (int pw = 0; pw < Sw; ++pw) {
+        const int grp = ph * Sw + pw;
+        for (int rh = 0; rh < tp.dh.K; ++rh)
+          for (int rw = 0; rw < tp.dw.K; ++rw) {
+            if (tp.dh.phi(rh) != ph || tp.dw.phi(rw) != pw) continue;
+            groups[grp].push_back({-tp.dh.delta(rh) * w.gdy_g.Wp - tp.dw.delta(rw), 0, rh * tp.dw.K + rw});
+          }
+        p.g_out_off[grp] = ph * tp.dh.xs + pw * tp.dw.xs;
+      }
+    rows_schedule(p, groups, bn);
+    p.tma_a = make_map(w.dycl_g, tp.Np, Fg, 1, tp.Np, Fg * tp.Np, p.a_rows);
+    p.tma_b = make_map(w.wt, tp.Np, tp.C, tp.nwin(), tp.Np, (int64_t)tp.C * tp.Np, bn);
+    p.Hp = w.gdy_g.Hp;
+    p.Wp = w.gdy_g.Wp;
+    p.lo_h = w.gdy_g.lo_h;
+    p.lo_w = w.gdy_g.lo_w;
+    p.H = (int)tp.dh.E;
+    p.W = (int)tp.dw.E;
+    p.n_img = tp.n_img;
+    p.o_img = tp.x_img;
+    p.o_h = tp.dh.xs * Sh;
+    p.o_w = tp.dw.xs * Sw;
+    p.o_n = tp.x_c;
+    p.n_ext = tp.C;
+    p.out_kind = OUT_BF16;
+    p.scale = (float)tp.scale;
+    w.bn_dg = bn;
+    w.t_dg[0] = (int)((Fg + BM - 1) / BM);
+    w.t_dg[1] = (tp.C + bn - 1) / bn;
+    w.t_dg[2] = Sh * Sw;
+  }
+
+  // ---- grad-weight: both operands channels-last over the forward's flat
+  // padded grid, read MN-major (K = pixel rows): a window is a row shift
+  {
+    // M = (window, 64-channel block of C_in) pairs, N = C_out, K = pixel rows
+    const int bn = pick_bn(tp.N);
+    TcGemmParams& p = w.wg;
+    memset(&p, 0, sizeof(p));
+    p.tma_a = make_map(w.xcl, tp.Cp, F, planes, tp.Cp, F * tp.Cp, 64);
+    p.tma_b = make_map(w.dycl_w, tp.Np, F, 1, tp.Np, F * tp.Np, 64);
+    p.mode = MODE_WGRAD;
+    p.n_cblocks = (int)((F + BK - 1) / BK);
+    p.n_win = tp.nwin();
+    const int ncb = (tp.Cp + 63) / 64;
+    for (int rh = 0; rh < tp.dh.K; ++rh)
+      for (int rw = 0; rw < tp.dw.K; ++rw) {
+        const int wi = rh * tp.dw.K + rw;
+        p.a_shift[wi] = tp.dh.delta(rh) * w.gx.Wp + tp.dw.delta(rw);
+        p.a_plane[wi] = tp.dh.phi(rh) * w.gx.Sw + tp.dw.phi(rw);
+        for (int cb = 0; cb < ncb; ++cb) {
+          if (p.n_pairs >= MAXPAIR) fail(SYNO_E_UNSUPPORTED, "too many (window, channel block) pairs");
+          p.pair_win[p.n_pairs] = (int16_t)wi;
+          p.pair_cb[p.n_pairs] = (int16_t)cb;
+          ++p.n_pairs;
+        }
+      }
+    const int m_tiles = (p.n_pairs + 1) / 2, n_tiles = (tp.N + bn - 1) / bn;
+    int ksplit = std::max(1, (4 * sm_count()) / std::max(1, m_tiles * n_tiles));
+    ksplit = std::min(ksplit, std::max(1, p.n_cblocks / 4));
+    p.ksplit = ksplit;
+    p.m_ext = tp.C;
+    p.n_ext = tp.N;
+    p.o_m = 1;
+    p.o_n = tp.C;
+    for (int wi = 0; wi < tp.nwin(); ++wi) p.g_out_off[wi] = (int64_t)wi * tp.N * tp.C;
+    p.out_kind = OUT_F32_ATOMIC;
+    p.scale = (float)tp.scale;
+    p.out = w.dwf;
+    p.a_rows = 64;
+    p.a_tx = (uint32_t)BM * BK * 2;
+    p.a_stage_bytes = BM * BK * 2;
+    p.b_tx = (uint32_t)bn * BK * 2;
+    w.bn_wg = bn;
+    w.t_wg[0] = m_tiles;
+    w.t_wg[1] = n_tiles;
+    w.t_wg[2] = ksplit;
+  }
+}
+
+static TcWs& workspace(TcPlan& tp, cudaStream_t stream) {
+  int dev = 0;
+  cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
+  std::lock_guard<std::mutex> lock(tp.mu);
+  auto key = std::make_pair(dev, (void*)stream);
+  auto it = tp.ws.find(key);
+  if (it != tp.ws.end()) return *it->second;
+  auto w = std::make_unique<TcWs>();
+  build_ws(tp, *w);
+  TcWs& ref = *w;
+  tp.ws[key] = std::move(w);
+  return ref;
+}
 
 bool tc_forward(TcPlan& tp, DType dt, const Bindings& b, cudaStream_t stream) {
   if (dt != DT_BF16) return false;
-  std::vector<void*> owned;
-  const PackGeom g = geom(tp, false, false);
-  const int planes = g.Sh * g.Sw;
-  const int64_t F = (int64_t)g.n_img * g.Hp * g.Wp;
-  auto* xcl = ws_alloc<__nv_bfloat16>((size_t)planes * F * tp.Cp, stream, &owned);
-  pack_cl(b.x, dt, g, xcl, stream);
-  auto* wf = ws_alloc<__nv_bfloat16>((size_t)tp.nwin() * tp.N * tp.Cp, stream, &owned);
-  run_stage(dt, tp.fold_fwd, b, wf, false, stream);
-
-  const int bn = pick_bn(tp.N);
-  TcGemmParams p;
-  memset(&p, 0, sizeof(p));
-  p.tma_a = make_map(xcl, tp.Cp, F, planes, tp.Cp, F * tp.Cp, BM);
-  p.tma_b = make_map(wf, tp.Cp, tp.N, tp.nwin(), tp.Cp, (int64_t)tp.N * tp.Cp, bn);
-  p.mode = MODE_ROWS;
-  p.n_cblocks = (tp.Cp + BK - 1) / BK;
-  p.n_win = tp.nwin();
-  for (int rh = 0; rh < tp.dh.K; ++rh)
-    for (int rw = 0; rw < tp.dw.K; ++rw) {
-      const int w = rh * tp.dw.K + rw;
-      p.a_shift[w] = tp.dh.delta(rh) * g.Wp + tp.dw.delta(rw);
-      p.a_plane[w] = tp.dh.phi(rh) * g.Sw + tp.dw.phi(rw);
-      p.b_plane[w] = w;
-    }
-  p.win_base[0] = 0;
-  p.win_count[0] = tp.nwin();
-  p.g_out_off[0] = 0;
-  p.Hp = g.Hp;
-  p.Wp = g.Wp;
-  p.lo_h = g.lo_h;
-  p.lo_w = g.lo_w;
-  p.H = (int)tp.dh.E;
-  p.W = (int)tp.dw.E;
-  p.n_img = tp.n_img;
-  p.o_img = tp.y_img;
-  p.o_h = tp.dh.ys;
-  p.o_w = tp.dw.ys;
-  p.o_n = tp.y_n;
-  p.n_ext = tp.N;
-  p.out_kind = OUT_BF16;
-  p.scale = (float)tp.scale;
+  TcWs& w = workspace(tp, stream);
+  pack_cl(b.x, dt, w.gx, w.xcl, stream);
+  run_stage(dt, tp.fold_fwd, b, w.wf, false, stream);
+  TcGemmParams& p = w.fwd;
   p.out = b.y;
-  p.tx_bytes = (uint32_t)((BM + bn) * BK * 2);
-  dim3 grid((unsigned)((F + BM - 1) / BM), (unsigned)((tp.N + bn - 1) / bn), 1);
-  gemm(p, bn, grid, stream);
-  for (void* q : owned) cuda_check(cudaFreeAsync(q, stream), "cudaFreeAsync(tc workspace)");
+  gemm(p, w.bn_fwd, w.t_fwd[0], w.t_fwd[1], w.t_fwd[2], stream);
   return true;
-}
-
-// ---------------------------------------------------------------------------
-// Backward
-// ---------------------------------------------------------------------------
-
-static void grad_input(TcPlan& tp, DType dt, const Bindings& b, cudaStream_t stream, std::vector<void*>* owned) {
-  const PackGeom g = geom(tp, true, true);
-  const int64_t F = (int64_t)g.n_img * g.Hp * g.Wp;
-  auto* dycl = ws_alloc<__nv_bfloat16>((size_t)F * tp.Np, stream, owned);
-  pack_cl(b.dy, dt, g, dycl, stream);
-  auto* wt = ws_alloc<__nv_bfloat16>((size_t)tp.nwin() * tp.C * tp.Np, stream, owned);
-  run_stage(dt, tp.fold_dgrad, b, wt, false, stream);
-
-  const int bn = pick_bn(tp.C);
-  TcGemmParams p;
-  memset(&p, 0, sizeof(p));
-  p.tma_a = make_map(dycl, tp.Np, F, 1, tp.Np, F * tp.Np, BM);
-  p.tma_b = make_map(wt, tp.Np, tp.C, tp.nwin(), tp.Np, (int64_t)tp.C * tp.Np, bn);
-  p.mode = MODE_ROWS;
-  p.n_cblocks = (tp.Np + BK - 1) / BK;
-  // group = output phase (psi_h, psi_w); its windows have phi(r) == psi
-  const int Sh = tp.dh.S, Sw = tp.dw.S;
-  int n = 0;
-  for (int ph = 0; ph < Sh; ++ph)
-    for (int pw = 0; pw < Sw; ++pw) {
-      const int grp = ph * Sw + pw;
-      p.win_base[grp] = n;
-      for (int rh = 0; rh < tp.dh.K; ++rh)
-        for (int rw = 0; rw < tp.dw.K; ++rw) {
-          if (tp.dh.phi(rh) != ph || tp.dw.phi(rw) != pw) continue;
-          p.a_shift[n] = -tp.dh.delta(rh) * g.Wp - tp.dw.delta(rw);
-          p.a_plane[n] = 0;
-          p.b_plane[n] = rh * tp.dw.K + rw;
-          ++n;
-        }
-      p.win_count[grp] = n - p.win_base[grp];
-      p.g_out_off[grp] = ph * tp.dh.xs + pw * tp.dw.xs;
-    }
-  p.n_win = n;
-  p.Hp = g.Hp;
-  p.Wp = g.Wp;
-  p.lo_h = g.lo_h;
-  p.lo_w = g.lo_w;
-  p.H = (int)tp.dh.E;
-  p.W = (int)tp.dw.E;
-  p.n_img = tp.n_img;
-  p.o_img = tp.x_img;
-  p.o_h = tp.dh.xs * Sh;
-  p.o_w = tp.dw.xs * Sw;
-  p.o_n = tp.x_c;
-  p.n_ext = tp.C;
-  p.out_kind = OUT_BF16;
-  p.scale = (float)tp.scale;
-  p.out = b.dx;
-  p.tx_bytes = (uint32_t)((BM + bn) * BK * 2);
-  dim3 grid((unsigned)((F + BM - 1) / BM), (unsigned)((tp.C + bn - 1) / bn), (unsigned)(Sh * Sw));
-  gemm(p, bn, grid, stream);
-}
-
-static void grad_weight(TcPlan& tp, DType dt, const Bindings& b, cudaStream_t stream, std::vector<void*>* owned) {
-  // both operands channels-last over the forward's flat padded grid; the
-  // GEMM reads them MN-major (K = pixel rows), so a window is a row shift
-  const PackGeom gx = geom(tp, false, false);
-  const PackGeom gy = geom(tp, true, false);
-  const int planes = gx.Sh * gx.Sw;
-  const int64_t F = (int64_t)gx.n_img * gx.Hp * gx.Wp;
-  auto* xcl = ws_alloc<__nv_bfloat16>((size_t)planes * F * tp.Cp, stream, owned);
-  auto* dycl = ws_alloc<__nv_bfloat16>((size_t)F * tp.Np, stream, owned);
-  pack_cl(b.x, dt, gx, xcl, stream);
-  pack_cl(b.dy, dt, gy, dycl, stream);
-  const size_t nwf = (size_t)tp.nwin() * tp.N * tp.C;
-  float* dwf = ws_alloc<float>(nwf, stream, owned);
-  cuda_check(cudaMemsetAsync(dwf, 0, nwf * sizeof(float), stream), "memset(dWf)");
-
-  const int bn = pick_bn(tp.C);
-  TcGemmParams p;
-  memset(&p, 0, sizeof(p));
-  p.tma_a = make_map(dycl, tp.Np, F, 1, tp.Np, F * tp.Np, 64);
-  p.tma_b = make_map(xcl, tp.Cp, F, planes, tp.Cp, F * tp.Cp, 64);
-  p.mode = MODE_WGRAD;
-  p.n_cblocks = (int)((F + BK - 1) / BK);
-  p.n_win = tp.nwin();
-  for (int rh = 0; rh < tp.dh.K; ++rh)
-    for (int rw = 0; rw < tp.dw.K; ++rw) {
-      const int w = rh * tp.dw.K + rw;
-      p.a_shift[w] = tp.dh.delta(rh) * gx.Wp + tp.dw.delta(rw);
-      p.a_plane[w] = tp.dh.phi(rh) * gx.Sw + tp.dw.phi(rw);
-    }
-  const int gx_tiles = (tp.N + BM - 1) / BM, gy_tiles = (tp.C + bn - 1) / bn;
-  int ksplit = std::max(1, (2 * 148) / std::max(1, gx_tiles * gy_tiles * tp.nwin()));
-  ksplit = std::min(ksplit, std::max(1, p.n_cblocks / 4));
-  p.ksplit = ksplit;
-  p.m_ext = tp.N;
-  p.n_ext = tp.C;
-  p.o_m = tp.C;
-  p.o_n = 1;
-  for (int w = 0; w < 8; ++w) p.g_out_off[w] = 0;
-  p.out_kind = OUT_F32_ATOMIC;
-  p.scale = (float)tp.scale;
-  p.out = dwf;
-  p.tx_bytes = (uint32_t)((BM + bn) * BK * 2);
-  // per-window output offset: the kernel adds g_out_off[g] only for g < 8, so
-  // wgrad launches one grid per block of 8 windows
-  for (int w0 = 0; w0 < tp.nwin(); w0 += 8) {
-    TcGemmParams q = p;
-    const int nw = std::min(8, tp.nwin() - w0);
-    for (int k = 0; k < nw; ++k) {
-      q.a_shift[k] = p.a_shift[w0 + k];
-      q.a_plane[k] = p.a_plane[w0 + k];
-      q.g_out_off[k] = (int64_t)(w0 + k) * tp.N * tp.C;
-    }
-    dim3 grid((unsigned)gx_tiles, (unsigned)gy_tiles, (unsigned)(nw * ksplit));
-    gemm(q, bn, grid, stream);
-  }
-  // chain rule through the fold, into each requested weight gradient
-  Bindings cb = b;
-  cb.stages = {dwf};
-  for (size_t j = 0; j < tp.chain.size(); ++j) {
-    if (j >= b.dw.size() || !b.dw[j]) continue;
-    run_stage(dt, tp.chain[j], cb, b.dw[j], false, stream);
-  }
 }
 
 bool tc_backward(TcPlan& tp, DType dt, const Bindings& b, cudaStream_t stream) {
   if (dt != DT_BF16) return false;
   if (b.dx && !tp.dgrad_ok) return false;
-  std::vector<void*> owned;
-  if (b.dx) grad_input(tp, dt, b, stream, &owned);
+  TcWs& w = workspace(tp, stream);
   bool any_w = false;
-  for (auto* p : b.dw) any_w = any_w || p;
-  if (any_w) grad_weight(tp, dt, b, stream, &owned);
-  for (void* q : owned) cuda_check(cudaFreeAsync(q, stream), "cudaFreeAsync(tc workspace)");
+  for (auto* q : b.dw) any_w = any_w || q;
+  bool dy_w_packed = false;
+  if (b.dx) {
+    pack_cl(b.dy, dt, w.gdy_g, w.dycl_g, stream);
+    dy_w_packed = w.share_dy;
+    run_stage(dt, tp.fold_dgrad, b, w.wt, false, stream);
+    TcGemmParams& p = w.dg;
+    p.out = b.dx;
+    gemm(p, w.bn_dg, w.t_dg[0], w.t_dg[1], w.t_dg[2], stream);
+  }
+  if (any_w) {
+    pack_cl(b.x, dt, w.gx, w.xcl, stream);
+    if (!dy_w_packed) pack_cl(b.dy, dt, w.gdy_w, w.dycl_w, stream);
+    cuda_check(cudaMemsetAsync(w.dwf, 0, (size_t)tp.nwin() * tp.N * tp.C * sizeof(float), stream), "memset(dWf)");
+    gemm(w.wg, w.bn_wg, w.t_wg[0], w.t_wg[1], w.t_wg[2], stream);
+    // chain rule through the fold, into each requested weight gradient
+    Bindings cb = b;
+    cb.stages = {w.dwf};
+    for (size_t j = 0; j < tp.chain.size(); ++j) {
+      if (j >= b.dw.size() || !b.dw[j]) continue;
+      run_stage(dt, tp.chain[j], cb, b.dw[j], false, stream);
+    }
+  }
   return true;
 }
 

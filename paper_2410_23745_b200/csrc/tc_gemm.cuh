@@ -1,14 +1,21 @@
 // tcgen05 implicit-GEMM kernel (sm_100a): TMA -> SMEM (128B swizzle) ->
 // tcgen05.mma (bf16 x bf16 -> fp32 in TMEM) -> tcgen05.ld -> masked affine
-// epilogue.  Both operands are K-major tiles fetched by TMA from packed
-// operand layouts (tc.cu); the k-block schedule and the epilogue address
-// map come from TcGemmParams, so one kernel serves forward (windows x
-// channel blocks), grad-input (flipped windows) and grad-weight (split-K
-// over pixels, one window per blockIdx.z group).
+// epilogue.  The operands are fetched by TMA from packed operand layouts
+// (tc.cu); the k schedule and the epilogue address map come from
+// TcGemmParams, so one kernel serves forward (windows x channel blocks),
+// grad-input (flipped windows, one group per output phase) and grad-weight
+// (split-K over pixel rows, one window per group, MN-major operands).
 //
-// Warp roles (192 threads): warp 0 = TMA producer, warp 1 = TMEM owner +
-// MMA issuer (one elected lane), warps 2..5 = epilogue (TMEM lane quarter
-// = warp % 4).
+// MODE_ROWS loads ONE halo tile of A per (phase plane, channel block) --
+// the 128 output rows plus the span of the window row shifts -- and
+// addresses every window as a row-shifted view of it (descriptor start
+// address + base offset), so A crosses L2 once instead of once per window.
+//
+// Persistent: a CTA walks tiles t = blockIdx.x, +gridDim.x, ...  Warp roles
+// (192 threads): warp 0 = TMA producer, warp 1 = TMEM owner + MMA issuer
+// (one lane), warps 2..5 = epilogue (TMEM lane quarter = warp % 4).  The
+// accumulator is double-buffered in TMEM so the epilogue of tile i overlaps
+// the main loop of tile i+1.
 #pragma once
 
 #include <cuda.h>
@@ -20,14 +27,33 @@ namespace tc {
 
 constexpr int BM = 128;
 constexpr int BK = 64;                 // one 128-byte swizzle row of bf16
-constexpr int STAGES = 4;
 constexpr int MAXWIN = 64;
+constexpr int MAXCHUNK = 32;
 constexpr int THREADS = 192;
+constexpr int EPI_WARPS = 4;
+constexpr int RING_BYTES = 192 * 1024;  // A ring (halo / dy tiles) + B ring
+
+// Narrow N tiles need few B bytes per k-step: give the A (halo) ring the room
+// so several tiles' A loads are in flight (the pipeline is TMA-latency bound).
+template <int BN>
+__host__ __device__ constexpr int a_region_bytes() {
+  return BN <= 64 ? 128 * 1024 : BN <= 128 ? 96 * 1024 : 64 * 1024;
+}
+template <int BN>
+__host__ __device__ constexpr int b_stages() {
+  return (RING_BYTES - a_region_bytes<BN>()) / (BN * BK * 2);
+}
 
 enum Mode : int32_t {
-  MODE_ROWS = 0,   // A rows = flat padded pixels (+ window shift); k = (cblock, window)
-  MODE_WGRAD = 1,  // M = C_out, N = C_in, k = pixel rows (MN-major channels-last tiles); window = group
+  MODE_ROWS = 0,   // A rows = flat padded pixels (halo tile, window = row shift); k = (chunk, cblock, window)
+  // M = (window, 64-channel block of C_in) pairs, two per tile; N = C_out;
+  // k = pixel rows; MN-major channels-last tiles of x (row-shifted per
+  // window) and dy.  Output dWf[window][co][ci], fp32 split-K atomics that
+  // coalesce along ci.
+  MODE_WGRAD = 1,
 };
+
+constexpr int MAXPAIR = 160;
 
 enum OutKind : int32_t { OUT_BF16 = 0, OUT_F32 = 1, OUT_F32_ATOMIC = 2 };
 
@@ -36,25 +62,34 @@ struct alignas(64) TcGemmParams {
   CUtensorMap tma_b;   // 3-D: [K elems][rows][plane]
   int32_t mode;
   int32_t n_cblocks;   // MODE_ROWS: channel blocks of 64; MODE_WGRAD: pixel blocks per window
-  int32_t n_win;       // windows per group (MODE_ROWS) or groups (MODE_WGRAD)
+  int32_t n_win;
   int32_t ksplit;      // MODE_WGRAD split of the pixel blocks
   int32_t a_shift[MAXWIN];   // MODE_ROWS: row shift of A per window; MODE_WGRAD: B row (pixel) shift
-  int32_t a_plane[MAXWIN];   // plane (phase) of the shifted operand per window
+  int32_t a_plane[MAXWIN];   // MODE_WGRAD: plane (phase) of x per window
   int32_t b_plane[MAXWIN];   // MODE_ROWS: B plane (packed weight window) per window
-  // groups (blockIdx.z): MODE_ROWS uses win_base[g]..win_base[g]+win_count[g]
-  int32_t win_base[8], win_count[8];
-  int64_t g_out_off[8];
-  int32_t a_row_base;        // MODE_ROWS: first flat row of the M tile grid
+  // MODE_ROWS chunks: windows [chunk_w0, chunk_w1) share A plane chunk_plane and min shift chunk_pmin
+  int32_t chunk_plane[MAXCHUNK], chunk_w0[MAXCHUNK], chunk_w1[MAXCHUNK], chunk_pmin[MAXCHUNK];
+  int32_t g_chunk0[8], g_chunk1[8];  // chunk range of each group (blockIdx-level z)
+  // MODE_WGRAD pairs: M rows [64h, 64h+64) of tile mt are pair 2*mt+h = (window, channel block)
+  int32_t n_pairs;
+  int16_t pair_win[MAXPAIR], pair_cb[MAXPAIR];
+  int64_t g_out_off[MAXWIN];
+  int32_t a_rows;       // rows of one A TMA box (halo rows in MODE_ROWS)
+  int32_t a_stage_bytes;  // smem slot of one A stage (multiple of 1024)
+  int32_t a_stages;
+  uint32_t a_tx, b_tx;  // transaction bytes of one A / B stage
+  int32_t base_mode;    // 1: set the descriptor base offset for row-shifted A views
+  // tile grid: t -> (nt fastest, then mt, then z)
+  int32_t m_tiles, n_tiles, z_tiles;
   // epilogue: row index r of the M tile -> output coordinates
-  //   MODE_ROWS: flat = mtile*128 + r + a_row_base; (img, hp, wp) by Hp, Wp; h = hp - lo_h ...
+  //   MODE_ROWS: flat = mtile*128 + r; (img, hp, wp) by Hp, Wp; h = hp - lo_h ...
   //   MODE_WGRAD: row = C_out index
   int32_t Hp, Wp, lo_h, lo_w, H, W, n_img;
-  int64_t o_img, o_h, o_w, o_n, o_m;   // output element strides (o_m used by MODE_WGRAD rows)
+  int64_t o_img, o_h, o_w, o_n, o_m;
   int32_t m_ext, n_ext;
   int32_t out_kind;
   float scale;
   void* out;
-  uint32_t tx_bytes;
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -93,14 +128,16 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, u
       : "memory");
 }
 
-// K-major, 128-byte swizzle smem descriptor (canonical ((8,m),(T,2)) : ((8T,SBO),(1,T))).
-__device__ __forceinline__ uint64_t sw128_desc(const void* smem) {
-  uint64_t addr = smem_u32(smem);
+// K-major, 128-byte swizzle smem descriptor (canonical ((8,m),(T,2)) : ((8T,SBO),(1,T))),
+// starting `row` 128-byte rows into a 1024-byte aligned tile.
+__device__ __forceinline__ uint64_t sw128_desc(const void* smem, int row = 0, int base_mode = 0) {
+  uint64_t addr = smem_u32(smem) + (uint32_t)row * 128u;
   uint64_t d = 0;
   d |= (addr >> 4) & 0x3FFF;              // start address
   d |= (uint64_t)(16 >> 4) << 16;         // leading byte offset (unused for swizzled K-major)
   d |= (uint64_t)(1024 >> 4) << 32;       // stride byte offset: 8 rows x 128 B
   d |= (uint64_t)1 << 46;                 // sm100 descriptor version
+  if (base_mode) d |= (uint64_t)((addr >> 7) & 7) << 49;  // swizzle phase of an unaligned start
   d |= (uint64_t)2 << 61;                 // SWIZZLE_128B
   return d;
 }
@@ -156,48 +193,77 @@ __device__ __forceinline__ void tmem_ld32(uint32_t addr, float* v) {
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+struct TileInfo {
+  int mt, nt, g, ks, kb0, nkb;
+};
+
+__device__ __forceinline__ TileInfo tile_info(const TcGemmParams& p, int t) {
+  TileInfo ti;
+  ti.nt = t % p.n_tiles;
+  int q = t / p.n_tiles;
+  ti.mt = q % p.m_tiles;
+  const int z = q / p.m_tiles;
+  if (p.mode == MODE_ROWS) {
+    ti.g = z;
+    ti.ks = 0;
+    ti.kb0 = 0;
+    ti.nkb = 0;
+    for (int c = p.g_chunk0[z]; c < p.g_chunk1[z]; ++c) ti.nkb += p.chunk_w1[c] - p.chunk_w0[c];
+    ti.nkb *= p.n_cblocks;  // MMA k-steps (one per window x channel block)
+  } else {
+    ti.ks = z % p.ksplit;
+    ti.g = z / p.ksplit;
+    const int per = (p.n_cblocks + p.ksplit - 1) / p.ksplit;
+    ti.kb0 = ti.ks * per;
+    const int kb1 = min(p.n_cblocks, ti.kb0 + per);
+    ti.nkb = kb1 > ti.kb0 ? kb1 - ti.kb0 : 0;
+  }
+  return ti;
+}
+
+// Ring position helper: slot index and phase parity of the i-th use.
+struct Ring {
+  uint32_t i = 0;
+  __device__ __forceinline__ int slot(int n) const { return (int)(i % (uint32_t)n); }
+  __device__ __forceinline__ uint32_t phase(int n) const { return (i / (uint32_t)n) & 1u; }
+};
+
 template <int BN>
 __global__ void __launch_bounds__(THREADS, 1) tc_gemm_kernel(const __grid_constant__ TcGemmParams p) {
-  constexpr int A_BYTES = BM * BK * 2;
+  constexpr int BSTAGES = b_stages<BN>();
   constexpr int B_BYTES = BN * BK * 2;
-  constexpr uint32_t TMEM_COLS = BN < 32 ? 32 : BN;
+  constexpr uint32_t ACC_COLS = BN < 32 ? 32 : BN;
+  constexpr uint32_t TMEM_COLS = 2 * ACC_COLS;  // two accumulator buffers (<= 512)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sa = smem;
-  uint8_t* sb = smem + STAGES * A_BYTES;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sb + STAGES * B_BYTES);
-  uint64_t* empty = full + STAGES;
-  uint64_t* tfull = empty + STAGES;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tfull + 1);
+  uint8_t* sb = smem + a_region_bytes<BN>();
+  uint64_t* a_full = reinterpret_cast<uint64_t*>(smem + RING_BYTES);
+  uint64_t* a_empty = a_full + 8;
+  uint64_t* b_full = a_empty + 8;
+  uint64_t* b_empty = b_full + BSTAGES;
+  uint64_t* tfull = b_empty + BSTAGES;  // [2]
+  uint64_t* tempty = tfull + 2;         // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int mt = blockIdx.x, nt = blockIdx.y;
-  int g = blockIdx.z, ks = 0;
-  if (p.mode == MODE_WGRAD) {
-    ks = blockIdx.z % p.ksplit;
-    g = blockIdx.z / p.ksplit;
-  }
-  // k-block range of this CTA
-  int kb0, kb1, win0 = 0;
-  if (p.mode == MODE_ROWS) {
-    win0 = p.win_base[g];
-    kb0 = 0;
-    kb1 = p.win_count[g] * p.n_cblocks;
-  } else {
-    int per = (p.n_cblocks + p.ksplit - 1) / p.ksplit;
-    kb0 = ks * per;
-    kb1 = min(p.n_cblocks, kb0 + per);
-    if (kb1 < kb0) kb1 = kb0;
-  }
-  const int nkb = kb1 - kb0;
+  const int n_tiles_total = p.m_tiles * p.n_tiles * p.z_tiles;
+  const int AST = p.a_stages;
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < STAGES; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+    for (int s = 0; s < AST; ++s) {
+      mbar_init(&a_full[s], 1);
+      mbar_init(&a_empty[s], 1);
     }
-    mbar_init(tfull, 1);
+    for (int s = 0; s < BSTAGES; ++s) {
+      mbar_init(&b_full[s], 1);
+      mbar_init(&b_empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], EPI_WARPS);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
@@ -215,29 +281,51 @@ __global__ void __launch_bounds__(THREADS, 1) tc_gemm_kernel(const __grid_consta
     if (lane == 0) {
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&p.tma_a)) : "memory");
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&p.tma_b)) : "memory");
-      for (int i = 0; i < nkb; ++i) {
-        const int s = i % STAGES;
-        const uint32_t ph = (uint32_t)(i / STAGES) & 1u;
-        mbar_wait(&empty[s], ph ^ 1u);
-        const int kb = kb0 + i;
-        mbar_expect_tx(&full[s], p.tx_bytes);
+      Ring ra, rb;
+      for (int t = blockIdx.x; t < n_tiles_total; t += gridDim.x) {
+        const TileInfo ti = tile_info(p, t);
         if (p.mode == MODE_ROWS) {
-          // K-major tiles: A = 128 pixel rows x 64 channels, B = BN rows x 64 channels
-          const int cb = kb % p.n_cblocks;
-          const int w = win0 + kb / p.n_cblocks;
-          tma_load_3d(sa + s * A_BYTES, &p.tma_a, &full[s], cb * BK, p.a_row_base + mt * BM + p.a_shift[w],
-                      p.a_plane[w]);
-          tma_load_3d(sb + s * B_BYTES, &p.tma_b, &full[s], cb * BK, nt * BN, p.b_plane[w]);
+          for (int c = p.g_chunk0[ti.g]; c < p.g_chunk1[ti.g]; ++c) {
+            for (int cb = 0; cb < p.n_cblocks; ++cb) {
+              // one halo tile of A for this plane and channel block
+              const int as = ra.slot(AST);
+              mbar_wait(&a_empty[as], ra.phase(AST) ^ 1u);
+              mbar_expect_tx(&a_full[as], p.a_tx);
+              tma_load_3d(sa + as * p.a_stage_bytes, &p.tma_a, &a_full[as], cb * BK,
+                          ti.mt * BM + p.chunk_pmin[c], p.chunk_plane[c]);
+              ++ra.i;
+              for (int w = p.chunk_w0[c]; w < p.chunk_w1[c]; ++w) {
+                const int bs = rb.slot(BSTAGES);
+                mbar_wait(&b_empty[bs], rb.phase(BSTAGES) ^ 1u);
+                mbar_expect_tx(&b_full[bs], p.b_tx);
+                tma_load_3d(sb + bs * B_BYTES, &p.tma_b, &b_full[bs], cb * BK, ti.nt * BN, p.b_plane[w]);
+                ++rb.i;
+              }
+            }
+          }
         } else {
-          // MN-major tiles from channels-last operands: 64 pixel rows (k) x 64 channels per box;
-          // the window is a pixel-row shift of the x operand.
+          for (int i = 0; i < ti.nkb; ++i) {
+            const int kb = ti.kb0 + i;
+            const int as = ra.slot(AST);
+            mbar_wait(&a_empty[as], ra.phase(AST) ^ 1u);
+            mbar_expect_tx(&a_full[as], p.a_tx);
 #pragma unroll
-          for (int h = 0; h < BM / 64; ++h)
-            tma_load_3d(sa + s * A_BYTES + h * 8192, &p.tma_a, &full[s], mt * BM + h * 64, kb * BK, 0);
+            for (int h = 0; h < BM / 64; ++h) {
+              int pr = ti.mt * 2 + h;
+              if (pr >= p.n_pairs) pr = ti.mt * 2;  // masked rows: reload a valid pair
+              const int w = p.pair_win[pr];
+              tma_load_3d(sa + as * p.a_stage_bytes + h * 8192, &p.tma_a, &a_full[as], p.pair_cb[pr] * 64,
+                          kb * BK + p.a_shift[w], p.a_plane[w]);
+            }
+            ++ra.i;
+            const int bs = rb.slot(BSTAGES);
+            mbar_wait(&b_empty[bs], rb.phase(BSTAGES) ^ 1u);
+            mbar_expect_tx(&b_full[bs], p.b_tx);
 #pragma unroll
-          for (int h = 0; h < BN / 64; ++h)
-            tma_load_3d(sb + s * B_BYTES + h * 8192, &p.tma_b, &full[s], nt * BN + h * 64, kb * BK + p.a_shift[g],
-                        p.a_plane[g]);
+            for (int h = 0; h < BN / 64; ++h)
+              tma_load_3d(sb + bs * B_BYTES + h * 8192, &p.tma_b, &b_full[bs], ti.nt * BN + h * 64, kb * BK, 0);
+            ++rb.i;
+          }
         }
       }
     }
@@ -245,73 +333,124 @@ __global__ void __launch_bounds__(THREADS, 1) tc_gemm_kernel(const __grid_consta
     if (lane == 0) {
       const bool mn = p.mode == MODE_WGRAD;
       const uint32_t idesc = mn ? idesc_bf16(BM, BN, 1, 1) : idesc_bf16(BM, BN);
-      // per UMMA_K = 16 step: K-major advances 32 B inside the swizzled row,
-      // MN-major advances two 8-row k groups (2 x 1024 B)
-      const uint64_t kstep = mn ? (2048 >> 4) : (32 >> 4);
-      for (int i = 0; i < nkb; ++i) {
-        const int s = i % STAGES;
-        const uint32_t ph = (uint32_t)(i / STAGES) & 1u;
-        mbar_wait(&full[s], ph);
+      Ring ra, rb;
+      uint32_t tcount = 0;
+      for (int t = blockIdx.x; t < n_tiles_total; t += gridDim.x, ++tcount) {
+        const TileInfo ti = tile_info(p, t);
+        const uint32_t acc = tcount & 1u;
+        mbar_wait(&tempty[acc], ((tcount >> 1) & 1u) ^ 1u);  // epilogue drained this buffer
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const uint64_t da = mn ? sw128_mn_desc(sa + s * A_BYTES, 8192) : sw128_desc(sa + s * A_BYTES);
-        const uint64_t db = mn ? sw128_mn_desc(sb + s * B_BYTES, 8192) : sw128_desc(sb + s * B_BYTES);
+        const uint32_t dst = tmem + acc * ACC_COLS;
+        uint32_t accumulate = 0;
+        if (!mn) {
+          for (int c = p.g_chunk0[ti.g]; c < p.g_chunk1[ti.g]; ++c) {
+            for (int cb = 0; cb < p.n_cblocks; ++cb) {
+              const int as = ra.slot(AST);
+              mbar_wait(&a_full[as], ra.phase(AST));
+              const uint8_t* abase = sa + as * p.a_stage_bytes;
+              for (int w = p.chunk_w0[c]; w < p.chunk_w1[c]; ++w) {
+                const int bs = rb.slot(BSTAGES);
+                mbar_wait(&b_full[bs], rb.phase(BSTAGES));
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                const uint64_t db = sw128_desc(sb + bs * B_BYTES);
+                const int row = p.a_shift[w] - p.chunk_pmin[c];
 #pragma unroll
-        for (int k = 0; k < BK / 16; ++k)
-          mma_bf16(tmem, da + (uint64_t)k * kstep, db + (uint64_t)k * kstep, idesc, (i > 0 || k > 0) ? 1u : 0u);
-        mma_commit(&empty[s]);
+                for (int k = 0; k < BK / 16; ++k) {
+                  // K advance: 32 B inside the swizzled 128 B row
+                  const uint64_t da = sw128_desc(abase + k * 32, row, p.base_mode);
+                  mma_bf16(dst, da, db + (uint64_t)(k * 2), idesc, accumulate);
+                  accumulate = 1;
+                }
+                mma_commit(&b_empty[bs]);
+                ++rb.i;
+              }
+              mma_commit(&a_empty[as]);  // halo tile free once its windows' MMAs finish
+              ++ra.i;
+            }
+          }
+        } else {
+          for (int i = 0; i < ti.nkb; ++i) {
+            const int as = ra.slot(AST), bs = rb.slot(BSTAGES);
+            mbar_wait(&a_full[as], ra.phase(AST));
+            mbar_wait(&b_full[bs], rb.phase(BSTAGES));
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            const uint64_t da = sw128_mn_desc(sa + as * p.a_stage_bytes, 8192);
+            const uint64_t db = sw128_mn_desc(sb + bs * B_BYTES, 8192);
+#pragma unroll
+            for (int k = 0; k < BK / 16; ++k) {
+              // MN-major K advance: two 8-row k groups (2 x 1024 B)
+              mma_bf16(dst, da + (uint64_t)(k * 128), db + (uint64_t)(k * 128), idesc, accumulate);
+              accumulate = 1;
+            }
+            mma_commit(&a_empty[as]);
+            mma_commit(&b_empty[bs]);
+            ++ra.i;
+            ++rb.i;
+          }
+        }
+        if (accumulate) mma_commit(&tfull[acc]);
+        else mbar_arrive(&tfull[acc]);
       }
-      if (nkb > 0) mma_commit(tfull);
-      else mbar_arrive(tfull);
     }
     __syncwarp();
   } else {
-    // epilogue: TMEM lane quarter = warp % 4
+    // epilogue warps: TMEM lane quarter = warp % 4
     const int q = warp & 3;
     const int r = q * 32 + lane;
-    mbar_wait(tfull, 0);
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    bool ok;
-    int64_t off;
-    if (p.mode == MODE_ROWS) {
-      const int64_t flat = (int64_t)mt * BM + r;
-      const int64_t wp = flat % p.Wp;
-      const int64_t t = flat / p.Wp;
-      const int64_t hp = t % p.Hp;
-      const int64_t img = t / p.Hp;
-      const int64_t h = hp - p.lo_h, w = wp - p.lo_w;
-      ok = img < p.n_img && h >= 0 && h < p.H && w >= 0 && w < p.W;
-      off = p.g_out_off[g] + img * p.o_img + h * p.o_h + w * p.o_w;
-    } else {
-      const int64_t row = (int64_t)mt * BM + r;
-      ok = row < p.m_ext;
-      off = p.g_out_off[g] + row * p.o_m;
-    }
+    uint32_t tcount = 0;
+    for (int t = blockIdx.x; t < n_tiles_total; t += gridDim.x, ++tcount) {
+      const TileInfo ti = tile_info(p, t);
+      const uint32_t acc = tcount & 1u;
+      mbar_wait(&tfull[acc], (tcount >> 1) & 1u);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      bool ok;
+      int64_t off;
+      if (p.mode == MODE_ROWS) {
+        const int64_t flat = (int64_t)ti.mt * BM + r;
+        const int64_t wp = flat % p.Wp;
+        const int64_t tq = flat / p.Wp;
+        const int64_t hp = tq % p.Hp;
+        const int64_t img = tq / p.Hp;
+        const int64_t h = hp - p.lo_h, w = wp - p.lo_w;
+        ok = img < p.n_img && h >= 0 && h < p.H && w >= 0 && w < p.W;
+        off = p.g_out_off[ti.g] + img * p.o_img + h * p.o_h + w * p.o_w;
+      } else {
+        const int pr = ti.mt * 2 + (r >> 6);
+        const int ci = pr < p.n_pairs ? p.pair_cb[pr] * 64 + (r & 63) : p.m_ext;
+        ok = pr < p.n_pairs && ci < p.m_ext;
+        off = ok ? p.g_out_off[p.pair_win[pr]] + (int64_t)ci * p.o_m : 0;
+      }
+      const bool have = ti.nkb > 0;
 #pragma unroll 1
-    for (int c = 0; c < BN; c += 32) {
-      float v[32];
-      tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)c, v);
-      if (ok && nkb > 0) {
+      for (int c = 0; c < BN; c += 32) {
+        const int n0 = ti.nt * BN + c;
+        if (n0 >= p.n_ext) break;  // warp-uniform
+        float v[32];
+        tmem_ld32(tmem + acc * ACC_COLS + ((uint32_t)(q * 32) << 16) + (uint32_t)c, v);
+        const int nlim = min(32, p.n_ext - n0);
+        if (!ok || (!have && p.out_kind == OUT_F32_ATOMIC)) {
+          // nothing to store for this row
+        } else if (p.out_kind == OUT_BF16) {
+          __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(p.out) + off + (int64_t)n0 * p.o_n;
 #pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          const int n = nt * BN + c + j;
-          if (n < p.n_ext) {
-            const int64_t o = off + (int64_t)n * p.o_n;
-            const float val = v[j] * p.scale;
-            if (p.out_kind == OUT_BF16) reinterpret_cast<__nv_bfloat16*>(p.out)[o] = __float2bfloat16(val);
-            else if (p.out_kind == OUT_F32) reinterpret_cast<float*>(p.out)[o] = val;
-            else atomicAdd(reinterpret_cast<float*>(p.out) + o, val);
-          }
-        }
-      } else if (ok && p.out_kind != OUT_F32_ATOMIC) {
-        for (int j = 0; j < 32; ++j) {
-          const int n = nt * BN + c + j;
-          if (n < p.n_ext) {
-            const int64_t o = off + (int64_t)n * p.o_n;
-            if (p.out_kind == OUT_BF16) reinterpret_cast<__nv_bfloat16*>(p.out)[o] = __float2bfloat16(0.f);
-            else reinterpret_cast<float*>(p.out)[o] = 0.f;
-          }
+          for (int j = 0; j < 32; ++j)
+            if (j < nlim) o[(int64_t)j * p.o_n] = __float2bfloat16(have ? v[j] * p.scale : 0.f);
+        } else if (p.out_kind == OUT_F32) {
+          float* o = reinterpret_cast<float*>(p.out) + off + (int64_t)n0 * p.o_n;
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            if (j < nlim) o[(int64_t)j * p.o_n] = have ? v[j] * p.scale : 0.f;
+        } else {
+          float* o = reinterpret_cast<float*>(p.out) + off + (int64_t)n0 * p.o_n;
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            if (j < nlim) atomicAdd(o + (int64_t)j * p.o_n, v[j] * p.scale);
         }
       }
+      // release the accumulator buffer to the MMA warp (one arrive per warp)
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -324,7 +463,7 @@ __global__ void __launch_bounds__(THREADS, 1) tc_gemm_kernel(const __grid_consta
 
 template <int BN>
 constexpr int smem_bytes() {
-  return 1024 + STAGES * (BM * BK * 2 + BN * BK * 2) + 256;
+  return 1024 + RING_BYTES + 512;
 }
 
 }  // namespace tc
