@@ -8,7 +8,7 @@ OBJ := build/obj
 HOST_SRCS := symbolic graph nest plan capi
 CUDA_SRCS := engine tc
 OBJS := $(addprefix $(OBJ)/,$(addsuffix .o,$(HOST_SRCS) $(CUDA_SRCS)))
-HDRS := $(wildcard $(SRC)/*.hpp) include/syno.h
+HDRS := $(wildcard $(SRC)/*.hpp) $(wildcard $(SRC)/*.cuh) include/syno.h
 
 all: $(PKG)/libsyno.so
 

@@ -422,7 +422,34 @@ static void launch_gemm(const TcGemmParams& p, unsigned grid, cudaStream_t strea
     configured.fetch_or(bit);
   }
   note_launch();
-  tc_gemm_kernel<BN><<<grid, THREADS, smem, stream>>>(p);
+  static unsigned long long* trace_buf = nullptr;
+  const bool want_trace = getenv("SYNO_TC_TRACE") != nullptr;
+  if (want_trace && !trace_buf) cuda_check(cudaMalloc(&trace_buf, 64 * sizeof(unsigned long long)), "trace");
+  if (!want_trace) {
+    tc_gemm_kernel<BN><<<grid, THREADS, smem, stream>>>(p);
+  } else {
+    TcGemmParams q = p;
+    q.trace = trace_buf;
+    cuda_check(cudaMemsetAsync(trace_buf, 0, 64 * sizeof(unsigned long long), stream), "trace memset");
+    tc_gemm_kernel<BN><<<grid, THREADS, smem, stream>>>(q);
+    unsigned long long h[64];
+    cuda_check(cudaMemcpyAsync(h, trace_buf, sizeof(h), cudaMemcpyDeviceToHost, stream), "trace copy");
+    cuda_check(cudaStreamSynchronize(stream), "trace sync");
+    fprintf(stderr, "[tc trace BN=%d mode=%d tiles=%d grid=%u] setup %.2f us |", BN, p.mode,
+            p.m_tiles * p.n_tiles * p.z_tiles, grid, (h[1] - h[0]) / 1e3);
+    for (int i = 0; i < 14 && h[2 + i * 4]; ++i)
+      fprintf(stderr, " t%d: prod %.2f mma %.2f epi %.2f-%.2f |", i, (h[2 + i * 4] - h[0]) / 1e3,
+              h[3 + i * 4] ? (h[3 + i * 4] - h[0]) / 1e3 : -1.0, h[4 + i * 4] ? (h[4 + i * 4] - h[0]) / 1e3 : -1.0,
+              h[5 + i * 4] ? (h[5 + i * 4] - h[0]) / 1e3 : -1.0);
+    fprintf(stderr, "\n   tile0 windows: b_full seen at");
+    for (int i = 40; i < 49; ++i) fprintf(stderr, " %.2f", h[i] ? (h[i] - h[0]) / 1e3 : -1.0);
+    fprintf(stderr, "\n   tile0 windows: b_empty free at");
+    for (int i = 50; i < 59; ++i) fprintf(stderr, " %.2f", h[i] ? (h[i] - h[0]) / 1e3 : -1.0);
+    fprintf(stderr, "\n   tile1 windows 1-4 cycles (wait, issue, commit):");
+    for (int i = 59; i < 63; ++i)
+      fprintf(stderr, " (%llu, %llu, %llu)", h[i] & 0xFFFFF, (h[i] >> 20) & 0xFFFFF, (h[i] >> 40) & 0xFFFFF);
+    fprintf(stderr, "\n");
+  }
   cuda_check(cudaGetLastError(), "tc_gemm_kernel");
 }
 
@@ -447,6 +474,8 @@ static void gemm(TcGemmParams& p, int bn, int m_tiles, int n_tiles, int z_tiles,
   else if (bn == 128) launch_gemm<128>(p, grid, stream);
   else launch_gemm<256>(p, grid, stream);
 }
+
+static int mgroup_of(int bn) { return bn == 64 ? mgroup<64>() : bn == 128 ? mgroup<128>() : mgroup<256>(); }
 
 static int pick_bn(int n) { return n <= 64 ? 64 : n <= 128 ? 128 : 256; }
 
@@ -538,11 +567,13 @@ static void rows_schedule(TcGemmParams& p, std::vector<std::vector<Win>> groups,
     p.g_chunk1[g] = nc;
   }
   p.n_win = n;
-  p.a_rows = BM + span;
+  const int G = bn >= 256 ? 1 : 256 / bn;  // tc::mgroup<BN>()
+  p.a_rows = (G * BM + span + 63) / 64 * 64;
   p.a_tx = (uint32_t)p.a_rows * BK * 2;
-  p.a_stage_bytes = (int)((p.a_tx + 1023) / 1024 * 1024);
+  p.a_stage_bytes = (int)p.a_tx;
   p.b_tx = (uint32_t)bn * BK * 2;
   p.base_mode = base_mode();
+  p.dbg = getenv("SYNO_TC_DEBUG") ? atoi(getenv("SYNO_TC_DEBUG")) : 0;
 }
 
 // Per (device, stream) workspace of an operator: packed operands, folded
@@ -604,7 +635,7 @@ static void build_ws(TcPlan& tp, TcWs& w) {
         groups[0].push_back({tp.dh.delta(rh) * w.gx.Wp + tp.dw.delta(rw), tp.dh.phi(rh) * w.gx.Sw + tp.dw.phi(rw),
                              rh * tp.dw.K + rw});
     rows_schedule(p, groups, bn);
-    p.tma_a = make_map(w.xcl, tp.Cp, F, planes, tp.Cp, F * tp.Cp, p.a_rows);
+    p.tma_a = make_map(w.xcl, tp.Cp, F, planes, tp.Cp, F * tp.Cp, 64);
     p.tma_b = make_map(w.wf, tp.Cp, tp.N, tp.nwin(), tp.Cp, (int64_t)tp.N * tp.Cp, bn);
     p.Hp = w.gx.Hp;
     p.Wp = w.gx.Wp;
@@ -621,7 +652,7 @@ static void build_ws(TcPlan& tp, TcWs& w) {
     p.out_kind = OUT_BF16;
     p.scale = (float)tp.scale;
     w.bn_fwd = bn;
-    w.t_fwd[0] = (int)((F + BM - 1) / BM);
+    w.t_fwd[0] = (int)((F + (int64_t)mgroup_of(bn) * BM - 1) / ((int64_t)mgroup_of(bn) * BM));
     w.t_fwd[1] = (tp.N + bn - 1) / bn;
     w.t_fwd[2] = 1;
   }
@@ -658,7 +689,7 @@ static void build_ws(TcPlan& tp, TcWs& w) {
         p.g_out_off[grp] = ph * tp.dh.xs + pw * tp.dw.xs;
       }
     rows_schedule(p, groups, bn);
-    p.tma_a = make_map(w.dycl_g, tp.Np, Fg, 1, tp.Np, Fg * tp.Np, p.a_rows);
+    p.tma_a = make_map(w.dycl_g, tp.Np, Fg, 1, tp.Np, Fg * tp.Np, 64);
     p.tma_b = make_map(w.wt, tp.Np, tp.C, tp.nwin(), tp.Np, (int64_t)tp.C * tp.Np, bn);
     p.Hp = w.gdy_g.Hp;
     p.Wp = w.gdy_g.Wp;
@@ -675,7 +706,7 @@ static void build_ws(TcPlan& tp, TcWs& w) {
     p.out_kind = OUT_BF16;
     p.scale = (float)tp.scale;
     w.bn_dg = bn;
-    w.t_dg[0] = (int)((Fg + BM - 1) / BM);
+    w.t_dg[0] = (int)((Fg + (int64_t)mgroup_of(bn) * BM - 1) / ((int64_t)mgroup_of(bn) * BM));
     w.t_dg[1] = (tp.C + bn - 1) / bn;
     w.t_dg[2] = Sh * Sw;
   }

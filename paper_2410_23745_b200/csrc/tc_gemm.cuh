@@ -12,8 +12,9 @@
 // address + base offset), so A crosses L2 once instead of once per window.
 //
 // Persistent: a CTA walks tiles t = blockIdx.x, +gridDim.x, ...  Warp roles
-// (192 threads): warp 0 = TMA producer, warp 1 = TMEM owner + MMA issuer
-// (one lane), warps 2..5 = epilogue (TMEM lane quarter = warp % 4).  The
+// (320 threads): warp 0 = TMA producer, warp 1 = TMEM owner + MMA issuer
+// (one lane), warps 2..9 = epilogue (TMEM lane quarter = warp % 4; the two
+// warps of a quarter take alternate 32-column chunks).  The
 // accumulator is double-buffered in TMEM so the epilogue of tile i overlaps
 // the main loop of tile i+1.
 #pragma once
@@ -29,19 +30,25 @@ constexpr int BM = 128;
 constexpr int BK = 64;                 // one 128-byte swizzle row of bf16
 constexpr int MAXWIN = 64;
 constexpr int MAXCHUNK = 32;
-constexpr int THREADS = 192;
-constexpr int EPI_WARPS = 4;
+constexpr int EPI_WARPS = 8;  // two per TMEM lane quarter, splitting the column chunks
+constexpr int THREADS = 64 + 32 * EPI_WARPS;
 constexpr int RING_BYTES = 192 * 1024;  // A ring (halo / dy tiles) + B ring
 
-// Narrow N tiles need few B bytes per k-step: give the A (halo) ring the room
-// so several tiles' A loads are in flight (the pipeline is TMA-latency bound).
+// MODE_ROWS processes G = 256/BN consecutive 128-row M tiles per step: one
+// contiguous A halo and one B tile per window feed G accumulators, cutting
+// the operand traffic per output row by ~G (B is the small weight tile that
+// every M tile needs).  Four B stages; the rest of the ring is A.
 template <int BN>
-__host__ __device__ constexpr int a_region_bytes() {
-  return BN <= 64 ? 128 * 1024 : BN <= 128 ? 96 * 1024 : 64 * 1024;
+__host__ __device__ constexpr int mgroup() {
+  return BN >= 256 ? 1 : 256 / BN;
 }
 template <int BN>
 __host__ __device__ constexpr int b_stages() {
-  return (RING_BYTES - a_region_bytes<BN>()) / (BN * BK * 2);
+  return 4;
+}
+template <int BN>
+__host__ __device__ constexpr int a_region_bytes() {
+  return RING_BYTES - b_stages<BN>() * BN * BK * 2;
 }
 
 enum Mode : int32_t {
@@ -74,11 +81,13 @@ struct alignas(64) TcGemmParams {
   int32_t n_pairs;
   int16_t pair_win[MAXPAIR], pair_cb[MAXPAIR];
   int64_t g_out_off[MAXWIN];
-  int32_t a_rows;       // rows of one A TMA box (halo rows in MODE_ROWS)
+  int32_t a_rows;       // MODE_ROWS: halo rows per A stage (G*128 + span, multiple of 64)
   int32_t a_stage_bytes;  // smem slot of one A stage (multiple of 1024)
   int32_t a_stages;
   uint32_t a_tx, b_tx;  // transaction bytes of one A / B stage
   int32_t base_mode;    // 1: set the descriptor base offset for row-shifted A views
+  int32_t dbg;          // profiling switches: 1 = skip epilogue stores, 2 = skip MMAs, 4/8 = skip A/B loads
+  unsigned long long* trace;  // profiling: %globaltimer stamps of CTA 0 (null = off)
   // tile grid: t -> (nt fastest, then mt, then z)
   int32_t m_tiles, n_tiles, z_tiles;
   // epilogue: row index r of the M tile -> output coordinates
@@ -110,6 +119,7 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 }
 
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+#ifdef SYNO_MBAR_SUSPEND
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
       "WAIT_%=:\n\t"
@@ -117,6 +127,17 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
       "r"(parity), "r"(0x989680)
       : "memory");
+#else
+  // spin on the non-suspending probe: the wait is on the critical path of
+  // the producer -> MMA -> epilogue hand-offs
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+#endif
 }
 
 __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
@@ -165,17 +186,35 @@ __host__ __device__ constexpr uint32_t idesc_bf16(int m, int n, int a_mn = 0, in
          | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(m >> 4) << 24);
 }
 
+// Issued by the whole (converged) warp with warp-uniform operands; one
+// elected lane executes the tcgen05 instruction.  Keeping the loop and the
+// operand math warp-wide lets ptxas hold descriptors in uniform registers
+// instead of wrapping every issue in an R2UR/ELECT waterfall loop.
 __device__ __forceinline__ void mma_bf16(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
   asm volatile(
-      "{\n\t.reg .pred p;\n\t"
+      "{\n\t.reg .pred p, e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
       "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
       "l"(a), "l"(b), "r"(idesc), "r"(acc));
 }
 
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
-               : "memory");
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ bool elect_one() {
+  uint32_t e;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "elect.sync _|p, 0xffffffff;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(e));
+  return e != 0;
 }
 
 __device__ __forceinline__ void tmem_ld32(uint32_t addr, float* v) {
@@ -232,8 +271,9 @@ template <int BN>
 __global__ void __launch_bounds__(THREADS, 1) tc_gemm_kernel(const __grid_constant__ TcGemmParams p) {
   constexpr int BSTAGES = b_stages<BN>();
   constexpr int B_BYTES = BN * BK * 2;
-  constexpr uint32_t ACC_COLS = BN < 32 ? 32 : BN;
-  constexpr uint32_t TMEM_COLS = 2 * ACC_COLS;  // two accumulator buffers (<= 512)
+  constexpr int G = mgroup<BN>();
+  constexpr uint32_t ACC_COLS = G * BN;          // one accumulator buffer: G sub-tiles
+  constexpr uint32_t TMEM_COLS = 2 * ACC_COLS;   // double-buffered (= 512)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sa = smem;
@@ -276,38 +316,73 @@ __global__ void __launch_bounds__(THREADS, 1) tc_gemm_kernel(const __grid_consta
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
+  const bool tr = p.trace != nullptr && blockIdx.x == 0;
+  auto stamp = [&](int i) {
+    if (tr && i < 64) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      p.trace[i] = t;
+    }
+  };
+  if (threadIdx.x == 0) stamp(0);
 
   if (warp == 0) {
-    if (lane == 0) {
+    // ---------------- TMA producer: the whole warp walks the schedule, one
+    // elected lane issues (operands stay warp-uniform).
+    if (elect_one()) {
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&p.tma_a)) : "memory");
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&p.tma_b)) : "memory");
-      Ring ra, rb;
-      for (int t = blockIdx.x; t < n_tiles_total; t += gridDim.x) {
-        const TileInfo ti = tile_info(p, t);
-        if (p.mode == MODE_ROWS) {
-          for (int c = p.g_chunk0[ti.g]; c < p.g_chunk1[ti.g]; ++c) {
-            for (int cb = 0; cb < p.n_cblocks; ++cb) {
-              // one halo tile of A for this plane and channel block
-              const int as = ra.slot(AST);
-              mbar_wait(&a_empty[as], ra.phase(AST) ^ 1u);
-              mbar_expect_tx(&a_full[as], p.a_tx);
-              tma_load_3d(sa + as * p.a_stage_bytes, &p.tma_a, &a_full[as], cb * BK,
-                          ti.mt * BM + p.chunk_pmin[c], p.chunk_plane[c]);
-              ++ra.i;
-              for (int w = p.chunk_w0[c]; w < p.chunk_w1[c]; ++w) {
-                const int bs = rb.slot(BSTAGES);
-                mbar_wait(&b_empty[bs], rb.phase(BSTAGES) ^ 1u);
-                mbar_expect_tx(&b_full[bs], p.b_tx);
-                tma_load_3d(sb + bs * B_BYTES, &p.tma_b, &b_full[bs], cb * BK, ti.nt * BN, p.b_plane[w]);
-                ++rb.i;
-              }
-            }
-          }
-        } else {
-          for (int i = 0; i < ti.nkb; ++i) {
-            const int kb = ti.kb0 + i;
+    }
+    __syncwarp();
+    Ring ra, rb;
+    if (lane == 0) stamp(1);
+    uint32_t pcount = 0;
+    for (int t = blockIdx.x; t < n_tiles_total; t += gridDim.x, ++pcount) {
+      const TileInfo ti = tile_info(p, t);
+      if (lane == 0 && pcount < 14) stamp(2 + pcount * 4);
+      if (p.mode == MODE_ROWS) {
+        for (int c = p.g_chunk0[ti.g]; c < p.g_chunk1[ti.g]; ++c) {
+          for (int cb = 0; cb < p.n_cblocks; ++cb) {
+            // one halo tile of A for this plane and channel block
             const int as = ra.slot(AST);
             mbar_wait(&a_empty[as], ra.phase(AST) ^ 1u);
+            const int row0 = ti.mt * G * BM + p.chunk_pmin[c];
+            const int nbox = p.a_rows / 64;
+            if (elect_one()) {
+              if (p.dbg & 4) {
+                mbar_arrive(&a_full[as]);
+              } else {
+                mbar_expect_tx(&a_full[as], p.a_tx);
+                for (int j = 0; j < nbox; ++j)
+                  tma_load_3d(sa + as * p.a_stage_bytes + j * 8192, &p.tma_a, &a_full[as], cb * BK, row0 + 64 * j,
+                              p.chunk_plane[c]);
+              }
+            }
+            __syncwarp();
+            ++ra.i;
+            for (int w = p.chunk_w0[c]; w < p.chunk_w1[c]; ++w) {
+              const int bs = rb.slot(BSTAGES);
+              mbar_wait(&b_empty[bs], rb.phase(BSTAGES) ^ 1u);
+              if (lane == 0 && pcount == 0 && w < 9) stamp(50 + w);
+              if (elect_one()) {
+                if (p.dbg & 8) {
+                  mbar_arrive(&b_full[bs]);
+                } else {
+                  mbar_expect_tx(&b_full[bs], p.b_tx);
+                  tma_load_3d(sb + bs * B_BYTES, &p.tma_b, &b_full[bs], cb * BK, ti.nt * BN, p.b_plane[w]);
+                }
+              }
+              __syncwarp();
+              ++rb.i;
+            }
+          }
+        }
+      } else {
+        for (int i = 0; i < ti.nkb; ++i) {
+          const int kb = ti.kb0 + i;
+          const int as = ra.slot(AST);
+          mbar_wait(&a_empty[as], ra.phase(AST) ^ 1u);
+          if (elect_one()) {
             mbar_expect_tx(&a_full[as], p.a_tx);
 #pragma unroll
             for (int h = 0; h < BM / 64; ++h) {
@@ -317,139 +392,178 @@ __global__ void __launch_bounds__(THREADS, 1) tc_gemm_kernel(const __grid_consta
               tma_load_3d(sa + as * p.a_stage_bytes + h * 8192, &p.tma_a, &a_full[as], p.pair_cb[pr] * 64,
                           kb * BK + p.a_shift[w], p.a_plane[w]);
             }
-            ++ra.i;
-            const int bs = rb.slot(BSTAGES);
-            mbar_wait(&b_empty[bs], rb.phase(BSTAGES) ^ 1u);
+          }
+          __syncwarp();
+          ++ra.i;
+          const int bs = rb.slot(BSTAGES);
+          mbar_wait(&b_empty[bs], rb.phase(BSTAGES) ^ 1u);
+          if (elect_one()) {
             mbar_expect_tx(&b_full[bs], p.b_tx);
 #pragma unroll
             for (int h = 0; h < BN / 64; ++h)
               tma_load_3d(sb + bs * B_BYTES + h * 8192, &p.tma_b, &b_full[bs], ti.nt * BN + h * 64, kb * BK, 0);
-            ++rb.i;
           }
+          __syncwarp();
+          ++rb.i;
         }
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      const bool mn = p.mode == MODE_WGRAD;
-      const uint32_t idesc = mn ? idesc_bf16(BM, BN, 1, 1) : idesc_bf16(BM, BN);
-      Ring ra, rb;
-      uint32_t tcount = 0;
-      for (int t = blockIdx.x; t < n_tiles_total; t += gridDim.x, ++tcount) {
-        const TileInfo ti = tile_info(p, t);
-        const uint32_t acc = tcount & 1u;
-        mbar_wait(&tempty[acc], ((tcount >> 1) & 1u) ^ 1u);  // epilogue drained this buffer
-        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const uint32_t dst = tmem + acc * ACC_COLS;
-        uint32_t accumulate = 0;
-        if (!mn) {
-          for (int c = p.g_chunk0[ti.g]; c < p.g_chunk1[ti.g]; ++c) {
-            for (int cb = 0; cb < p.n_cblocks; ++cb) {
-              const int as = ra.slot(AST);
-              mbar_wait(&a_full[as], ra.phase(AST));
-              const uint8_t* abase = sa + as * p.a_stage_bytes;
-              for (int w = p.chunk_w0[c]; w < p.chunk_w1[c]; ++w) {
-                const int bs = rb.slot(BSTAGES);
-                mbar_wait(&b_full[bs], rb.phase(BSTAGES));
-                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-                const uint64_t db = sw128_desc(sb + bs * B_BYTES);
-                const int row = p.a_shift[w] - p.chunk_pmin[c];
-#pragma unroll
-                for (int k = 0; k < BK / 16; ++k) {
-                  // K advance: 32 B inside the swizzled 128 B row
-                  const uint64_t da = sw128_desc(abase + k * 32, row, p.base_mode);
-                  mma_bf16(dst, da, db + (uint64_t)(k * 2), idesc, accumulate);
-                  accumulate = 1;
-                }
-                mma_commit(&b_empty[bs]);
-                ++rb.i;
-              }
-              mma_commit(&a_empty[as]);  // halo tile free once its windows' MMAs finish
-              ++ra.i;
-            }
-          }
-        } else {
-          for (int i = 0; i < ti.nkb; ++i) {
-            const int as = ra.slot(AST), bs = rb.slot(BSTAGES);
+    // ---------------- MMA issuer: warp-wide loop, elected-lane issue
+    const bool mn = p.mode == MODE_WGRAD;
+    const uint32_t idesc = mn ? idesc_bf16(BM, BN, 1, 1) : idesc_bf16(BM, BN);
+    Ring ra, rb;
+    uint32_t tcount = 0;
+    for (int t = blockIdx.x; t < n_tiles_total; t += gridDim.x, ++tcount) {
+      const TileInfo ti = tile_info(p, t);
+      const uint32_t acc = tcount & 1u;
+      mbar_wait(&tempty[acc], ((tcount >> 1) & 1u) ^ 1u);  // epilogue drained this buffer
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const uint32_t dst = tmem + acc * ACC_COLS;
+      uint32_t accumulate = 0;
+      if (!mn) {
+        for (int c = p.g_chunk0[ti.g]; c < p.g_chunk1[ti.g]; ++c) {
+          for (int cb = 0; cb < p.n_cblocks; ++cb) {
+            const int as = ra.slot(AST);
             mbar_wait(&a_full[as], ra.phase(AST));
-            mbar_wait(&b_full[bs], rb.phase(BSTAGES));
-            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-            const uint64_t da = sw128_mn_desc(sa + as * p.a_stage_bytes, 8192);
-            const uint64_t db = sw128_mn_desc(sb + bs * B_BYTES, 8192);
+            const uint32_t abase = smem_u32(sa + as * p.a_stage_bytes);
+            for (int w = p.chunk_w0[c]; w < p.chunk_w1[c]; ++w) {
+              const int bs = rb.slot(BSTAGES);
+              mbar_wait(&b_full[bs], rb.phase(BSTAGES));
+              if (lane == 0 && tcount == 0 && w < 9) stamp(40 + w);
+              asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+              const uint64_t db = sw128_desc(sb + bs * B_BYTES);
+              const uint32_t arow = abase + (uint32_t)(p.a_shift[w] - p.chunk_pmin[c]) * 128u;
+              if (!(p.dbg & 2)) {
 #pragma unroll
-            for (int k = 0; k < BK / 16; ++k) {
-              // MN-major K advance: two 8-row k groups (2 x 1024 B)
-              mma_bf16(dst, da + (uint64_t)(k * 128), db + (uint64_t)(k * 128), idesc, accumulate);
+                for (int g = 0; g < G; ++g) {
+                  // start = halo + (g*128 + shift) rows; K advance: 32 B inside the swizzled row
+                  const uint64_t da = (((uint64_t)((arow + g * BM * 128u) >> 4)) & 0x3FFF) | (1ull << 16) |
+                                      ((uint64_t)(1024 >> 4) << 32) | (1ull << 46) | (2ull << 61);
+#pragma unroll
+                  for (int k = 0; k < BK / 16; ++k)
+                    mma_bf16(dst + g * BN, da + (uint64_t)(k * 2), db + (uint64_t)(k * 2), idesc,
+                             (accumulate || k > 0) ? 1u : 0u);
+                }
+              }
               accumulate = 1;
+              if (p.dbg & 16) {
+                if (elect_one()) mbar_arrive(&b_empty[bs]);  // profiling only: no MMA reads B
+                __syncwarp();
+              } else {
+                mma_commit(&b_empty[bs]);
+              }
+              ++rb.i;
             }
-            mma_commit(&a_empty[as]);
-            mma_commit(&b_empty[bs]);
+            mma_commit(&a_empty[as]);  // halo tile free once its windows' MMAs finish
             ++ra.i;
-            ++rb.i;
           }
         }
-        if (accumulate) mma_commit(&tfull[acc]);
-        else mbar_arrive(&tfull[acc]);
+      } else {
+        for (int i = 0; i < ti.nkb; ++i) {
+          const int as = ra.slot(AST), bs = rb.slot(BSTAGES);
+          mbar_wait(&a_full[as], ra.phase(AST));
+          mbar_wait(&b_full[bs], rb.phase(BSTAGES));
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint64_t da = sw128_mn_desc(sa + as * p.a_stage_bytes, 8192);
+          const uint64_t db = sw128_mn_desc(sb + bs * B_BYTES, 8192);
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) {
+            // MN-major K advance: two 8-row k groups (2 x 1024 B)
+            mma_bf16(dst, da + (uint64_t)(k * 128), db + (uint64_t)(k * 128), idesc, accumulate);
+            accumulate = 1;
+          }
+          mma_commit(&a_empty[as]);
+          mma_commit(&b_empty[bs]);
+          ++ra.i;
+          ++rb.i;
+        }
+      }
+      if (lane == 0 && tcount < 14) stamp(2 + tcount * 4 + 1);
+      if (accumulate) {
+        mma_commit(&tfull[acc]);
+      } else {
+        if (elect_one()) mbar_arrive(&tfull[acc]);
+        __syncwarp();
       }
     }
-    __syncwarp();
   } else {
-    // epilogue warps: TMEM lane quarter = warp % 4
+    // epilogue warps: TMEM lane quarter = warp % 4, column-chunk parity = (warp - 2) / 4
     const int q = warp & 3;
+    const int half = (warp - 2) >> 2;
     const int r = q * 32 + lane;
     uint32_t tcount = 0;
     for (int t = blockIdx.x; t < n_tiles_total; t += gridDim.x, ++tcount) {
       const TileInfo ti = tile_info(p, t);
       const uint32_t acc = tcount & 1u;
       mbar_wait(&tfull[acc], (tcount >> 1) & 1u);
+      if (warp == 2 && lane == 0 && tcount < 14) stamp(2 + tcount * 4 + 2);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      bool ok;
-      int64_t off;
-      if (p.mode == MODE_ROWS) {
-        const int64_t flat = (int64_t)ti.mt * BM + r;
-        const int64_t wp = flat % p.Wp;
-        const int64_t tq = flat / p.Wp;
-        const int64_t hp = tq % p.Hp;
-        const int64_t img = tq / p.Hp;
-        const int64_t h = hp - p.lo_h, w = wp - p.lo_w;
-        ok = img < p.n_img && h >= 0 && h < p.H && w >= 0 && w < p.W;
-        off = p.g_out_off[ti.g] + img * p.o_img + h * p.o_h + w * p.o_w;
-      } else {
-        const int pr = ti.mt * 2 + (r >> 6);
-        const int ci = pr < p.n_pairs ? p.pair_cb[pr] * 64 + (r & 63) : p.m_ext;
-        ok = pr < p.n_pairs && ci < p.m_ext;
-        off = ok ? p.g_out_off[p.pair_win[pr]] + (int64_t)ci * p.o_m : 0;
-      }
+      const int nsub = p.mode == MODE_ROWS ? G : 1;
       const bool have = ti.nkb > 0;
+      const float scale = p.scale;
 #pragma unroll 1
-      for (int c = 0; c < BN; c += 32) {
-        const int n0 = ti.nt * BN + c;
-        if (n0 >= p.n_ext) break;  // warp-uniform
-        float v[32];
-        tmem_ld32(tmem + acc * ACC_COLS + ((uint32_t)(q * 32) << 16) + (uint32_t)c, v);
-        const int nlim = min(32, p.n_ext - n0);
-        if (!ok || (!have && p.out_kind == OUT_F32_ATOMIC)) {
-          // nothing to store for this row
-        } else if (p.out_kind == OUT_BF16) {
-          __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(p.out) + off + (int64_t)n0 * p.o_n;
-#pragma unroll
-          for (int j = 0; j < 32; ++j)
-            if (j < nlim) o[(int64_t)j * p.o_n] = __float2bfloat16(have ? v[j] * p.scale : 0.f);
-        } else if (p.out_kind == OUT_F32) {
-          float* o = reinterpret_cast<float*>(p.out) + off + (int64_t)n0 * p.o_n;
-#pragma unroll
-          for (int j = 0; j < 32; ++j)
-            if (j < nlim) o[(int64_t)j * p.o_n] = have ? v[j] * p.scale : 0.f;
+      for (int g = 0; g < nsub; ++g) {
+        bool ok;
+        int64_t off;
+        if (p.mode == MODE_ROWS) {
+          const int64_t flat = ((int64_t)ti.mt * G + g) * BM + r;
+          const int64_t wp = flat % p.Wp;
+          const int64_t tq = flat / p.Wp;
+          const int64_t hp = tq % p.Hp;
+          const int64_t img = tq / p.Hp;
+          const int64_t h = hp - p.lo_h, w = wp - p.lo_w;
+          ok = img < p.n_img && h >= 0 && h < p.H && w >= 0 && w < p.W;
+          off = p.g_out_off[ti.g] + img * p.o_img + h * p.o_h + w * p.o_w;
         } else {
-          float* o = reinterpret_cast<float*>(p.out) + off + (int64_t)n0 * p.o_n;
-#pragma unroll
-          for (int j = 0; j < 32; ++j)
-            if (j < nlim) atomicAdd(o + (int64_t)j * p.o_n, v[j] * p.scale);
+          const int pr = ti.mt * 2 + (r >> 6);
+          const int ci = pr < p.n_pairs ? p.pair_cb[pr] * 64 + (r & 63) : p.m_ext;
+          ok = pr < p.n_pairs && ci < p.m_ext;
+          off = ok ? p.g_out_off[p.pair_win[pr]] + (int64_t)ci * p.o_m : 0;
         }
-      }
+        if (!have && p.out_kind == OUT_F32_ATOMIC) ok = false;
+#pragma unroll 1
+        for (int c = half * 32; c < BN; c += 64) {
+          const int n0 = ti.nt * BN + c;
+          if (n0 >= p.n_ext) break;  // warp-uniform
+          float v[32];
+          tmem_ld32(tmem + acc * ACC_COLS + (uint32_t)(g * BN) + ((uint32_t)(q * 32) << 16) + (uint32_t)c, v);
+          const int nlim = min(32, p.n_ext - n0);
+          const int64_t os = p.o_n;
+          if (!ok || (p.dbg & 1)) {
+            // masked row (pad pixel / beyond the extent): nothing to store
+          } else if (p.out_kind == OUT_BF16) {
+            __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(p.out) + off + (int64_t)n0 * os;
+            if (nlim == 32) {
+#pragma unroll
+              for (int j = 0; j < 32; ++j) {
+                *o = __float2bfloat16_rn(have ? v[j] * scale : 0.f);
+                o += os;
+              }
+            } else {
+              for (int j = 0; j < nlim; ++j) o[(int64_t)j * os] = __float2bfloat16_rn(have ? v[j] * scale : 0.f);
+            }
+          } else if (p.out_kind == OUT_F32) {
+            float* o = reinterpret_cast<float*>(p.out) + off + (int64_t)n0 * os;
+            for (int j = 0; j < nlim; ++j) o[(int64_t)j * os] = have ? v[j] * scale : 0.f;
+          } else {
+            float* o = reinterpret_cast<float*>(p.out) + off + (int64_t)n0 * os;
+            if (nlim == 32) {
+#pragma unroll
+              for (int j = 0; j < 32; ++j) {
+                atomicAdd(o, v[j] * scale);
+                o += os;
+              }
+            } else {
+              for (int j = 0; j < nlim; ++j) atomicAdd(o + (int64_t)j * os, v[j] * scale);
+            }
+          }
+        }
+      }  // sub-tiles
       // release the accumulator buffer to the MMA warp (one arrive per warp)
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       __syncwarp();
+      if (warp == 2 && lane == 0 && tcount < 14) stamp(2 + tcount * 4 + 3);
       if (lane == 0) mbar_arrive(&tempty[acc]);
     }
   }
