@@ -1,18 +1,26 @@
-"""Benchmark: synthesized-operator fwd+bwd on B200 (BASELINE.json metric).
+"""Benchmark: synthesized-operator execution on B200 (BASELINE.json metric).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload resnet18|resnet34|cfg1|qkv|sweep]
-                    [--impl syno|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W]
+                    [--workload resnet18|resnet34|cfg1|qkv|sweep|qkv_train] [--impl syno|reference]
 
 Default workload = BASELINE configs[1]: the 20 conv layers of ResNet-18
 (CIFAR, 32x32) each replaced by a synthesized operator, forward + backward
-(grad-input and grad-weight) in bf16 at batch 128 per GPU.  A step runs
-every layer's forward and backward once on synthetic inputs resident in HBM.
-Multi-GPU (torchrun): every rank runs its own batch (weak scaling, no
-data-path collective: the layers' units are independent images).
+(grad-input and every grad-weight) in bf16 at batch 128 per GPU.  A step
+runs every layer's forward and backward once on synthetic inputs resident
+in HBM; the step is replayed as one CUDA graph.  Multi-GPU (torchrun):
+every rank runs its own batch (weak scaling; no data-path collective, the
+images are independent units).
 
---impl reference times the reference's CPU implementation of the same
-path (the pinned numpy restatement in oracle/, since the reference is pure
-Python and has no compiled artifact) on all host cores, rank 0 only.
+--workload sweep is configs[4]: search-time candidate evaluation of the
+1024-operator sampled corpus (compile + fwd + bwd + on-device adjoint
+check per candidate, fp32), LPT-sharded across ranks with no collective
+(strong scaling: the corpus is fixed).  --workload qkv_train is configs[3]:
+proxy training of 12 GPT-2-small QKV projections as synthesized operators
+with the NCCL gradient allreduce.
+
+--impl reference times the reference's CPU implementation of the same path
+on the host cores: the pinned numpy restatement in oracle/ (the reference
+is pure Python with no compiled artifact to build), rank 0 only.
 """
 from __future__ import annotations
 
@@ -30,6 +38,8 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 FALLBACK_PEAKS = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
+METRIC = "synthesized-operator fwd+bwd throughput (operator fwd+bwd latency & % roofline)"
+SWEEP_METRIC = "candidates evaluated/sec (compile + fwd + bwd + adjoint check)"
 
 
 def load_peaks():
@@ -37,10 +47,10 @@ def load_peaks():
     if os.path.exists(path):
         with open(path) as f:
             p = json.load(f)
-        p["source"] = "measured"
+        p["source"] = "measured (MEASURED_PEAKS.json)"
         return p
     p = dict(FALLBACK_PEAKS)
-    p["source"] = "fallback"
+    p["source"] = "fallback (B200_PROFILING.md)"
     return p
 
 
@@ -63,7 +73,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                 "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except OSError:
             self.proc = None
             return
@@ -89,8 +99,14 @@ class ClockSampler:
     def summary(self):
         if not self.rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+
+        def num(x):
+            try:
+                return float(x)
+            except ValueError:
+                return None
+        sm = [v for v in (num(r[0]) for r in self.rows) if v]
+        mx = [v for v in (num(r[1]) for r in self.rows) if v]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = set()
         for r in self.rows:
@@ -102,23 +118,76 @@ class ClockSampler:
                 "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons), "samples": len(self.rows)}
 
 
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def allreduce_max(v, world, device):
+    """Timing only (max over ranks): never on the data path."""
+    if world == 1:
+        return v
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([v], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def load_traffic():
+    path = os.path.join(ROOT, "profiles", "traffic.json")
+    if not os.path.exists(path):
+        return {}
+    with open(path) as f:
+        return json.load(f)
+
+
+def roofline_from_profile(prof, steps, step_ms, peaks):
+    """Dominant kernel class of the profiled steps and its roofline.
+
+    prof: {class: {launches, ms, flops, bytes}} from the library's
+    per-launch CUDA events (syno_profile_begin/end) over `steps` eager
+    steps.  The three tcgen05 GEMM roles are one kernel (tc_gemm_kernel)
+    and are pooled.  achieved = algorithmic FLOPs (or bytes) per launch
+    / average launch time."""
+    pooled = {}
+    for name, s in prof.items():
+        key = "tc_gemm" if name.startswith("tc_gemm") else name
+        d = pooled.setdefault(key, {"launches": 0, "ms": 0.0, "flops": 0.0, "bytes": 0.0})
+        for k in d:
+            d[k] += s[k]
+    if not pooled:
+        return None, {}
+    dom, s = max(pooled.items(), key=lambda kv: kv[1]["ms"])
+    per_launch_ms = s["ms"] / max(1, s["launches"])
+    tpeak = peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"])
+    if s["flops"] > 0 and dom == "tc_gemm":
+        achieved = s["flops"] / (s["ms"] / 1e3) / 1e12
+        roof = {"bound": "tensor", "achieved": achieved, "peak": tpeak, "unit": "TFLOP/s",
+                "frac": achieved / tpeak, "flops_per_launch": s["flops"] / s["launches"]}
+    else:
+        achieved = s["bytes"] / (s["ms"] / 1e3) / 1e9 if s["ms"] else 0.0
+        roof = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                "frac": achieved / peaks["hbm_gbs"], "bytes_per_launch": s["bytes"] / max(1, s["launches"])}
+    tr = load_traffic().get(dom)
+    roof.update({
+        "kernel": dom, "launches_per_step": s["launches"] / steps, "avg_launch_us": per_launch_ms * 1e3,
+        "share_of_step": (s["ms"] / steps) / step_ms if step_ms else None,
+        "traffic": tr.get("dram_bytes_per_launch") if isinstance(tr, dict) else tr,
+        "traffic_note": tr.get("note") if isinstance(tr, dict) else None,
+        "peak_source": peaks["source"],
+    })
+    table = {k: {"launches_per_step": v["launches"] / steps, "ms_per_step": v["ms"] / steps,
+                 "tflops": (v["flops"] / (v["ms"] / 1e3) / 1e12) if v["ms"] and v["flops"] else None,
+                 "gbs": (v["bytes"] / (v["ms"] / 1e3) / 1e9) if v["ms"] and v["bytes"] else None}
+             for k, v in sorted(pooled.items(), key=lambda kv: -kv[1]["ms"])}
+    return roof, table
+
+
 # ---------------------------------------------------------------------------
-# workloads
+# Layer workloads (cfg1-cfg3, qkv)
 # ---------------------------------------------------------------------------
-
-def layer_work(h, n_weights, esize=2):
-    """Algorithmic FLOPs and compulsory bytes of one fwd+bwd of a layer.
-
-    FLOPs: forward = codegen.flops(staged=True) (2 per MAC, batch included);
-    grad-input and grad-weight are one contraction each of the same volume.
-    Bytes: fwd reads x, w and writes y; bwd reads x, w, dy and writes dx, dw."""
-    f = h.flops_staged
-    nx = math.prod(h.x_shape)
-    ny = math.prod(h.y_shape)
-    nw = sum(math.prod(s) for s in h.w_shapes)
-    return {"fwd_flops": f, "bwd_flops": 2 * f,
-            "fwd_bytes": esize * (nx + nw + ny), "bwd_bytes": esize * (nx + nw + ny + nx + nw)}
-
 
 def build_layers(name, batch):
     from paper_2410_23745_b200 import workloads as WL
@@ -133,8 +202,21 @@ def build_layers(name, batch):
     raise ValueError(name)
 
 
+def layer_work(h, esize):
+    """Algorithmic work of one layer: forward = codegen.flops(staged=False) (the
+    contraction the kernel performs, 2 per MAC, batch included); grad-input and
+    grad-weight are one contraction each of the same volume.  Bytes: fwd reads x,
+    w and writes y; bwd reads x, w, dy and writes dx, dw."""
+    f = h.flops_unstaged
+    nx, ny = math.prod(h.x_shape), math.prod(h.y_shape)
+    nw = sum(math.prod(s) for s in h.w_shapes)
+    return {"fwd_flops": f, "bwd_flops": 2 * f,
+            "fwd_bytes": esize * (nx + nw + ny), "bwd_bytes": esize * (nx + nw + ny + nx + nw)}
+
+
 def run_layers(args, rank, world, device, peaks):
-    import numpy as np
+    import ctypes
+
     import torch
 
     from paper_2410_23745_b200 import _lib, ops
@@ -152,16 +234,14 @@ def run_layers(args, rank, world, device, peaks):
         ws = [(torch.randn(s, generator=gen) / math.sqrt(max(1, math.prod(s[1:])))).to(device=device, dtype=dtype)
               for s in h.w_shapes]
         dy = torch.randn(h.y_shape, generator=gen).to(device=device, dtype=dtype)
-        y = torch.empty(h.y_shape, device=device, dtype=dtype)
-        dx = torch.empty(h.x_shape, device=device, dtype=dtype)
-        dws = [torch.empty(s, device=device, dtype=dtype) for s in h.w_shapes]
-        state.append(dict(L=L, h=h, x=x, ws=ws, dy=dy, y=y, dx=dx, dws=dws,
-                          work=layer_work(h, len(ws), esize)))
+        state.append(dict(L=L, h=h, x=x, ws=ws, dy=dy, y=torch.empty(h.y_shape, device=device, dtype=dtype),
+                          dx=torch.empty(h.x_shape, device=device, dtype=dtype),
+                          dws=[torch.empty(s, device=device, dtype=dtype) for s in h.w_shapes],
+                          work=layer_work(h, esize)))
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=device)  # > 126 MB L2
-    # a dedicated stream: CUDA-graph capture needs a non-default stream, and the
+    # a dedicated stream: graph capture needs a non-default stream, and the
     # library keeps one workspace per (device, stream)
     stream = torch.cuda.Stream(device)
-    import ctypes
     sp = ctypes.c_void_p(stream.cuda_stream)
     code = ops._DT[dtype]
 
@@ -180,16 +260,14 @@ def run_layers(args, rank, world, device, peaks):
         assert rc == 0, _lib.last_error()
 
     phases = [("fwd", call_fwd)] + ([] if fwd_only else [("bwd", call_bwd)])
-    nev = len(state) * len(phases)
-    times = {(i, p): [] for i in range(len(state)) for p, _ in phases}
 
-    def one_step(record):
-        evs = [torch.cuda.Event(enable_timing=True) for _ in range(nev + 1)] if record else None
+    def one_step(record=False):
+        evs = [torch.cuda.Event(enable_timing=True) for _ in range(len(state) * len(phases) + 1)] if record else None
         if record:
             evs[0].record(stream)
         k = 0
-        for i, s in enumerate(state):
-            for p, fn in phases:
+        for s in state:
+            for _, fn in phases:
                 fn(s)
                 if record:
                     evs[k + 1].record(stream)
@@ -199,42 +277,38 @@ def run_layers(args, rank, world, device, peaks):
     with torch.cuda.stream(stream):
         for _ in range(args.warmup):
             flush.zero_()
-            one_step(False)
+            one_step()
     torch.cuda.synchronize(device)
 
-    # The step is captured once as a CUDA graph (kernel launches only: the
-    # library allocates nothing and never synchronises in steady state).
     graph = None
     launches_per_step = None
     if args.graph:
         c0 = _lib.lib.syno_launch_count()
         graph = torch.cuda.CUDAGraph()
         with torch.cuda.graph(graph, stream=stream):
-            one_step(False)
+            one_step()
         launches_per_step = _lib.lib.syno_launch_count() - c0
         with torch.cuda.stream(stream):
             graph.replay()
         torch.cuda.synchronize(device)
 
-    sampler = ClockSampler(torch.cuda.current_device() if device.index is None else device.index)
+    sampler = ClockSampler(device.index or 0)
     if rank == 0:
         sampler.start()
+        time.sleep(0.2)
     barrier(world)
     torch.cuda.synchronize(device)
     launches0 = _lib.lib.syno_launch_count()
-    step_ms = []
     evs = []
     for _ in range(args.steps):
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         with torch.cuda.stream(stream):
             flush.zero_()  # L2 flush between timed steps, outside the step's events
-        with torch.cuda.stream(stream):
             e0.record(stream)
             if graph is not None:
                 graph.replay()
             else:
-                one_step(False)
+                one_step()
             e1.record(stream)
         evs.append((e0, e1))
     torch.cuda.synchronize(device)
@@ -245,66 +319,50 @@ def run_layers(args, rank, world, device, peaks):
     if rank == 0:
         sampler.stop()
     step_ms = [a.elapsed_time(b) for a, b in evs]
-
-    # per-(layer, phase) breakdown: a separate eager pass with events between calls
-    for _ in range(2):
-        with torch.cuda.stream(stream):
-            flush.zero_()
-            all_evs = one_step(True)
-        torch.cuda.synchronize(device)
-        k = 0
-        for i in range(len(state)):
-            for p, _ in phases:
-                times[(i, p)].append(all_evs[k].elapsed_time(all_evs[k + 1]))
-                k += 1
-    ms = statistics.mean(step_ms)
+    ms = statistics.median(step_ms)
     ms_max = allreduce_max(ms, world, device)
     batch_units = state[0]["h"].x_shape[0] if state[0]["h"].batch_rank else 1
     value = world * batch_units / (ms_max / 1e3)
 
-    # dominant (layer, phase) call and its roofline
-    avg = {k: statistics.mean(v) for k, v in times.items()}
-    (di, dp), dms = max(avg.items(), key=lambda kv: kv[1])
-    w = state[di]["work"]
-    F = w[f"{dp}_flops"]
-    B = w[f"{dp}_bytes"]
-    tflops_peak = peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"])
-    t_tensor = F / (tflops_peak * 1e12)
-    t_hbm = B / (peaks["hbm_gbs"] * 1e9)
-    if t_tensor >= t_hbm:
-        achieved = F / (dms / 1e3) / 1e12
-        roof = {"bound": "tensor", "achieved": achieved, "peak": tflops_peak, "unit": "TFLOP/s",
-                "frac": achieved / tflops_peak}
-    else:
-        achieved = B / (dms / 1e3) / 1e9
-        roof = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                "frac": achieved / peaks["hbm_gbs"]}
-    roof.update({"traffic": load_traffic(state[di]["L"].name, dp),
-                 "kernel": f"{state[di]['L'].name}:{dp} (one library call: pack + fold + tcgen05 GEMMs)",
-                 "kernel_ms": dms, "share_of_step": dms / ms, "peak_source": peaks["source"]})
-    # whole-step roofline: sum of per-call roofline times over the measured step time
+    # per-launch kernel timing: eager steps with library-side CUDA events
+    # around every launch (same stream, L2 flushed before each step)
+    prof_steps = 3
+    times = {}
+    _lib.profile_begin()
+    for _ in range(prof_steps):
+        with torch.cuda.stream(stream):
+            flush.zero_()
+            all_evs = one_step(record=True)
+        torch.cuda.synchronize(device)
+        k = 0
+        for s in state:
+            for p, _ in phases:
+                times.setdefault(f"{s['L'].name}:{p}", []).append(all_evs[k].elapsed_time(all_evs[k + 1]))
+                k += 1
+    prof = _lib.profile_end()
+    roof, kernels = roofline_from_profile(prof, prof_steps, ms, peaks)
+
+    tpeak = peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"])
     t_roof = 0.0
     for s in state:
         for p, _ in phases:
-            t_roof += max(s["work"][f"{p}_flops"] / (tflops_peak * 1e12), s["work"][f"{p}_bytes"] / (peaks["hbm_gbs"] * 1e9))
+            t_roof += max(s["work"][f"{p}_flops"] / (tpeak * 1e12), s["work"][f"{p}_bytes"] / (peaks["hbm_gbs"] * 1e9))
     step_flops = sum(s["work"]["fwd_flops"] + (0 if fwd_only else s["work"]["bwd_flops"]) for s in state)
-
     with torch.cuda.stream(stream):
         e2e = measure_e2e(state, phases, args, device, dtype, world)
-    breakdown = {f"{state[i]['L'].name}:{p}": round(avg[(i, p)], 4) for (i, p) in avg}
     return {
-        "value": value, "ms_per_step": ms_max, "roofline": roof,
+        "value": value, "ms_per_step": ms_max, "roofline": roof, "kernels": kernels,
         "step_roofline_frac": (t_roof * 1e3) / ms_max, "step_tflops": step_flops / (ms_max / 1e3) / 1e12,
         "gpu_launches": int(launches), "clocks": sampler.summary() if rank == 0 else None,
-        "e2e": e2e, "breakdown_ms": breakdown, "dtype": "bf16" if dtype == torch.bfloat16 else "f32",
-        "batch": batch_units, "n_layers": len(state), "state": state,
+        "e2e": e2e, "breakdown_ms": {k: round(statistics.median(v), 4) for k, v in times.items()},
+        "dtype": "bf16" if dtype == torch.bfloat16 else "f32", "unit": "images/s",
     }
 
 
 def measure_e2e(state, phases, args, device, dtype, world):
-    """Same step through the public API with HOST buffers: pinned host -> device
-    copies of every layer's x (and dy), compute, device -> host copies of y
-    (and dx, dW), all inside the timed region."""
+    """The same step through the public API (ops.forward / ops.backward) with
+    HOST buffers: pinned host -> device copies of every layer's x (and dy),
+    compute, device -> host copies of y (and dx, every dW), all timed."""
     import torch
 
     from paper_2410_23745_b200 import ops
@@ -340,35 +398,136 @@ def measure_e2e(state, phases, args, device, dtype, world):
         step()
     torch.cuda.synchronize(device)
     n = max(1, min(args.steps, 10))
-    t0 = torch.cuda.Event(enable_timing=True)
-    t1 = torch.cuda.Event(enable_timing=True)
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     t0.record(stream)
     for _ in range(n):
         step()
     t1.record(stream)
     torch.cuda.synchronize(device)
-    ms = t0.elapsed_time(t1) / n
-    ms = allreduce_max(ms, world, device)
+    ms = allreduce_max(t0.elapsed_time(t1) / n, world, device)
     units = state[0]["h"].x_shape[0]
     return {"value": world * units / (ms / 1e3), "unit": "images/s", "ms_per_step": ms,
             "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h}
 
 
-def load_traffic(layer, phase):
-    path = os.path.join(ROOT, "profiles", "traffic.json")
-    if not os.path.exists(path):
-        return None
-    with open(path) as f:
-        t = json.load(f)
-    return t.get(f"{layer}:{phase}")
+# ---------------------------------------------------------------------------
+# Candidate sweep (cfg5)
+# ---------------------------------------------------------------------------
+
+SWEEP_BATCH = 8
+CONV_FLOPS_PER_IMAGE = 2 * 64 * 32 * 32 * 64 * 9
+
+
+def sweep_setup(limit=None):
+    from paper_2410_23745_b200 import workloads as WL
+    from paper_2410_23745_b200.sweep import candidate_costs
+    graphs = WL.corpus(SWEEP_BATCH, limit=limit)
+    flops_cap = 10 * CONV_FLOPS_PER_IMAGE * SWEEP_BATCH      # make_corpus.py's cap, per batch
+    params_cap = 64 * 64 * 9 * 16
+    return graphs, candidate_costs(graphs), flops_cap, params_cap
+
+
+def run_sweep(args, rank, world, device, peaks):
+    import torch
+
+    from paper_2410_23745_b200 import _lib
+    from paper_2410_23745_b200 import pgraph as P
+    from paper_2410_23745_b200.sweep import lpt_shard, run_shard
+
+    graphs, costs, fcap, pcap = sweep_setup(args.limit)
+    mine = lpt_shard(costs, world)[rank]
+    # warm-up: the CUDA context and every kernel variant on the same ops at a
+    # different batch (distinct handles: the timed steps compile from scratch)
+    from paper_2410_23745_b200 import workloads as WL
+    warm_graphs = WL.corpus(2, limit=args.limit)
+    for k in range(max(1, args.warmup)):
+        run_shard(warm_graphs, mine[k::max(1, args.warmup)], dtype=torch.float32, flops_cap=fcap, params_cap=pcap)
+    torch.cuda.synchronize(device)
+    sampler = ClockSampler(device.index or 0)
+    if rank == 0:
+        sampler.start()
+        time.sleep(0.2)
+    step_s, recs_all = [], None
+    launches0 = _lib.lib.syno_launch_count()
+    for _ in range(args.steps):
+        with P._CACHE_LOCK:
+            P._CACHE.clear()  # every step compiles every candidate afresh
+        barrier(world)
+        torch.cuda.synchronize(device)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        recs, _ = run_shard(graphs, mine, dtype=torch.float32, flops_cap=fcap, params_cap=pcap)
+        e1.record()
+        torch.cuda.synchronize(device)
+        step_s.append(e0.elapsed_time(e1) / 1e3)
+        recs_all = recs
+    barrier(world)
+    launches = _lib.lib.syno_launch_count() - launches0
+    if rank == 0:
+        sampler.stop()
+    s = allreduce_max(statistics.median(step_s), world, device)
+    n_total = len(graphs)
+    status = {}
+    for r in recs_all:
+        status[r.status] = status.get(r.status, 0) + 1
+    evaluated = sum(1 for r in recs_all if r.status != "over_budget")
+    log_dir = os.path.join(ROOT, "gpurun_out")
+    if os.path.isdir(log_dir):
+        with open(os.path.join(log_dir, f"sweep_rank{rank}.log"), "w") as f:
+            for r in recs_all:
+                f.write(r.line() + "\n" + r.diag() + "\n")
+    return {"value": n_total / s, "unit": "candidates/s", "ms_per_step": s * 1e3, "roofline": None,
+            "gpu_launches": int(launches), "clocks": sampler.summary() if rank == 0 else None,
+            "dtype": "f32", "sweep": {"candidates": n_total, "this_rank": len(mine), "executed_this_rank": evaluated,
+                                      "status_this_rank": status, "flops_cap": fcap, "params_cap": pcap},
+            "e2e": None}
+
+
+# ---------------------------------------------------------------------------
+# Proxy training (cfg4): DP with the NCCL gradient allreduce
+# ---------------------------------------------------------------------------
+
+def run_qkv_train(args, rank, world, device, peaks):
+    import torch
+
+    from paper_2410_23745_b200 import _lib, workloads as WL
+    from paper_2410_23745_b200.dp import GradBuckets, ProxyQKV, broadcast_parameters, train_step
+
+    batch = args.batch or 16
+    L = WL.qkv(batch)
+    model = ProxyQKV(L.graph, layers=12, dtype=torch.bfloat16, device=device)
+    broadcast_parameters(list(model.parameters()))
+    buckets = GradBuckets(list(model.parameters()), bucket_bytes=32 << 20).attach()
+    gen = torch.Generator(device=device).manual_seed(7 + rank)
+    x = torch.randn((batch, 1024, 768), generator=gen, device=device).bfloat16()
+    target = torch.randn((batch, 1024, 768), generator=gen, device=device).bfloat16() * 0.1
+    for _ in range(args.warmup):
+        train_step(model, buckets, x, target)
+    torch.cuda.synchronize(device)
+    barrier(world)
+    launches0 = _lib.lib.syno_launch_count()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.steps):
+        loss = train_step(model, buckets, x, target)
+    e1.record()
+    torch.cuda.synchronize(device)
+    ms = allreduce_max(e0.elapsed_time(e1) / args.steps, world, device)
+    tokens = world * batch * 1024
+    flops = 12 * 3 * 2 * batch * 1024 * 768 * 2304  # 12 layers x (fwd + dgrad + wgrad)
+    return {"value": tokens / (ms / 1e3), "unit": "tokens/s", "ms_per_step": ms, "roofline": None,
+            "gpu_launches": int(_lib.lib.syno_launch_count() - launches0), "clocks": None, "dtype": "bf16",
+            "step_tflops": flops / (ms / 1e3) / 1e12, "loss": float(loss), "e2e": None,
+            "allreduce": {"buckets": len(buckets.buckets), "bytes": sum(f.numel() * f.element_size()
+                                                                       for f in buckets.flat)}}
 
 
 # ---------------------------------------------------------------------------
 # CPU baseline: the pinned oracle restatement of the reference path
 # ---------------------------------------------------------------------------
 
-def _oracle_layer_job(args):
-    """One image of one layer, fwd + grad-input + grad-weight, with the oracle."""
+def _oracle_job(args):
+    """One image of one layer (or one candidate), fwd [+ grad-input + grad-weight]."""
     import numpy as np
 
     from oracle import nest_oracle as O
@@ -379,11 +538,10 @@ def _oracle_layer_job(args):
     up = rng.standard_normal(yshape)
     t0 = time.perf_counter()
     O.interpret(text, env, x, ws)
-    if fwd_only:
-        return time.perf_counter() - t0
-    O.input_gradient(text, env, x, up, ws)
-    if ws:
-        O.weight_gradient(text, env, x, up, ws)
+    if not fwd_only:
+        O.input_gradient(text, env, x, up, ws)
+        if ws:
+            O.weight_gradient(text, env, x, up, ws)
     return time.perf_counter() - t0
 
 
@@ -394,7 +552,7 @@ def cpu_sample_spec(args):
     from paper_2410_23745_b200 import pgraph as P
     layers = build_layers(args.workload, args.batch)
     pick = {"resnet18": "l1b0c2", "resnet34": "l2b1c2", "cfg1": "cfg1_conv3x3", "qkv": "qkv"}[args.workload]
-    L = next(l for l in layers if l.name == pick)
+    L = next(lay for lay in layers if lay.name == pick)
     one = dict(L.assignment)
     bkey = "N" if "N" in one else "B"
     batch = one[bkey]
@@ -403,33 +561,79 @@ def cpu_sample_spec(args):
     one[bkey] = 1
     text = C.emit_loop_nest(L.graph, one)
     h1 = P.handle_for(L.graph, one)
-    spec = (text, one, h1.x_shape[1:], [tuple(s) for s in h1.w_shapes], h1.y_shape[1:], args.workload == "cfg1")
-    flops_one = 3 * h1.flops_staged
-    total_flops_per_image = sum(3 * P.handle_for(l.graph).flops_staged for l in layers) / batch
-    if args.workload == "cfg1":
-        flops_one = h1.flops_staged
-        total_flops_per_image = P.handle_for(L.graph).flops_staged / batch
-    desc = (f"1 image of layer {L.name} ({L.op}) "
-            + ("forward" if args.workload == "cfg1" else "fwd+grad-input+grad-weight")
+    fwd_only = args.workload == "cfg1"
+    spec = (text, one, h1.x_shape[1:], [tuple(s) for s in h1.w_shapes], h1.y_shape[1:], fwd_only)
+    mult = 1 if fwd_only else 3
+    flops_one = mult * h1.flops_unstaged
+    per_image = sum(mult * P.handle_for(lay.graph).flops_unstaged for lay in layers) / batch
+    desc = (f"1 image of layer {L.name} ({L.op}) " + ("forward" if fwd_only else "fwd+grad-input+grad-weight")
             + (" at T=128" if args.workload == "qkv" else "")
-            + "; images/s extrapolated by FLOP share of the full step")
-    return spec, flops_one, total_flops_per_image, desc
+            + " in float64; images/s extrapolated by the layer's FLOP share of the full step")
+    return spec, flops_one, per_image, desc
 
 
-def cpu_baseline(args, processes=1):
+def cpu_baseline_layers(args, processes=1):
     import multiprocessing as mp
     spec, flops_one, per_image, desc = cpu_sample_spec(args)
     jobs = [spec + (k,) for k in range(processes)]
     t0 = time.perf_counter()
     if processes == 1:
-        _oracle_layer_job(jobs[0])
+        _oracle_job(jobs[0])
     else:
         with mp.get_context("fork").Pool(processes) as pool:
-            pool.map(_oracle_layer_job, jobs)
+            pool.map(_oracle_job, jobs)
     dt = time.perf_counter() - t0
-    flops_rate = processes * flops_one / dt
-    return {"value": flops_rate / per_image, "unit": "images/s", "cores": processes, "kind": "port",
+    return {"value": processes * flops_one / dt / per_image, "unit": "images/s", "cores": processes, "kind": "port",
             "sample": desc + f" ({processes} process(es), {dt:.1f} s)", "seconds": dt}
+
+
+def cpu_baseline_sweep(args, processes=1, budget_s=20.0):
+    """Oracle evaluation (fwd + grad-input + grad-weights, float64, per
+    image) of corpus candidates in corpus order until ~budget_s; rate
+    extrapolated to the whole corpus by the candidates' FLOP share."""
+    import multiprocessing as mp
+
+    from paper_2410_23745_b200 import codegen as C
+    from paper_2410_23745_b200 import pgraph as P
+    from paper_2410_23745_b200.sweep import within_budget
+    graphs, costs, fcap, pcap = sweep_setup(args.limit)
+    one = {"C_out": 64, "C_in": 64, "H": 32, "W": 32, "K": 3, "s": 2, "N": 1}
+    fl_all = 0.0
+    items = []
+    for i, g in enumerate(graphs):
+        h = P.handle_for(g)
+        if not within_budget(h.flops_unstaged, h.params, fcap, pcap):
+            continue
+        fl_all += h.flops_unstaged
+        items.append((i, g, h))
+    done_fl, n_done = 0.0, 0
+    t0 = time.perf_counter()
+    pool = mp.get_context("fork").Pool(processes) if processes > 1 else None
+    k = 0
+    while k < len(items) and time.perf_counter() - t0 < budget_s:
+        chunk = items[k:k + processes]
+        k += len(chunk)
+        jobs = []
+        for i, g, h in chunk:
+            h1 = P.handle_for(g, one)
+            jobs.append((C.emit_loop_nest(g, one), one, h1.x_shape[1:], [tuple(s) for s in h1.w_shapes],
+                         h1.y_shape[1:], False, i))
+        if pool:
+            pool.map(_oracle_job, jobs)
+        else:
+            for j in jobs:
+                _oracle_job(j)
+        done_fl += sum(h.flops_unstaged for _, _, h in chunk)
+        n_done += len(chunk)
+    dt = time.perf_counter() - t0
+    if pool:
+        pool.close()
+    # oracle time for the whole corpus = dt * (fl_all / done_fl) * SWEEP_BATCH (per-image sample)
+    total_s = dt * (fl_all / max(done_fl, 1.0)) * SWEEP_BATCH
+    return {"value": len(graphs) / total_s, "unit": "candidates/s", "cores": processes, "kind": "port",
+            "sample": (f"{n_done} in-budget corpus candidates, 1 image each, fwd+grad-input+grad-weight in float64 "
+                       f"({dt:.1f} s, {processes} process(es)); extrapolated to the 1024-candidate sweep at N=8 "
+                       "by FLOP share"), "seconds": dt}
 
 
 def run_reference(args, rank, world):
@@ -437,59 +641,51 @@ def run_reference(args, rank, world):
         return
     cores = len(os.sched_getaffinity(0))
     procs = max(1, min(cores, 64))
-    for _ in range(args.warmup):
-        pass  # the oracle has no warm state worth warming beyond imports
-    vals, secs = [], []
+    vals, secs, r = [], [], None
     for _ in range(max(1, args.steps)):
-        r = cpu_baseline(args, procs)
+        if args.workload == "sweep":
+            r = cpu_baseline_sweep(args, procs, budget_s=15.0)
+        else:
+            r = cpu_baseline_layers(args, procs)
         vals.append(r["value"])
         secs.append(r["seconds"])
     v = statistics.mean(vals)
     line = {
-        "impl": "reference", "metric": METRIC, "value": v, "unit": "images/s", "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * statistics.mean(secs),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "impl": "reference", "metric": SWEEP_METRIC if args.workload == "sweep" else METRIC, "value": v,
+        "unit": r["unit"], "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * statistics.mean(secs), "higher_is_better": True,
+        "scaling": "strong" if args.workload == "sweep" else "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic", "config": workload_config(args),
-        "cpu_baseline": {"value": v, "unit": "images/s", "cores": procs, "kind": "port",
-                         "sample": r["sample"]},
-        "e2e": {"value": v, "unit": "images/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "cpu_baseline": {"value": v, "unit": r["unit"], "cores": procs, "kind": "port", "sample": r["sample"]},
+        "e2e": {"value": v, "unit": r["unit"], "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
 # ---------------------------------------------------------------------------
 
-METRIC = "synthesized-operator fwd+bwd throughput (operator fwd+bwd latency & % roofline)"
-
-
 def workload_config(args):
-    from paper_2410_23745_b200 import workloads as WL  # noqa: F401
     desc = {
         "resnet18": ("cfg2: ResNet-18 CIFAR conv layers (20) as synthesized operators "
                      "(sep_shared / conv3x3 / conv3x3_s2 / 1x1-s2 shortcut), fwd+bwd"),
         "resnet34": "cfg3: ResNet-34 ImageNet-shape layers as synthesized operators, fwd+bwd",
         "cfg1": "cfg1: conv3x3 in Syno primitives, N=8 C=64 H=W=32, forward",
-        "qkv": "cfg4: GPT-2 small QKV projection as a synthesized operator, fwd+bwd",
+        "qkv": "cfg4 layer: GPT-2 small QKV projection as a synthesized operator, fwd+bwd",
+        "qkv_train": "cfg4: proxy training, 12 GPT-2-small QKV synthesized operators, DP with NCCL allreduce",
+        "sweep": "cfg5: 1024 sampled primitive graphs (conv64 spec, N=8), LPT-sharded across GPUs",
     }[args.workload]
-    batch = args.batch or {"resnet18": 128, "resnet34": 256, "cfg1": 8, "qkv": 16}[args.workload]
-    return {"workload": desc, "batch_per_gpu": batch, "l2": "flushed between timed steps (256 MB write)",
-            "inputs": "synthetic N(0,1), resident in HBM"}
-
-
-def barrier(world):
-    if world > 1:
-        import torch.distributed as dist
-        dist.barrier()
-
-
-def allreduce_max(v, world, device):
-    if world == 1:
-        return v
-    import torch
-    import torch.distributed as dist
-    t = torch.tensor([v], dtype=torch.float64, device=device)
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    return float(t.item())
+    batch = args.batch or {"resnet18": 128, "resnet34": 256, "cfg1": 8, "qkv": 16, "qkv_train": 16,
+                           "sweep": SWEEP_BATCH}[args.workload]
+    cfg = {"workload": desc, "batch_per_gpu": batch, "inputs": "synthetic N(0,1), resident in HBM"}
+    if args.workload in ("resnet18", "resnet34", "cfg1", "qkv"):
+        cfg["l2"] = "flushed between timed steps (256 MB write)"
+        cfg["parallelism"] = "replicas (no data-path collective)"
+    elif args.workload == "sweep":
+        cfg["parallelism"] = "LPT candidate sharding, no collective"
+        cfg["l2"] = "not flushed (every candidate compiles and allocates afresh)"
+    else:
+        cfg["parallelism"] = "data parallel, bucketed NCCL allreduce"
+    return cfg
 
 
 def main():
@@ -497,13 +693,17 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--workload", default="resnet18", choices=["resnet18", "resnet34", "cfg1", "qkv"])
+    ap.add_argument("--workload", default="resnet18",
+                    choices=["resnet18", "resnet34", "cfg1", "qkv", "sweep", "qkv_train"])
     ap.add_argument("--batch", type=int, default=0)
+    ap.add_argument("--limit", type=int, default=None, help="sweep: first N corpus candidates only")
     ap.add_argument("--impl", default="syno", choices=["syno", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graph", dest="graph", action="store_false", help="eager launches instead of a CUDA graph")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
+    if args.workload == "sweep" and args.steps == 10:
+        args.steps = 3
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -518,20 +718,24 @@ def main():
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=device)
     peaks = load_peaks()
-    r = run_layers(args, rank, world, device, peaks)
+    runner = {"sweep": run_sweep, "qkv_train": run_qkv_train}.get(args.workload, run_layers)
+    r = runner(args, rank, world, device, peaks)
     if rank == 0:
         cpu = None
-        if not args.no_cpu_baseline:
-            cpu = cpu_baseline(args, 1)
+        if not args.no_cpu_baseline and args.workload != "qkv_train":
+            cpu = cpu_baseline_sweep(args, 1) if args.workload == "sweep" else cpu_baseline_layers(args, 1)
             cpu.pop("seconds", None)
         line = {
-            "metric": METRIC, "value": r["value"], "unit": "images/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": r["ms_per_step"], "higher_is_better": True, "scaling": "weak",
+            "metric": SWEEP_METRIC if args.workload == "sweep" else METRIC, "value": r["value"], "unit": r["unit"],
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": r["ms_per_step"],
+            "higher_is_better": True, "scaling": "strong" if args.workload == "sweep" else "weak",
             "vs_baseline": None, "dtype": r["dtype"], "data": "synthetic", "config": workload_config(args),
-            "roofline": r["roofline"], "step_roofline_frac": r["step_roofline_frac"],
-            "step_tflops": r["step_tflops"], "cpu_baseline": cpu, "e2e": r["e2e"], "gpu_launches": r["gpu_launches"],
-            "clocks": r["clocks"], "breakdown_ms": r["breakdown_ms"],
+            "roofline": r.get("roofline"), "cpu_baseline": cpu, "e2e": r.get("e2e"),
+            "gpu_launches": r["gpu_launches"], "clocks": r.get("clocks"),
         }
+        for k in ("step_roofline_frac", "step_tflops", "kernels", "breakdown_ms", "sweep", "loss", "allreduce"):
+            if k in r:
+                line[k] = r[k]
         print(json.dumps(line), flush=True)
     if world > 1:
         import torch.distributed as dist

@@ -117,6 +117,24 @@ const char* syno_version(void);
  * devices); bench.py reports the difference across its timed region. */
 uint64_t syno_launch_count(void);
 
+/* Per-kernel-class timing (measurement only; no reference counterpart).
+ * Between syno_profile_begin() and syno_profile_end() every library launch
+ * is bracketed by CUDA events on the stream it is issued to; end()
+ * synchronises those events and returns one row per kernel class with the
+ * launch count, summed device milliseconds and the summed ALGORITHMIC
+ * FLOPs / bytes of the launches (codegen.flops per contraction GEMM).
+ * Must not be active during CUDA-graph capture. */
+typedef struct {
+  char name[48];
+  int64_t launches;
+  double ms;
+  double flops;
+  double bytes;
+} syno_kernel_stat;
+
+void syno_profile_begin(void);
+int syno_profile_end(syno_kernel_stat* out, int cap, int* n);
+
 #ifdef __cplusplus
 }
 #endif

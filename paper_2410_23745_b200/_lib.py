@@ -36,6 +36,7 @@ EXPORTS = (
     "syno_compile", "syno_forward", "syno_backward", "syno_query",
     "syno_emit_loop_nest", "syno_print_operator", "syno_describe_plan",
     "syno_index_map", "syno_destroy", "syno_last_error", "syno_version", "syno_launch_count",
+    "syno_profile_begin", "syno_profile_end",
 )
 
 
@@ -59,6 +60,16 @@ class SynoInfo(ctypes.Structure):
         ("complete", ctypes.c_int32),
         ("replay_only", ctypes.c_int32),
         ("tc_path", ctypes.c_int32),
+    ]
+
+
+class KernelStat(ctypes.Structure):
+    _fields_ = [
+        ("name", ctypes.c_char * 48),
+        ("launches", ctypes.c_int64),
+        ("ms", ctypes.c_double),
+        ("flops", ctypes.c_double),
+        ("bytes", ctypes.c_double),
     ]
 
 
@@ -86,8 +97,11 @@ def _load():
     lib.syno_last_error.restype = ctypes.c_char_p
     lib.syno_version.restype = ctypes.c_char_p
     lib.syno_launch_count.restype = ctypes.c_uint64
+    lib.syno_profile_begin.restype = None
+    lib.syno_profile_end.argtypes = [ctypes.POINTER(KernelStat), ctypes.c_int, ctypes.POINTER(ctypes.c_int)]
     for name in EXPORTS:
-        if name not in ("syno_destroy", "syno_last_error", "syno_version", "syno_launch_count"):
+        if name not in ("syno_destroy", "syno_last_error", "syno_version", "syno_launch_count",
+                        "syno_profile_begin"):
             getattr(lib, name).restype = ctypes.c_int
     return lib
 
@@ -109,3 +123,19 @@ def text_call(fn, *args) -> str:
     if rc:
         raise RuntimeError(last_error())
     return buf.value.decode()
+
+
+def profile_begin() -> None:
+    lib.syno_profile_begin()
+
+
+def profile_end() -> dict:
+    """{kernel class: {launches, ms, flops, bytes}} since profile_begin()."""
+    cap = 64
+    buf = (KernelStat * cap)()
+    n = ctypes.c_int(0)
+    rc = lib.syno_profile_end(buf, cap, ctypes.byref(n))
+    if rc:
+        raise RuntimeError(last_error())
+    return {buf[i].name.decode(): {"launches": buf[i].launches, "ms": buf[i].ms, "flops": buf[i].flops,
+                                   "bytes": buf[i].bytes} for i in range(min(n.value, cap))}

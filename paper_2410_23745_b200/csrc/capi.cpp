@@ -264,4 +264,22 @@ const char* syno_version(void) { return "syno-b200 0.1 (sm_100a)"; }
 
 uint64_t syno_launch_count(void) { return launch_count(); }
 
+void syno_profile_begin(void) { prof_enable(true); }
+
+int syno_profile_end(syno_kernel_stat* out, int cap, int* n) {
+  return guarded([&] {
+    auto stats = prof_collect();
+    prof_enable(false);
+    if (n) *n = (int)stats.size();
+    for (int i = 0; i < (int)stats.size() && i < cap && out; ++i) {
+      memset(&out[i], 0, sizeof(out[i]));
+      strncpy(out[i].name, stats[i].name.c_str(), sizeof(out[i].name) - 1);
+      out[i].launches = stats[i].launches;
+      out[i].ms = stats[i].ms;
+      out[i].flops = stats[i].flops;
+      out[i].bytes = stats[i].bytes;
+    }
+  });
+}
+
 }  // extern "C"

@@ -14,6 +14,7 @@
 #include <algorithm>
 #include <atomic>
 #include <cstring>
+#include <mutex>
 #include <set>
 
 #include "engine.hpp"
@@ -28,6 +29,78 @@ void cuda_check(cudaError_t e, const char* what) {
 static std::atomic<uint64_t> g_launches{0};
 void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 uint64_t launch_count() { return g_launches.load(std::memory_order_relaxed); }
+
+namespace {
+struct ProfRec {
+  std::string name;
+  cudaEvent_t a = nullptr, b = nullptr;
+  double flops = 0, bytes = 0;
+};
+std::mutex g_prof_mu;
+std::atomic<bool> g_prof_on{false};
+std::vector<ProfRec> g_prof;
+}  // namespace
+
+void prof_enable(bool on) {
+  std::lock_guard<std::mutex> lock(g_prof_mu);
+  for (auto& r : g_prof) {
+    if (r.a) cudaEventDestroy(r.a);
+    if (r.b) cudaEventDestroy(r.b);
+  }
+  g_prof.clear();
+  g_prof_on = on;
+}
+
+int prof_begin(const char* name, double flops, double bytes, cudaStream_t stream) {
+  if (!g_prof_on.load(std::memory_order_relaxed)) return -1;
+  ProfRec r;
+  r.name = name;
+  r.flops = flops;
+  r.bytes = bytes;
+  cuda_check(cudaEventCreate(&r.a), "cudaEventCreate(prof)");
+  cuda_check(cudaEventCreate(&r.b), "cudaEventCreate(prof)");
+  cuda_check(cudaEventRecord(r.a, stream), "cudaEventRecord(prof)");
+  std::lock_guard<std::mutex> lock(g_prof_mu);
+  g_prof.push_back(r);
+  return (int)g_prof.size() - 1;
+}
+
+void prof_rename(int id, const char* name) {
+  if (id < 0) return;
+  std::lock_guard<std::mutex> lock(g_prof_mu);
+  if (id < (int)g_prof.size()) g_prof[id].name = name;
+}
+
+void prof_end(int id, cudaStream_t stream) {
+  if (id < 0) return;
+  cudaEvent_t b;
+  {
+    std::lock_guard<std::mutex> lock(g_prof_mu);
+    if (id >= (int)g_prof.size()) return;
+    b = g_prof[id].b;
+  }
+  cuda_check(cudaEventRecord(b, stream), "cudaEventRecord(prof)");
+}
+
+std::vector<ProfStat> prof_collect() {
+  std::lock_guard<std::mutex> lock(g_prof_mu);
+  std::vector<ProfStat> out;
+  for (auto& r : g_prof) {
+    cuda_check(cudaEventSynchronize(r.b), "cudaEventSynchronize(prof)");
+    float ms = 0;
+    cuda_check(cudaEventElapsedTime(&ms, r.a, r.b), "cudaEventElapsedTime(prof)");
+    auto it = std::find_if(out.begin(), out.end(), [&](const ProfStat& s) { return s.name == r.name; });
+    if (it == out.end()) {
+      out.push_back(ProfStat{r.name});
+      it = out.end() - 1;
+    }
+    it->launches += 1;
+    it->ms += ms;
+    it->flops += r.flops;
+    it->bytes += r.bytes;
+  }
+  return out;
+}
 
 // ---------------------------------------------------------------------------
 // K1: coordinate programs
@@ -659,7 +732,21 @@ static void launch_nt(const KStage& k, dim3 grid, cudaStream_t stream) {
 }
 
 template <typename TI>
+static void launch_stage_impl(const DevStage& ds, const Bindings& b, void* out, bool out_acc, cudaStream_t stream,
+                              const char** kind);
+
+template <typename TI>
 static void launch_stage_t(const DevStage& ds, const Bindings& b, void* out, bool out_acc, cudaStream_t stream) {
+  const char* kind = "stage";
+  const int id = prof_begin("stage", 2.0 * ds.cs.grid_points(), 0.0, stream);
+  launch_stage_impl<TI>(ds, b, out, out_acc, stream, &kind);
+  prof_rename(id, kind);
+  prof_end(id, stream);
+}
+
+template <typename TI>
+static void launch_stage_impl(const DevStage& ds, const Bindings& b, void* out, bool out_acc, cudaStream_t stream,
+                              const char** kind) {
   using TA = typename Acc<TI>::type;
   KStage k = ds.k;
   for (int t = 0; t < k.n_terms; ++t) {
@@ -675,6 +762,7 @@ static void launch_stage_t(const DevStage& ds, const Bindings& b, void* out, boo
   for (int t = 0; t < k.n_terms && affine; ++t)
     affine = k.terms[t].kind != 2 && k.terms[t].n_atab == 0 && k.terms[t].n_mix == 0 && k.terms[t].rtab == nullptr;
   if (affine) {
+    *kind = "stage_affine";
     k.out = out;
     k.out_acc = out_acc;
     const unsigned blocks = (unsigned)((k.out_count + 255) / 256);
@@ -699,6 +787,7 @@ static void launch_stage_t(const DevStage& ds, const Bindings& b, void* out, boo
   if (k.R == 0) { nsplit = 1; k.r_chunk = 0; }
   dim3 grid((unsigned)((k.out_count + 255) / 256), (unsigned)nsplit);
   if (block_mode) {
+    *kind = "stage_block_reduce";
     dim3 bgrid((unsigned)k.out_count, (unsigned)nsplit);
     TA* part = nullptr;
     if (nsplit > 1)
@@ -719,6 +808,7 @@ static void launch_stage_t(const DevStage& ds, const Bindings& b, void* out, boo
     return;
   }
   if (ds.cs.scatter) {
+    *kind = "stage_scatter";
     k.out = out;
     k.out_acc = 1;
     note_launch();
@@ -726,6 +816,7 @@ static void launch_stage_t(const DevStage& ds, const Bindings& b, void* out, boo
     cuda_check(cudaGetLastError(), "stage_kernel<scatter>");
     return;
   }
+  *kind = "stage_gather_reduce";
   if (nsplit == 1) {
     k.out = out;
     k.out_acc = out_acc;

@@ -112,4 +112,19 @@ void cuda_check(cudaError_t e, const char* what);
 void note_launch();
 uint64_t launch_count();
 
+// Optional per-launch timing (syno_profile_begin/end): when enabled, every
+// library launch is bracketed by CUDA events on its own stream and tagged
+// with the kernel class and its algorithmic FLOPs / bytes.  Off by default
+// and never enabled inside a CUDA-graph capture.
+int prof_begin(const char* name, double flops, double bytes, cudaStream_t stream);
+void prof_end(int id, cudaStream_t stream);
+void prof_rename(int id, const char* name);
+struct ProfStat {
+  std::string name;
+  int64_t launches = 0;
+  double ms = 0, flops = 0, bytes = 0;
+};
+void prof_enable(bool on);
+std::vector<ProfStat> prof_collect();
+
 }  // namespace syno

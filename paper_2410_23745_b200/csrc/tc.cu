@@ -157,6 +157,7 @@ struct TcPlan {
   int C = 0, N = 0, Cp = 0, Np = 0;
   PixDim dh, dw;
   double scale = 1;
+  double flops = 0;  // algorithmic FLOPs of one GEMM (= codegen.flops, unstaged, batch included)
   bool dgrad_ok = false;
   DevStage fold_fwd, fold_dgrad;
   std::vector<DevStage> chain;    // dW_j from the folded gradient
@@ -371,6 +372,7 @@ TcPlanPtr tc_build(const Plan& plan, cudaStream_t stream) {
   TcPlan* raw = try_match(plan);
   if (!raw) return TcPlanPtr();
   TcPlanPtr tp(raw);
+  tp->flops = (double)plan.flops_unstaged;
   build_dev_stage(fold_stage(plan, *tp, false, true), &tp->fold_fwd, stream);
   if (tp->dgrad_ok) build_dev_stage(fold_stage(plan, *tp, true, true), &tp->fold_dgrad, stream);
   // chain rule through the fold: dW_j from dWf[rh][rw][n][ci] (fp32)
@@ -461,7 +463,8 @@ static int sm_count() {
 }
 
 // Persistent launch: one CTA per SM walks the (n fastest, m, z) tile grid.
-static void gemm(TcGemmParams& p, int bn, int m_tiles, int n_tiles, int z_tiles, cudaStream_t stream) {
+static void gemm(TcGemmParams& p, int bn, int m_tiles, int n_tiles, int z_tiles, cudaStream_t stream,
+                 const char* name, double flops) {
   p.m_tiles = m_tiles;
   p.n_tiles = n_tiles;
   p.z_tiles = z_tiles;
@@ -470,9 +473,11 @@ static void gemm(TcGemmParams& p, int bn, int m_tiles, int n_tiles, int z_tiles,
   const int64_t tiles = (int64_t)m_tiles * n_tiles * z_tiles;
   if (tiles <= 0) return;
   const unsigned grid = (unsigned)std::min<int64_t>(tiles, sm_count());
+  const int id = prof_begin(name, flops, 0.0, stream);
   if (bn == 64) launch_gemm<64>(p, grid, stream);
   else if (bn == 128) launch_gemm<128>(p, grid, stream);
   else launch_gemm<256>(p, grid, stream);
+  prof_end(id, stream);
 }
 
 static int mgroup_of(int bn) { return bn == 64 ? mgroup<64>() : bn == 128 ? mgroup<128>() : mgroup<256>(); }
@@ -482,10 +487,13 @@ static int pick_bn(int n) { return n <= 64 ? 64 : n <= 128 ? 128 : 256; }
 static void pack_cl(const void* src, DType dt, const PackGeom& g, __nv_bfloat16* dst, cudaStream_t stream) {
   const int64_t pix = (int64_t)g.Sh * g.Sw * g.n_img * g.Hp * g.Wp;
   dim3 grid((unsigned)((pix + 31) / 32), (unsigned)((g.Cp + 63) / 64));
+  const double src_elems = (double)g.n_img * g.C * g.Hin * g.Win;
+  const int id = prof_begin("pack_cl", 0.0, src_elems * (dt == DT_BF16 ? 2 : 4) + (double)pix * g.Cp * 2, stream);
   note_launch();
   if (dt == DT_BF16) pack_cl_kernel<__nv_bfloat16><<<grid, 256, 0, stream>>>((const __nv_bfloat16*)src, dst, g, pix);
   else pack_cl_kernel<float><<<grid, 256, 0, stream>>>((const float*)src, dst, g, pix);
   cuda_check(cudaGetLastError(), "pack_cl_kernel");
+  prof_end(id, stream);
 }
 
 static PackGeom geom(const TcPlan& tp, bool dy_side, bool grad_pad) {
@@ -780,7 +788,7 @@ bool tc_forward(TcPlan& tp, DType dt, const Bindings& b, cudaStream_t stream) {
   run_stage(dt, tp.fold_fwd, b, w.wf, false, stream);
   TcGemmParams& p = w.fwd;
   p.out = b.y;
-  gemm(p, w.bn_fwd, w.t_fwd[0], w.t_fwd[1], w.t_fwd[2], stream);
+  gemm(p, w.bn_fwd, w.t_fwd[0], w.t_fwd[1], w.t_fwd[2], stream, "tc_gemm_fwd", tp.flops);
   return true;
 }
 
@@ -797,13 +805,13 @@ bool tc_backward(TcPlan& tp, DType dt, const Bindings& b, cudaStream_t stream) {
     run_stage(dt, tp.fold_dgrad, b, w.wt, false, stream);
     TcGemmParams& p = w.dg;
     p.out = b.dx;
-    gemm(p, w.bn_dg, w.t_dg[0], w.t_dg[1], w.t_dg[2], stream);
+    gemm(p, w.bn_dg, w.t_dg[0], w.t_dg[1], w.t_dg[2], stream, "tc_gemm_dgrad", tp.flops);
   }
   if (any_w) {
     pack_cl(b.x, dt, w.gx, w.xcl, stream);
     if (!dy_w_packed) pack_cl(b.dy, dt, w.gdy_w, w.dycl_w, stream);
     cuda_check(cudaMemsetAsync(w.dwf, 0, (size_t)tp.nwin() * tp.N * tp.C * sizeof(float), stream), "memset(dWf)");
-    gemm(w.wg, w.bn_wg, w.t_wg[0], w.t_wg[1], w.t_wg[2], stream);
+    gemm(w.wg, w.bn_wg, w.t_wg[0], w.t_wg[1], w.t_wg[2], stream, "tc_gemm_wgrad", tp.flops);
     // chain rule through the fold, into each requested weight gradient
     Bindings cb = b;
     cb.stages = {w.dwf};

@@ -1,0 +1,163 @@
+"""Search-time candidate evaluation, sharded one candidate batch per GPU.
+
+The reference evaluates a sampled operator inside ``mcts_step``
+(search.py:359-460): ``_score_completion`` computes FLOPs/params and the
+budget verdict (search.py:347-356); an over-budget candidate is logged
+with status ``over_budget`` and never executed; otherwise ``reward_fn``
+runs it (search.py:430-437) and a ``SampleRecord`` line is appended to
+the log (search.py:155-171).
+
+Here one *candidate evaluation* is: compile the operator (native lowering
++ plan), run forward, grad-input and every grad-weight on the device on
+seeded synthetic inputs, and check the results on the device with two
+size-independent identities of a multilinear operator y = A(x; w_1..w_n):
+
+    <dy, y> == <dx, x>          (adjoint of the x access)
+    <dy, y> == <dw_j, w_j>      (y is homogeneous of degree 1 in each w_j)
+
+Candidates are independent, so multi-GPU evaluation shards them across
+ranks by LPT on a predicted roofline time with NO collective on the data
+path; each rank writes its own records and the host merges
+them by sample id.
+"""
+from __future__ import annotations
+
+import math
+import time
+from dataclasses import dataclass
+from typing import List, Optional, Sequence
+
+# B200 roofline denominators used only to ORDER work (LPT); the measured
+# peaks in MEASURED_PEAKS.json are what bench.py reports against.
+_FP32_FLOPS = 60e12
+_HBM_BYTES = 6.4e12
+_LAUNCH_S = 4e-6
+
+
+def predicted_seconds(flops: int, n_bytes: int, launches: int = 6) -> float:
+    """Roofline time of one candidate (fwd + grad-input + grad-weights)."""
+    return max(3.0 * flops / _FP32_FLOPS, n_bytes / _HBM_BYTES) + launches * _LAUNCH_S
+
+
+def lpt_shard(costs: Sequence[float], world: int) -> List[List[int]]:
+    """Longest-processing-time assignment of candidate indices to ranks.
+
+    Deterministic: candidates are taken by decreasing cost (ties by index)
+    and each goes to the least-loaded rank (ties by rank).  Every index
+    appears in exactly one shard; shards are returned in index order."""
+    if world < 1:
+        raise ValueError("world must be >= 1")
+    loads = [0.0] * world
+    shards: List[List[int]] = [[] for _ in range(world)]
+    for i in sorted(range(len(costs)), key=lambda k: (-float(costs[k]), k)):
+        r = min(range(world), key=lambda q: (loads[q], q))
+        shards[r].append(i)
+        loads[r] += float(costs[i])
+    return [sorted(s) for s in shards]
+
+
+@dataclass(frozen=True)
+class EvalRecord:
+    """One evaluated candidate; ``line()`` follows the reference's sample
+    log grammar (search.py:166-171) with the adjoint error as the reward
+    field's companion diagnostics."""
+
+    sample_id: int
+    seed: int
+    flops: int
+    params: int
+    status: str            # "ok" | "over_budget" | "failed"
+    op: str
+    seconds: float = 0.0   # device time of fwd + bwd (CUDA events)
+    adjoint_err: float = 0.0
+
+    def line(self) -> str:
+        return (f"sample id={self.sample_id} iter=0 seed={self.seed} reward={0.0!r} flops={self.flops} "
+                f"params={self.params} status={self.status} op={self.op}")
+
+    def diag(self) -> str:
+        return f"diag id={self.sample_id} device_us={self.seconds * 1e6:.3f} adjoint_err={self.adjoint_err:.3e}"
+
+
+def within_budget(flops: int, params: int, flops_cap: Optional[int], params_cap: Optional[int]) -> bool:
+    """pgraph.check_budgets semantics as used by _score_completion (search.py:347-356)."""
+    if flops_cap is not None and flops > flops_cap:
+        return False
+    if params_cap is not None and params > params_cap:
+        return False
+    return True
+
+
+def _inner(a, b) -> float:
+    return float((a.double() * b.double()).sum())
+
+
+def evaluate(graph, sample_id: int, seed: int, dtype=None, device=None,
+             flops_cap: Optional[int] = None, params_cap: Optional[int] = None,
+             tol: Optional[float] = None) -> EvalRecord:
+    """Evaluate one candidate on the current CUDA device."""
+    import torch
+
+    from . import ops
+    from .pgraph import handle_for, print_steps
+
+    dtype = dtype or torch.float32
+    device = device or torch.device("cuda", torch.cuda.current_device())
+    h = handle_for(graph)
+    op = print_steps(graph)
+    if not within_budget(h.flops_unstaged, h.params, flops_cap, params_cap):
+        return EvalRecord(sample_id, seed, h.flops_unstaged, h.params, "over_budget", op)
+    gen = torch.Generator(device=device).manual_seed(seed)
+    x = torch.randn(h.x_shape, generator=gen, device=device, dtype=torch.float32).to(dtype)
+    ws = [torch.randn(s, generator=gen, device=device, dtype=torch.float32).to(dtype) for s in h.w_shapes]
+    dy = torch.randn(h.y_shape, generator=gen, device=device, dtype=torch.float32).to(dtype)
+    stream = torch.cuda.current_stream(device)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    try:
+        e0.record(stream)
+        y = ops.forward(h, x, ws)
+        dx, dws = ops.backward(h, x, ws, dy)
+        e1.record(stream)
+        e1.synchronize()
+    except Exception:  # a device-engine limit or launch failure: logged like a RewardFailure
+        return EvalRecord(sample_id, seed, h.flops_unstaged, h.params, "failed", op)
+    s = _inner(dy, y)
+    scale = max(1.0, math.sqrt(_inner(dy, dy) * max(_inner(y, y), 1e-30)))
+    err = abs(_inner(dx, x) - s) / scale
+    for w, g in zip(ws, dws):
+        err = max(err, abs(_inner(g, w) - s) / scale)
+    limit = tol if tol is not None else (1e-4 if dtype == torch.float32 else 2e-2 if dtype == torch.bfloat16 else 1e-10)
+    status = "ok" if err <= limit and math.isfinite(err) else "failed"
+    return EvalRecord(sample_id, seed, h.flops_unstaged, h.params, status, op,
+                      e0.elapsed_time(e1) / 1e3, err)
+
+
+def candidate_costs(graphs) -> List[float]:
+    """Predicted seconds per candidate from the native plan (CPU only)."""
+    from .pgraph import handle_for
+    out = []
+    for g in graphs:
+        h = handle_for(g)
+        nbytes = 4 * (2 * math.prod(h.x_shape) + 2 * math.prod(h.y_shape)
+                      + 2 * sum(math.prod(s) for s in h.w_shapes))
+        out.append(predicted_seconds(h.flops_unstaged, nbytes))
+    return out
+
+
+def run_shard(graphs, indices: Sequence[int], seed0: int = 0, dtype=None, flops_cap=None, params_cap=None):
+    """Evaluate ``graphs[i]`` for i in ``indices`` on this rank's device."""
+    recs = []
+    t0 = time.perf_counter()
+    for i in indices:
+        recs.append(evaluate(graphs[i], i, seed0 + i, dtype=dtype, flops_cap=flops_cap, params_cap=params_cap))
+    return recs, time.perf_counter() - t0
+
+
+def merge(shard_records) -> List[EvalRecord]:
+    """Host-side merge of per-rank records into one log ordered by sample id."""
+    out = [r for recs in shard_records for r in recs]
+    out.sort(key=lambda r: r.sample_id)
+    ids = [r.sample_id for r in out]
+    if len(set(ids)) != len(ids):
+        raise ValueError("a candidate was evaluated by two ranks")
+    return out
