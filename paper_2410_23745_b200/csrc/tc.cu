@@ -25,12 +25,15 @@
 #include <mutex>
 #include <set>
 #include <sstream>
+#include <tuple>
 
 #include "tc_gemm.cuh"
 
 namespace syno {
 
 using namespace tc;
+
+constexpr int MAXFW = 4;  // weights of a fast fold
 
 // ---------------------------------------------------------------------------
 // TMA descriptors
@@ -53,6 +56,11 @@ static EncodeTiledFn encode_fn() {
 }
 
 // 3-D bf16 map [d0 (K, contiguous)][d1 (rows)][d2 (planes)], box [64][box1][1], 128B swizzle.
+struct MapSpec {
+  uint64_t d0 = 0, d1 = 0, d2 = 0, p1 = 0, p2 = 0;
+  uint32_t box1 = 0;
+};
+
 static CUtensorMap make_map(const void* base, uint64_t d0, uint64_t d1, uint64_t d2, uint64_t pitch1_elems,
                             uint64_t pitch2_elems, uint32_t box1) {
   CUtensorMap m;
@@ -67,43 +75,81 @@ static CUtensorMap make_map(const void* base, uint64_t d0, uint64_t d1, uint64_t
   return m;
 }
 
+static CUtensorMap make_map(const void* base, const MapSpec& m) {
+  return make_map(base, m.d0, m.d1, m.d2, m.p1, m.p2, m.box1);
+}
+
+static MapSpec map_spec(uint64_t d0, uint64_t d1, uint64_t d2, uint64_t p1, uint64_t p2, uint32_t box1) {
+  MapSpec m;
+  m.d0 = d0;
+  m.d1 = d1;
+  m.d2 = d2;
+  m.p1 = p1;
+  m.p2 = p2;
+  m.box1 = box1;
+  return m;
+}
+
 // ---------------------------------------------------------------------------
 // Packing kernels (bandwidth-bound layout transforms)
 // ---------------------------------------------------------------------------
+
+// fp32 operands run on the bf16 tensor cores as split pairs v = hi + lo
+// (hi = bf16(v), lo = bf16(v - hi)); a product x*w is recovered to ~2^-17
+// relative as xh*wh + xh*wl + xl*wh, i.e. a GEMM over THREE parts of the
+// contraction dim with operand patterns A = (hi, hi, lo), B = (hi, lo, hi).
+enum Split : int32_t {
+  SPLIT_NONE = 0,
+  SPLIT_CH = 1,   // parts along the channel (K) dim: dst channel c' = part*Cp + c
+  SPLIT_IMG = 2,  // parts along the image dim (wgrad, K = pixels): dst image = part*n_img + img
+};
 
 struct PackGeom {
   int64_t s_img, s_c, s_h, s_w;  // source element strides
   int32_t C, Hin, Win;           // source extents
   int32_t Sh, Sw;                // phase counts (strides)
   int32_t lo_h, lo_w, Hp, Wp;    // padded plane grid
-  int32_t n_img;
-  int32_t Cp;                    // channels-last pitch (multiple of 8)
+  int32_t n_img;                 // source images
+  int32_t Cp;                    // channels-last pitch of one part (multiple of 8)
+  int32_t split;                 // Split
+  uint32_t lo_mask;              // bit k: part k holds lo(v), else hi(v)
   int64_t Fpitch;                // channel-major row pitch (multiple of 8)
+  __host__ __device__ int32_t parts() const { return split == SPLIT_NONE ? 1 : 3; }
+  __host__ __device__ int32_t n_img_out() const { return split == SPLIT_IMG ? 3 * n_img : n_img; }
+  __host__ __device__ int32_t Ct() const { return split == SPLIT_CH ? 3 * Cp : Cp; }  // dst channel pitch
 };
 
-// dst[plane][img][hp][wp][cp] (flat pixel f = ((plane*n_img + img)*Hp + hp)*Wp + wp),
-// zero outside the source.  A block moves 32 consecutive flat pixels x 64
-// channels through shared memory: lanes walk pixels for the NCHW reads
-// (coalesced along w), 8 threads per pixel write 16-byte channel chunks.
+// dst[plane][img'][hp][wp][c'] (flat pixel f = ((plane*n_img' + img')*Hp + hp)*Wp + wp),
+// zero outside the source.  A block moves 64 consecutive flat pixels x 64
+// destination channels through shared memory: lanes walk pixels for the
+// NCHW reads (coalesced along w), 8 threads per pixel write 16-byte
+// channel chunks.
 template <typename TI>
 __global__ void __launch_bounds__(256) pack_cl_kernel(const TI* __restrict__ src, __nv_bfloat16* __restrict__ dst,
                                                       PackGeom g, int64_t total_pix) {
-  __shared__ __nv_bfloat16 tile[64][34];
-  const int64_t f0 = (int64_t)blockIdx.x * 32;
+  __shared__ __nv_bfloat16 tile[64][66];
+  const int64_t f0 = (int64_t)blockIdx.x * 64;
   const int cb = blockIdx.y;
   const int t = threadIdx.x;
-  {
-    const int lane = t & 31, warp = t >> 5;
-    const int64_t f = f0 + lane;
+  const int lane = t & 31, warp = t >> 5;
+  const int n_out = g.n_img_out();
+#pragma unroll
+  for (int half = 0; half < 2; ++half) {
+    const int64_t f = f0 + lane + 32 * half;
     bool inb = f < total_pix;
     const TI* row = src;
+    int part = 0;
     if (inb) {
       const int wp = (int)(f % g.Wp);
       int64_t q = f / g.Wp;
       const int hp = (int)(q % g.Hp);
       q /= g.Hp;
-      const int img = (int)(q % g.n_img);
-      const int plane = (int)(q / g.n_img);
+      int img = (int)(q % n_out);
+      const int plane = (int)(q / n_out);
+      if (g.split == SPLIT_IMG) {
+        part = img / g.n_img;
+        img -= part * g.n_img;
+      }
       const int hi = g.Sh * (hp - g.lo_h) + plane / g.Sw;
       const int wi = g.Sw * (wp - g.lo_w) + plane % g.Sw;
       inb = hi >= 0 && hi < g.Hin && wi >= 0 && wi < g.Win;
@@ -112,21 +158,294 @@ __global__ void __launch_bounds__(256) pack_cl_kernel(const TI* __restrict__ src
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
       const int cl = warp * 8 + k;
-      const int c = cb * 64 + cl;
+      int c = cb * 64 + cl;
+      int pt = part;
+      if (g.split == SPLIT_CH) {
+        pt = c / g.Cp;
+        c -= pt * g.Cp;
+      }
       float v = 0.f;
-      if (inb && c < g.C) v = (float)row[c * g.s_c];
-      tile[cl][lane] = __float2bfloat16(v);
+      if (inb && c < g.C && pt < g.parts()) v = (float)row[c * g.s_c];
+      __nv_bfloat16 hv = __float2bfloat16(v);
+      if (g.split != SPLIT_NONE && ((g.lo_mask >> pt) & 1u)) hv = __float2bfloat16(v - __bfloat162float(hv));
+      tile[cl][lane + 32 * half] = hv;
     }
   }
   __syncthreads();
-  const int w = t / 8, cc = (t % 8) * 8;
-  const int64_t f = f0 + w;
-  const int c0 = cb * 64 + cc;
-  if (f < total_pix && c0 < g.Cp) {
-    __align__(16) __nv_bfloat16 v[8];
+  const int Ct = g.Ct();
 #pragma unroll
-    for (int k = 0; k < 8; ++k) v[k] = tile[cc + k][w];
-    *reinterpret_cast<uint4*>(dst + f * g.Cp + c0) = *reinterpret_cast<const uint4*>(v);
+  for (int half = 0; half < 2; ++half) {
+    const int w = t / 8 + 32 * half, cc = (t % 8) * 8;
+    const int64_t f = f0 + w;
+    const int c0 = cb * 64 + cc;
+    if (f < total_pix && c0 < Ct) {
+      __align__(16) __nv_bfloat16 v[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) v[k] = tile[cc + k][w];
+      *reinterpret_cast<uint4*>(dst + f * Ct + c0) = *reinterpret_cast<const uint4*>(v);
+    }
+  }
+}
+
+// Folded fp32 weights [rows][Cp] -> bf16 split parts [rows][3*Cp] (pattern lo_mask).
+__global__ void __launch_bounds__(256) split_rows_kernel(const float* __restrict__ src, __nv_bfloat16* __restrict__ dst,
+                                                         int64_t rows, int32_t Cp, uint32_t lo_mask) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t total = rows * 3 * (int64_t)Cp;
+  if (i >= total) return;
+  const int64_t r = i / (3 * (int64_t)Cp);
+  const int cc = (int)(i - r * 3 * (int64_t)Cp);
+  const int part = cc / Cp, c = cc - part * Cp;
+  const float v = src[r * Cp + c];
+  __nv_bfloat16 hv = __float2bfloat16(v);
+  if ((lo_mask >> part) & 1u) hv = __float2bfloat16(v - __bfloat162float(hv));
+  dst[i] = hv;
+}
+
+// Source-row packer: each block moves PK_PIX consecutive source pixels
+// (whole rows of one image plane) x 64 destination channels.  Reads walk
+// each channel's pixels contiguously (vectorised when the row allows),
+// the tile is transposed in shared memory, and every destination pixel's
+// 64 channels go out as 128 contiguous bytes.  Only data positions are
+// written: the padding of the flat grid is zeroed once when the workspace
+// is built and never changes.
+constexpr int PK_PIX = 128;
+
+template <typename TI, int V>
+__global__ void __launch_bounds__(256) pack_rows_kernel(const TI* __restrict__ src, __nv_bfloat16* __restrict__ dst,
+                                                        PackGeom g, int32_t rows_per_block, int64_t total_rows) {
+  __shared__ __align__(16) __nv_bfloat16 tile[PK_PIX][72];
+  const int t = threadIdx.x;
+  const int cb = blockIdx.y;
+  const int n_out = g.n_img_out();
+  // rows of <= PK_PIX pixels: rows_per_block whole rows; wider rows: one PK_PIX segment per block
+  int64_t row0;
+  int nrows, wbeg, Win;
+  if (g.Win <= PK_PIX) {
+    row0 = (int64_t)blockIdx.x * rows_per_block;
+    nrows = (int)min((int64_t)rows_per_block, total_rows - row0);
+    wbeg = 0;
+    Win = g.Win;
+  } else {
+    const int nseg = (g.Win + PK_PIX - 1) / PK_PIX;
+    row0 = blockIdx.x / nseg;
+    nrows = 1;
+    wbeg = (int)(blockIdx.x % nseg) * PK_PIX;
+    Win = min(PK_PIX, g.Win - wbeg);
+  }
+  const int npix = nrows * Win;
+  // ---- read: (channel, pixel-vector) pairs, pixels fastest
+  const int vpr = Win / V;                  // vectors per row
+  const int nvec = nrows * vpr;
+  for (int i = t; i < 64 * nvec; i += 256) {
+    const int cl = i / nvec;
+    const int vi = i - cl * nvec;
+    const int rr = vi / vpr;
+    const int w0 = (vi - rr * vpr) * V;
+    const int64_t row = row0 + rr;          // (img', hi) flattened
+    int img = (int)(row / g.Hin);
+    const int hi = (int)(row - (int64_t)img * g.Hin);
+    int c = cb * 64 + cl;
+    int part = 0;
+    if (g.split == SPLIT_IMG) {
+      part = img / g.n_img;
+      img -= part * g.n_img;
+    } else if (g.split == SPLIT_CH) {
+      part = c / g.Cp;
+      c -= part * g.Cp;
+    }
+    float v[V];
+    if (c < g.C && part < g.parts()) {
+      const TI* p = src + img * g.s_img + (int64_t)c * g.s_c + (int64_t)hi * g.s_h + (int64_t)(wbeg + w0) * g.s_w;
+      if (V == 8 && sizeof(TI) == 2) {
+        const uint4 q = __ldg(reinterpret_cast<const uint4*>(p));
+        const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&q);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float2 f2 = __bfloat1622float2(h2[e]);
+          v[2 * e] = f2.x;
+          v[2 * e + 1] = f2.y;
+        }
+      } else if (V == 4 && sizeof(TI) == 4) {
+        const float4 q = __ldg(reinterpret_cast<const float4*>(p));
+        v[0] = q.x;
+        v[1] = q.y;
+        v[2] = q.z;
+        v[3] = q.w;
+      } else {
+#pragma unroll
+        for (int e = 0; e < V; ++e) v[e] = (float)p[(int64_t)e * g.s_w];
+      }
+    } else {
+#pragma unroll
+      for (int e = 0; e < V; ++e) v[e] = 0.f;
+    }
+    const bool lo = g.split != SPLIT_NONE && ((g.lo_mask >> part) & 1u);
+#pragma unroll
+    for (int e = 0; e < V; ++e) {
+      __nv_bfloat16 hv = __float2bfloat16(v[e]);
+      if (lo) hv = __float2bfloat16(v[e] - __bfloat162float(hv));
+      tile[rr * Win + w0 + e][cl] = hv;
+    }
+  }
+  __syncthreads();
+  // ---- write: 8 threads per destination pixel, 16 bytes each
+  const int Ct = g.Ct();
+  for (int i = t; i < npix * 8; i += 256) {
+    const int px = i >> 3, chunk = i & 7;
+    const int c0 = cb * 64 + chunk * 8;
+    if (c0 >= Ct) continue;
+    const int rr = px / Win;
+    const int wi = wbeg + px - rr * Win;
+    const int64_t row = row0 + rr;
+    const int img = (int)(row / g.Hin);
+    const int hi = (int)(row - (int64_t)img * g.Hin);
+    const int ph = hi % g.Sh, pw = wi % g.Sw;
+    const int hp = hi / g.Sh + g.lo_h, wp = wi / g.Sw + g.lo_w;
+    if (hp >= g.Hp || wp >= g.Wp) continue;  // never read by any window
+    const int plane = ph * g.Sw + pw;
+    const int64_t f = (((int64_t)plane * n_out + img) * g.Hp + hp) * g.Wp + wp;
+    *reinterpret_cast<uint4*>(dst + f * Ct + c0) = *reinterpret_cast<const uint4*>(&tile[px][chunk * 8]);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Weight transforms (fold into the B operand, chain rule out of dWf)
+// ---------------------------------------------------------------------------
+
+struct FoldArgs {
+  const void* w[MAXFW];
+  int64_t s[MAXFW][4];   // strides along fold slots (rh, rw, n, ci)
+  int32_t nw, f32;       // weight dtype: f32 or bf16
+  int32_t ext[4];        // Kh, Kw, A, B extents (A/B = rows/cols of the operand)
+  int32_t sl_a, sl_b;    // fold slots of A and B (2 = n, 3 = ci)
+  int32_t Bp;            // padded B pitch of one part
+  int32_t split;         // 1: three bf16 parts (hi, lo, hi) at pitch 3*Bp
+  __nv_bfloat16* out;
+};
+
+// out[rh][rw][a][b'] = prod_j w_j[...]; one block row per (rh, rw, a).
+__global__ void __launch_bounds__(128) fold_kernel(const __grid_constant__ FoldArgs f) {
+  const int row = blockIdx.y;
+  const int a = row % f.ext[2];
+  const int rw = (row / f.ext[2]) % f.ext[1];
+  const int rh = row / (f.ext[2] * f.ext[1]);
+  const int parts = f.split ? 3 : 1;
+  for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < f.Bp; b += gridDim.x * blockDim.x) {
+    float v = 0.f;
+    if (b < f.ext[3]) {
+      v = 1.f;
+      for (int j = 0; j < f.nw; ++j) {
+        const int64_t off = rh * f.s[j][0] + rw * f.s[j][1] + (int64_t)a * f.s[j][f.sl_a] + (int64_t)b * f.s[j][f.sl_b];
+        v *= f.f32 ? __ldg(reinterpret_cast<const float*>(f.w[j]) + off)
+                   : __bfloat162float(__ldg(reinterpret_cast<const __nv_bfloat16*>(f.w[j]) + off));
+      }
+    }
+    __nv_bfloat16* o = f.out + (int64_t)row * parts * f.Bp + b;
+    const __nv_bfloat16 hi = __float2bfloat16(v);
+    o[0] = hi;
+    if (parts == 3) {
+      o[f.Bp] = __float2bfloat16(v - __bfloat162float(hi));
+      o[2 * f.Bp] = hi;
+    }
+  }
+}
+
+struct ChainArgs {
+  const float* dwf;      // [Kh][Kw][N][C] fp32
+  const void* w[MAXFW];
+  int64_t s[MAXFW][4];
+  int32_t nw, j, f32;    // weights, the weight differentiated, dtype of w / out
+  int32_t ext[4];        // Kh, Kw, N, C
+  int32_t nout, nred;
+  int32_t out_l[4], red_l[4];  // fold slots of the output / reduced loops (ascending)
+  int64_t out_count, R, r_chunk;
+  void* out;
+  float* partial;        // [out_count][nsplit] (block mode)
+  unsigned* counter;     // [out_count], zero between calls (block mode)
+};
+
+__device__ __forceinline__ float chain_term(const ChainArgs& c, const int* d) {
+  const int64_t df = ((int64_t)(d[0] * c.ext[1] + d[1]) * c.ext[2] + d[2]) * c.ext[3] + d[3];
+  float v = __ldg(c.dwf + df);
+  for (int k = 0; k < c.nw; ++k) {
+    if (k == c.j) continue;
+    const int64_t off = d[0] * c.s[k][0] + d[1] * c.s[k][1] + (int64_t)d[2] * c.s[k][2] + (int64_t)d[3] * c.s[k][3];
+    v *= c.f32 ? __ldg(reinterpret_cast<const float*>(c.w[k]) + off)
+               : __bfloat162float(__ldg(reinterpret_cast<const __nv_bfloat16*>(c.w[k]) + off));
+  }
+  return v;
+}
+
+__device__ __forceinline__ void chain_decode(const ChainArgs& c, int64_t o, int64_t r, int* d) {
+  d[0] = d[1] = d[2] = d[3] = 0;
+  for (int k = c.nout - 1; k >= 0; --k) {
+    const int l = c.out_l[k];
+    d[l] = (int)(o % c.ext[l]);
+    o /= c.ext[l];
+  }
+  for (int k = c.nred - 1; k >= 0; --k) {
+    const int l = c.red_l[k];
+    d[l] = (int)(r % c.ext[l]);
+    r /= c.ext[l];
+  }
+}
+
+__device__ __forceinline__ void chain_store(const ChainArgs& c, const int* d, float v) {
+  const int64_t off = d[0] * c.s[c.j][0] + d[1] * c.s[c.j][1] + (int64_t)d[2] * c.s[c.j][2] + (int64_t)d[3] * c.s[c.j][3];
+  if (c.f32) reinterpret_cast<float*>(c.out)[off] = v;
+  else reinterpret_cast<__nv_bfloat16*>(c.out)[off] = __float2bfloat16(v);
+}
+
+// dW_j = sum over the loops w_j does not use of dWf * prod_{k != j} w_k.
+// Thread per output (short reductions), outputs ordered like dWf (ci fastest).
+__global__ void __launch_bounds__(256) chain_thread_kernel(const __grid_constant__ ChainArgs c) {
+  const int64_t o = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (o >= c.out_count) return;
+  int d[4];
+  float acc = 0.f;
+  for (int64_t r = 0; r < c.R; ++r) {
+    chain_decode(c, o, r, d);
+    acc += chain_term(c, d);
+  }
+  chain_decode(c, o, 0, d);
+  chain_store(c, d, acc);
+}
+
+// Long reductions: block (o, split) reduces one chunk; the last block of an
+// output sums the partials in split order (deterministic) and stores.
+__global__ void __launch_bounds__(256) chain_block_kernel(const __grid_constant__ ChainArgs c) {
+  const int64_t o = blockIdx.x;
+  const int nsplit = gridDim.y;
+  const int64_t r0 = (int64_t)blockIdx.y * c.r_chunk;
+  const int64_t r1 = min(c.R, r0 + c.r_chunk);
+  int d[4];
+  float acc = 0.f;
+  for (int64_t r = r0 + threadIdx.x; r < r1; r += blockDim.x) {
+    chain_decode(c, o, r, d);
+    acc += chain_term(c, d);
+  }
+#pragma unroll
+  for (int k = 16; k > 0; k >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, k);
+  __shared__ float part[8];
+  __shared__ bool last;
+  if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float t = 0.f;
+    for (int k = 0; k < (int)(blockDim.x >> 5); ++k) t += part[k];
+    c.partial[o * nsplit + blockIdx.y] = t;
+    __threadfence();
+    last = atomicAdd(c.counter + o, 1u) == (unsigned)nsplit - 1;
+  }
+  __syncthreads();
+  if (last && threadIdx.x == 0) {
+    __threadfence();
+    float t = 0.f;
+    for (int k = 0; k < nsplit; ++k) t += *((volatile float*)c.partial + o * nsplit + k);
+    chain_decode(c, o, 0, d);
+    chain_store(c, d, t);
+    c.counter[o] = 0;  // ready for the next call (stream order)
   }
 }
 
@@ -144,8 +463,13 @@ struct PixDim {
   int64_t xs = 0, ys = 0;  // element strides of the coordinate in x and y
   int lo = 0, hi = 0;  // forward padding of the phase planes
   int dlo = 0, dhi = 0;  // grad-input padding of dy
-  int64_t Ep() const { return E + lo + hi; }
-  int64_t dEp() const { return E + dlo + dhi; }
+  bool share = false;   // pad rows may be shared between neighbours (all pads read zero)
+  // Padded extent of the flat grid.  When every out-of-footprint read is a
+  // zero (x has exactly S*E rows), the trailing pad of one row / image is
+  // the leading pad of the next, so max(lo, hi) pad rows suffice instead of
+  // lo + hi (a 4x4 map: 25 instead of 36 rows per image).
+  int64_t Ep() const { return E + (share ? std::max(lo, hi) : lo + hi); }
+  int64_t dEp() const { return E + std::max(dlo, dhi); }
   int delta(int r) const { return (int)std::floor((double)(r - c) / S); }
   int phi(int r) const { return (int)(((r - c) % S + S) % S); }
 };
@@ -162,9 +486,17 @@ struct TcPlan {
   DevStage fold_fwd, fold_dgrad;
   std::vector<DevStage> chain;    // dW_j from the folded gradient
   std::vector<int64_t> w_numel;
+  // Direct weight transforms: every weight coordinate is a bare fold loop
+  // (rh, rw, n, ci) with the loop's full extent and there are no weight-only
+  // reduces, so a weight offset is affine in the fold loops.
+  bool fast_fold = false;
+  int nw = 0;
+  int64_t wstr[MAXFW][4] = {};  // element strides of w_j along (rh, rw, n, ci)
   std::mutex mu;                  // guards ws
-  std::map<std::pair<int, void*>, std::unique_ptr<struct TcWs>> ws;  // per (device, stream)
+  std::map<std::tuple<int, void*, int>, std::unique_ptr<struct TcWs>> ws;  // per (device, stream, dtype)
   int nwin() const { return dh.K * dw.K; }
+  int64_t y_numel() const { return (int64_t)n_img * dh.E * dw.E * N; }
+  int64_t x_numel() const { return (int64_t)n_img * dh.Ein * dw.Ein * C; }
 };
 
 static std::vector<int64_t> rm_strides(const std::vector<int64_t>& ext) {
@@ -292,6 +624,7 @@ static TcPlan* try_match(const Plan& plan) {
     // grad-input reads dy at u - delta(r)
     p->dlo = dmax;
     p->dhi = -dmin;
+    p->share = p->Ein <= (int64_t)p->S * p->E;
     if (p->S > 2 || p->E * p->S < 1) return nullptr;
   }
   if (tp->nwin() > MAXWIN) return nullptr;
@@ -368,11 +701,53 @@ bool tc_matches(const Plan& plan) {
   return true;
 }
 
+// Fast weight transforms apply when each weight coordinate is a bare fold
+// loop (rh, rw, n, ci) of full extent: no weight-only reduces, no range checks.
+static void setup_fast_fold(const Plan& plan, TcPlan& tp) {
+  const CStage& S = plan.unstaged;
+  const int A = (int)S.axis_ext.size();
+  int naxis = -1, chan = -1;
+  for (int a = 0; a < A; ++a) {
+    bool in_x = false;
+    for (auto& e : S.terms[0].coords) {
+      std::vector<int> ls;
+      c_loops(e, &ls);
+      in_x = in_x || std::count(ls.begin(), ls.end(), a);
+    }
+    if (!in_x) naxis = a;
+  }
+  for (auto& e : S.terms[0].coords)
+    if (e->op == COp::Loop && e->loop >= A) chan = e->loop;
+  std::map<int, int> slot;
+  if (tp.dh.win >= 0) slot[tp.dh.win] = 0;
+  if (tp.dw.win >= 0) slot[tp.dw.win] = 1;
+  slot[naxis] = 2;
+  slot[chan] = 3;
+  const int nw = (int)S.terms.size() - 1;
+  if (nw < 1 || nw > MAXFW) return;
+  for (int j = 0; j < nw; ++j) {
+    const CTerm& t = S.terms[j + 1];
+    auto st = rm_strides(t.t.extents);
+    for (size_t d = 0; d < t.coords.size(); ++d) {
+      const CE& e = t.coords[d];
+      if (e->op != COp::Loop) return;
+      auto it = slot.find(e->loop);
+      if (it == slot.end()) return;  // weight-only reduce: the general fold stage handles it
+      if (t.t.extents[d] != S.ext(e->loop)) return;
+      if (tp.wstr[j][it->second] != 0) return;
+      tp.wstr[j][it->second] = st[d];
+    }
+  }
+  tp.nw = nw;
+  tp.fast_fold = getenv("SYNO_TC_SLOW_FOLD") == nullptr;
+}
+
 TcPlanPtr tc_build(const Plan& plan, cudaStream_t stream) {
   TcPlan* raw = try_match(plan);
   if (!raw) return TcPlanPtr();
   TcPlanPtr tp(raw);
   tp->flops = (double)plan.flops_unstaged;
+  setup_fast_fold(plan, *tp);
   build_dev_stage(fold_stage(plan, *tp, false, true), &tp->fold_fwd, stream);
   if (tp->dgrad_ok) build_dev_stage(fold_stage(plan, *tp, true, true), &tp->fold_dgrad, stream);
   // chain rule through the fold: dW_j from dWf[rh][rw][n][ci] (fp32)
@@ -482,23 +857,95 @@ static void gemm(TcGemmParams& p, int bn, int m_tiles, int n_tiles, int z_tiles,
 
 static int mgroup_of(int bn) { return bn == 64 ? mgroup<64>() : bn == 128 ? mgroup<128>() : mgroup<256>(); }
 
-static int pick_bn(int n) { return n <= 64 ? 64 : n <= 128 ? 128 : 256; }
+// MODE_ROWS work split for small problems: fewer M tiles per step (G) and
+// then a split of the channel blocks across CTAs (fp32 atomic output), until
+// the persistent grid has at least one tile per SM.
+struct RowsTiling {
+  int G, rs;
+  int64_t m_tiles;
+};
 
-static void pack_cl(const void* src, DType dt, const PackGeom& g, __nv_bfloat16* dst, cudaStream_t stream) {
-  const int64_t pix = (int64_t)g.Sh * g.Sw * g.n_img * g.Hp * g.Wp;
-  dim3 grid((unsigned)((pix + 31) / 32), (unsigned)((g.Cp + 63) / 64));
-  const double src_elems = (double)g.n_img * g.C * g.Hin * g.Win;
-  const int id = prof_begin("pack_cl", 0.0, src_elems * (dt == DT_BF16 ? 2 : 4) + (double)pix * g.Cp * 2, stream);
+static RowsTiling rows_tiling(int64_t F, int n_tiles, int groups, int bn, int n_cblocks) {
+  const int sms = sm_count();
+  auto mt = [&](int g) { return (F + (int64_t)g * BM - 1) / ((int64_t)g * BM); };
+  int G = mgroup_of(bn);
+  while (G > 1 && mt(G) * n_tiles * groups < sms) G /= 2;
+  const int64_t tiles = mt(G) * n_tiles * groups;
+  int rs = 1;
+  if (tiles < sms && n_cblocks > 1 && getenv("SYNO_TC_NO_RSPLIT") == nullptr)
+    rs = (int)std::min<int64_t>(n_cblocks, (sms + tiles - 1) / tiles);
+  return {G, rs, mt(G)};
+}
+
+__global__ void cast_f32_bf16_kernel(const float* __restrict__ in, __nv_bfloat16* __restrict__ out, int64_t n) {
+  const int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4;
+  if (i + 3 < n) {
+    const float4 v = *reinterpret_cast<const float4*>(in + i);
+    __nv_bfloat162 a = __floats2bfloat162_rn(v.x, v.y), b = __floats2bfloat162_rn(v.z, v.w);
+    *reinterpret_cast<__nv_bfloat162*>(out + i) = a;
+    *reinterpret_cast<__nv_bfloat162*>(out + i + 2) = b;
+  } else {
+    for (int64_t k = i; k < n; ++k) out[k] = __float2bfloat16(in[k]);
+  }
+}
+
+static void cast_to_bf16(const float* in, void* out, int64_t n, cudaStream_t stream) {
+  const int id = prof_begin("cast_f32_bf16", 0.0, (double)n * 6, stream);
   note_launch();
-  if (dt == DT_BF16) pack_cl_kernel<__nv_bfloat16><<<grid, 256, 0, stream>>>((const __nv_bfloat16*)src, dst, g, pix);
-  else pack_cl_kernel<float><<<grid, 256, 0, stream>>>((const float*)src, dst, g, pix);
-  cuda_check(cudaGetLastError(), "pack_cl_kernel");
+  cast_f32_bf16_kernel<<<(unsigned)((n / 4 + 256) / 256), 256, 0, stream>>>(in, static_cast<__nv_bfloat16*>(out), n);
+  cuda_check(cudaGetLastError(), "cast_f32_bf16_kernel");
   prof_end(id, stream);
 }
 
-static PackGeom geom(const TcPlan& tp, bool dy_side, bool grad_pad) {
+static int pick_bn(int n) { return n <= 64 ? 64 : n <= 128 ? 128 : 256; }
+
+template <typename TI, int V>
+static void launch_pack_rows(const void* src, const PackGeom& g, __nv_bfloat16* dst, dim3 grid, int rpb,
+                             int64_t rows, cudaStream_t stream) {
+  pack_rows_kernel<TI, V><<<grid, 256, 0, stream>>>(static_cast<const TI*>(src), dst, g, rpb, rows);
+}
+
+static void pack_cl(const void* src, DType dt, const PackGeom& g, __nv_bfloat16* dst, cudaStream_t stream) {
+  // one block = whole source rows (<= PK_PIX pixels) or one PK_PIX segment of a wider row
+  const int rpb = std::max(1, PK_PIX / g.Win);
+  const int64_t rows = (int64_t)g.n_img_out() * g.Hin;
+  const int64_t blocks = g.Win <= PK_PIX ? (rows + rpb - 1) / rpb : rows * ((g.Win + PK_PIX - 1) / PK_PIX);
+  dim3 grid((unsigned)blocks, (unsigned)((g.Ct() + 63) / 64));
+  const double src_elems = (double)g.n_img_out() * g.C * g.Hin * g.Win;
+  const int id = prof_begin("pack_cl", 0.0, src_elems * (dt == DT_BF16 ? 2 : 4) * (g.split == SPLIT_CH ? 1 : 1) +
+                                                src_elems * (g.split == SPLIT_CH ? 3 : 1) * 2, stream);
+  note_launch();
+  const uintptr_t base = reinterpret_cast<uintptr_t>(src);
+  const bool unit_w = g.s_w == 1;
+  auto aligned = [&](int v, int es) {
+    return unit_w && g.Win % v == 0 && (g.Win <= PK_PIX || PK_PIX % v == 0) && g.s_h % v == 0 && g.s_c % v == 0 && g.s_img % v == 0 && base % (v * es) == 0;
+  };
+  if (dt == DT_BF16) {
+    if (aligned(8, 2)) launch_pack_rows<__nv_bfloat16, 8>(src, g, dst, grid, rpb, rows, stream);
+    else launch_pack_rows<__nv_bfloat16, 1>(src, g, dst, grid, rpb, rows, stream);
+  } else {
+    if (aligned(4, 4)) launch_pack_rows<float, 4>(src, g, dst, grid, rpb, rows, stream);
+    else launch_pack_rows<float, 1>(src, g, dst, grid, rpb, rows, stream);
+  }
+  cuda_check(cudaGetLastError(), "pack_rows_kernel");
+  prof_end(id, stream);
+}
+
+static void split_rows(const float* src, __nv_bfloat16* dst, int64_t rows, int Cp, uint32_t lo_mask,
+                       cudaStream_t stream) {
+  const int64_t total = rows * 3 * (int64_t)Cp;
+  const int id = prof_begin("split_weights", 0.0, (double)rows * Cp * 4 + (double)total * 2, stream);
+  note_launch();
+  split_rows_kernel<<<(unsigned)((total + 255) / 256), 256, 0, stream>>>(src, dst, rows, Cp, lo_mask);
+  cuda_check(cudaGetLastError(), "split_rows_kernel");
+  prof_end(id, stream);
+}
+
+static PackGeom geom(const TcPlan& tp, bool dy_side, bool grad_pad, int split = SPLIT_NONE, uint32_t lo_mask = 0) {
   PackGeom g{};
   g.n_img = tp.n_img;
+  g.split = split;
+  g.lo_mask = lo_mask;
   if (!dy_side) {
     g.s_img = tp.x_img;
     g.s_c = tp.x_c;
@@ -525,7 +972,7 @@ static PackGeom geom(const TcPlan& tp, bool dy_side, bool grad_pad) {
   g.lo_w = grad_pad ? tp.dw.dlo : tp.dw.lo;
   g.Hp = (int)(grad_pad ? tp.dh.dEp() : tp.dh.Ep());
   g.Wp = (int)(grad_pad ? tp.dw.dEp() : tp.dw.Ep());
-  const int64_t F = (int64_t)g.n_img * g.Hp * g.Wp;
+  const int64_t F = (int64_t)g.n_img_out() * g.Hp * g.Wp;
   g.Fpitch = (F + 7) / 8 * 8;
   return g;
 }
@@ -547,7 +994,7 @@ static int base_mode() {
   return m;
 }
 
-static void rows_schedule(TcGemmParams& p, std::vector<std::vector<Win>> groups, int bn) {
+static void rows_schedule(TcGemmParams& p, std::vector<std::vector<Win>> groups, int bn, int G) {
   int n = 0, nc = 0, span = 0;
   if (groups.size() > 8) fail(SYNO_E_UNSUPPORTED, "too many window groups");
   for (size_t g = 0; g < groups.size(); ++g) {
@@ -575,7 +1022,7 @@ static void rows_schedule(TcGemmParams& p, std::vector<std::vector<Win>> groups,
     p.g_chunk1[g] = nc;
   }
   p.n_win = n;
-  const int G = bn >= 256 ? 1 : 256 / bn;  // tc::mgroup<BN>()
+  p.G = G;
   p.a_rows = (G * BM + span + 63) / 64 * 64;
   p.a_tx = (uint32_t)p.a_rows * BK * 2;
   p.a_stage_bytes = (int)p.a_tx;
@@ -584,16 +1031,30 @@ static void rows_schedule(TcGemmParams& p, std::vector<std::vector<Win>> groups,
   p.dbg = getenv("SYNO_TC_DEBUG") ? atoi(getenv("SYNO_TC_DEBUG")) : 0;
 }
 
-// Per (device, stream) workspace of an operator: packed operands, folded
-// weights, the fp32 grad-weight accumulator and the fully built GEMM
+// Per (device, stream, dtype) workspace of an operator: packed operands,
+// folded weights, the fp32 grad-weight accumulator and the fully built GEMM
 // parameters (their TMA maps point into the workspace, so they are encoded
 // once).  Steady-state calls only launch kernels: no allocation, no host
 // synchronisation, CUDA-graph capturable.
+//
+// bf16: operands are packed once.  fp32: every operand is packed as three
+// bf16 parts along the GEMM's contraction dim (channels for fwd / dgrad,
+// images for wgrad), A = (hi, hi, lo) and B = (hi, lo, hi), so the same
+// tcgen05 kernel accumulates xh*wh + xh*wl + xl*wh in fp32 (see Split).
 struct TcWs {
-  __nv_bfloat16 *xcl = nullptr, *wf = nullptr, *dycl_g = nullptr, *dycl_w = nullptr, *wt = nullptr;
-  float* dwf = nullptr;
-  PackGeom gx{}, gdy_g{}, gdy_w{};
-  bool share_dy = false;
+  bool f32 = false;
+  __nv_bfloat16 *xcl = nullptr, *xclw = nullptr, *wf = nullptr, *dycl_g = nullptr, *dycl_w = nullptr, *wt = nullptr;
+  float *dwf = nullptr, *wf32 = nullptr, *wt32 = nullptr;
+  float *ysc = nullptr, *dxsc = nullptr;  // fp32 accumulators of split-K (bf16 outputs)
+  float* chain_partial = nullptr;     // fast chain rule, block mode
+  unsigned* chain_counter = nullptr;
+  int chain_nsplit[MAXFW] = {};       // 0: thread mode
+  // zero-copy operands: a source already in the packed layout (channels-last,
+  // unpadded, e.g. QKV activations) is read by TMA in place
+  bool x_ident = false, xw_ident = false, dyg_ident = false, dyw_ident = false;
+  MapSpec ms_fwd_a, ms_dg_a, ms_wg_a, ms_wg_b;
+  PackGeom gx{}, gxw{}, gdy_g{}, gdy_w{};
+  bool share_dy = false, share_x = false;
   TcGemmParams fwd, dg, wg;
   int bn_fwd = 0, bn_dg = 0, bn_wg = 0;
   int t_fwd[3] = {0, 0, 0}, t_dg[3] = {0, 0, 0}, t_wg[3] = {0, 0, 0};
@@ -612,7 +1073,8 @@ void TcPlanDeleter::operator()(TcPlan* p) const {
 }
 
 static bool same_grid(const PackGeom& a, const PackGeom& b) {
-  return a.lo_h == b.lo_h && a.lo_w == b.lo_w && a.Hp == b.Hp && a.Wp == b.Wp;
+  return a.lo_h == b.lo_h && a.lo_w == b.lo_w && a.Hp == b.Hp && a.Wp == b.Wp && a.split == b.split &&
+         a.lo_mask == b.lo_mask;
 }
 
 template <typename T>
@@ -620,15 +1082,34 @@ static T* ws_alloc(TcWs& w, size_t count) {
   void* p = nullptr;
   cuda_check(cudaMalloc(&p, std::max<size_t>(count, 1) * sizeof(T)), "cudaMalloc(tc workspace)");
   w.owned.push_back(p);
+  // packed operands rely on this: their padding is written once, here
+  cuda_check(cudaMemset(p, 0, std::max<size_t>(count, 1) * sizeof(T)), "cudaMemset(tc workspace)");
   return static_cast<T*>(p);
 }
 
-static void build_ws(TcPlan& tp, TcWs& w) {
-  w.gx = geom(tp, false, false);
+// The packed layout of g equals the source's own memory layout.
+static bool pack_identity(const PackGeom& g, DType dt) {
+  return dt == DT_BF16 && g.split == SPLIT_NONE && g.Sh == 1 && g.Sw == 1 && g.lo_h == 0 && g.lo_w == 0 &&
+         g.Hp == g.Hin && g.Wp == g.Win && g.Cp == g.C && g.s_c == 1 && g.s_w == g.C &&
+         g.s_h == (int64_t)g.Win * g.C && (g.n_img == 1 || g.s_img == (int64_t)g.Hin * g.Win * g.C) &&
+         getenv("SYNO_TC_NO_ZEROCOPY") == nullptr;
+}
+
+static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+constexpr uint32_t LO_A = 0b100;  // A parts (hi, hi, lo)
+constexpr uint32_t LO_B = 0b010;  // B parts (hi, lo, hi)
+
+static void build_ws(TcPlan& tp, TcWs& w, DType dt) {
+  w.f32 = dt == DT_F32;
+  const int chs = w.f32 ? SPLIT_CH : SPLIT_NONE;
+  w.gx = geom(tp, false, false, chs, LO_A);
   const int planes = w.gx.Sh * w.gx.Sw;
   const int64_t F = (int64_t)w.gx.n_img * w.gx.Hp * w.gx.Wp;
-  w.xcl = ws_alloc<__nv_bfloat16>(w, (size_t)planes * F * tp.Cp);
-  w.wf = ws_alloc<__nv_bfloat16>(w, (size_t)tp.nwin() * tp.N * tp.Cp);
+  const int Ck = w.gx.Ct();  // contraction channels of the forward A / B operands
+  w.xcl = ws_alloc<__nv_bfloat16>(w, (size_t)planes * F * Ck);
+  w.wf = ws_alloc<__nv_bfloat16>(w, (size_t)tp.nwin() * tp.N * Ck);
+  if (w.f32) w.wf32 = ws_alloc<float>(w, (size_t)tp.nwin() * tp.N * tp.Cp);
 
   // ---- forward: y = sum_win sum_ci Xcl[plane][flat + shift] Wf[win][n][ci]
   {
@@ -636,15 +1117,18 @@ static void build_ws(TcPlan& tp, TcWs& w) {
     TcGemmParams& p = w.fwd;
     memset(&p, 0, sizeof(p));
     p.mode = MODE_ROWS;
-    p.n_cblocks = (tp.Cp + BK - 1) / BK;
+    p.n_cblocks = (Ck + BK - 1) / BK;
     std::vector<std::vector<Win>> groups(1);
     for (int rh = 0; rh < tp.dh.K; ++rh)
       for (int rw = 0; rw < tp.dw.K; ++rw)
         groups[0].push_back({tp.dh.delta(rh) * w.gx.Wp + tp.dw.delta(rw), tp.dh.phi(rh) * w.gx.Sw + tp.dw.phi(rw),
                              rh * tp.dw.K + rw});
-    rows_schedule(p, groups, bn);
-    p.tma_a = make_map(w.xcl, tp.Cp, F, planes, tp.Cp, F * tp.Cp, 64);
-    p.tma_b = make_map(w.wf, tp.Cp, tp.N, tp.nwin(), tp.Cp, (int64_t)tp.N * tp.Cp, bn);
+    const RowsTiling rt = rows_tiling(F, (tp.N + bn - 1) / bn, 1, bn, p.n_cblocks);
+    rows_schedule(p, groups, bn, rt.G);
+    p.rsplit = rt.rs;
+    w.ms_fwd_a = map_spec(Ck, F, planes, Ck, F * Ck, 64);
+    p.tma_a = make_map(w.xcl, w.ms_fwd_a);
+    p.tma_b = make_map(w.wf, Ck, tp.N, tp.nwin(), Ck, (int64_t)tp.N * Ck, bn);
     p.Hp = w.gx.Hp;
     p.Wp = w.gx.Wp;
     p.lo_h = w.gx.lo_h;
@@ -657,24 +1141,37 @@ static void build_ws(TcPlan& tp, TcWs& w) {
     p.o_w = tp.dw.ys;
     p.o_n = tp.y_n;
     p.n_ext = tp.N;
-    p.out_kind = OUT_BF16;
+    p.out_kind = rt.rs > 1 ? OUT_F32_ATOMIC : w.f32 ? OUT_F32 : OUT_BF16;
     p.scale = (float)tp.scale;
     w.bn_fwd = bn;
-    w.t_fwd[0] = (int)((F + (int64_t)mgroup_of(bn) * BM - 1) / ((int64_t)mgroup_of(bn) * BM));
+    w.t_fwd[0] = (int)rt.m_tiles;
     w.t_fwd[1] = (tp.N + bn - 1) / bn;
-    w.t_fwd[2] = 1;
+    w.t_fwd[2] = rt.rs;
+    if (rt.rs > 1 && !w.f32) w.ysc = ws_alloc<float>(w, (size_t)tp.y_numel());
   }
 
   // ---- backward operands
-  w.gdy_g = geom(tp, true, true);
-  w.gdy_w = geom(tp, true, false);
-  w.share_dy = same_grid(w.gdy_g, w.gdy_w);
+  w.gdy_g = geom(tp, true, true, chs, LO_A);
   const int64_t Fg = (int64_t)w.gdy_g.n_img * w.gdy_g.Hp * w.gdy_g.Wp;
-  if (tp.dgrad_ok) {
-    w.dycl_g = ws_alloc<__nv_bfloat16>(w, (size_t)Fg * tp.Np);
-    w.wt = ws_alloc<__nv_bfloat16>(w, (size_t)tp.nwin() * tp.C * tp.Np);
+  const int Nk = w.gdy_g.Ct();
+  if (w.f32) {
+    // wgrad operands split along the images (its contraction dim)
+    w.gxw = geom(tp, false, false, SPLIT_IMG, LO_A);
+    w.gdy_w = geom(tp, true, false, SPLIT_IMG, LO_B);
+  } else {
+    w.gxw = w.gx;
+    w.gdy_w = geom(tp, true, false);
   }
-  w.dycl_w = (w.share_dy && w.dycl_g) ? w.dycl_g : ws_alloc<__nv_bfloat16>(w, (size_t)F * tp.Np);
+  w.share_x = !w.f32;
+  w.share_dy = same_grid(w.gdy_g, w.gdy_w);
+  const int64_t Fw = (int64_t)w.gxw.n_img_out() * w.gxw.Hp * w.gxw.Wp;  // wgrad K rows per plane
+  if (tp.dgrad_ok) {
+    w.dycl_g = ws_alloc<__nv_bfloat16>(w, (size_t)Fg * Nk);
+    w.wt = ws_alloc<__nv_bfloat16>(w, (size_t)tp.nwin() * tp.C * Nk);
+    if (w.f32) w.wt32 = ws_alloc<float>(w, (size_t)tp.nwin() * tp.C * tp.Np);
+  }
+  w.xclw = w.share_x ? w.xcl : ws_alloc<__nv_bfloat16>(w, (size_t)planes * Fw * tp.Cp);
+  w.dycl_w = (w.share_dy && w.dycl_g) ? w.dycl_g : ws_alloc<__nv_bfloat16>(w, (size_t)Fw * tp.Np);
   w.dwf = ws_alloc<float>(w, (size_t)tp.nwin() * tp.N * tp.C);
 
   // ---- grad-input: one group per output phase (psi_h, psi_w); its windows have phi(r) == psi
@@ -683,7 +1180,7 @@ static void build_ws(TcPlan& tp, TcWs& w) {
     TcGemmParams& p = w.dg;
     memset(&p, 0, sizeof(p));
     p.mode = MODE_ROWS;
-    p.n_cblocks = (tp.Np + BK - 1) / BK;
+    p.n_cblocks = (Nk + BK - 1) / BK;
     const int Sh = tp.dh.S, Sw = tp.dw.S;
     std::vector<std::vector<Win>> groups(Sh * Sw);
     for (int ph = 0; ph < Sh; ++ph)
@@ -696,9 +1193,12 @@ static void build_ws(TcPlan& tp, TcWs& w) {
           }
         p.g_out_off[grp] = ph * tp.dh.xs + pw * tp.dw.xs;
       }
-    rows_schedule(p, groups, bn);
-    p.tma_a = make_map(w.dycl_g, tp.Np, Fg, 1, tp.Np, Fg * tp.Np, 64);
-    p.tma_b = make_map(w.wt, tp.Np, tp.C, tp.nwin(), tp.Np, (int64_t)tp.C * tp.Np, bn);
+    const RowsTiling rt = rows_tiling(Fg, (tp.C + bn - 1) / bn, Sh * Sw, bn, p.n_cblocks);
+    rows_schedule(p, groups, bn, rt.G);
+    p.rsplit = rt.rs;
+    w.ms_dg_a = map_spec(Nk, Fg, 1, Nk, Fg * Nk, 64);
+    p.tma_a = make_map(w.dycl_g, w.ms_dg_a);
+    p.tma_b = make_map(w.wt, Nk, tp.C, tp.nwin(), Nk, (int64_t)tp.C * Nk, bn);
     p.Hp = w.gdy_g.Hp;
     p.Wp = w.gdy_g.Wp;
     p.lo_h = w.gdy_g.lo_h;
@@ -711,12 +1211,13 @@ static void build_ws(TcPlan& tp, TcWs& w) {
     p.o_w = tp.dw.xs * Sw;
     p.o_n = tp.x_c;
     p.n_ext = tp.C;
-    p.out_kind = OUT_BF16;
+    p.out_kind = rt.rs > 1 ? OUT_F32_ATOMIC : w.f32 ? OUT_F32 : OUT_BF16;
     p.scale = (float)tp.scale;
     w.bn_dg = bn;
-    w.t_dg[0] = (int)((Fg + (int64_t)mgroup_of(bn) * BM - 1) / ((int64_t)mgroup_of(bn) * BM));
+    w.t_dg[0] = (int)rt.m_tiles;
     w.t_dg[1] = (tp.C + bn - 1) / bn;
-    w.t_dg[2] = Sh * Sw;
+    w.t_dg[2] = Sh * Sw * rt.rs;
+    if (rt.rs > 1 && !w.f32) w.dxsc = ws_alloc<float>(w, (size_t)tp.x_numel());
   }
 
   // ---- grad-weight: both operands channels-last over the forward's flat
@@ -726,10 +1227,12 @@ static void build_ws(TcPlan& tp, TcWs& w) {
     const int bn = pick_bn(tp.N);
     TcGemmParams& p = w.wg;
     memset(&p, 0, sizeof(p));
-    p.tma_a = make_map(w.xcl, tp.Cp, F, planes, tp.Cp, F * tp.Cp, 64);
-    p.tma_b = make_map(w.dycl_w, tp.Np, F, 1, tp.Np, F * tp.Np, 64);
+    w.ms_wg_a = map_spec(tp.Cp, Fw, planes, tp.Cp, Fw * tp.Cp, 64);
+    w.ms_wg_b = map_spec(tp.Np, Fw, 1, tp.Np, Fw * tp.Np, 64);
+    p.tma_a = make_map(w.xclw, w.ms_wg_a);
+    p.tma_b = make_map(w.dycl_w, w.ms_wg_b);
     p.mode = MODE_WGRAD;
-    p.n_cblocks = (int)((F + BK - 1) / BK);
+    p.n_cblocks = (int)((Fw + BK - 1) / BK);
     p.n_win = tp.nwin();
     const int ncb = (tp.Cp + 63) / 64;
     for (int rh = 0; rh < tp.dh.K; ++rh)
@@ -765,59 +1268,195 @@ static void build_ws(TcPlan& tp, TcWs& w) {
     w.t_wg[1] = n_tiles;
     w.t_wg[2] = ksplit;
   }
+
+  w.x_ident = pack_identity(w.gx, dt);
+  w.xw_ident = pack_identity(w.gxw, dt);
+  w.dyg_ident = tp.dgrad_ok && pack_identity(w.gdy_g, dt);
+  w.dyw_ident = pack_identity(w.gdy_w, dt);
+
+  // ---- fast chain rule: per weight, thread mode or split block mode
+  if (tp.fast_fold) {
+    const int64_t ext[4] = {tp.dh.K, tp.dw.K, tp.N, tp.C};
+    int64_t need = 0, outs = 0;
+    for (int j = 0; j < tp.nw; ++j) {
+      int64_t oc = 1, R = 1;
+      for (int l = 0; l < 4; ++l) (tp.wstr[j][l] ? oc : R) *= ext[l];
+      int nsplit = 0;
+      if (R > 64) nsplit = (int)std::max<int64_t>(1, std::min<int64_t>(256, R / 2048));
+      w.chain_nsplit[j] = nsplit;
+      if (nsplit) {
+        need = std::max(need, oc * nsplit);
+        outs = std::max(outs, oc);
+      }
+    }
+    if (need) {
+      w.chain_partial = ws_alloc<float>(w, (size_t)need);
+      w.chain_counter = ws_alloc<unsigned>(w, (size_t)outs);
+      cuda_check(cudaMemset(w.chain_counter, 0, (size_t)outs * sizeof(unsigned)), "memset(chain counter)");
+    }
+  }
 }
 
-static TcWs& workspace(TcPlan& tp, cudaStream_t stream) {
+static void fold_fast(const TcPlan& tp, const Bindings& b, DType dt, bool dgrad, bool split, __nv_bfloat16* dst,
+                      cudaStream_t stream) {
+  FoldArgs f{};
+  f.nw = tp.nw;
+  f.f32 = dt == DT_F32;
+  for (int j = 0; j < tp.nw; ++j) {
+    f.w[j] = b.w.at(j);
+    for (int l = 0; l < 4; ++l) f.s[j][l] = tp.wstr[j][l];
+  }
+  f.ext[0] = tp.dh.K;
+  f.ext[1] = tp.dw.K;
+  f.ext[2] = dgrad ? tp.C : tp.N;
+  f.ext[3] = dgrad ? tp.N : tp.C;
+  f.sl_a = dgrad ? 3 : 2;
+  f.sl_b = dgrad ? 2 : 3;
+  f.Bp = dgrad ? tp.Np : tp.Cp;
+  f.split = split;
+  f.out = dst;
+  const int64_t rows = (int64_t)f.ext[0] * f.ext[1] * f.ext[2];
+  if (rows > 65535) fail(SYNO_E_UNSUPPORTED, "fold: too many operand rows");
+  dim3 grid((unsigned)std::min(8, (f.Bp + 127) / 128), (unsigned)rows);
+  const double elems = (double)rows * f.Bp;
+  const int id = prof_begin("weight_fold", 0.0, elems * (split ? 6 : 2) + elems * tp.nw * (f.f32 ? 4 : 2), stream);
+  note_launch();
+  fold_kernel<<<grid, 128, 0, stream>>>(f);
+  cuda_check(cudaGetLastError(), "fold_kernel");
+  prof_end(id, stream);
+}
+
+static void chain_fast(const TcPlan& tp, const TcWs& w, const Bindings& b, DType dt, int j, cudaStream_t stream) {
+  ChainArgs c{};
+  c.dwf = w.dwf;
+  c.nw = tp.nw;
+  c.j = j;
+  c.f32 = dt == DT_F32;
+  for (int k = 0; k < tp.nw; ++k) {
+    c.w[k] = b.w.at(k);
+    for (int l = 0; l < 4; ++l) c.s[k][l] = tp.wstr[k][l];
+  }
+  c.ext[0] = tp.dh.K;
+  c.ext[1] = tp.dw.K;
+  c.ext[2] = tp.N;
+  c.ext[3] = tp.C;
+  c.out_count = c.R = 1;
+  for (int l = 0; l < 4; ++l) {
+    if (tp.wstr[j][l]) {
+      c.out_l[c.nout++] = l;
+      c.out_count *= c.ext[l];
+    } else {
+      c.red_l[c.nred++] = l;
+      c.R *= c.ext[l];
+    }
+  }
+  c.out = b.dw.at(j);
+  const double bytes = (double)c.out_count * c.R * 4 + (double)c.out_count * (c.f32 ? 4 : 2);
+  const int id = prof_begin("weight_chain", 0.0, bytes, stream);
+  note_launch();
+  const int nsplit = w.chain_nsplit[j];
+  if (!nsplit) {
+    chain_thread_kernel<<<(unsigned)((c.out_count + 255) / 256), 256, 0, stream>>>(c);
+  } else {
+    c.r_chunk = (c.R + nsplit - 1) / nsplit;
+    c.partial = w.chain_partial;
+    c.counter = w.chain_counter;
+    const int ns = (int)((c.R + c.r_chunk - 1) / c.r_chunk);
+    chain_block_kernel<<<dim3((unsigned)c.out_count, (unsigned)ns), 256, 0, stream>>>(c);
+  }
+  cuda_check(cudaGetLastError(), "chain kernel");
+  prof_end(id, stream);
+}
+
+static TcWs& workspace(TcPlan& tp, DType dt, cudaStream_t stream) {
   int dev = 0;
   cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
   std::lock_guard<std::mutex> lock(tp.mu);
-  auto key = std::make_pair(dev, (void*)stream);
+  auto key = std::make_tuple(dev, (void*)stream, (int)dt);
   auto it = tp.ws.find(key);
   if (it != tp.ws.end()) return *it->second;
   auto w = std::make_unique<TcWs>();
-  build_ws(tp, *w);
+  build_ws(tp, *w, dt);
   TcWs& ref = *w;
   tp.ws[key] = std::move(w);
   return ref;
 }
 
+// Folded weights into the B operand: bf16 folds straight into it; fp32
+// folds in fp32 and is split into (hi, lo, hi) parts.
+static void fold_into(TcWs& w, const DevStage& fold, DType dt, const Bindings& b, float* f32_tmp,
+                      __nv_bfloat16* dst, int64_t rows, int Cp, cudaStream_t stream) {
+  if (!w.f32) {
+    run_stage(dt, fold, b, dst, false, stream);
+    return;
+  }
+  run_stage(dt, fold, b, f32_tmp, false, stream);
+  split_rows(f32_tmp, dst, rows, Cp, LO_B, stream);
+}
+
+static bool tc_dtype(DType dt) { return dt == DT_BF16 || dt == DT_F32; }
+
+// MODE_ROWS launch into `out`; a split-K launch accumulates fp32 atomically
+// (into `out` itself for fp32, else into `acc` followed by a cast).
+static void rows_gemm(TcGemmParams& p, int bn, const int* t, void* out, bool f32, float* acc, int64_t numel,
+                      cudaStream_t stream, const char* name, double flops) {
+  if (p.rsplit <= 1) {
+    p.out = out;
+    gemm(p, bn, t[0], t[1], t[2], stream, name, flops);
+    return;
+  }
+  float* target = f32 ? static_cast<float*>(out) : acc;
+  cuda_check(cudaMemsetAsync(target, 0, (size_t)numel * sizeof(float), stream), "memset(split-K output)");
+  p.out = target;
+  gemm(p, bn, t[0], t[1], t[2], stream, name, flops);
+  if (!f32) cast_to_bf16(target, out, numel, stream);
+}
+
 bool tc_forward(TcPlan& tp, DType dt, const Bindings& b, cudaStream_t stream) {
-  if (dt != DT_BF16) return false;
-  TcWs& w = workspace(tp, stream);
-  pack_cl(b.x, dt, w.gx, w.xcl, stream);
-  run_stage(dt, tp.fold_fwd, b, w.wf, false, stream);
-  TcGemmParams& p = w.fwd;
-  p.out = b.y;
-  gemm(p, w.bn_fwd, w.t_fwd[0], w.t_fwd[1], w.t_fwd[2], stream, "tc_gemm_fwd", tp.flops);
+  if (!tc_dtype(dt)) return false;
+  TcWs& w = workspace(tp, dt, stream);
+  TcGemmParams p = w.fwd;
+  if (w.x_ident && aligned16(b.x)) p.tma_a = make_map(b.x, w.ms_fwd_a);
+  else pack_cl(b.x, dt, w.gx, w.xcl, stream);
+  if (tp.fast_fold) fold_fast(tp, b, dt, false, w.f32, w.wf, stream);
+  else fold_into(w, tp.fold_fwd, dt, b, w.wf32, w.wf, (int64_t)tp.nwin() * tp.N, tp.Cp, stream);
+  rows_gemm(p, w.bn_fwd, w.t_fwd, b.y, w.f32, w.ysc, tp.y_numel(), stream, "tc_gemm_fwd", tp.flops);
   return true;
 }
 
 bool tc_backward(TcPlan& tp, DType dt, const Bindings& b, cudaStream_t stream) {
-  if (dt != DT_BF16) return false;
+  if (!tc_dtype(dt)) return false;
   if (b.dx && !tp.dgrad_ok) return false;
-  TcWs& w = workspace(tp, stream);
+  TcWs& w = workspace(tp, dt, stream);
   bool any_w = false;
   for (auto* q : b.dw) any_w = any_w || q;
   bool dy_w_packed = false;
   if (b.dx) {
-    pack_cl(b.dy, dt, w.gdy_g, w.dycl_g, stream);
-    dy_w_packed = w.share_dy;
-    run_stage(dt, tp.fold_dgrad, b, w.wt, false, stream);
-    TcGemmParams& p = w.dg;
-    p.out = b.dx;
-    gemm(p, w.bn_dg, w.t_dg[0], w.t_dg[1], w.t_dg[2], stream, "tc_gemm_dgrad", tp.flops);
+    TcGemmParams p = w.dg;
+    if (w.dyg_ident && aligned16(b.dy)) p.tma_a = make_map(b.dy, w.ms_dg_a);
+    else {
+      pack_cl(b.dy, dt, w.gdy_g, w.dycl_g, stream);
+      dy_w_packed = w.share_dy;
+    }
+    if (tp.fast_fold) fold_fast(tp, b, dt, true, w.f32, w.wt, stream);
+    else fold_into(w, tp.fold_dgrad, dt, b, w.wt32, w.wt, (int64_t)tp.nwin() * tp.C, tp.Np, stream);
+    rows_gemm(p, w.bn_dg, w.t_dg, b.dx, w.f32, w.dxsc, tp.x_numel(), stream, "tc_gemm_dgrad", tp.flops);
   }
   if (any_w) {
-    pack_cl(b.x, dt, w.gx, w.xcl, stream);
-    if (!dy_w_packed) pack_cl(b.dy, dt, w.gdy_w, w.dycl_w, stream);
+    TcGemmParams p = w.wg;
+    if (w.xw_ident && aligned16(b.x)) p.tma_a = make_map(b.x, w.ms_wg_a);
+    else pack_cl(b.x, dt, w.gxw, w.xclw, stream);
+    if (w.dyw_ident && aligned16(b.dy)) p.tma_b = make_map(b.dy, w.ms_wg_b);
+    else if (!dy_w_packed) pack_cl(b.dy, dt, w.gdy_w, w.dycl_w, stream);
     cuda_check(cudaMemsetAsync(w.dwf, 0, (size_t)tp.nwin() * tp.N * tp.C * sizeof(float), stream), "memset(dWf)");
-    gemm(w.wg, w.bn_wg, w.t_wg[0], w.t_wg[1], w.t_wg[2], stream, "tc_gemm_wgrad", tp.flops);
+    gemm(p, w.bn_wg, w.t_wg[0], w.t_wg[1], w.t_wg[2], stream, "tc_gemm_wgrad", tp.flops);
     // chain rule through the fold, into each requested weight gradient
     Bindings cb = b;
     cb.stages = {w.dwf};
     for (size_t j = 0; j < tp.chain.size(); ++j) {
       if (j >= b.dw.size() || !b.dw[j]) continue;
-      run_stage(dt, tp.chain[j], cb, b.dw[j], false, stream);
+      if (tp.fast_fold) chain_fast(tp, w, b, dt, (int)j, stream);
+      else run_stage(dt, tp.chain[j], cb, b.dw[j], false, stream);
     }
   }
   return true;

@@ -71,6 +71,8 @@ struct alignas(64) TcGemmParams {
   int32_t n_cblocks;   // MODE_ROWS: channel blocks of 64; MODE_WGRAD: pixel blocks per window
   int32_t n_win;
   int32_t ksplit;      // MODE_WGRAD split of the pixel blocks
+  int32_t rsplit;      // MODE_ROWS split of the channel blocks (>1: fp32 atomic output)
+  int32_t G;           // MODE_ROWS M tiles per step (<= mgroup<BN>(); fewer for small problems)
   int32_t a_shift[MAXWIN];   // MODE_ROWS: row shift of A per window; MODE_WGRAD: B row (pixel) shift
   int32_t a_plane[MAXWIN];   // MODE_WGRAD: plane (phase) of x per window
   int32_t b_plane[MAXWIN];   // MODE_ROWS: B plane (packed weight window) per window
@@ -234,6 +236,7 @@ __device__ __forceinline__ void tmem_ld32(uint32_t addr, float* v) {
 
 struct TileInfo {
   int mt, nt, g, ks, kb0, nkb;
+  int cb0, cb1;  // MODE_ROWS channel-block range of this split
 };
 
 __device__ __forceinline__ TileInfo tile_info(const TcGemmParams& p, int t) {
@@ -243,13 +246,18 @@ __device__ __forceinline__ TileInfo tile_info(const TcGemmParams& p, int t) {
   ti.mt = q % p.m_tiles;
   const int z = q / p.m_tiles;
   if (p.mode == MODE_ROWS) {
-    ti.g = z;
-    ti.ks = 0;
+    const int rs = p.rsplit > 1 ? p.rsplit : 1;
+    ti.g = z / rs;
+    ti.ks = z - ti.g * rs;
+    const int per = (p.n_cblocks + rs - 1) / rs;
+    ti.cb0 = ti.ks * per;
+    ti.cb1 = min(p.n_cblocks, ti.cb0 + per);
     ti.kb0 = 0;
     ti.nkb = 0;
-    for (int c = p.g_chunk0[z]; c < p.g_chunk1[z]; ++c) ti.nkb += p.chunk_w1[c] - p.chunk_w0[c];
-    ti.nkb *= p.n_cblocks;  // MMA k-steps (one per window x channel block)
+    for (int c = p.g_chunk0[ti.g]; c < p.g_chunk1[ti.g]; ++c) ti.nkb += p.chunk_w1[c] - p.chunk_w0[c];
+    ti.nkb *= max(0, ti.cb1 - ti.cb0);  // MMA k-steps (one per window x channel block)
   } else {
+    ti.cb0 = ti.cb1 = 0;
     ti.ks = z % p.ksplit;
     ti.g = z / p.ksplit;
     const int per = (p.n_cblocks + p.ksplit - 1) / p.ksplit;
@@ -342,11 +350,11 @@ __global__ void __launch_bounds__(THREADS, 1) tc_gemm_kernel(const __grid_consta
       if (lane == 0 && pcount < 14) stamp(2 + pcount * 4);
       if (p.mode == MODE_ROWS) {
         for (int c = p.g_chunk0[ti.g]; c < p.g_chunk1[ti.g]; ++c) {
-          for (int cb = 0; cb < p.n_cblocks; ++cb) {
+          for (int cb = ti.cb0; cb < ti.cb1; ++cb) {
             // one halo tile of A for this plane and channel block
             const int as = ra.slot(AST);
             mbar_wait(&a_empty[as], ra.phase(AST) ^ 1u);
-            const int row0 = ti.mt * G * BM + p.chunk_pmin[c];
+            const int row0 = ti.mt * p.G * BM + p.chunk_pmin[c];
             const int nbox = p.a_rows / 64;
             if (elect_one()) {
               if (p.dbg & 4) {
@@ -423,7 +431,7 @@ __global__ void __launch_bounds__(THREADS, 1) tc_gemm_kernel(const __grid_consta
       uint32_t accumulate = 0;
       if (!mn) {
         for (int c = p.g_chunk0[ti.g]; c < p.g_chunk1[ti.g]; ++c) {
-          for (int cb = 0; cb < p.n_cblocks; ++cb) {
+          for (int cb = ti.cb0; cb < ti.cb1; ++cb) {
             const int as = ra.slot(AST);
             mbar_wait(&a_full[as], ra.phase(AST));
             const uint32_t abase = smem_u32(sa + as * p.a_stage_bytes);
@@ -437,6 +445,7 @@ __global__ void __launch_bounds__(THREADS, 1) tc_gemm_kernel(const __grid_consta
               if (!(p.dbg & 2)) {
 #pragma unroll
                 for (int g = 0; g < G; ++g) {
+                  if (g >= p.G) break;
                   // start = halo + (g*128 + shift) rows; K advance: 32 B inside the swizzled row
                   const uint64_t da = (((uint64_t)((arow + g * BM * 128u) >> 4)) & 0x3FFF) | (1ull << 16) |
                                       ((uint64_t)(1024 >> 4) << 32) | (1ull << 46) | (2ull << 61);
@@ -499,7 +508,7 @@ __global__ void __launch_bounds__(THREADS, 1) tc_gemm_kernel(const __grid_consta
       mbar_wait(&tfull[acc], (tcount >> 1) & 1u);
       if (warp == 2 && lane == 0 && tcount < 14) stamp(2 + tcount * 4 + 2);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const int nsub = p.mode == MODE_ROWS ? G : 1;
+      const int nsub = p.mode == MODE_ROWS ? p.G : 1;
       const bool have = ti.nkb > 0;
       const float scale = p.scale;
 #pragma unroll 1
@@ -507,7 +516,7 @@ __global__ void __launch_bounds__(THREADS, 1) tc_gemm_kernel(const __grid_consta
         bool ok;
         int64_t off;
         if (p.mode == MODE_ROWS) {
-          const int64_t flat = ((int64_t)ti.mt * G + g) * BM + r;
+          const int64_t flat = ((int64_t)ti.mt * p.G + g) * BM + r;
           const int64_t wp = flat % p.Wp;
           const int64_t tq = flat / p.Wp;
           const int64_t hp = tq % p.Hp;
@@ -534,18 +543,46 @@ __global__ void __launch_bounds__(THREADS, 1) tc_gemm_kernel(const __grid_consta
             // masked row (pad pixel / beyond the extent): nothing to store
           } else if (p.out_kind == OUT_BF16) {
             __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(p.out) + off + (int64_t)n0 * os;
-            if (nlim == 32) {
+            if (nlim == 32 && os == 1 && (reinterpret_cast<uintptr_t>(o) & 15) == 0) {
+              // N contiguous in the output (QKV-like): four 16-byte stores per thread
+              uint4* o4 = reinterpret_cast<uint4*>(o);
+#pragma unroll
+              for (int q4 = 0; q4 < 4; ++q4) {
+                __align__(16) __nv_bfloat162 h2[4];
+#pragma unroll
+                for (int e = 0; e < 4; ++e)
+                  h2[e] = __floats2bfloat162_rn(have ? v[q4 * 8 + 2 * e] * scale : 0.f,
+                                                have ? v[q4 * 8 + 2 * e + 1] * scale : 0.f);
+                o4[q4] = *reinterpret_cast<const uint4*>(h2);
+              }
+            } else if (nlim == 32) {
 #pragma unroll
               for (int j = 0; j < 32; ++j) {
                 *o = __float2bfloat16_rn(have ? v[j] * scale : 0.f);
                 o += os;
               }
             } else {
-              for (int j = 0; j < nlim; ++j) o[(int64_t)j * os] = __float2bfloat16_rn(have ? v[j] * scale : 0.f);
+#pragma unroll
+              for (int j = 0; j < 32; ++j)
+                if (j < nlim) o[(int64_t)j * os] = __float2bfloat16_rn(have ? v[j] * scale : 0.f);
             }
           } else if (p.out_kind == OUT_F32) {
             float* o = reinterpret_cast<float*>(p.out) + off + (int64_t)n0 * os;
-            for (int j = 0; j < nlim; ++j) o[(int64_t)j * os] = have ? v[j] * scale : 0.f;
+            if (nlim == 32 && os == 1 && (reinterpret_cast<uintptr_t>(o) & 15) == 0) {
+              float4* o4 = reinterpret_cast<float4*>(o);
+#pragma unroll
+              for (int q4 = 0; q4 < 8; ++q4)
+                o4[q4] = have ? make_float4(v[4 * q4] * scale, v[4 * q4 + 1] * scale, v[4 * q4 + 2] * scale,
+                                            v[4 * q4 + 3] * scale)
+                              : make_float4(0.f, 0.f, 0.f, 0.f);
+            } else if (nlim == 32) {
+#pragma unroll
+              for (int j = 0; j < 32; ++j) o[(int64_t)j * os] = have ? v[j] * scale : 0.f;
+            } else {
+#pragma unroll
+              for (int j = 0; j < 32; ++j)
+                if (j < nlim) o[(int64_t)j * os] = have ? v[j] * scale : 0.f;
+            }
           } else {
             float* o = reinterpret_cast<float*>(p.out) + off + (int64_t)n0 * os;
             if (nlim == 32) {
@@ -555,7 +592,9 @@ __global__ void __launch_bounds__(THREADS, 1) tc_gemm_kernel(const __grid_consta
                 o += os;
               }
             } else {
-              for (int j = 0; j < nlim; ++j) atomicAdd(o + (int64_t)j * os, v[j] * scale);
+#pragma unroll
+              for (int j = 0; j < 32; ++j)
+                if (j < nlim) atomicAdd(o + (int64_t)j * os, v[j] * scale);
             }
           }
         }

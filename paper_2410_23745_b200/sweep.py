@@ -70,13 +70,15 @@ class EvalRecord:
     op: str
     seconds: float = 0.0   # device time of fwd + bwd (CUDA events)
     adjoint_err: float = 0.0
+    error: str = ""
 
     def line(self) -> str:
         return (f"sample id={self.sample_id} iter=0 seed={self.seed} reward={0.0!r} flops={self.flops} "
                 f"params={self.params} status={self.status} op={self.op}")
 
     def diag(self) -> str:
-        return f"diag id={self.sample_id} device_us={self.seconds * 1e6:.3f} adjoint_err={self.adjoint_err:.3e}"
+        d = f"diag id={self.sample_id} device_us={self.seconds * 1e6:.3f} adjoint_err={self.adjoint_err:.3e}"
+        return d + (f" error={self.error}" if self.error else "")
 
 
 def within_budget(flops: int, params: int, flops_cap: Optional[int], params_cap: Optional[int]) -> bool:
@@ -119,8 +121,9 @@ def evaluate(graph, sample_id: int, seed: int, dtype=None, device=None,
         dx, dws = ops.backward(h, x, ws, dy)
         e1.record(stream)
         e1.synchronize()
-    except Exception:  # a device-engine limit or launch failure: logged like a RewardFailure
-        return EvalRecord(sample_id, seed, h.flops_unstaged, h.params, "failed", op)
+    except Exception as exc:  # a device-engine limit or launch failure: logged like a RewardFailure
+        return EvalRecord(sample_id, seed, h.flops_unstaged, h.params, "failed", op,
+                          error=f"{type(exc).__name__}: {str(exc).splitlines()[0] if str(exc) else ''}"[:200])
     s = _inner(dy, y)
     scale = max(1.0, math.sqrt(_inner(dy, dy) * max(_inner(y, y), 1e-30)))
     err = abs(_inner(dx, x) - s) / scale
