@@ -168,11 +168,14 @@ __device__ int64_t eval_prog(const int64_t* code, int64_t len, const int64_t* va
   return st[0];
 }
 
+constexpr int K1_INLINE = 256;  // int64 words of program code passed in the kernel parameters
+
 struct K1Args {
   int32_t nprog, ndeps;
   int64_t dep_ext[MAXL];
   int64_t count;
-  const int64_t* code;
+  const int64_t* code;      // device code, or null: icode
+  int64_t icode[K1_INLINE];
   int64_t prog_off[MAXPROG];
   int64_t prog_len[MAXPROG];
   int64_t n[MAXPROG];       // extent for the range check, <= 0: no check
@@ -191,17 +194,25 @@ __global__ void k1_build_table(const __grid_constant__ K1Args a) {
     rem /= a.dep_ext[k];
   }
   if (a.out_raw) {
-    a.out_raw[i] = eval_prog(a.code + a.prog_off[0], a.prog_len[0], vals);
+    a.out_raw[i] = eval_prog((a.code ? a.code : a.icode) + a.prog_off[0], a.prog_len[0], vals);
     return;
   }
   int64_t sum = 0;
   bool ok = true;
   for (int p = 0; p < a.nprog; ++p) {
-    int64_t v = eval_prog(a.code + a.prog_off[p], a.prog_len[p], vals);
+    int64_t v = eval_prog((a.code ? a.code : a.icode) + a.prog_off[p], a.prog_len[p], vals);
     if (a.n[p] > 0 && (v < 0 || v >= a.n[p])) ok = false;
     sum += v * a.stride[p];
   }
   a.out[i] = ok ? (int32_t)sum : -1;
+}
+
+// Largest index table (entries) a coordinate may get before the stage
+// falls back to on-the-fly programs.  SYNO_TABLE_LIMIT lowers it (tests use
+// it to drive the program path on small operators).
+static int64_t table_limit() {
+  const char* e = getenv("SYNO_TABLE_LIMIT");
+  return e ? std::max<int64_t>(1, atoll(e)) : ((int64_t)1 << 28);
 }
 
 struct ProgSpec {
@@ -237,10 +248,16 @@ static void launch_k1(const TabSpec& t, int32_t* out, int64_t* out_raw, cudaStre
   }
   if (code.empty()) code.push_back(0);
   int64_t* dcode = nullptr;
-  cuda_check(cudaMallocAsync((void**)&dcode, code.size() * sizeof(int64_t), stream), "cudaMallocAsync(code)");
-  cuda_check(cudaMemcpyAsync(dcode, code.data(), code.size() * sizeof(int64_t), cudaMemcpyHostToDevice, stream),
-             "cudaMemcpyAsync(code)");
-  a.code = dcode;
+  if (code.size() <= (size_t)K1_INLINE) {
+    // small programs travel in the launch parameters: no copy, no host sync
+    memcpy(a.icode, code.data(), code.size() * sizeof(int64_t));
+    a.code = nullptr;
+  } else {
+    cuda_check(cudaMallocAsync((void**)&dcode, code.size() * sizeof(int64_t), stream), "cudaMallocAsync(code)");
+    cuda_check(cudaMemcpyAsync(dcode, code.data(), code.size() * sizeof(int64_t), cudaMemcpyHostToDevice, stream),
+               "cudaMemcpyAsync(code)");
+    a.code = dcode;
+  }
   a.out = out;
   a.out_raw = out_raw;
   if (t.count > 0) {
@@ -249,10 +266,11 @@ static void launch_k1(const TabSpec& t, int32_t* out, int64_t* out_raw, cudaStre
     k1_build_table<<<(unsigned)blocks, 256, 0, stream>>>(a);
     cuda_check(cudaGetLastError(), "k1_build_table");
   }
-  // The host copy of `code` must outlive the async memcpy: synchronize the
-  // (rare, compile-time) table build before the vector goes away.
-  cuda_check(cudaStreamSynchronize(stream), "k1 sync");
-  cuda_check(cudaFreeAsync(dcode, stream), "cudaFreeAsync(code)");
+  if (dcode) {
+    // the host copy of `code` must outlive the async memcpy (rare: long programs)
+    cuda_check(cudaStreamSynchronize(stream), "k1 sync");
+    cuda_check(cudaFreeAsync(dcode, stream), "cudaFreeAsync(code)");
+  }
 }
 
 void eval_coordinate_grid(const CStage& s, int term, int coord, int64_t* out_dev, cudaStream_t stream) {
@@ -328,7 +346,7 @@ static void build_kterm(const CStage& s, const CTerm& t, KTerm* k, std::vector<T
       tab.count *= s.ext(l);
     }
     tab.progs.push_back({c, n, st});
-    if (tab.count >= (int64_t)1 << 28) fail(SYNO_E_UNSUPPORTED, "index table too large");
+    if (tab.count >= table_limit()) fail(SYNO_E_UNSUPPORTED, "index table too large");
     auto tstr = row_major_strides(tab.dep_ext);
     int tid = (int)tabs->size();
     tabs->push_back(tab);
@@ -367,8 +385,65 @@ static void build_kterm(const CStage& s, const CTerm& t, KTerm* k, std::vector<T
 }
 
 void release_dev_stage(DevStage& ds) {
-  if (ds.tables) cudaFree(ds.tables);
+  // callers have synchronised the device (DevPlan / TcPlan teardown)
+  if (ds.tables) cudaFreeAsync(ds.tables, nullptr);
   ds.tables = nullptr;
+  if (ds.prog) cudaFree(ds.prog);
+  ds.prog = nullptr;
+}
+
+// Program fallback: every coordinate of every term is kept as postfix code
+// over the loop digits (axes, then reduces) and evaluated per grid point.
+static void build_prog_stage(const CStage& cs, DevStage* ds) {
+  KStage& k = ds->k;
+  const int L = cs.nloops();
+  if ((int)cs.red_ext.size() > 16) fail(SYNO_E_UNSUPPORTED, "stage has too many reduces for the program fallback");
+  std::vector<int> loops(L);
+  for (int l = 0; l < L; ++l) loops[l] = l;
+  std::vector<int64_t> meta, code;
+  std::vector<const CTerm*> terms;
+  for (auto& t : cs.terms) terms.push_back(&t);
+  if (cs.scatter) terms.push_back(&cs.target);
+  std::vector<std::vector<int64_t>> recs;
+  for (size_t ti = 0; ti < terms.size(); ++ti) {
+    const CTerm& t = *terms[ti];
+    auto strides = row_major_strides(t.t.extents);
+    std::vector<int64_t> rec{(int64_t)t.coords.size()};
+    for (size_t d = 0; d < t.coords.size(); ++d) {
+      if (prog_depth(t.coords[d]) > MAXSTACK) fail(SYNO_E_UNSUPPORTED, "coordinate expression too deep");
+      const int64_t off = (int64_t)code.size();
+      compile_prog(t.coords[d], loops, &code);
+      rec.push_back(off);
+      rec.push_back(((int64_t)code.size() - off) / 2);
+      rec.push_back(t.t.extents[d]);
+      rec.push_back(strides[d]);
+    }
+    recs.push_back(rec);
+  }
+  for (size_t ti = 0; ti < recs.size(); ++ti) {
+    k.prog_term_off[ti] = (int32_t)meta.size();
+    meta.insert(meta.end(), recs[ti].begin(), recs[ti].end());
+  }
+  // code offsets become absolute (code follows the metadata)
+  const int64_t base = (int64_t)meta.size();
+  for (size_t ti = 0; ti < recs.size(); ++ti) {
+    int64_t* r = meta.data() + k.prog_term_off[ti];
+    for (int64_t d = 0; d < r[0]; ++d) r[1 + 4 * d] += base;
+  }
+  meta.insert(meta.end(), code.begin(), code.end());
+  cuda_check(cudaMalloc((void**)&ds->prog, meta.size() * sizeof(int64_t)), "cudaMalloc(programs)");
+  cuda_check(cudaMemcpy(ds->prog, meta.data(), meta.size() * sizeof(int64_t), cudaMemcpyHostToDevice),
+             "cudaMemcpy(programs)");
+  k.prog = ds->prog;
+  k.n_red = (int)cs.red_ext.size();
+  for (size_t r = 0; r < cs.red_ext.size(); ++r) k.red_ext[r] = cs.red_ext[r];
+  for (int t = 0; t < k.n_terms; ++t) {
+    KTerm& kt = k.terms[t];
+    memset(&kt, 0, sizeof(KTerm));
+    const int tk = cs.terms[t].t.kind;
+    kt.kind = tk == TK_PHANTOM ? 2 : (tk == TK_STAGE ? 1 : 0);
+  }
+  memset(&k.target, 0, sizeof(KTerm));
 }
 
 void build_dev_stage(const CStage& cs, DevStage* ds, cudaStream_t stream) {
@@ -395,8 +470,16 @@ void build_dev_stage(const CStage& cs, DevStage* ds, cudaStream_t stream) {
   std::vector<TabSpec> tabs;
   std::vector<Fixup> fix;
   bool dead = false;
-  for (size_t t = 0; t < cs.terms.size(); ++t) build_kterm(cs, cs.terms[t], &k.terms[t], &tabs, &fix, &dead);
-  if (cs.scatter) build_kterm(cs, cs.target, &k.target, &tabs, &fix, &dead);
+  try {
+    for (size_t t = 0; t < cs.terms.size(); ++t) build_kterm(cs, cs.terms[t], &k.terms[t], &tabs, &fix, &dead);
+    if (cs.scatter) build_kterm(cs, cs.target, &k.target, &tabs, &fix, &dead);
+  } catch (const Error& e) {
+    if (e.code != SYNO_E_UNSUPPORTED) throw;
+    // table budget exceeded: evaluate the coordinate programs on the fly
+    ds->dead = cs.dead;
+    build_prog_stage(cs, ds);
+    return;
+  }
   ds->dead = dead || cs.dead;
   size_t total = 0;
   for (auto& t : tabs) {
@@ -405,19 +488,26 @@ void build_dev_stage(const CStage& cs, DevStage* ds, cudaStream_t stream) {
   }
   ds->table_entries = total;
   if (total) {
-    cuda_check(cudaMalloc((void**)&ds->tables, total * sizeof(int32_t)), "cudaMalloc(tables)");
+    cuda_check(cudaMallocAsync((void**)&ds->tables, total * sizeof(int32_t), stream), "cudaMallocAsync(tables)");
     for (auto& t : tabs) launch_k1(t, ds->tables + t.offset, nullptr, stream);
   }
   for (auto& f : fix) *f.field = ds->tables + tabs[f.table].offset;
 }
 
 DevPlan::~DevPlan() {
+  // in-flight work on any stream may still read the tables
+  int cur = -1;
+  cudaGetDevice(&cur);
+  if (device >= 0 && device != cur) cudaSetDevice(device);
+  cudaDeviceSynchronize();
   auto rel = [](std::vector<DevStage>& v) {
     for (auto& s : v) release_dev_stage(s);
   };
   rel(forward);
   rel(grad_x);
   for (auto& g : grad_w) rel(g);
+  tc.reset();
+  if (device >= 0 && device != cur && cur >= 0) cudaSetDevice(cur);
 }
 
 static void ensure_forward(const Plan& plan, DevPlan& dp, cudaStream_t stream) {
@@ -427,6 +517,8 @@ static void ensure_forward(const Plan& plan, DevPlan& dp, cudaStream_t stream) {
     dp.forward.emplace_back();
     build_dev_stage(s, &dp.forward.back(), stream);
   }
+  // tables are filled on `stream`; other streams may use them next
+  cuda_check(cudaStreamSynchronize(stream), "ensure_forward");
   dp.have_forward = true;
 }
 
@@ -444,12 +536,25 @@ static void ensure_backward(const Plan& plan, DevPlan& dp, cudaStream_t stream) 
       build_dev_stage(s, &dp.grad_w.back().back(), stream);
     }
   }
+  cuda_check(cudaStreamSynchronize(stream), "ensure_backward");
   dp.have_backward = true;
 }
 
 DevPlan* build_dev_plan(const Plan& plan, cudaStream_t stream) {
   auto dp = std::make_unique<DevPlan>();
   cuda_check(cudaGetDevice(&dp->device), "cudaGetDevice");
+  {
+    // keep stream-ordered allocations (tables, stage buffers, partials) cached
+    static std::atomic<uint64_t> pooled{0};
+    const uint64_t bit = 1ull << (dp->device & 63);
+    if (!(pooled.fetch_or(bit) & bit)) {
+      cudaMemPool_t pool;
+      if (cudaDeviceGetDefaultMemPool(&pool, dp->device) == cudaSuccess) {
+        uint64_t thr = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+      }
+    }
+  }
   dp->tc = tc_build(plan, stream);
   cuda_check(cudaStreamSynchronize(stream), "build_dev_plan");
   return dp.release();
@@ -595,6 +700,65 @@ __global__ void __launch_bounds__(256, NT <= 2 ? 4 : 2) stage_kernel(const __gri
   }
 }
 
+// Program fallback (index tables over budget): every coordinate is
+// evaluated from its postfix program at every grid point.
+__device__ __forceinline__ bool prog_offset(const int64_t* prog, int rec, const int64_t* vals, int64_t* off) {
+  const int64_t* r = prog + rec;
+  int64_t o = 0;
+  bool ok = true;
+  for (int64_t d = 0; d < r[0]; ++d) {
+    const int64_t* c = r + 1 + 4 * d;
+    const int64_t v = eval_prog(prog + c[0], c[1], vals);
+    ok = ok && v >= 0 && v < c[2];
+    o += v * c[3];
+  }
+  *off = o;
+  return ok;
+}
+
+template <typename TI, typename TA, bool SCATTER>
+__global__ void __launch_bounds__(128) stage_prog_kernel(const __grid_constant__ KStage S) {
+  const int64_t o = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (o >= S.out_count) return;
+  const int64_t r0 = (int64_t)blockIdx.y * S.r_chunk;
+  const int64_t r1 = min(S.R, r0 + S.r_chunk);
+  int64_t vals[MAXA + 16];
+  {
+    int64_t rem = o;
+    for (int k = S.n_axes - 1; k >= 0; --k) {
+      vals[k] = rem % S.axis_ext[k];
+      rem /= S.axis_ext[k];
+    }
+  }
+  const TA scale = (TA)S.scale;
+  TA acc = 0;
+  for (int64_t r = r0; r < r1; ++r) {
+    int64_t rem = r;
+    for (int k = S.n_red - 1; k >= 0; --k) {
+      vals[S.n_axes + k] = rem % S.red_ext[k];
+      rem /= S.red_ext[k];
+    }
+    TA prod = 1;
+    bool ok = true;
+    for (int t = 0; t < S.n_terms && ok; ++t) {
+      int64_t off;
+      if (!prog_offset(S.prog, S.prog_term_off[t], vals, &off)) ok = false;
+      else if (S.terms[t].kind != 2) prod *= load_term<TI, TA>(S.terms[t], off);
+    }
+    if (!ok) continue;
+    if (SCATTER) {
+      int64_t off;
+      if (prog_offset(S.prog, S.prog_term_off[S.n_terms], vals, &off)) atomic_add((TA*)S.out + off, prod * scale);
+    } else {
+      acc += prod;
+    }
+  }
+  if (!SCATTER) {
+    if (S.out_acc) ((TA*)S.out)[(int64_t)blockIdx.y * S.out_count * (gridDim.y > 1) + o] = acc * scale;
+    else ((TI*)S.out)[o] = from_acc<TI, TA>(acc * scale);
+  }
+}
+
 // Affine form: no reduction and every coordinate a bare iterator (weight
 // folds and re-layouts, identity-like gathers): offsets are linear in the
 // output digits, so the kernel is a plain strided gather-product.
@@ -726,6 +890,11 @@ static const void* bind_ptr(const CTensor& t, const Bindings& b) {
 
 template <typename TI, typename TA, bool SCATTER>
 static void launch_nt(const KStage& k, dim3 grid, cudaStream_t stream) {
+  if (k.prog) {
+    dim3 g2((unsigned)((k.out_count + 127) / 128), grid.y);
+    stage_prog_kernel<TI, TA, SCATTER><<<g2, 128, 0, stream>>>(k);
+    return;
+  }
   if (k.n_terms <= 2) stage_kernel<TI, TA, SCATTER, 2><<<grid, 256, 0, stream>>>(k);
   else if (k.n_terms <= 4) stage_kernel<TI, TA, SCATTER, 4><<<grid, 256, 0, stream>>>(k);
   else stage_kernel<TI, TA, SCATTER, MAXT><<<grid, 256, 0, stream>>>(k);
@@ -758,7 +927,7 @@ static void launch_stage_impl(const DevStage& ds, const Bindings& b, void* out, 
     if (!ds.cs.scatter && out_bytes) cuda_check(cudaMemsetAsync(out, 0, out_bytes, stream), "memset(dead)");
     return;
   }
-  bool affine = !ds.cs.scatter && k.R == 1;
+  bool affine = !ds.cs.scatter && k.R == 1 && !k.prog;
   for (int t = 0; t < k.n_terms && affine; ++t)
     affine = k.terms[t].kind != 2 && k.terms[t].n_atab == 0 && k.terms[t].n_mix == 0 && k.terms[t].rtab == nullptr;
   if (affine) {
@@ -772,7 +941,7 @@ static void launch_stage_impl(const DevStage& ds, const Bindings& b, void* out, 
     cuda_check(cudaGetLastError(), "affine_kernel");
     return;
   }
-  const bool block_mode = !ds.cs.scatter && k.out_count <= 16384 && k.R >= 2048;
+  const bool block_mode = !ds.cs.scatter && k.out_count <= 16384 && k.R >= 2048 && !k.prog;
   // Reduce split: enough threads to fill the chip about twice.
   const int64_t want = 148LL * 2048;
   int64_t nsplit = 1;

@@ -47,6 +47,15 @@ struct KStage {
   void* out;
   KTerm terms[MAXT];
   KTerm target;             // scatter form only
+  // On-the-fly coordinate programs (stages whose index tables would exceed
+  // the table budget): per term (terms, then target) a record
+  //   [ncoord, (code_off, code_len, n, stride) x ncoord]
+  // followed by the int64 postfix code; null when tables are used.
+  const int64_t* prog;
+  int32_t prog_term_off[MAXT + 1];
+  int32_t n_red;
+  int32_t pad2_;
+  int64_t red_ext[16];
 };
 
 // One device-resident stage: tables plus a descriptor with null pointers
@@ -56,6 +65,7 @@ struct DevStage {
   KStage k;
   std::vector<int> term_slot;   // CTensor of each term, to bind pointers
   int32_t* tables = nullptr;    // owned device allocation
+  int64_t* prog = nullptr;      // owned device allocation (program fallback)
   size_t table_entries = 0;
   bool dead = false;
 };

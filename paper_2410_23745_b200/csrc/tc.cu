@@ -214,7 +214,13 @@ constexpr int PK_PIX = 128;
 template <typename TI, int V>
 __global__ void __launch_bounds__(256) pack_rows_kernel(const TI* __restrict__ src, __nv_bfloat16* __restrict__ dst,
                                                         PackGeom g, int32_t rows_per_block, int64_t total_rows) {
-  __shared__ __align__(16) __nv_bfloat16 tile[PK_PIX][72];
+  // channel-major tile: row cl holds the block's pixels; each group of 8
+  // channel rows is rotated by 8 pixels so the transposed reads of the write
+  // phase spread over all banks (the rotation keeps 16-byte alignment)
+  __shared__ __align__(16) __nv_bfloat16 tile[64][PK_PIX + 8];
+  __shared__ int64_t s_src[PK_PIX];  // per block row: source offset of (image, row, first pixel)
+  __shared__ int64_t s_dst[PK_PIX];  // per block row: destination flat index of its first pixel (-1: unused row)
+  __shared__ int32_t s_part[PK_PIX];
   const int t = threadIdx.x;
   const int cb = blockIdx.y;
   const int n_out = g.n_img_out();
@@ -233,35 +239,54 @@ __global__ void __launch_bounds__(256) pack_rows_kernel(const TI* __restrict__ s
     wbeg = (int)(blockIdx.x % nseg) * PK_PIX;
     Win = min(PK_PIX, g.Win - wbeg);
   }
-  const int npix = nrows * Win;
+  if (t < nrows) {
+    const int64_t row = row0 + t;  // (img', hi) flattened
+    int img = (int)(row / g.Hin);
+    const int hi = (int)(row - (int64_t)img * g.Hin);
+    const int imgo = img;
+    int part = 0;
+    if (g.split == SPLIT_IMG) {
+      part = img / g.n_img;
+      img -= part * g.n_img;
+    }
+    s_part[t] = part;
+    s_src[t] = img * g.s_img + (int64_t)hi * g.s_h + (int64_t)wbeg * g.s_w;
+    const int ph = hi % g.Sh, hp = hi / g.Sh + g.lo_h;
+    s_dst[t] = hp < g.Hp ? (((int64_t)(ph * g.Sw) * n_out + imgo) * g.Hp + hp) * g.Wp + g.lo_w : -1;
+  }
+  __syncthreads();
   // ---- read: (channel, pixel-vector) pairs, pixels fastest
-  const int vpr = Win / V;                  // vectors per row
+  const int vpr = Win / V;  // vectors per row
   const int nvec = nrows * vpr;
+#pragma unroll 4
   for (int i = t; i < 64 * nvec; i += 256) {
     const int cl = i / nvec;
     const int vi = i - cl * nvec;
     const int rr = vi / vpr;
     const int w0 = (vi - rr * vpr) * V;
-    const int64_t row = row0 + rr;          // (img', hi) flattened
-    int img = (int)(row / g.Hin);
-    const int hi = (int)(row - (int64_t)img * g.Hin);
     int c = cb * 64 + cl;
-    int part = 0;
-    if (g.split == SPLIT_IMG) {
-      part = img / g.n_img;
-      img -= part * g.n_img;
-    } else if (g.split == SPLIT_CH) {
+    int part = s_part[rr];
+    if (g.split == SPLIT_CH) {
       part = c / g.Cp;
       c -= part * g.Cp;
     }
     float v[V];
     if (c < g.C && part < g.parts()) {
-      const TI* p = src + img * g.s_img + (int64_t)c * g.s_c + (int64_t)hi * g.s_h + (int64_t)(wbeg + w0) * g.s_w;
+      const TI* p = src + s_src[rr] + (int64_t)c * g.s_c + (int64_t)w0 * g.s_w;
       if (V == 8 && sizeof(TI) == 2) {
         const uint4 q = __ldg(reinterpret_cast<const uint4*>(p));
         const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&q);
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
+          const float2 f2 = __bfloat1622float2(h2[e]);
+          v[2 * e] = f2.x;
+          v[2 * e + 1] = f2.y;
+        }
+      } else if (V == 4 && sizeof(TI) == 2) {
+        const uint2 q = __ldg(reinterpret_cast<const uint2*>(p));
+        const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&q);
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
           const float2 f2 = __bfloat1622float2(h2[e]);
           v[2 * e] = f2.x;
           v[2 * e + 1] = f2.y;
@@ -281,31 +306,41 @@ __global__ void __launch_bounds__(256) pack_rows_kernel(const TI* __restrict__ s
       for (int e = 0; e < V; ++e) v[e] = 0.f;
     }
     const bool lo = g.split != SPLIT_NONE && ((g.lo_mask >> part) & 1u);
+    const int px0 = rr * Win + w0;
+    __align__(16) __nv_bfloat16 hv[V];
 #pragma unroll
     for (int e = 0; e < V; ++e) {
-      __nv_bfloat16 hv = __float2bfloat16(v[e]);
-      if (lo) hv = __float2bfloat16(v[e] - __bfloat162float(hv));
-      tile[rr * Win + w0 + e][cl] = hv;
+      hv[e] = __float2bfloat16(v[e]);
+      if (lo) hv[e] = __float2bfloat16(v[e] - __bfloat162float(hv[e]));
+    }
+    if (V == 8) {  // px0 and the rotation are multiples of 8: one 16-byte store
+      *reinterpret_cast<uint4*>(&tile[cl][(px0 + 8 * (cl >> 3)) & (PK_PIX - 1)]) = *reinterpret_cast<const uint4*>(hv);
+    } else {
+#pragma unroll
+      for (int e = 0; e < V; ++e) tile[cl][(px0 + e + 8 * (cl >> 3)) & (PK_PIX - 1)] = hv[e];
     }
   }
   __syncthreads();
   // ---- write: 8 threads per destination pixel, 16 bytes each
   const int Ct = g.Ct();
+  if (cb * 64 >= Ct) return;
+  const int64_t plane_stride = (int64_t)n_out * g.Hp * g.Wp;
+  const int npix = nrows * Win;
+#pragma unroll 4
   for (int i = t; i < npix * 8; i += 256) {
     const int px = i >> 3, chunk = i & 7;
     const int c0 = cb * 64 + chunk * 8;
-    if (c0 >= Ct) continue;
     const int rr = px / Win;
+    const int64_t base = s_dst[rr];
     const int wi = wbeg + px - rr * Win;
-    const int64_t row = row0 + rr;
-    const int img = (int)(row / g.Hin);
-    const int hi = (int)(row - (int64_t)img * g.Hin);
-    const int ph = hi % g.Sh, pw = wi % g.Sw;
-    const int hp = hi / g.Sh + g.lo_h, wp = wi / g.Sw + g.lo_w;
-    if (hp >= g.Hp || wp >= g.Wp) continue;  // never read by any window
-    const int plane = ph * g.Sw + pw;
-    const int64_t f = (((int64_t)plane * n_out + img) * g.Hp + hp) * g.Wp + wp;
-    *reinterpret_cast<uint4*>(dst + f * Ct + c0) = *reinterpret_cast<const uint4*>(&tile[px][chunk * 8]);
+    const int pw = wi % g.Sw, wp = wi / g.Sw;
+    if (base < 0 || c0 >= Ct || wp + g.lo_w >= g.Wp) continue;  // never read by any window
+    const int64_t f = base + pw * plane_stride + wp;
+    __align__(16) __nv_bfloat16 q[8];
+    const int col = (px + 8 * chunk) & (PK_PIX - 1);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) q[k] = tile[chunk * 8 + k][col];
+    *reinterpret_cast<uint4*>(dst + f * Ct + c0) = *reinterpret_cast<const uint4*>(q);
   }
 }
 
@@ -342,6 +377,71 @@ __global__ void __launch_bounds__(128) fold_kernel(const __grid_constant__ FoldA
       }
     }
     __nv_bfloat16* o = f.out + (int64_t)row * parts * f.Bp + b;
+    const __nv_bfloat16 hi = __float2bfloat16(v);
+    o[0] = hi;
+    if (parts == 3) {
+      o[f.Bp] = __float2bfloat16(v - __bfloat162float(hi));
+      o[2 * f.Bp] = hi;
+    }
+  }
+}
+
+// Tiled fold: a block covers TA operand rows x TB operand columns for every
+// window k = (rh, rw).  Weights are read in an order that follows the
+// dominant weight's memory layout (k fastest, then the loop with the smaller
+// stride), staged in shared memory as fp32, and written back as coalesced
+// bf16 rows (split into (hi, lo, hi) parts for fp32 operands).
+template <int TA, int TB>
+__global__ void __launch_bounds__(256) fold_tile_kernel(const __grid_constant__ FoldArgs f, int a_inner) {
+  extern __shared__ float sv[];  // [KK][TA][TB + 1]
+  __shared__ int32_t koff[MAXFW][16];
+  const int KK = f.ext[0] * f.ext[1];
+  if ((int)threadIdx.x < KK) {
+    const int rh = threadIdx.x / f.ext[1], rw = threadIdx.x - rh * f.ext[1];
+#pragma unroll
+    for (int j = 0; j < MAXFW; ++j)
+      if (j < f.nw) koff[j][threadIdx.x] = (int32_t)(rh * f.s[j][0] + rw * f.s[j][1]);
+  }
+  int32_t sa[MAXFW], sb[MAXFW];
+#pragma unroll
+  for (int j = 0; j < MAXFW; ++j) {
+    sa[j] = j < f.nw ? (int32_t)f.s[j][f.sl_a] : 0;
+    sb[j] = j < f.nw ? (int32_t)f.s[j][f.sl_b] : 0;
+  }
+  __syncthreads();
+  const int a0 = blockIdx.x * TA, b0 = blockIdx.y * TB;
+  const int n_el = KK * TA * TB;
+#pragma unroll 4
+  for (int i = threadIdx.x; i < n_el; i += blockDim.x) {
+    const int q = i / KK;
+    const int k = i - q * KK;
+    const int al = a_inner ? q % TA : q / TB;
+    const int bl = a_inner ? q / TA : q % TB;
+    const int a = a0 + al, b = b0 + bl;
+    float v = 0.f;
+    if (a < f.ext[2] && b < f.ext[3]) {
+      v = 1.f;
+#pragma unroll
+      for (int j = 0; j < MAXFW; ++j) {
+        if (j >= f.nw) break;
+        const int32_t off = koff[j][k] + a * sa[j] + b * sb[j];
+        v *= f.f32 ? __ldg(reinterpret_cast<const float*>(f.w[j]) + off)
+                   : __bfloat162float(__ldg(reinterpret_cast<const __nv_bfloat16*>(f.w[j]) + off));
+      }
+    }
+    sv[(k * TA + al) * (TB + 1) + bl] = v;
+  }
+  __syncthreads();
+  const int parts = f.split ? 3 : 1;
+#pragma unroll 4
+  for (int i = threadIdx.x; i < n_el; i += blockDim.x) {
+    const int bl = i % TB;
+    const int al = (i / TB) % TA;
+    const int k = i / (TA * TB);
+    const int a = a0 + al, b = b0 + bl;
+    if (a >= f.ext[2] || b >= f.Bp) continue;
+    const float v = sv[(k * TA + al) * (TB + 1) + bl];
+    __nv_bfloat16* o = f.out + ((int64_t)k * f.ext[2] + a) * parts * f.Bp + b;
     const __nv_bfloat16 hi = __float2bfloat16(v);
     o[0] = hi;
     if (parts == 3) {
@@ -410,6 +510,96 @@ __global__ void __launch_bounds__(256) chain_thread_kernel(const __grid_constant
   }
   chain_decode(c, o, 0, d);
   chain_store(c, d, acc);
+}
+
+// Chain rule for a weight that uses the n loop (every main weight): one
+// block per (output channel n, chunk of input channels) stages
+// dWf[:, :, n, chunk] (coalesced) in shared memory and produces those dW_j
+// entries in dW_j's memory order, reducing over the loops the weight does
+// not use (a window at most).  All index arithmetic is int32 with
+// host-precomputed multipliers (digit -> smem / output / weight offsets).
+struct ChainN {
+  int32_t n_ol, n_rl;
+  int32_t ol_ext[3], ol_sm[3], ol_out[3], ol_w[3][MAXFW];  // output loops in memory order (ci: chunk-local)
+  int32_t rl_ext[3], rl_sm[3], rl_w[3][MAXFW];             // reduced loops
+  int32_t n_out, n_w[MAXFW];                               // per-n offsets
+  int32_t ci_q;                                            // position of ci among the output loops, -1 none
+  int32_t ci_chunk;
+  int32_t KK, C, Kw;
+};
+
+__global__ void __launch_bounds__(256) chain_n_kernel(const __grid_constant__ ChainArgs c, const __grid_constant__ ChainN h) {
+  extern __shared__ float sd[];  // [KK][cw + 1]
+  const int n = blockIdx.x;
+  const int c_lo = h.ci_q >= 0 ? blockIdx.y * h.ci_chunk : 0;
+  const int cw = h.ci_q >= 0 ? min(h.C - c_lo, h.ci_chunk) : h.C;
+  const int P = cw + 1;
+#pragma unroll 4
+  for (int i = threadIdx.x; i < h.KK * cw; i += blockDim.x) {
+    const int k = i / cw, ci = i - k * cw;
+    sd[k * P + ci] = __ldg(c.dwf + ((int64_t)k * c.ext[2] + n) * h.C + c_lo + ci);
+  }
+  __syncthreads();
+  // per-block bases: n and the chunk start of ci
+  int32_t base_out = n * h.n_out, base_w[MAXFW];
+#pragma unroll
+  for (int k = 0; k < MAXFW; ++k) base_w[k] = n * h.n_w[k];
+  if (h.ci_q >= 0) {
+    base_out += c_lo * h.ol_out[h.ci_q];
+#pragma unroll
+    for (int k = 0; k < MAXFW; ++k) base_w[k] += c_lo * h.ol_w[h.ci_q][k];
+  }
+  int ext[3];
+  int m = 1;
+#pragma unroll
+  for (int q = 0; q < 3; ++q) {
+    ext[q] = q < h.n_ol ? (q == h.ci_q ? cw : h.ol_ext[q]) : 1;
+    m *= ext[q];
+  }
+  int R = 1;
+#pragma unroll
+  for (int q = 0; q < 3; ++q) R *= q < h.n_rl ? h.rl_ext[q] : 1;
+#pragma unroll 2
+  for (int i = threadIdx.x; i < m; i += blockDim.x) {
+    int rem = i, o_out = base_out, o_sm = 0, o_w[MAXFW];
+#pragma unroll
+    for (int k = 0; k < MAXFW; ++k) o_w[k] = base_w[k];
+#pragma unroll
+    for (int q = 2; q >= 0; --q) {
+      if (q >= h.n_ol) continue;
+      const int dq = rem % ext[q];
+      rem /= ext[q];
+      o_out += dq * h.ol_out[q];
+      o_sm += dq * h.ol_sm[q];
+#pragma unroll
+      for (int k = 0; k < MAXFW; ++k) o_w[k] += dq * h.ol_w[q][k];
+    }
+    float acc = 0.f;
+    for (int r = 0; r < R; ++r) {
+      int rr = r, r_sm = o_sm, r_w[MAXFW];
+#pragma unroll
+      for (int k = 0; k < MAXFW; ++k) r_w[k] = o_w[k];
+#pragma unroll
+      for (int q = 2; q >= 0; --q) {
+        if (q >= h.n_rl) continue;
+        const int dq = rr % h.rl_ext[q];
+        rr /= h.rl_ext[q];
+        r_sm += dq * h.rl_sm[q];
+#pragma unroll
+        for (int k = 0; k < MAXFW; ++k) r_w[k] += dq * h.rl_w[q][k];
+      }
+      float v = sd[r_sm];
+#pragma unroll
+      for (int k = 0; k < MAXFW; ++k) {
+        if (k >= c.nw || k == c.j) continue;
+        v *= c.f32 ? __ldg(reinterpret_cast<const float*>(c.w[k]) + r_w[k])
+                   : __bfloat162float(__ldg(reinterpret_cast<const __nv_bfloat16*>(c.w[k]) + r_w[k]));
+      }
+      acc += v;
+    }
+    if (c.f32) reinterpret_cast<float*>(c.out)[o_out] = acc;
+    else reinterpret_cast<__nv_bfloat16*>(c.out)[o_out] = __float2bfloat16(acc);
+  }
 }
 
 // Long reductions: block (o, split) reduces one chunk; the last block of an
@@ -922,6 +1112,7 @@ static void pack_cl(const void* src, DType dt, const PackGeom& g, __nv_bfloat16*
   };
   if (dt == DT_BF16) {
     if (aligned(8, 2)) launch_pack_rows<__nv_bfloat16, 8>(src, g, dst, grid, rpb, rows, stream);
+    else if (aligned(4, 2)) launch_pack_rows<__nv_bfloat16, 4>(src, g, dst, grid, rpb, rows, stream);
     else launch_pack_rows<__nv_bfloat16, 1>(src, g, dst, grid, rpb, rows, stream);
   } else {
     if (aligned(4, 4)) launch_pack_rows<float, 4>(src, g, dst, grid, rpb, rows, stream);
@@ -1315,14 +1506,26 @@ static void fold_fast(const TcPlan& tp, const Bindings& b, DType dt, bool dgrad,
   f.Bp = dgrad ? tp.Np : tp.Cp;
   f.split = split;
   f.out = dst;
-  const int64_t rows = (int64_t)f.ext[0] * f.ext[1] * f.ext[2];
-  if (rows > 65535) fail(SYNO_E_UNSUPPORTED, "fold: too many operand rows");
-  dim3 grid((unsigned)std::min(8, (f.Bp + 127) / 128), (unsigned)rows);
+  const int KK = f.ext[0] * f.ext[1];
+  const int64_t rows = (int64_t)KK * f.ext[2];
   const double elems = (double)rows * f.Bp;
   const int id = prof_begin("weight_fold", 0.0, elems * (split ? 6 : 2) + elems * tp.nw * (f.f32 ? 4 : 2), stream);
   note_launch();
-  fold_kernel<<<grid, 128, 0, stream>>>(f);
-  cuda_check(cudaGetLastError(), "fold_kernel");
+  // read order: the first weight's smaller stride of (a, b) goes inner
+  const int a_inner = std::llabs(tp.wstr[0][f.sl_a]) < std::llabs(tp.wstr[0][f.sl_b]) ? 1 : 0;
+  if (KK == 1) {
+    const size_t sm = (size_t)32 * 33 * sizeof(float);
+    fold_tile_kernel<32, 32><<<dim3((unsigned)((f.ext[2] + 31) / 32), (unsigned)((f.Bp + 31) / 32)), 256, sm, stream>>>(
+        f, a_inner);
+  } else if (KK <= 16) {
+    const size_t sm = (size_t)KK * 65 * sizeof(float);
+    fold_tile_kernel<1, 64><<<dim3((unsigned)f.ext[2], (unsigned)((f.Bp + 63) / 64)), 256, sm, stream>>>(f, a_inner);
+  } else {
+    if (rows > 65535) fail(SYNO_E_UNSUPPORTED, "fold: too many operand rows");
+    dim3 grid((unsigned)std::min(8, (f.Bp + 127) / 128), (unsigned)rows);
+    fold_kernel<<<grid, 128, 0, stream>>>(f);
+  }
+  cuda_check(cudaGetLastError(), "fold kernel");
   prof_end(id, stream);
 }
 
@@ -1355,7 +1558,48 @@ static void chain_fast(const TcPlan& tp, const TcWs& w, const Bindings& b, DType
   const int id = prof_begin("weight_chain", 0.0, bytes, stream);
   note_launch();
   const int nsplit = w.chain_nsplit[j];
-  if (!nsplit) {
+  const bool ci_out = tp.wstr[j][3] != 0;
+  const int chunk = ci_out ? 64 : 0;
+  const int cw_max = ci_out ? std::min(64, (int)c.ext[3]) : (int)c.ext[3];
+  const size_t sm_n = (size_t)c.ext[0] * c.ext[1] * (cw_max + 1) * sizeof(float);
+  if (!nsplit && tp.wstr[j][2] != 0 && sm_n <= 48 * 1024) {
+    // n is an output loop: one block per (output channel, 64 input channels)
+    ChainN h{};
+    h.KK = (int)(c.ext[0] * c.ext[1]);
+    h.C = (int)c.ext[3];
+    h.Kw = (int)c.ext[1];
+    h.ci_chunk = chunk;
+    h.ci_q = -1;
+    const int P = cw_max + 1;
+    const int32_t smul[4] = {(int32_t)c.ext[1] * P, P, 0, 1};
+    int ol[3], n_ol = 0, rl[3], n_rl = 0;
+    for (int l : {0, 1, 3}) {
+      if (tp.wstr[j][l]) ol[n_ol++] = l;
+      else if (c.ext[l] > 1) rl[n_rl++] = l;
+    }
+    std::sort(ol, ol + n_ol, [&](int x, int y) { return tp.wstr[j][x] > tp.wstr[j][y]; });
+    h.n_ol = n_ol;
+    h.n_rl = n_rl;
+    for (int q = 0; q < n_ol; ++q) {
+      const int l = ol[q];
+      if (l == 3) h.ci_q = q;
+      h.ol_ext[q] = (int)c.ext[l];
+      h.ol_sm[q] = smul[l];
+      h.ol_out[q] = (int32_t)tp.wstr[j][l];
+      for (int k = 0; k < tp.nw; ++k) h.ol_w[q][k] = k == j ? 0 : (int32_t)tp.wstr[k][l];
+    }
+    for (int q = 0; q < n_rl; ++q) {
+      const int l = rl[q];
+      h.rl_ext[q] = (int)c.ext[l];
+      h.rl_sm[q] = smul[l];
+      for (int k = 0; k < tp.nw; ++k) h.rl_w[q][k] = k == j ? 0 : (int32_t)tp.wstr[k][l];
+    }
+    h.n_out = (int32_t)tp.wstr[j][2];
+    for (int k = 0; k < tp.nw; ++k) h.n_w[k] = k == j ? 0 : (int32_t)tp.wstr[k][2];
+    if (!ci_out) h.ci_chunk = 0;
+    const unsigned gy = ci_out ? (unsigned)((c.ext[3] + chunk - 1) / chunk) : 1u;
+    chain_n_kernel<<<dim3((unsigned)c.ext[2], gy), 256, sm_n, stream>>>(c, h);
+  } else if (!nsplit) {
     chain_thread_kernel<<<(unsigned)((c.out_count + 255) / 256), 256, 0, stream>>>(c);
   } else {
     c.r_chunk = (c.R + nsplit - 1) / nsplit;

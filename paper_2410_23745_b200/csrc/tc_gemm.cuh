@@ -142,6 +142,20 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 #endif
 }
 
+// Long waits (the epilogue warps waiting a whole tile for the accumulator):
+// the suspending probe with a time hint parks the warp instead of spinning,
+// so eight idle epilogue warps do not compete with the producer / MMA warps
+// for issue slots and the barrier unit.
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity), "r"(0x10000)
+      : "memory");
+}
+
 __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
                                             int c2) {
   asm volatile(
@@ -441,7 +455,8 @@ __global__ void __launch_bounds__(THREADS, 1) tc_gemm_kernel(const __grid_consta
               if (lane == 0 && tcount == 0 && w < 9) stamp(40 + w);
               asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
               const uint64_t db = sw128_desc(sb + bs * B_BYTES);
-              const uint32_t arow = abase + (uint32_t)(p.a_shift[w] - p.chunk_pmin[c]) * 128u;
+              // profiling switch 32: every window reads the aligned halo start (wrong values, timing only)
+              const uint32_t arow = abase + ((p.dbg & 32) ? 0u : (uint32_t)(p.a_shift[w] - p.chunk_pmin[c]) * 128u);
               if (!(p.dbg & 2)) {
 #pragma unroll
                 for (int g = 0; g < G; ++g) {
@@ -505,7 +520,8 @@ __global__ void __launch_bounds__(THREADS, 1) tc_gemm_kernel(const __grid_consta
     for (int t = blockIdx.x; t < n_tiles_total; t += gridDim.x, ++tcount) {
       const TileInfo ti = tile_info(p, t);
       const uint32_t acc = tcount & 1u;
-      mbar_wait(&tfull[acc], (tcount >> 1) & 1u);
+      if (p.dbg & 64) mbar_wait(&tfull[acc], (tcount >> 1) & 1u);
+      else mbar_wait_sleep(&tfull[acc], (tcount >> 1) & 1u);
       if (warp == 2 && lane == 0 && tcount < 14) stamp(2 + tcount * 4 + 2);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const int nsub = p.mode == MODE_ROWS ? p.G : 1;

@@ -194,3 +194,28 @@ def test_torch_autograd_module(cuda):
     x = torch.randn(m.h.x_shape, dtype=torch.float64, device="cuda", requires_grad=True)
     assert torch.autograd.gradcheck(lambda a, *w: ops.SynoFunction.apply(m.h, a, *w), (x, *m.weight),
                                     eps=1e-6, atol=1e-7)
+
+
+@pytest.mark.parametrize("name", ["conv2d_8", "strided_conv1d", "sep_shared", "bpool", "corpus0003", "corpus0011"])
+def test_program_fallback_matches_oracle(cuda, name, monkeypatch):
+    """Stages whose index tables exceed the budget evaluate coordinate programs
+    on the fly; SYNO_TABLE_LIMIT=2 forces that path on golden cases."""
+    from paper_2410_23745_b200 import ops
+    from paper_2410_23745_b200 import pgraph as P
+    torch = _torch()
+    case = next(c for c in CASES if c["name"] == name)
+    monkeypatch.setenv("SYNO_TABLE_LIMIT", "2")
+    h = P.Handle(case["document"], case["assignment"], False)  # uncached: a fresh device plan
+    x, ws, up, y, _, dws = case_tensors(case)
+    xd = ops.to_device(x, "float64")
+    wd = [ops.to_device(w, "float64") for w in ws]
+    ud = ops.to_device(up, "float64")
+    gy = ops.forward(h, xd, wd)
+    gdx, gdw = ops.backward(h, xd, wd, ud)
+    torch.cuda.synchronize()
+    f = lambda t: t.double().cpu().numpy()  # noqa: E731
+    env, bs = case["env"], case["batch_shape"]
+    assert O.rel_err(f(gy), y) < 1e-10
+    assert O.rel_err(f(gdx), O.input_gradient(case["nest"], env, x, up, ws, bs)) < 1e-10
+    for a, b in zip(gdw, dws):
+        assert O.rel_err(f(a), b) < 1e-10
