@@ -254,9 +254,10 @@ def run_layers(args, rank, world, device, peaks):
     def call_bwd(s):
         warr = (ctypes.c_void_p * max(1, len(s["ws"])))(*[w.data_ptr() for w in s["ws"]])
         dwarr = (ctypes.c_void_p * max(1, len(s["ws"])))(*[g.data_ptr() for g in s["dws"]])
-        rc = _lib.lib.syno_backward(s["h"].ptr, code, ctypes.c_void_p(s["x"].data_ptr()), warr, len(s["ws"]),
-                                    ctypes.c_void_p(s["dy"].data_ptr()), ctypes.c_void_p(s["dx"].data_ptr()),
-                                    dwarr, sp)
+        # training-step contract: backward follows this layer's forward on the same x
+        rc = _lib.lib.syno_backward_ex(s["h"].ptr, code, ctypes.c_void_p(s["x"].data_ptr()), warr, len(s["ws"]),
+                                       ctypes.c_void_p(s["dy"].data_ptr()), ctypes.c_void_p(s["dx"].data_ptr()),
+                                       dwarr, _lib.SYNO_BWD_X_UNCHANGED, sp)
         assert rc == 0, _lib.last_error()
 
     phases = [("fwd", call_fwd)] + ([] if fwd_only else [("bwd", call_bwd)])
@@ -441,7 +442,8 @@ def run_sweep(args, rank, world, device, peaks):
     from paper_2410_23745_b200 import workloads as WL
     warm_graphs = WL.corpus(2, limit=args.limit)
     for k in range(max(1, args.warmup)):
-        run_shard(warm_graphs, mine[k::max(1, args.warmup)], dtype=torch.float32, flops_cap=fcap, params_cap=pcap)
+        run_shard(warm_graphs, mine[k::max(1, args.warmup)], dtype=torch.float32, flops_cap=fcap, params_cap=pcap,
+                  workers=args.workers)
     torch.cuda.synchronize(device)
     sampler = ClockSampler(device.index or 0)
     if rank == 0:
@@ -456,7 +458,8 @@ def run_sweep(args, rank, world, device, peaks):
         torch.cuda.synchronize(device)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        recs, _ = run_shard(graphs, mine, dtype=torch.float32, flops_cap=fcap, params_cap=pcap)
+        recs, _ = run_shard(graphs, mine, dtype=torch.float32, flops_cap=fcap, params_cap=pcap,
+                            workers=args.workers)
         e1.record()
         torch.cuda.synchronize(device)
         step_s.append(e0.elapsed_time(e1) / 1e3)
@@ -479,6 +482,7 @@ def run_sweep(args, rank, world, device, peaks):
     return {"value": n_total / s, "unit": "candidates/s", "ms_per_step": s * 1e3, "roofline": None,
             "gpu_launches": int(launches), "clocks": sampler.summary() if rank == 0 else None,
             "dtype": "f32", "sweep": {"candidates": n_total, "this_rank": len(mine), "executed_this_rank": evaluated,
+                                      "workers_per_gpu": args.workers,
                                       "status_this_rank": status, "flops_cap": fcap, "params_cap": pcap},
             "e2e": None}
 
@@ -697,6 +701,7 @@ def main():
                     choices=["resnet18", "resnet34", "cfg1", "qkv", "sweep", "qkv_train"])
     ap.add_argument("--batch", type=int, default=0)
     ap.add_argument("--limit", type=int, default=None, help="sweep: first N corpus candidates only")
+    ap.add_argument("--workers", type=int, default=8, help="sweep: concurrent candidates per GPU (own streams)")
     ap.add_argument("--impl", default="syno", choices=["syno", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graph", dest="graph", action="store_false", help="eager launches instead of a CUDA graph")

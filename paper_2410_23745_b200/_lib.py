@@ -25,6 +25,7 @@ SYNO_E_UNSUPPORTED = 9
 SYNO_F32 = 0
 SYNO_BF16 = 1
 SYNO_F64 = 2
+SYNO_BWD_X_UNCHANGED = 1
 SYNO_STAGED = 1
 SYNO_REPLAY_ONLY = 2
 
@@ -36,7 +37,7 @@ EXPORTS = (
     "syno_compile", "syno_forward", "syno_backward", "syno_query",
     "syno_emit_loop_nest", "syno_print_operator", "syno_describe_plan",
     "syno_index_map", "syno_destroy", "syno_last_error", "syno_version", "syno_launch_count",
-    "syno_profile_begin", "syno_profile_end",
+    "syno_profile_begin", "syno_profile_end", "syno_backward_ex",
 )
 
 
@@ -85,6 +86,8 @@ def _load():
     lib.syno_forward.argtypes = [vp, ctypes.c_int, vp, ctypes.POINTER(vp), ctypes.c_int, vp, vp]
     lib.syno_backward.argtypes = [vp, ctypes.c_int, vp, ctypes.POINTER(vp), ctypes.c_int, vp, vp,
                                   ctypes.POINTER(vp), vp]
+    lib.syno_backward_ex.argtypes = [vp, ctypes.c_int, vp, ctypes.POINTER(vp), ctypes.c_int, vp, vp,
+                                     ctypes.POINTER(vp), ctypes.c_int, vp]
     lib.syno_query.argtypes = [vp, ctypes.POINTER(SynoInfo)]
     for name in ("syno_emit_loop_nest",):
         getattr(lib, name).argtypes = [vp, ctypes.c_int, ctypes.c_char_p, ctypes.c_size_t,

@@ -129,11 +129,12 @@ int syno_forward(syno_op_t op, int dtype, const void* x, const void* const* w, i
   });
 }
 
-int syno_backward(syno_op_t op, int dtype, const void* x, const void* const* w, int n_w, const void* dy, void* dx,
-                  void* const* dw, void* stream) {
+int syno_backward_ex(syno_op_t op, int dtype, const void* x, const void* const* w, int n_w, const void* dy,
+                     void* dx, void* const* dw, int flags, void* stream) {
   return guarded([&] {
     if (!op || !x || !dy || (n_w && !w)) fail(SYNO_E_INVALID, "null argument");
     if (dtype < 0 || dtype > 2) fail(SYNO_E_INVALID, "unknown dtype");
+    if (flags & ~SYNO_BWD_X_UNCHANGED) fail(SYNO_E_INVALID, "unknown backward flag");
     check_weights(op, w, n_w);
     cudaStream_t s = (cudaStream_t)stream;
     DevPlan& dp = dev_plan(op, s);
@@ -143,8 +144,14 @@ int syno_backward(syno_op_t op, int dtype, const void* x, const void* const* w, 
     b.dy = dy;
     b.dx = dx;
     for (int j = 0; j < n_w; ++j) b.dw.push_back(dw ? dw[j] : nullptr);
+    b.x_unchanged = (flags & SYNO_BWD_X_UNCHANGED) != 0;
     run_backward(op->plan, dp, (DType)dtype, b, s);
   });
+}
+
+int syno_backward(syno_op_t op, int dtype, const void* x, const void* const* w, int n_w, const void* dy, void* dx,
+                  void* const* dw, void* stream) {
+  return syno_backward_ex(op, dtype, x, w, n_w, dy, dx, dw, 0, stream);
 }
 
 int syno_query(syno_op_t op, syno_info* info) {

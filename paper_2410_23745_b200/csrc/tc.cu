@@ -1243,6 +1243,7 @@ struct TcWs {
   // zero-copy operands: a source already in the packed layout (channels-last,
   // unpadded, e.g. QKV activations) is read by TMA in place
   bool x_ident = false, xw_ident = false, dyg_ident = false, dyw_ident = false;
+  const void* packed_x_src = nullptr;  // x whose packed operand xcl currently holds (last forward)
   MapSpec ms_fwd_a, ms_dg_a, ms_wg_a, ms_wg_b;
   PackGeom gx{}, gxw{}, gdy_g{}, gdy_w{};
   bool share_dy = false, share_x = false;
@@ -1265,7 +1266,7 @@ void TcPlanDeleter::operator()(TcPlan* p) const {
 
 static bool same_grid(const PackGeom& a, const PackGeom& b) {
   return a.lo_h == b.lo_h && a.lo_w == b.lo_w && a.Hp == b.Hp && a.Wp == b.Wp && a.split == b.split &&
-         a.lo_mask == b.lo_mask;
+         (a.split == SPLIT_NONE || a.lo_mask == b.lo_mask);
 }
 
 template <typename T>
@@ -1660,8 +1661,12 @@ bool tc_forward(TcPlan& tp, DType dt, const Bindings& b, cudaStream_t stream) {
   if (!tc_dtype(dt)) return false;
   TcWs& w = workspace(tp, dt, stream);
   TcGemmParams p = w.fwd;
-  if (w.x_ident && aligned16(b.x)) p.tma_a = make_map(b.x, w.ms_fwd_a);
-  else pack_cl(b.x, dt, w.gx, w.xcl, stream);
+  if (w.x_ident && aligned16(b.x)) {
+    p.tma_a = make_map(b.x, w.ms_fwd_a);
+  } else {
+    pack_cl(b.x, dt, w.gx, w.xcl, stream);
+    w.packed_x_src = b.x;
+  }
   if (tp.fast_fold) fold_fast(tp, b, dt, false, w.f32, w.wf, stream);
   else fold_into(w, tp.fold_fwd, dt, b, w.wf32, w.wf, (int64_t)tp.nwin() * tp.N, tp.Cp, stream);
   rows_gemm(p, w.bn_fwd, w.t_fwd, b.y, w.f32, w.ysc, tp.y_numel(), stream, "tc_gemm_fwd", tp.flops);
@@ -1689,7 +1694,7 @@ bool tc_backward(TcPlan& tp, DType dt, const Bindings& b, cudaStream_t stream) {
   if (any_w) {
     TcGemmParams p = w.wg;
     if (w.xw_ident && aligned16(b.x)) p.tma_a = make_map(b.x, w.ms_wg_a);
-    else pack_cl(b.x, dt, w.gxw, w.xclw, stream);
+    else if (!(b.x_unchanged && w.share_x && w.packed_x_src == b.x)) pack_cl(b.x, dt, w.gxw, w.xclw, stream);
     if (w.dyw_ident && aligned16(b.dy)) p.tma_b = make_map(b.dy, w.ms_wg_b);
     else if (!dy_w_packed) pack_cl(b.dy, dt, w.gdy_w, w.dycl_w, stream);
     cuda_check(cudaMemsetAsync(w.dwf, 0, (size_t)tp.nwin() * tp.N * tp.C * sizeof(float), stream), "memset(dWf)");
