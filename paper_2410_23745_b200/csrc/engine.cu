@@ -26,9 +26,38 @@ void cuda_check(cudaError_t e, const char* what) {
   if (e != cudaSuccess) fail(SYNO_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
 }
 
+bool pdl_enabled() {
+  static const bool on = getenv("SYNO_NO_PDL") == nullptr;
+  return on;
+}
+
+__global__ void __launch_bounds__(256) zero_fill_kernel(uint4* p, int64_t n16, uint8_t* tail, int tail_bytes) {
+  pdl_trigger();
+  pdl_wait();
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n16; i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = make_uint4(0, 0, 0, 0);
+  if (blockIdx.x == 0 && (int)threadIdx.x < tail_bytes) tail[threadIdx.x] = 0;
+}
+
 static std::atomic<uint64_t> g_launches{0};
 void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 uint64_t launch_count() { return g_launches.load(std::memory_order_relaxed); }
+
+void zero_fill(void* ptr, size_t bytes, cudaStream_t stream) {
+  if (!bytes) return;
+  // library buffers are 16-byte aligned (cudaMalloc / pool); a misaligned
+  // pointer falls back to the runtime memset
+  if (reinterpret_cast<uintptr_t>(ptr) & 15) {
+    cuda_check(cudaMemsetAsync(ptr, 0, bytes, stream), "cudaMemsetAsync");
+    return;
+  }
+  const int64_t n16 = (int64_t)(bytes / 16);
+  const int tail = (int)(bytes - (size_t)n16 * 16);
+  const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((n16 + 255) / 256, 148 * 8));
+  note_launch();
+  launch_k(zero_fill_kernel, (unsigned)blocks, 256, 0, stream, static_cast<uint4*>(ptr), n16,
+           static_cast<uint8_t*>(ptr) + n16 * 16, tail);
+}
 
 namespace {
 struct ProfRec {
@@ -185,6 +214,8 @@ struct K1Args {
 };
 
 __global__ void k1_build_table(const __grid_constant__ K1Args a) {
+  pdl_trigger();
+  pdl_wait();
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= a.count) return;
   int64_t vals[MAXL];
@@ -263,7 +294,7 @@ static void launch_k1(const TabSpec& t, int32_t* out, int64_t* out_raw, cudaStre
   if (t.count > 0) {
     int64_t blocks = (t.count + 255) / 256;
     note_launch();
-    k1_build_table<<<(unsigned)blocks, 256, 0, stream>>>(a);
+    launch_k(k1_build_table, (unsigned)blocks, 256, 0, stream, a);
     cuda_check(cudaGetLastError(), "k1_build_table");
   }
   if (dcode) {
@@ -642,6 +673,8 @@ template <typename T> __device__ __forceinline__ void atomic_add(T* p, T v) { at
 // higher occupancy for the common 1-3 term stages.
 template <typename TI, typename TA, bool SCATTER, int NT>
 __global__ void __launch_bounds__(256, NT <= 2 ? 4 : 2) stage_kernel(const __grid_constant__ KStage S) {
+  pdl_trigger();
+  pdl_wait();
   const int64_t o = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (o >= S.out_count) return;
   const int64_t r0 = (int64_t)blockIdx.y * S.r_chunk;
@@ -718,6 +751,8 @@ __device__ __forceinline__ bool prog_offset(const int64_t* prog, int rec, const 
 
 template <typename TI, typename TA, bool SCATTER>
 __global__ void __launch_bounds__(128) stage_prog_kernel(const __grid_constant__ KStage S) {
+  pdl_trigger();
+  pdl_wait();
   const int64_t o = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (o >= S.out_count) return;
   const int64_t r0 = (int64_t)blockIdx.y * S.r_chunk;
@@ -764,6 +799,8 @@ __global__ void __launch_bounds__(128) stage_prog_kernel(const __grid_constant__
 // output digits, so the kernel is a plain strided gather-product.
 template <typename TI, typename TA, int NT>
 __global__ void __launch_bounds__(256) affine_kernel(const __grid_constant__ KStage S) {
+  pdl_trigger();
+  pdl_wait();
   const int64_t o = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (o >= S.out_count) return;
   int64_t off[NT];
@@ -794,6 +831,8 @@ __global__ void __launch_bounds__(256) affine_kernel(const __grid_constant__ KSt
 // output, threads stride the reduce range, warp-shuffle + smem tree reduce.
 template <typename TI, typename TA>
 __global__ void __launch_bounds__(256) stage_block_kernel(const __grid_constant__ KStage S) {
+  pdl_trigger();
+  pdl_wait();
   const int64_t o = blockIdx.x;
   const int64_t r0 = (int64_t)blockIdx.y * S.r_chunk;
   const int64_t r1 = min(S.R, r0 + S.r_chunk);
@@ -855,6 +894,8 @@ __global__ void __launch_bounds__(256) stage_block_kernel(const __grid_constant_
 
 template <typename TO, typename TA>
 __global__ void sum_partials(const TA* part, int64_t count, int nsplit, TO* out) {
+  pdl_trigger();
+  pdl_wait();
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= count) return;
   TA s = 0;
@@ -864,6 +905,8 @@ __global__ void sum_partials(const TA* part, int64_t count, int nsplit, TO* out)
 
 template <typename TO, typename TA>
 __global__ void cast_kernel(const TA* in, int64_t count, TO* out) {
+  pdl_trigger();
+  pdl_wait();
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < count) out[i] = from_acc<TO, TA>(in[i]);
 }
@@ -892,12 +935,12 @@ template <typename TI, typename TA, bool SCATTER>
 static void launch_nt(const KStage& k, dim3 grid, cudaStream_t stream) {
   if (k.prog) {
     dim3 g2((unsigned)((k.out_count + 127) / 128), grid.y);
-    stage_prog_kernel<TI, TA, SCATTER><<<g2, 128, 0, stream>>>(k);
+    launch_k(stage_prog_kernel<TI, TA, SCATTER>, g2, 128, 0, stream, k);
     return;
   }
-  if (k.n_terms <= 2) stage_kernel<TI, TA, SCATTER, 2><<<grid, 256, 0, stream>>>(k);
-  else if (k.n_terms <= 4) stage_kernel<TI, TA, SCATTER, 4><<<grid, 256, 0, stream>>>(k);
-  else stage_kernel<TI, TA, SCATTER, MAXT><<<grid, 256, 0, stream>>>(k);
+  if (k.n_terms <= 2) launch_k(stage_kernel<TI, TA, SCATTER, 2>, grid, 256, 0, stream, k);
+  else if (k.n_terms <= 4) launch_k(stage_kernel<TI, TA, SCATTER, 4>, grid, 256, 0, stream, k);
+  else launch_k(stage_kernel<TI, TA, SCATTER, MAXT>, grid, 256, 0, stream, k);
 }
 
 template <typename TI>
@@ -924,7 +967,7 @@ static void launch_stage_impl(const DevStage& ds, const Bindings& b, void* out, 
   }
   const int64_t out_bytes = k.out_count * (int64_t)(out_acc ? sizeof(TA) : sizeof(TI));
   if (ds.dead || k.out_count == 0) {
-    if (!ds.cs.scatter && out_bytes) cuda_check(cudaMemsetAsync(out, 0, out_bytes, stream), "memset(dead)");
+    if (!ds.cs.scatter && out_bytes) zero_fill(out, out_bytes, stream);
     return;
   }
   bool affine = !ds.cs.scatter && k.R == 1 && !k.prog;
@@ -936,8 +979,8 @@ static void launch_stage_impl(const DevStage& ds, const Bindings& b, void* out, 
     k.out_acc = out_acc;
     const unsigned blocks = (unsigned)((k.out_count + 255) / 256);
     note_launch();
-    if (k.n_terms <= 2) affine_kernel<TI, TA, 2><<<blocks, 256, 0, stream>>>(k);
-    else affine_kernel<TI, TA, MAXT><<<blocks, 256, 0, stream>>>(k);
+    if (k.n_terms <= 2) launch_k(affine_kernel<TI, TA, 2>, blocks, 256, 0, stream, k);
+    else launch_k(affine_kernel<TI, TA, MAXT>, blocks, 256, 0, stream, k);
     cuda_check(cudaGetLastError(), "affine_kernel");
     return;
   }
@@ -964,13 +1007,13 @@ static void launch_stage_impl(const DevStage& ds, const Bindings& b, void* out, 
     k.out = nsplit > 1 ? (void*)part : out;
     k.out_acc = nsplit > 1 ? 1 : out_acc;
     note_launch();
-    stage_block_kernel<TI, TA><<<bgrid, 256, 0, stream>>>(k);
+    launch_k(stage_block_kernel<TI, TA>, bgrid, 256, 0, stream, k);
     cuda_check(cudaGetLastError(), "stage_block_kernel");
     if (nsplit > 1) {
       unsigned blocks = (unsigned)((k.out_count + 255) / 256);
       note_launch();
-      if (out_acc) sum_partials<TA, TA><<<blocks, 256, 0, stream>>>(part, k.out_count, (int)nsplit, (TA*)out);
-      else sum_partials<TI, TA><<<blocks, 256, 0, stream>>>(part, k.out_count, (int)nsplit, (TI*)out);
+      if (out_acc) launch_k(sum_partials<TA, TA>, blocks, 256, 0, stream, part, k.out_count, (int)nsplit, (TA*)out);
+      else launch_k(sum_partials<TI, TA>, blocks, 256, 0, stream, part, k.out_count, (int)nsplit, (TI*)out);
       cuda_check(cudaGetLastError(), "sum_partials");
       cuda_check(cudaFreeAsync(part, stream), "free partials");
     }
@@ -1003,8 +1046,8 @@ static void launch_stage_impl(const DevStage& ds, const Bindings& b, void* out, 
   cuda_check(cudaGetLastError(), "stage_kernel<split>");
   unsigned blocks = (unsigned)((k.out_count + 255) / 256);
   note_launch();
-  if (out_acc) sum_partials<TA, TA><<<blocks, 256, 0, stream>>>(part, k.out_count, (int)nsplit, (TA*)out);
-  else sum_partials<TI, TA><<<blocks, 256, 0, stream>>>(part, k.out_count, (int)nsplit, (TI*)out);
+  if (out_acc) launch_k(sum_partials<TA, TA>, blocks, 256, 0, stream, part, k.out_count, (int)nsplit, (TA*)out);
+  else launch_k(sum_partials<TI, TA>, blocks, 256, 0, stream, part, k.out_count, (int)nsplit, (TI*)out);
   cuda_check(cudaGetLastError(), "sum_partials");
   cuda_check(cudaFreeAsync(part, stream), "free partials");
 }
@@ -1022,7 +1065,7 @@ static void launch_cast(DType dt, const void* acc, int64_t count, void* out, cud
   unsigned blocks = (unsigned)((count + 255) / 256);
   if (!count || dt != DT_BF16) return;
   note_launch();
-  cast_kernel<__nv_bfloat16, float><<<blocks, 256, 0, stream>>>((const float*)acc, count, (__nv_bfloat16*)out);
+  launch_k(cast_kernel<__nv_bfloat16, float>, blocks, 256, 0, stream, (const float*)acc, count, (__nv_bfloat16*)out);
   cuda_check(cudaGetLastError(), "cast_kernel");
 }
 
@@ -1058,13 +1101,13 @@ static void run_grad(DType dt, const DevStage& ds, const Bindings& b, void* out,
   }
   const size_t asz = acc_size(dt);
   if (dt != DT_BF16) {
-    cuda_check(cudaMemsetAsync(out, 0, count * asz, stream), "memset(grad)");
+    zero_fill(out, count * asz, stream);
     if (!ds.dead) run_stage(dt, ds, b, out, true, stream);
     return;
   }
   void* acc = nullptr;
   cuda_check(cudaMallocAsync(&acc, std::max<int64_t>(count, 1) * asz, stream), "alloc grad acc");
-  cuda_check(cudaMemsetAsync(acc, 0, count * asz, stream), "memset(grad acc)");
+  zero_fill(acc, count * asz, stream);
   if (!ds.dead) run_stage(dt, ds, b, acc, true, stream);
   launch_cast(dt, acc, count, out, stream);
   cuda_check(cudaFreeAsync(acc, stream), "free grad acc");

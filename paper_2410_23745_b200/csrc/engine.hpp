@@ -7,6 +7,7 @@
 #include <memory>
 #include <mutex>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "plan.hpp"
@@ -118,6 +119,37 @@ void run_backward(const Plan& plan, DevPlan& dp, DType dt, const Bindings& b, cu
 void eval_coordinate_grid(const CStage& s, int term, int coord, int64_t* out_dev, cudaStream_t stream);
 
 void cuda_check(cudaError_t e, const char* what);
+
+// Programmatic dependent launch: every library kernel is launched with
+// programmatic stream serialization, triggers its dependents as soon as it
+// starts and waits for its predecessor grid before its first global memory
+// access.  The next kernel's launch and CTA scheduling then overlap this
+// kernel's tail; semantics stay serial because every kernel waits before
+// touching memory (griddepcontrol.wait is a no-op without the attribute).
+// SYNO_NO_PDL=1 disables the attribute.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+bool pdl_enabled();
+
+// Stream-ordered zero fill as a library kernel (part of the PDL chain,
+// unlike cudaMemsetAsync).
+void zero_fill(void* ptr, size_t bytes, cudaStream_t stream);
+
+template <typename... KArgs, typename... Args>
+inline void launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t stream,
+                     Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cuda_check(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...), "cudaLaunchKernelEx");
+}
 
 // Process-wide count of kernels this library launched (syno_launch_count).
 void note_launch();

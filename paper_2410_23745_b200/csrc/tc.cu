@@ -127,6 +127,8 @@ struct PackGeom {
 template <typename TI>
 __global__ void __launch_bounds__(256) pack_cl_kernel(const TI* __restrict__ src, __nv_bfloat16* __restrict__ dst,
                                                       PackGeom g, int64_t total_pix) {
+  pdl_trigger();
+  pdl_wait();
   __shared__ __nv_bfloat16 tile[64][66];
   const int64_t f0 = (int64_t)blockIdx.x * 64;
   const int cb = blockIdx.y;
@@ -190,6 +192,8 @@ __global__ void __launch_bounds__(256) pack_cl_kernel(const TI* __restrict__ src
 // Folded fp32 weights [rows][Cp] -> bf16 split parts [rows][3*Cp] (pattern lo_mask).
 __global__ void __launch_bounds__(256) split_rows_kernel(const float* __restrict__ src, __nv_bfloat16* __restrict__ dst,
                                                          int64_t rows, int32_t Cp, uint32_t lo_mask) {
+  pdl_trigger();
+  pdl_wait();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t total = rows * 3 * (int64_t)Cp;
   if (i >= total) return;
@@ -214,6 +218,8 @@ constexpr int PK_PIX = 128;
 template <typename TI, int V>
 __global__ void __launch_bounds__(256) pack_rows_kernel(const TI* __restrict__ src, __nv_bfloat16* __restrict__ dst,
                                                         PackGeom g, int32_t rows_per_block, int64_t total_rows) {
+  pdl_trigger();
+  pdl_wait();
   // channel-major tile: row cl holds the block's pixels; each group of 8
   // channel rows is rotated by 8 pixels so the transposed reads of the write
   // phase spread over all banks (the rotation keeps 16-byte alignment)
@@ -361,6 +367,8 @@ struct FoldArgs {
 
 // out[rh][rw][a][b'] = prod_j w_j[...]; one block row per (rh, rw, a).
 __global__ void __launch_bounds__(128) fold_kernel(const __grid_constant__ FoldArgs f) {
+  pdl_trigger();
+  pdl_wait();
   const int row = blockIdx.y;
   const int a = row % f.ext[2];
   const int rw = (row / f.ext[2]) % f.ext[1];
@@ -393,6 +401,8 @@ __global__ void __launch_bounds__(128) fold_kernel(const __grid_constant__ FoldA
 // bf16 rows (split into (hi, lo, hi) parts for fp32 operands).
 template <int TA, int TB>
 __global__ void __launch_bounds__(256) fold_tile_kernel(const __grid_constant__ FoldArgs f, int a_inner) {
+  pdl_trigger();
+  pdl_wait();
   extern __shared__ float sv[];  // [KK][TA][TB + 1]
   __shared__ int32_t koff[MAXFW][16];
   const int KK = f.ext[0] * f.ext[1];
@@ -500,6 +510,8 @@ __device__ __forceinline__ void chain_store(const ChainArgs& c, const int* d, fl
 // dW_j = sum over the loops w_j does not use of dWf * prod_{k != j} w_k.
 // Thread per output (short reductions), outputs ordered like dWf (ci fastest).
 __global__ void __launch_bounds__(256) chain_thread_kernel(const __grid_constant__ ChainArgs c) {
+  pdl_trigger();
+  pdl_wait();
   const int64_t o = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (o >= c.out_count) return;
   int d[4];
@@ -529,6 +541,8 @@ struct ChainN {
 };
 
 __global__ void __launch_bounds__(256) chain_n_kernel(const __grid_constant__ ChainArgs c, const __grid_constant__ ChainN h) {
+  pdl_trigger();
+  pdl_wait();
   extern __shared__ float sd[];  // [KK][cw + 1]
   const int n = blockIdx.x;
   const int c_lo = h.ci_q >= 0 ? blockIdx.y * h.ci_chunk : 0;
@@ -605,6 +619,8 @@ __global__ void __launch_bounds__(256) chain_n_kernel(const __grid_constant__ Ch
 // Long reductions: block (o, split) reduces one chunk; the last block of an
 // output sums the partials in split order (deterministic) and stores.
 __global__ void __launch_bounds__(256) chain_block_kernel(const __grid_constant__ ChainArgs c) {
+  pdl_trigger();
+  pdl_wait();
   const int64_t o = blockIdx.x;
   const int nsplit = gridDim.y;
   const int64_t r0 = (int64_t)blockIdx.y * c.r_chunk;
@@ -993,12 +1009,12 @@ static void launch_gemm(const TcGemmParams& p, unsigned grid, cudaStream_t strea
   const bool want_trace = getenv("SYNO_TC_TRACE") != nullptr;
   if (want_trace && !trace_buf) cuda_check(cudaMalloc(&trace_buf, 64 * sizeof(unsigned long long)), "trace");
   if (!want_trace) {
-    tc_gemm_kernel<BN><<<grid, THREADS, smem, stream>>>(p);
+    launch_k(tc_gemm_kernel<BN>, grid, THREADS, smem, stream, p);
   } else {
     TcGemmParams q = p;
     q.trace = trace_buf;
     cuda_check(cudaMemsetAsync(trace_buf, 0, 64 * sizeof(unsigned long long), stream), "trace memset");
-    tc_gemm_kernel<BN><<<grid, THREADS, smem, stream>>>(q);
+    launch_k(tc_gemm_kernel<BN>, grid, THREADS, smem, stream, q);
     unsigned long long h[64];
     cuda_check(cudaMemcpyAsync(h, trace_buf, sizeof(h), cudaMemcpyDeviceToHost, stream), "trace copy");
     cuda_check(cudaStreamSynchronize(stream), "trace sync");
@@ -1068,6 +1084,8 @@ static RowsTiling rows_tiling(int64_t F, int n_tiles, int groups, int bn, int n_
 }
 
 __global__ void cast_f32_bf16_kernel(const float* __restrict__ in, __nv_bfloat16* __restrict__ out, int64_t n) {
+  pdl_trigger();
+  pdl_wait();
   const int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4;
   if (i + 3 < n) {
     const float4 v = *reinterpret_cast<const float4*>(in + i);
@@ -1082,7 +1100,7 @@ __global__ void cast_f32_bf16_kernel(const float* __restrict__ in, __nv_bfloat16
 static void cast_to_bf16(const float* in, void* out, int64_t n, cudaStream_t stream) {
   const int id = prof_begin("cast_f32_bf16", 0.0, (double)n * 6, stream);
   note_launch();
-  cast_f32_bf16_kernel<<<(unsigned)((n / 4 + 256) / 256), 256, 0, stream>>>(in, static_cast<__nv_bfloat16*>(out), n);
+  launch_k(cast_f32_bf16_kernel, (unsigned)((n / 4 + 256) / 256), 256, 0, stream, in, static_cast<__nv_bfloat16*>(out), n);
   cuda_check(cudaGetLastError(), "cast_f32_bf16_kernel");
   prof_end(id, stream);
 }
@@ -1092,7 +1110,7 @@ static int pick_bn(int n) { return n <= 64 ? 64 : n <= 128 ? 128 : 256; }
 template <typename TI, int V>
 static void launch_pack_rows(const void* src, const PackGeom& g, __nv_bfloat16* dst, dim3 grid, int rpb,
                              int64_t rows, cudaStream_t stream) {
-  pack_rows_kernel<TI, V><<<grid, 256, 0, stream>>>(static_cast<const TI*>(src), dst, g, rpb, rows);
+  launch_k(pack_rows_kernel<TI, V>, grid, 256, 0, stream, static_cast<const TI*>(src), dst, g, rpb, rows);
 }
 
 static void pack_cl(const void* src, DType dt, const PackGeom& g, __nv_bfloat16* dst, cudaStream_t stream) {
@@ -1127,7 +1145,7 @@ static void split_rows(const float* src, __nv_bfloat16* dst, int64_t rows, int C
   const int64_t total = rows * 3 * (int64_t)Cp;
   const int id = prof_begin("split_weights", 0.0, (double)rows * Cp * 4 + (double)total * 2, stream);
   note_launch();
-  split_rows_kernel<<<(unsigned)((total + 255) / 256), 256, 0, stream>>>(src, dst, rows, Cp, lo_mask);
+  launch_k(split_rows_kernel, (unsigned)((total + 255) / 256), 256, 0, stream, src, dst, rows, Cp, lo_mask);
   cuda_check(cudaGetLastError(), "split_rows_kernel");
   prof_end(id, stream);
 }
@@ -1516,15 +1534,14 @@ static void fold_fast(const TcPlan& tp, const Bindings& b, DType dt, bool dgrad,
   const int a_inner = std::llabs(tp.wstr[0][f.sl_a]) < std::llabs(tp.wstr[0][f.sl_b]) ? 1 : 0;
   if (KK == 1) {
     const size_t sm = (size_t)32 * 33 * sizeof(float);
-    fold_tile_kernel<32, 32><<<dim3((unsigned)((f.ext[2] + 31) / 32), (unsigned)((f.Bp + 31) / 32)), 256, sm, stream>>>(
-        f, a_inner);
+    launch_k(fold_tile_kernel<32, 32>, dim3((unsigned)((f.ext[2] + 31) / 32), (unsigned)((f.Bp + 31) / 32)), 256, sm, stream, f, a_inner);
   } else if (KK <= 16) {
     const size_t sm = (size_t)KK * 65 * sizeof(float);
-    fold_tile_kernel<1, 64><<<dim3((unsigned)f.ext[2], (unsigned)((f.Bp + 63) / 64)), 256, sm, stream>>>(f, a_inner);
+    launch_k(fold_tile_kernel<1, 64>, dim3((unsigned)f.ext[2], (unsigned)((f.Bp + 63) / 64)), 256, sm, stream, f, a_inner);
   } else {
     if (rows > 65535) fail(SYNO_E_UNSUPPORTED, "fold: too many operand rows");
     dim3 grid((unsigned)std::min(8, (f.Bp + 127) / 128), (unsigned)rows);
-    fold_kernel<<<grid, 128, 0, stream>>>(f);
+    launch_k(fold_kernel, grid, 128, 0, stream, f);
   }
   cuda_check(cudaGetLastError(), "fold kernel");
   prof_end(id, stream);
@@ -1599,15 +1616,15 @@ static void chain_fast(const TcPlan& tp, const TcWs& w, const Bindings& b, DType
     for (int k = 0; k < tp.nw; ++k) h.n_w[k] = k == j ? 0 : (int32_t)tp.wstr[k][2];
     if (!ci_out) h.ci_chunk = 0;
     const unsigned gy = ci_out ? (unsigned)((c.ext[3] + chunk - 1) / chunk) : 1u;
-    chain_n_kernel<<<dim3((unsigned)c.ext[2], gy), 256, sm_n, stream>>>(c, h);
+    launch_k(chain_n_kernel, dim3((unsigned)c.ext[2], gy), 256, sm_n, stream, c, h);
   } else if (!nsplit) {
-    chain_thread_kernel<<<(unsigned)((c.out_count + 255) / 256), 256, 0, stream>>>(c);
+    launch_k(chain_thread_kernel, (unsigned)((c.out_count + 255) / 256), 256, 0, stream, c);
   } else {
     c.r_chunk = (c.R + nsplit - 1) / nsplit;
     c.partial = w.chain_partial;
     c.counter = w.chain_counter;
     const int ns = (int)((c.R + c.r_chunk - 1) / c.r_chunk);
-    chain_block_kernel<<<dim3((unsigned)c.out_count, (unsigned)ns), 256, 0, stream>>>(c);
+    launch_k(chain_block_kernel, dim3((unsigned)c.out_count, (unsigned)ns), 256, 0, stream, c);
   }
   cuda_check(cudaGetLastError(), "chain kernel");
   prof_end(id, stream);
@@ -1651,7 +1668,7 @@ static void rows_gemm(TcGemmParams& p, int bn, const int* t, void* out, bool f32
     return;
   }
   float* target = f32 ? static_cast<float*>(out) : acc;
-  cuda_check(cudaMemsetAsync(target, 0, (size_t)numel * sizeof(float), stream), "memset(split-K output)");
+  zero_fill(target, (size_t)numel * sizeof(float), stream);
   p.out = target;
   gemm(p, bn, t[0], t[1], t[2], stream, name, flops);
   if (!f32) cast_to_bf16(target, out, numel, stream);
@@ -1697,7 +1714,7 @@ bool tc_backward(TcPlan& tp, DType dt, const Bindings& b, cudaStream_t stream) {
     else if (!(b.x_unchanged && w.share_x && w.packed_x_src == b.x)) pack_cl(b.x, dt, w.gxw, w.xclw, stream);
     if (w.dyw_ident && aligned16(b.dy)) p.tma_b = make_map(b.dy, w.ms_wg_b);
     else if (!dy_w_packed) pack_cl(b.dy, dt, w.gdy_w, w.dycl_w, stream);
-    cuda_check(cudaMemsetAsync(w.dwf, 0, (size_t)tp.nwin() * tp.N * tp.C * sizeof(float), stream), "memset(dWf)");
+    zero_fill(w.dwf, (size_t)tp.nwin() * tp.N * tp.C * sizeof(float), stream);
     gemm(p, w.bn_wg, w.t_wg[0], w.t_wg[1], w.t_wg[2], stream, "tc_gemm_wgrad", tp.flops);
     // chain rule through the fold, into each requested weight gradient
     Bindings cb = b;

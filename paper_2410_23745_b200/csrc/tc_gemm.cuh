@@ -291,6 +291,7 @@ struct Ring {
 
 template <int BN>
 __global__ void __launch_bounds__(THREADS, 1) tc_gemm_kernel(const __grid_constant__ TcGemmParams p) {
+  pdl_trigger();
   constexpr int BSTAGES = b_stages<BN>();
   constexpr int B_BYTES = BN * BK * 2;
   constexpr int G = mgroup<BN>();
@@ -338,6 +339,9 @@ __global__ void __launch_bounds__(THREADS, 1) tc_gemm_kernel(const __grid_consta
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
+  // barrier init, TMEM allocation and the tensormap prefetch overlapped the
+  // previous kernel; from here on global memory is touched
+  pdl_wait();
   const bool tr = p.trace != nullptr && blockIdx.x == 0;
   auto stamp = [&](int i) {
     if (tr && i < 64) {
