@@ -26,6 +26,15 @@ void cuda_check(cudaError_t e, const char* what) {
   if (e != cudaSuccess) fail(SYNO_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
 }
 
+bool skip_class(const char* name) {
+  static const std::string list = [] {
+    const char* e = getenv("SYNO_SKIP");
+    return std::string(e ? e : "");
+  }();
+  if (list.empty()) return false;
+  return ("," + list + ",").find("," + std::string(name) + ",") != std::string::npos;
+}
+
 bool pdl_enabled() {
   static const bool on = getenv("SYNO_NO_PDL") == nullptr;
   return on;
@@ -44,7 +53,7 @@ void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 uint64_t launch_count() { return g_launches.load(std::memory_order_relaxed); }
 
 void zero_fill(void* ptr, size_t bytes, cudaStream_t stream) {
-  if (!bytes) return;
+  if (!bytes || skip_class("zero")) return;
   // library buffers are 16-byte aligned (cudaMalloc / pool); a misaligned
   // pointer falls back to the runtime memset
   if (reinterpret_cast<uintptr_t>(ptr) & 15) {

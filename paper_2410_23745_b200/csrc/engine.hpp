@@ -131,6 +131,10 @@ __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;"
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 bool pdl_enabled();
 
+// Profiling only: SYNO_SKIP=pack,fold,chain,cast,zero,gemm suppresses those
+// launches (wrong results) so a step's time can be attributed per class.
+bool skip_class(const char* name);
+
 // Stream-ordered zero fill as a library kernel (part of the PDL chain,
 // unlike cudaMemsetAsync).
 void zero_fill(void* ptr, size_t bytes, cudaStream_t stream);

@@ -224,8 +224,8 @@ __global__ void __launch_bounds__(256) pack_rows_kernel(const TI* __restrict__ s
   // channel rows is rotated by 8 pixels so the transposed reads of the write
   // phase spread over all banks (the rotation keeps 16-byte alignment)
   __shared__ __align__(16) __nv_bfloat16 tile[64][PK_PIX + 8];
-  __shared__ int64_t s_src[PK_PIX];  // per block row: source offset of (image, row, first pixel)
-  __shared__ int64_t s_dst[PK_PIX];  // per block row: destination flat index of its first pixel (-1: unused row)
+  __shared__ int64_t s_src[PK_PIX];    // per block row: source offset of (image, row, first pixel)
+  __shared__ int64_t s_dst[PK_PIX];    // per block pixel: destination flat pixel index (-1: not stored)
   __shared__ int32_t s_part[PK_PIX];
   const int t = threadIdx.x;
   const int cb = blockIdx.y;
@@ -245,11 +245,11 @@ __global__ void __launch_bounds__(256) pack_rows_kernel(const TI* __restrict__ s
     wbeg = (int)(blockIdx.x % nseg) * PK_PIX;
     Win = min(PK_PIX, g.Win - wbeg);
   }
+  const int npix = nrows * Win;
   if (t < nrows) {
     const int64_t row = row0 + t;  // (img', hi) flattened
     int img = (int)(row / g.Hin);
     const int hi = (int)(row - (int64_t)img * g.Hin);
-    const int imgo = img;
     int part = 0;
     if (g.split == SPLIT_IMG) {
       part = img / g.n_img;
@@ -257,91 +257,119 @@ __global__ void __launch_bounds__(256) pack_rows_kernel(const TI* __restrict__ s
     }
     s_part[t] = part;
     s_src[t] = img * g.s_img + (int64_t)hi * g.s_h + (int64_t)wbeg * g.s_w;
+  }
+  if (t < npix) {
+    const int rr = t / Win, wi = wbeg + t - rr * Win;
+    const int64_t row = row0 + rr;
+    const int imgo = (int)(row / g.Hin);
+    const int hi = (int)(row - (int64_t)imgo * g.Hin);
     const int ph = hi % g.Sh, hp = hi / g.Sh + g.lo_h;
-    s_dst[t] = hp < g.Hp ? (((int64_t)(ph * g.Sw) * n_out + imgo) * g.Hp + hp) * g.Wp + g.lo_w : -1;
+    const int pw = wi % g.Sw, wp = wi / g.Sw + g.lo_w;
+    s_dst[t] = (hp < g.Hp && wp < g.Wp)
+                   ? (((int64_t)(ph * g.Sw + pw) * n_out + imgo) * g.Hp + hp) * g.Wp + wp
+                   : -1;  // never read by any window
   }
   __syncthreads();
-  // ---- read: (channel, pixel-vector) pairs, pixels fastest
-  const int vpr = Win / V;  // vectors per row
-  const int nvec = nrows * vpr;
-#pragma unroll 4
-  for (int i = t; i < 64 * nvec; i += 256) {
-    const int cl = i / nvec;
-    const int vi = i - cl * nvec;
+  // ---- read: each thread keeps one pixel vector and walks the channels
+  const int vpr = Win / V;       // vectors per row
+  const int nvec = nrows * vpr;  // <= PK_PIX / V
+  const int cstep = max(1, 256 / nvec);
+  if (t < cstep * nvec) {
+    const int vi = t % nvec;
     const int rr = vi / vpr;
     const int w0 = (vi - rr * vpr) * V;
-    int c = cb * 64 + cl;
-    int part = s_part[rr];
-    if (g.split == SPLIT_CH) {
-      part = c / g.Cp;
-      c -= part * g.Cp;
-    }
-    float v[V];
-    if (c < g.C && part < g.parts()) {
-      const TI* p = src + s_src[rr] + (int64_t)c * g.s_c + (int64_t)w0 * g.s_w;
-      if (V == 8 && sizeof(TI) == 2) {
-        const uint4 q = __ldg(reinterpret_cast<const uint4*>(p));
-        const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&q);
+    const int px0 = rr * Win + w0;
+    const TI* rowp = src + s_src[rr] + (int64_t)w0 * g.s_w;
+#pragma unroll 2
+    for (int cl = t / nvec; cl < 64; cl += cstep) {
+      int c = cb * 64 + cl;
+      int part = s_part[rr];
+      if (g.split == SPLIT_CH) {
+        part = c / g.Cp;
+        c -= part * g.Cp;
+      }
+      const bool have = c < g.C && part < g.parts();
+      __nv_bfloat16* trow = &tile[cl][0];
+      const int col0 = (px0 + 8 * (cl >> 3)) & (PK_PIX - 1);
+      if constexpr (sizeof(TI) == 2) {
+        // bf16 sources are never split: move the bits untouched
+        if constexpr (V == 8) {
+          uint4 q = make_uint4(0, 0, 0, 0);
+          if (have) q = __ldg(reinterpret_cast<const uint4*>(rowp + (int64_t)c * g.s_c));
+          *reinterpret_cast<uint4*>(trow + col0) = q;
+        } else if constexpr (V == 4) {
+          uint2 q = make_uint2(0, 0);
+          if (have) q = __ldg(reinterpret_cast<const uint2*>(rowp + (int64_t)c * g.s_c));
+          const __nv_bfloat16* hq = reinterpret_cast<const __nv_bfloat16*>(&q);
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const float2 f2 = __bfloat1622float2(h2[e]);
-          v[2 * e] = f2.x;
-          v[2 * e + 1] = f2.y;
+          for (int e = 0; e < 4; ++e) trow[(px0 + e + 8 * (cl >> 3)) & (PK_PIX - 1)] = hq[e];
+        } else {
+          const __nv_bfloat16 z = __float2bfloat16(0.f);
+          trow[(px0 + 8 * (cl >> 3)) & (PK_PIX - 1)] = have ? rowp[(int64_t)c * g.s_c] : z;
         }
-      } else if (V == 4 && sizeof(TI) == 2) {
-        const uint2 q = __ldg(reinterpret_cast<const uint2*>(p));
-        const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&q);
+        continue;
+      } else {
+      float v[V];
+      if (have) {
+        const TI* p = rowp + (int64_t)c * g.s_c;
+        if (V == 8 && sizeof(TI) == 2) {
+          const uint4 q = __ldg(reinterpret_cast<const uint4*>(p));
+          const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&q);
 #pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const float2 f2 = __bfloat1622float2(h2[e]);
-          v[2 * e] = f2.x;
-          v[2 * e + 1] = f2.y;
+          for (int e = 0; e < 4; ++e) {
+            const float2 f2 = __bfloat1622float2(h2[e]);
+            v[2 * e] = f2.x;
+            v[2 * e + 1] = f2.y;
+          }
+        } else if (V == 4 && sizeof(TI) == 2) {
+          const uint2 q = __ldg(reinterpret_cast<const uint2*>(p));
+          const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&q);
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const float2 f2 = __bfloat1622float2(h2[e]);
+            v[2 * e] = f2.x;
+            v[2 * e + 1] = f2.y;
+          }
+        } else if (V == 4 && sizeof(TI) == 4) {
+          const float4 q = __ldg(reinterpret_cast<const float4*>(p));
+          v[0] = q.x;
+          v[1] = q.y;
+          v[2] = q.z;
+          v[3] = q.w;
+        } else {
+#pragma unroll
+          for (int e = 0; e < V; ++e) v[e] = (float)p[(int64_t)e * g.s_w];
         }
-      } else if (V == 4 && sizeof(TI) == 4) {
-        const float4 q = __ldg(reinterpret_cast<const float4*>(p));
-        v[0] = q.x;
-        v[1] = q.y;
-        v[2] = q.z;
-        v[3] = q.w;
       } else {
 #pragma unroll
-        for (int e = 0; e < V; ++e) v[e] = (float)p[(int64_t)e * g.s_w];
+        for (int e = 0; e < V; ++e) v[e] = 0.f;
       }
-    } else {
+      const bool lo = g.split != SPLIT_NONE && ((g.lo_mask >> part) & 1u);
+      __align__(16) __nv_bfloat16 hv[V];
 #pragma unroll
-      for (int e = 0; e < V; ++e) v[e] = 0.f;
-    }
-    const bool lo = g.split != SPLIT_NONE && ((g.lo_mask >> part) & 1u);
-    const int px0 = rr * Win + w0;
-    __align__(16) __nv_bfloat16 hv[V];
+      for (int e = 0; e < V; ++e) {
+        hv[e] = __float2bfloat16(v[e]);
+        if (lo) hv[e] = __float2bfloat16(v[e] - __bfloat162float(hv[e]));
+      }
+      if (V == 8) {  // px0 and the rotation are multiples of 8: one 16-byte store
+        *reinterpret_cast<uint4*>(trow + col0) = *reinterpret_cast<const uint4*>(hv);
+      } else {
 #pragma unroll
-    for (int e = 0; e < V; ++e) {
-      hv[e] = __float2bfloat16(v[e]);
-      if (lo) hv[e] = __float2bfloat16(v[e] - __bfloat162float(hv[e]));
-    }
-    if (V == 8) {  // px0 and the rotation are multiples of 8: one 16-byte store
-      *reinterpret_cast<uint4*>(&tile[cl][(px0 + 8 * (cl >> 3)) & (PK_PIX - 1)]) = *reinterpret_cast<const uint4*>(hv);
-    } else {
-#pragma unroll
-      for (int e = 0; e < V; ++e) tile[cl][(px0 + e + 8 * (cl >> 3)) & (PK_PIX - 1)] = hv[e];
+        for (int e = 0; e < V; ++e) trow[(px0 + e + 8 * (cl >> 3)) & (PK_PIX - 1)] = hv[e];
+      }
+      }
     }
   }
   __syncthreads();
   // ---- write: 8 threads per destination pixel, 16 bytes each
   const int Ct = g.Ct();
-  if (cb * 64 >= Ct) return;
-  const int64_t plane_stride = (int64_t)n_out * g.Hp * g.Wp;
-  const int npix = nrows * Win;
+  const int chunk = t & 7;
+  const int c0 = cb * 64 + chunk * 8;
+  if (c0 >= Ct) return;
 #pragma unroll 4
-  for (int i = t; i < npix * 8; i += 256) {
-    const int px = i >> 3, chunk = i & 7;
-    const int c0 = cb * 64 + chunk * 8;
-    const int rr = px / Win;
-    const int64_t base = s_dst[rr];
-    const int wi = wbeg + px - rr * Win;
-    const int pw = wi % g.Sw, wp = wi / g.Sw;
-    if (base < 0 || c0 >= Ct || wp + g.lo_w >= g.Wp) continue;  // never read by any window
-    const int64_t f = base + pw * plane_stride + wp;
+  for (int px = t >> 3; px < npix; px += 32) {
+    const int64_t f = s_dst[px];
+    if (f < 0) continue;
     __align__(16) __nv_bfloat16 q[8];
     const int col = (px + 8 * chunk) & (PK_PIX - 1);
 #pragma unroll
@@ -399,6 +427,54 @@ __global__ void __launch_bounds__(128) fold_kernel(const __grid_constant__ FoldA
 // dominant weight's memory layout (k fastest, then the loop with the smaller
 // stride), staged in shared memory as fp32, and written back as coalesced
 // bf16 rows (split into (hi, lo, hi) parts for fp32 operands).
+// Direct fold: block = (operand row a, 64 operand columns); thread =
+// (column, window phase).  Output rows are written coalesced along b; the
+// weights are read through the read-only cache (neighbouring windows of the
+// same weight element run in other iterations / threads of the block).
+__global__ void __launch_bounds__(256) fold_direct_kernel(const __grid_constant__ FoldArgs f) {
+  pdl_trigger();
+  pdl_wait();
+  __shared__ int32_t koff[MAXFW][16];
+  const int KK = f.ext[0] * f.ext[1];
+  if ((int)threadIdx.x < KK) {
+    const int rh = threadIdx.x / f.ext[1], rw = threadIdx.x - rh * f.ext[1];
+#pragma unroll
+    for (int j = 0; j < MAXFW; ++j)
+      if (j < f.nw) koff[j][threadIdx.x] = (int32_t)(rh * f.s[j][0] + rw * f.s[j][1]);
+  }
+  __syncthreads();
+  const int a = blockIdx.x;
+  const int b = blockIdx.y * 64 + (threadIdx.x & 63);
+  if (b >= f.Bp) return;
+  const bool inb = b < f.ext[3];
+  int32_t base[MAXFW];
+#pragma unroll
+  for (int j = 0; j < MAXFW; ++j)
+    base[j] = j < f.nw ? (int32_t)(a * f.s[j][f.sl_a] + (int64_t)b * f.s[j][f.sl_b]) : 0;
+  const int parts = f.split ? 3 : 1;
+#pragma unroll 4
+  for (int k = threadIdx.x >> 6; k < KK; k += 4) {
+    float v = 0.f;
+    if (inb) {
+      v = 1.f;
+#pragma unroll
+      for (int j = 0; j < MAXFW; ++j) {
+        if (j >= f.nw) break;
+        const int32_t off = base[j] + koff[j][k];
+        v *= f.f32 ? __ldg(reinterpret_cast<const float*>(f.w[j]) + off)
+                   : __bfloat162float(__ldg(reinterpret_cast<const __nv_bfloat16*>(f.w[j]) + off));
+      }
+    }
+    __nv_bfloat16* o = f.out + ((int64_t)k * f.ext[2] + a) * parts * f.Bp + b;
+    const __nv_bfloat16 hi = __float2bfloat16(v);
+    o[0] = hi;
+    if (parts == 3) {
+      o[f.Bp] = __float2bfloat16(v - __bfloat162float(hi));
+      o[2 * f.Bp] = hi;
+    }
+  }
+}
+
 template <int TA, int TB>
 __global__ void __launch_bounds__(256) fold_tile_kernel(const __grid_constant__ FoldArgs f, int a_inner) {
   pdl_trigger();
@@ -462,7 +538,8 @@ __global__ void __launch_bounds__(256) fold_tile_kernel(const __grid_constant__ 
 }
 
 struct ChainArgs {
-  const float* dwf;      // [Kh][Kw][N][C] fp32
+  float* dwf;            // [Kh][Kw][N][C] fp32
+  int32_t zero_dwf;      // last reader: leave dWf zeroed for the next grad-weight (no memset)
   const void* w[MAXFW];
   int64_t s[MAXFW][4];
   int32_t nw, j, f32;    // weights, the weight differentiated, dtype of w / out
@@ -478,6 +555,7 @@ struct ChainArgs {
 __device__ __forceinline__ float chain_term(const ChainArgs& c, const int* d) {
   const int64_t df = ((int64_t)(d[0] * c.ext[1] + d[1]) * c.ext[2] + d[2]) * c.ext[3] + d[3];
   float v = __ldg(c.dwf + df);
+#pragma unroll 1
   for (int k = 0; k < c.nw; ++k) {
     if (k == c.j) continue;
     const int64_t off = d[0] * c.s[k][0] + d[1] * c.s[k][1] + (int64_t)d[2] * c.s[k][2] + (int64_t)d[3] * c.s[k][3];
@@ -487,17 +565,25 @@ __device__ __forceinline__ float chain_term(const ChainArgs& c, const int* d) {
   return v;
 }
 
-__device__ __forceinline__ void chain_decode(const ChainArgs& c, int64_t o, int64_t r, int* d) {
+__device__ __forceinline__ void chain_decode(const ChainArgs& c, int64_t o64, int64_t r64, int* d) {
+  // int32 digits: out_count and R are < 2^31 (checked on the host)
+  int o = (int)o64, r = (int)r64;
   d[0] = d[1] = d[2] = d[3] = 0;
-  for (int k = c.nout - 1; k >= 0; --k) {
+#pragma unroll 1
+  for (int k = 3; k >= 0; --k) {
+    if (k >= c.nout) continue;
     const int l = c.out_l[k];
-    d[l] = (int)(o % c.ext[l]);
-    o /= c.ext[l];
+    const int e = c.ext[l];
+    d[l] = o % e;
+    o /= e;
   }
-  for (int k = c.nred - 1; k >= 0; --k) {
+#pragma unroll 1
+  for (int k = 3; k >= 0; --k) {
+    if (k >= c.nred) continue;
     const int l = c.red_l[k];
-    d[l] = (int)(r % c.ext[l]);
-    r /= c.ext[l];
+    const int e = c.ext[l];
+    d[l] = r % e;
+    r /= e;
   }
 }
 
@@ -519,6 +605,7 @@ __global__ void __launch_bounds__(256) chain_thread_kernel(const __grid_constant
   for (int64_t r = 0; r < c.R; ++r) {
     chain_decode(c, o, r, d);
     acc += chain_term(c, d);
+    if (c.zero_dwf) c.dwf[((int64_t)(d[0] * c.ext[1] + d[1]) * c.ext[2] + d[2]) * c.ext[3] + d[3]] = 0.f;
   }
   chain_decode(c, o, 0, d);
   chain_store(c, d, acc);
@@ -551,7 +638,9 @@ __global__ void __launch_bounds__(256) chain_n_kernel(const __grid_constant__ Ch
 #pragma unroll 4
   for (int i = threadIdx.x; i < h.KK * cw; i += blockDim.x) {
     const int k = i / cw, ci = i - k * cw;
-    sd[k * P + ci] = __ldg(c.dwf + ((int64_t)k * c.ext[2] + n) * h.C + c_lo + ci);
+    float* src = c.dwf + ((int64_t)k * c.ext[2] + n) * h.C + c_lo + ci;
+    sd[k * P + ci] = *src;
+    if (c.zero_dwf) *src = 0.f;
   }
   __syncthreads();
   // per-block bases: n and the chunk start of ci
@@ -616,6 +705,72 @@ __global__ void __launch_bounds__(256) chain_n_kernel(const __grid_constant__ Ch
   }
 }
 
+// Chain rule for a weight that uses both channel loops (n, ci): one thread
+// per (n, ci) walks the windows; dWf reads are coalesced along ci and each
+// thread's outputs are contiguous in dW_j (window loops innermost in OIHW-
+// style layouts).  Windows the weight does not use are reduced in-thread.
+struct ChainNC {
+  int32_t Kh, Kw, N, C;
+  int32_t so_n, so_c, so_h, so_w;  // output strides (so_h / so_w = 0: reduced window loop)
+  int32_t oh, ow;                  // rh / rw is an output loop
+  int32_t sw[MAXFW][4];            // other weights' strides (0 for the differentiated one)
+  int32_t dense;                   // dW_j is [n][ci][window outputs] dense: stage the block's outputs in smem
+};
+
+__global__ void __launch_bounds__(256) chain_nc_kernel(const __grid_constant__ ChainArgs c, const __grid_constant__ ChainNC h) {
+  pdl_trigger();
+  pdl_wait();
+  extern __shared__ float stage[];  // dense: blockDim.x * so_c outputs
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t blk_base = (int64_t)blockIdx.x * blockDim.x * h.so_c;
+  const bool live = i < (int64_t)h.N * h.C;
+  const int n = (int)(i / h.C), ci = (int)(i - (int64_t)n * h.C);
+  const int64_t plane = (int64_t)h.N * h.C;
+  const int64_t obase = (int64_t)n * h.so_n + (int64_t)ci * h.so_c;
+  const int KKo_h = live ? (h.oh ? h.Kh : 1) : 0, KKo_w = h.ow ? h.Kw : 1;
+  const int KKr_h = h.oh ? 1 : h.Kh, KKr_w = h.ow ? 1 : h.Kw;
+  // compact code on purpose: these kernels run once per call, cold in the
+  // instruction cache, so rolled loops beat unrolled ones
+#pragma unroll 1
+  for (int ah = 0; ah < KKo_h; ++ah) {
+#pragma unroll 1
+    for (int aw = 0; aw < KKo_w; ++aw) {
+      float acc = 0.f;
+#pragma unroll 1
+      for (int bh = 0; bh < KKr_h; ++bh) {
+#pragma unroll 1
+        for (int bw = 0; bw < KKr_w; ++bw) {
+          const int kh = h.oh ? ah : bh, kw = h.ow ? aw : bw;
+          float* src = c.dwf + (int64_t)(kh * h.Kw + kw) * plane + i;
+          float v = *src;
+          if (c.zero_dwf) *src = 0.f;
+#pragma unroll 1
+          for (int q = 0; q < c.nw; ++q) {
+            if (q == c.j) continue;
+            const int32_t off = kh * h.sw[q][0] + kw * h.sw[q][1] + n * h.sw[q][2] + ci * h.sw[q][3];
+            v *= c.f32 ? __ldg(reinterpret_cast<const float*>(c.w[q]) + off)
+                       : __bfloat162float(__ldg(reinterpret_cast<const __nv_bfloat16*>(c.w[q]) + off));
+          }
+          acc += v;
+        }
+      }
+      const int64_t o = obase + (int64_t)ah * h.so_h + (int64_t)aw * h.so_w;
+      if (h.dense) stage[(int)(o - blk_base)] = acc;
+      else if (c.f32) reinterpret_cast<float*>(c.out)[o] = acc;
+      else reinterpret_cast<__nv_bfloat16*>(c.out)[o] = __float2bfloat16(acc);
+    }
+  }
+  if (!h.dense) return;
+  // the block's outputs are one contiguous run of dW_j: write it coalesced
+  __syncthreads();
+  const int64_t total = (int64_t)h.N * h.C * h.so_c;
+  const int run = (int)min((int64_t)blockDim.x * h.so_c, total - blk_base);
+  for (int e = threadIdx.x; e < run; e += blockDim.x) {
+    if (c.f32) reinterpret_cast<float*>(c.out)[blk_base + e] = stage[e];
+    else reinterpret_cast<__nv_bfloat16*>(c.out)[blk_base + e] = __float2bfloat16(stage[e]);
+  }
+}
+
 // Long reductions: block (o, split) reduces one chunk; the last block of an
 // output sums the partials in split order (deterministic) and stores.
 __global__ void __launch_bounds__(256) chain_block_kernel(const __grid_constant__ ChainArgs c) {
@@ -630,6 +785,7 @@ __global__ void __launch_bounds__(256) chain_block_kernel(const __grid_constant_
   for (int64_t r = r0 + threadIdx.x; r < r1; r += blockDim.x) {
     chain_decode(c, o, r, d);
     acc += chain_term(c, d);
+    if (c.zero_dwf) c.dwf[((int64_t)(d[0] * c.ext[1] + d[1]) * c.ext[2] + d[2]) * c.ext[3] + d[3]] = 0.f;
   }
 #pragma unroll
   for (int k = 16; k > 0; k >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, k);
@@ -992,7 +1148,7 @@ std::string tc_describe(const TcPlan* tp) {
 // Launch helpers
 // ---------------------------------------------------------------------------
 
-template <int BN>
+template <int BN, int MODE>
 static void launch_gemm(const TcGemmParams& p, unsigned grid, cudaStream_t stream) {
   static std::atomic<uint64_t> configured{0};  // per-device bit
   constexpr int smem = smem_bytes<BN>();
@@ -1000,7 +1156,7 @@ static void launch_gemm(const TcGemmParams& p, unsigned grid, cudaStream_t strea
   cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
   const uint64_t bit = 1ull << (dev & 63);
   if (!(configured.load() & bit)) {
-    cuda_check(cudaFuncSetAttribute(tc_gemm_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
+    cuda_check(cudaFuncSetAttribute(tc_gemm_kernel<BN, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
                "cudaFuncSetAttribute(tc_gemm)");
     configured.fetch_or(bit);
   }
@@ -1009,12 +1165,12 @@ static void launch_gemm(const TcGemmParams& p, unsigned grid, cudaStream_t strea
   const bool want_trace = getenv("SYNO_TC_TRACE") != nullptr;
   if (want_trace && !trace_buf) cuda_check(cudaMalloc(&trace_buf, 64 * sizeof(unsigned long long)), "trace");
   if (!want_trace) {
-    launch_k(tc_gemm_kernel<BN>, grid, THREADS, smem, stream, p);
+    launch_k(tc_gemm_kernel<BN, MODE>, grid, THREADS, smem, stream, p);
   } else {
     TcGemmParams q = p;
     q.trace = trace_buf;
     cuda_check(cudaMemsetAsync(trace_buf, 0, 64 * sizeof(unsigned long long), stream), "trace memset");
-    launch_k(tc_gemm_kernel<BN>, grid, THREADS, smem, stream, q);
+    launch_k(tc_gemm_kernel<BN, MODE>, grid, THREADS, smem, stream, q);
     unsigned long long h[64];
     cuda_check(cudaMemcpyAsync(h, trace_buf, sizeof(h), cudaMemcpyDeviceToHost, stream), "trace copy");
     cuda_check(cudaStreamSynchronize(stream), "trace sync");
@@ -1046,6 +1202,7 @@ static int sm_count() {
 // Persistent launch: one CTA per SM walks the (n fastest, m, z) tile grid.
 static void gemm(TcGemmParams& p, int bn, int m_tiles, int n_tiles, int z_tiles, cudaStream_t stream,
                  const char* name, double flops) {
+  if (skip_class("gemm")) return;
   p.m_tiles = m_tiles;
   p.n_tiles = n_tiles;
   p.z_tiles = z_tiles;
@@ -1055,9 +1212,15 @@ static void gemm(TcGemmParams& p, int bn, int m_tiles, int n_tiles, int z_tiles,
   if (tiles <= 0) return;
   const unsigned grid = (unsigned)std::min<int64_t>(tiles, sm_count());
   const int id = prof_begin(name, flops, 0.0, stream);
-  if (bn == 64) launch_gemm<64>(p, grid, stream);
-  else if (bn == 128) launch_gemm<128>(p, grid, stream);
-  else launch_gemm<256>(p, grid, stream);
+  if (p.mode == MODE_ROWS) {
+    if (bn == 64) launch_gemm<64, MODE_ROWS>(p, grid, stream);
+    else if (bn == 128) launch_gemm<128, MODE_ROWS>(p, grid, stream);
+    else launch_gemm<256, MODE_ROWS>(p, grid, stream);
+  } else {
+    if (bn == 64) launch_gemm<64, MODE_WGRAD>(p, grid, stream);
+    else if (bn == 128) launch_gemm<128, MODE_WGRAD>(p, grid, stream);
+    else launch_gemm<256, MODE_WGRAD>(p, grid, stream);
+  }
   prof_end(id, stream);
 }
 
@@ -1071,19 +1234,38 @@ struct RowsTiling {
   int64_t m_tiles;
 };
 
-static RowsTiling rows_tiling(int64_t F, int n_tiles, int groups, int bn, int n_cblocks) {
+static RowsTiling rows_tiling(int64_t F, int n_tiles, int groups, int bn, int n_cblocks, int nwin) {
+  // Cost model (measured on B200, profiles/r01_gemm_trace_dbg.txt): a
+  // 128 x BN x 16 MMA from shared memory takes ~80 cycles for BN <= 128 and
+  // ~160 for BN = 256; the epilogue of a 128-row sub-tile costs about as
+  // much as 16 such MMAs (more with split-K atomics).  A CTA's time is the
+  // number of waves times one tile; pick the (G, split) with the least.
   const int sms = sm_count();
   auto mt = [&](int g) { return (F + (int64_t)g * BM - 1) / ((int64_t)g * BM); };
-  int G = mgroup_of(bn);
-  while (G > 1 && mt(G) * n_tiles * groups < sms) G /= 2;
-  const int64_t tiles = mt(G) * n_tiles * groups;
-  int rs = 1;
-  if (tiles < sms && n_cblocks > 1 && getenv("SYNO_TC_NO_RSPLIT") == nullptr)
-    rs = (int)std::min<int64_t>(n_cblocks, (sms + tiles - 1) / tiles);
-  return {G, rs, mt(G)};
+  const double mma = bn >= 256 ? 2.0 : 1.0;
+  const bool no_split = getenv("SYNO_TC_NO_RSPLIT") != nullptr;
+  RowsTiling best{mgroup_of(bn), 1, mt(mgroup_of(bn))};
+  double best_cost = 1e300;
+  for (int G = mgroup_of(bn); G >= 1; G /= 2) {
+    for (int rs = 1; rs <= (no_split ? 1 : n_cblocks); ++rs) {
+      const int per = (n_cblocks + rs - 1) / rs;
+      if (rs > 1 && (n_cblocks + per - 1) / per != rs) continue;  // an empty split: same as fewer splits
+      const int64_t tiles = mt(G) * n_tiles * groups * rs;
+      const int64_t waves = (tiles + sms - 1) / sms;
+      const double tile = G * (nwin * per * 4.0 * mma + 16.0 * mma * (rs > 1 ? 2.0 : 1.0));
+      const double cost = waves * tile + (rs > 1 ? 8.0 * mma : 0.0);  // + the cast / zero fill
+      if (cost < best_cost * 0.98) {
+        best_cost = cost;
+        best = {G, rs, mt(G)};
+      }
+    }
+  }
+  return best;
 }
 
-__global__ void cast_f32_bf16_kernel(const float* __restrict__ in, __nv_bfloat16* __restrict__ out, int64_t n) {
+// Split-K accumulator -> bf16 output; the accumulator is left zeroed for
+// the next call (it starts zeroed), so no memset precedes the GEMM.
+__global__ void cast_f32_bf16_kernel(float* __restrict__ in, __nv_bfloat16* __restrict__ out, int64_t n) {
   pdl_trigger();
   pdl_wait();
   const int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4;
@@ -1092,13 +1274,18 @@ __global__ void cast_f32_bf16_kernel(const float* __restrict__ in, __nv_bfloat16
     __nv_bfloat162 a = __floats2bfloat162_rn(v.x, v.y), b = __floats2bfloat162_rn(v.z, v.w);
     *reinterpret_cast<__nv_bfloat162*>(out + i) = a;
     *reinterpret_cast<__nv_bfloat162*>(out + i + 2) = b;
+    *reinterpret_cast<float4*>(in + i) = make_float4(0.f, 0.f, 0.f, 0.f);
   } else {
-    for (int64_t k = i; k < n; ++k) out[k] = __float2bfloat16(in[k]);
+    for (int64_t k = i; k < n; ++k) {
+      out[k] = __float2bfloat16(in[k]);
+      in[k] = 0.f;
+    }
   }
 }
 
-static void cast_to_bf16(const float* in, void* out, int64_t n, cudaStream_t stream) {
-  const int id = prof_begin("cast_f32_bf16", 0.0, (double)n * 6, stream);
+static void cast_to_bf16(float* in, void* out, int64_t n, cudaStream_t stream) {
+  if (skip_class("cast")) return;
+  const int id = prof_begin("cast_f32_bf16", 0.0, (double)n * 10, stream);
   note_launch();
   launch_k(cast_f32_bf16_kernel, (unsigned)((n / 4 + 256) / 256), 256, 0, stream, in, static_cast<__nv_bfloat16*>(out), n);
   cuda_check(cudaGetLastError(), "cast_f32_bf16_kernel");
@@ -1114,6 +1301,7 @@ static void launch_pack_rows(const void* src, const PackGeom& g, __nv_bfloat16* 
 }
 
 static void pack_cl(const void* src, DType dt, const PackGeom& g, __nv_bfloat16* dst, cudaStream_t stream) {
+  if (skip_class("pack")) return;
   // one block = whole source rows (<= PK_PIX pixels) or one PK_PIX segment of a wider row
   const int rpb = std::max(1, PK_PIX / g.Win);
   const int64_t rows = (int64_t)g.n_img_out() * g.Hin;
@@ -1333,7 +1521,7 @@ static void build_ws(TcPlan& tp, TcWs& w, DType dt) {
       for (int rw = 0; rw < tp.dw.K; ++rw)
         groups[0].push_back({tp.dh.delta(rh) * w.gx.Wp + tp.dw.delta(rw), tp.dh.phi(rh) * w.gx.Sw + tp.dw.phi(rw),
                              rh * tp.dw.K + rw});
-    const RowsTiling rt = rows_tiling(F, (tp.N + bn - 1) / bn, 1, bn, p.n_cblocks);
+    const RowsTiling rt = rows_tiling(F, (tp.N + bn - 1) / bn, 1, bn, p.n_cblocks, tp.nwin());
     rows_schedule(p, groups, bn, rt.G);
     p.rsplit = rt.rs;
     w.ms_fwd_a = map_spec(Ck, F, planes, Ck, F * Ck, 64);
@@ -1403,7 +1591,7 @@ static void build_ws(TcPlan& tp, TcWs& w, DType dt) {
           }
         p.g_out_off[grp] = ph * tp.dh.xs + pw * tp.dw.xs;
       }
-    const RowsTiling rt = rows_tiling(Fg, (tp.C + bn - 1) / bn, Sh * Sw, bn, p.n_cblocks);
+    const RowsTiling rt = rows_tiling(Fg, (tp.C + bn - 1) / bn, Sh * Sw, bn, p.n_cblocks, tp.nwin() / (Sh * Sw));
     rows_schedule(p, groups, bn, rt.G);
     p.rsplit = rt.rs;
     w.ms_dg_a = map_spec(Nk, Fg, 1, Nk, Fg * Nk, 64);
@@ -1492,7 +1680,7 @@ static void build_ws(TcPlan& tp, TcWs& w, DType dt) {
       int64_t oc = 1, R = 1;
       for (int l = 0; l < 4; ++l) (tp.wstr[j][l] ? oc : R) *= ext[l];
       int nsplit = 0;
-      if (R > 64) nsplit = (int)std::max<int64_t>(1, std::min<int64_t>(256, R / 2048));
+      if (R > 64) nsplit = (int)std::max<int64_t>(1, std::min<int64_t>(256, R / 1024));
       w.chain_nsplit[j] = nsplit;
       if (nsplit) {
         need = std::max(need, oc * nsplit);
@@ -1509,6 +1697,7 @@ static void build_ws(TcPlan& tp, TcWs& w, DType dt) {
 
 static void fold_fast(const TcPlan& tp, const Bindings& b, DType dt, bool dgrad, bool split, __nv_bfloat16* dst,
                       cudaStream_t stream) {
+  if (skip_class("fold")) return;
   FoldArgs f{};
   f.nw = tp.nw;
   f.f32 = dt == DT_F32;
@@ -1536,8 +1725,7 @@ static void fold_fast(const TcPlan& tp, const Bindings& b, DType dt, bool dgrad,
     const size_t sm = (size_t)32 * 33 * sizeof(float);
     launch_k(fold_tile_kernel<32, 32>, dim3((unsigned)((f.ext[2] + 31) / 32), (unsigned)((f.Bp + 31) / 32)), 256, sm, stream, f, a_inner);
   } else if (KK <= 16) {
-    const size_t sm = (size_t)KK * 65 * sizeof(float);
-    launch_k(fold_tile_kernel<1, 64>, dim3((unsigned)f.ext[2], (unsigned)((f.Bp + 63) / 64)), 256, sm, stream, f, a_inner);
+    launch_k(fold_direct_kernel, dim3((unsigned)f.ext[2], (unsigned)((f.Bp + 63) / 64)), 256, 0, stream, f);
   } else {
     if (rows > 65535) fail(SYNO_E_UNSUPPORTED, "fold: too many operand rows");
     dim3 grid((unsigned)std::min(8, (f.Bp + 127) / 128), (unsigned)rows);
@@ -1547,9 +1735,12 @@ static void fold_fast(const TcPlan& tp, const Bindings& b, DType dt, bool dgrad,
   prof_end(id, stream);
 }
 
-static void chain_fast(const TcPlan& tp, const TcWs& w, const Bindings& b, DType dt, int j, cudaStream_t stream) {
+static void chain_fast(const TcPlan& tp, const TcWs& w, const Bindings& b, DType dt, int j, bool zero_dwf,
+                       cudaStream_t stream) {
+  if (skip_class("chain")) return;
   ChainArgs c{};
   c.dwf = w.dwf;
+  c.zero_dwf = zero_dwf ? 1 : 0;
   c.nw = tp.nw;
   c.j = j;
   c.f32 = dt == DT_F32;
@@ -1571,11 +1762,39 @@ static void chain_fast(const TcPlan& tp, const TcWs& w, const Bindings& b, DType
       c.R *= c.ext[l];
     }
   }
+  if (c.out_count >= INT32_MAX || c.R >= INT32_MAX) fail(SYNO_E_UNSUPPORTED, "chain rule: 2^31 or more elements");
   c.out = b.dw.at(j);
   const double bytes = (double)c.out_count * c.R * 4 + (double)c.out_count * (c.f32 ? 4 : 2);
   const int id = prof_begin("weight_chain", 0.0, bytes, stream);
   note_launch();
   const int nsplit = w.chain_nsplit[j];
+  if (!nsplit && tp.wstr[j][2] != 0 && tp.wstr[j][3] != 0 && c.ext[0] * c.ext[1] <= 16) {
+    ChainNC h{};
+    h.Kh = (int)c.ext[0];
+    h.Kw = (int)c.ext[1];
+    h.N = (int)c.ext[2];
+    h.C = (int)c.ext[3];
+    h.so_n = (int32_t)tp.wstr[j][2];
+    h.so_c = (int32_t)tp.wstr[j][3];
+    h.oh = tp.wstr[j][0] != 0 || h.Kh == 1;
+    h.ow = tp.wstr[j][1] != 0 || h.Kw == 1;
+    h.so_h = (int32_t)tp.wstr[j][0];
+    h.so_w = (int32_t)tp.wstr[j][1];
+    for (int k = 0; k < tp.nw; ++k)
+      for (int l = 0; l < 4; ++l) h.sw[k][l] = k == j ? 0 : (int32_t)tp.wstr[k][l];
+    const int64_t nthreads = (int64_t)h.N * h.C;
+    // dense [n][ci][windows] layout (OIHW-like): outputs of consecutive (n, ci) are contiguous
+    const int kko = (h.oh ? h.Kh : 1) * (h.ow ? h.Kw : 1);
+    const bool win_dense = (h.oh && h.ow) ? (h.so_w == 1 && h.so_h == h.Kw) || (h.Kh == 1 && h.so_w == 1) ||
+                                                (h.Kw == 1 && h.so_h == 1)
+                           : h.oh ? (h.Kh == 1 || h.so_h == 1) : h.ow ? (h.Kw == 1 || h.so_w == 1) : true;
+    h.dense = win_dense && h.so_c == kko && h.so_n == h.C * kko;
+    const size_t sm = h.dense ? (size_t)256 * kko * sizeof(float) : 0;
+    launch_k(chain_nc_kernel, (unsigned)((nthreads + 255) / 256), 256, sm, stream, c, h);
+    cuda_check(cudaGetLastError(), "chain kernel");
+    prof_end(id, stream);
+    return;
+  }
   const bool ci_out = tp.wstr[j][3] != 0;
   const int chunk = ci_out ? 64 : 0;
   const int cw_max = ci_out ? std::min(64, (int)c.ext[3]) : (int)c.ext[3];
@@ -1668,7 +1887,7 @@ static void rows_gemm(TcGemmParams& p, int bn, const int* t, void* out, bool f32
     return;
   }
   float* target = f32 ? static_cast<float*>(out) : acc;
-  zero_fill(target, (size_t)numel * sizeof(float), stream);
+  if (f32) zero_fill(target, (size_t)numel * sizeof(float), stream);  // acc is kept zeroed by the cast
   p.out = target;
   gemm(p, bn, t[0], t[1], t[2], stream, name, flops);
   if (!f32) cast_to_bf16(target, out, numel, stream);
@@ -1714,14 +1933,19 @@ bool tc_backward(TcPlan& tp, DType dt, const Bindings& b, cudaStream_t stream) {
     else if (!(b.x_unchanged && w.share_x && w.packed_x_src == b.x)) pack_cl(b.x, dt, w.gxw, w.xclw, stream);
     if (w.dyw_ident && aligned16(b.dy)) p.tma_b = make_map(b.dy, w.ms_wg_b);
     else if (!dy_w_packed) pack_cl(b.dy, dt, w.gdy_w, w.dycl_w, stream);
-    zero_fill(w.dwf, (size_t)tp.nwin() * tp.N * tp.C * sizeof(float), stream);
+    // fast chain kernels leave dWf zeroed behind them (it starts zeroed)
+    static const bool memset_dwf = getenv("SYNO_TC_ZERO_FILL") != nullptr;  // A/B switch
+    if (!tp.fast_fold || memset_dwf) zero_fill(w.dwf, (size_t)tp.nwin() * tp.N * tp.C * sizeof(float), stream);
     gemm(p, w.bn_wg, w.t_wg[0], w.t_wg[1], w.t_wg[2], stream, "tc_gemm_wgrad", tp.flops);
     // chain rule through the fold, into each requested weight gradient
     Bindings cb = b;
     cb.stages = {w.dwf};
+    int last = -1;
+    for (size_t j = 0; j < tp.chain.size(); ++j)
+      if (j < b.dw.size() && b.dw[j]) last = (int)j;
     for (size_t j = 0; j < tp.chain.size(); ++j) {
       if (j >= b.dw.size() || !b.dw[j]) continue;
-      if (tp.fast_fold) chain_fast(tp, w, b, dt, (int)j, stream);
+      if (tp.fast_fold) chain_fast(tp, w, b, dt, (int)j, (int)j == last && !memset_dwf, stream);
       else run_stage(dt, tp.chain[j], cb, b.dw[j], false, stream);
     }
   }

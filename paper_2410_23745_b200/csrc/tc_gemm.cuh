@@ -289,7 +289,7 @@ struct Ring {
   __device__ __forceinline__ uint32_t phase(int n) const { return (i / (uint32_t)n) & 1u; }
 };
 
-template <int BN>
+template <int BN, int MODE>
 __global__ void __launch_bounds__(THREADS, 1) tc_gemm_kernel(const __grid_constant__ TcGemmParams p) {
   pdl_trigger();
   constexpr int BSTAGES = b_stages<BN>();
@@ -366,7 +366,7 @@ __global__ void __launch_bounds__(THREADS, 1) tc_gemm_kernel(const __grid_consta
     for (int t = blockIdx.x; t < n_tiles_total; t += gridDim.x, ++pcount) {
       const TileInfo ti = tile_info(p, t);
       if (lane == 0 && pcount < 14) stamp(2 + pcount * 4);
-      if (p.mode == MODE_ROWS) {
+      if constexpr (MODE == MODE_ROWS) {
         for (int c = p.g_chunk0[ti.g]; c < p.g_chunk1[ti.g]; ++c) {
           for (int cb = ti.cb0; cb < ti.cb1; ++cb) {
             // one halo tile of A for this plane and channel block
@@ -436,7 +436,7 @@ __global__ void __launch_bounds__(THREADS, 1) tc_gemm_kernel(const __grid_consta
     }
   } else if (warp == 1) {
     // ---------------- MMA issuer: warp-wide loop, elected-lane issue
-    const bool mn = p.mode == MODE_WGRAD;
+    constexpr bool mn = MODE == MODE_WGRAD;
     const uint32_t idesc = mn ? idesc_bf16(BM, BN, 1, 1) : idesc_bf16(BM, BN);
     Ring ra, rb;
     uint32_t tcount = 0;
@@ -447,7 +447,7 @@ __global__ void __launch_bounds__(THREADS, 1) tc_gemm_kernel(const __grid_consta
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const uint32_t dst = tmem + acc * ACC_COLS;
       uint32_t accumulate = 0;
-      if (!mn) {
+      if constexpr (!mn) {
         for (int c = p.g_chunk0[ti.g]; c < p.g_chunk1[ti.g]; ++c) {
           for (int cb = ti.cb0; cb < ti.cb1; ++cb) {
             const int as = ra.slot(AST);
@@ -528,14 +528,14 @@ __global__ void __launch_bounds__(THREADS, 1) tc_gemm_kernel(const __grid_consta
       else mbar_wait_sleep(&tfull[acc], (tcount >> 1) & 1u);
       if (warp == 2 && lane == 0 && tcount < 14) stamp(2 + tcount * 4 + 2);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const int nsub = p.mode == MODE_ROWS ? p.G : 1;
+      const int nsub = MODE == MODE_ROWS ? p.G : 1;
       const bool have = ti.nkb > 0;
       const float scale = p.scale;
 #pragma unroll 1
       for (int g = 0; g < nsub; ++g) {
         bool ok;
         int64_t off;
-        if (p.mode == MODE_ROWS) {
+        if constexpr (MODE == MODE_ROWS) {
           const int64_t flat = ((int64_t)ti.mt * p.G + g) * BM + r;
           const int64_t wp = flat % p.Wp;
           const int64_t tq = flat / p.Wp;
@@ -561,6 +561,11 @@ __global__ void __launch_bounds__(THREADS, 1) tc_gemm_kernel(const __grid_consta
           const int64_t os = p.o_n;
           if (!ok || (p.dbg & 1)) {
             // masked row (pad pixel / beyond the extent): nothing to store
+          } else if (MODE == MODE_WGRAD || p.out_kind == OUT_F32_ATOMIC) {
+            float* o = reinterpret_cast<float*>(p.out) + off + (int64_t)n0 * os;
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              if (j < nlim) atomicAdd(o + (int64_t)j * os, v[j] * scale);
           } else if (p.out_kind == OUT_BF16) {
             __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(p.out) + off + (int64_t)n0 * os;
             if (nlim == 32 && os == 1 && (reinterpret_cast<uintptr_t>(o) & 15) == 0) {
@@ -575,18 +580,12 @@ __global__ void __launch_bounds__(THREADS, 1) tc_gemm_kernel(const __grid_consta
                                                 have ? v[q4 * 8 + 2 * e + 1] * scale : 0.f);
                 o4[q4] = *reinterpret_cast<const uint4*>(h2);
               }
-            } else if (nlim == 32) {
-#pragma unroll
-              for (int j = 0; j < 32; ++j) {
-                *o = __float2bfloat16_rn(have ? v[j] * scale : 0.f);
-                o += os;
-              }
             } else {
 #pragma unroll
               for (int j = 0; j < 32; ++j)
                 if (j < nlim) o[(int64_t)j * os] = __float2bfloat16_rn(have ? v[j] * scale : 0.f);
             }
-          } else if (p.out_kind == OUT_F32) {
+          } else {
             float* o = reinterpret_cast<float*>(p.out) + off + (int64_t)n0 * os;
             if (nlim == 32 && os == 1 && (reinterpret_cast<uintptr_t>(o) & 15) == 0) {
               float4* o4 = reinterpret_cast<float4*>(o);
@@ -595,26 +594,10 @@ __global__ void __launch_bounds__(THREADS, 1) tc_gemm_kernel(const __grid_consta
                 o4[q4] = have ? make_float4(v[4 * q4] * scale, v[4 * q4 + 1] * scale, v[4 * q4 + 2] * scale,
                                             v[4 * q4 + 3] * scale)
                               : make_float4(0.f, 0.f, 0.f, 0.f);
-            } else if (nlim == 32) {
-#pragma unroll
-              for (int j = 0; j < 32; ++j) o[(int64_t)j * os] = have ? v[j] * scale : 0.f;
             } else {
 #pragma unroll
               for (int j = 0; j < 32; ++j)
                 if (j < nlim) o[(int64_t)j * os] = have ? v[j] * scale : 0.f;
-            }
-          } else {
-            float* o = reinterpret_cast<float*>(p.out) + off + (int64_t)n0 * os;
-            if (nlim == 32) {
-#pragma unroll
-              for (int j = 0; j < 32; ++j) {
-                atomicAdd(o, v[j] * scale);
-                o += os;
-              }
-            } else {
-#pragma unroll
-              for (int j = 0; j < 32; ++j)
-                if (j < nlim) atomicAdd(o + (int64_t)j * os, v[j] * scale);
             }
           }
         }
