@@ -720,51 +720,63 @@ struct ChainNC {
 __global__ void __launch_bounds__(256) chain_nc_kernel(const __grid_constant__ ChainArgs c, const __grid_constant__ ChainNC h) {
   pdl_trigger();
   pdl_wait();
-  extern __shared__ float stage[];  // dense: blockDim.x * so_c outputs
+  extern __shared__ float stage[];  // [blockDim.x][KKo]: each thread's window outputs
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int64_t blk_base = (int64_t)blockIdx.x * blockDim.x * h.so_c;
   const bool live = i < (int64_t)h.N * h.C;
-  const int n = (int)(i / h.C), ci = (int)(i - (int64_t)n * h.C);
+  const int n = live ? (int)(i / h.C) : 0, ci = live ? (int)(i - (int64_t)n * h.C) : 0;
   const int64_t plane = (int64_t)h.N * h.C;
-  const int64_t obase = (int64_t)n * h.so_n + (int64_t)ci * h.so_c;
-  const int KKo_h = live ? (h.oh ? h.Kh : 1) : 0, KKo_w = h.ow ? h.Kw : 1;
-  const int KKr_h = h.oh ? 1 : h.Kh, KKr_w = h.ow ? 1 : h.Kw;
-  // compact code on purpose: these kernels run once per call, cold in the
-  // instruction cache, so rolled loops beat unrolled ones
+  const int KK = h.Kh * h.Kw;  // <= 16 (host-checked)
+  const int KKo_w = h.ow ? h.Kw : 1;
+  const int KKo = (h.oh ? h.Kh : 1) * KKo_w;
+  float* my = stage + threadIdx.x * KKo;
+  for (int q = 0; q < KKo; ++q) my[q] = 0.f;
+  if (live) {
+    // all windows' loads in flight together, then the zeroing stores
+    float* __restrict__ src = c.dwf + i;
+    float v[16];
+#pragma unroll
+    for (int k = 0; k < 16; ++k)
+      if (k < KK) v[k] = src[k * plane];
+    if (c.zero_dwf) {
+#pragma unroll
+      for (int k = 0; k < 16; ++k)
+        if (k < KK) src[k * plane] = 0.f;
+    }
+    float* vs = stage + blockDim.x * KKo + threadIdx.x * 16;  // per-thread window values
+#pragma unroll
+    for (int k = 0; k < 16; ++k)
+      if (k < KK) vs[k] = v[k];
 #pragma unroll 1
-  for (int ah = 0; ah < KKo_h; ++ah) {
+    for (int k = 0; k < KK; ++k) {
+      const int kh = k / h.Kw, kw = k - kh * h.Kw;
+      float x = vs[k];
 #pragma unroll 1
-    for (int aw = 0; aw < KKo_w; ++aw) {
-      float acc = 0.f;
-#pragma unroll 1
-      for (int bh = 0; bh < KKr_h; ++bh) {
-#pragma unroll 1
-        for (int bw = 0; bw < KKr_w; ++bw) {
-          const int kh = h.oh ? ah : bh, kw = h.ow ? aw : bw;
-          float* src = c.dwf + (int64_t)(kh * h.Kw + kw) * plane + i;
-          float v = *src;
-          if (c.zero_dwf) *src = 0.f;
-#pragma unroll 1
-          for (int q = 0; q < c.nw; ++q) {
-            if (q == c.j) continue;
-            const int32_t off = kh * h.sw[q][0] + kw * h.sw[q][1] + n * h.sw[q][2] + ci * h.sw[q][3];
-            v *= c.f32 ? __ldg(reinterpret_cast<const float*>(c.w[q]) + off)
-                       : __bfloat162float(__ldg(reinterpret_cast<const __nv_bfloat16*>(c.w[q]) + off));
-          }
-          acc += v;
-        }
+      for (int q = 0; q < c.nw; ++q) {
+        if (q == c.j) continue;
+        const int32_t off = kh * h.sw[q][0] + kw * h.sw[q][1] + n * h.sw[q][2] + ci * h.sw[q][3];
+        x *= c.f32 ? __ldg(reinterpret_cast<const float*>(c.w[q]) + off)
+                   : __bfloat162float(__ldg(reinterpret_cast<const __nv_bfloat16*>(c.w[q]) + off));
       }
-      const int64_t o = obase + (int64_t)ah * h.so_h + (int64_t)aw * h.so_w;
-      if (h.dense) stage[(int)(o - blk_base)] = acc;
-      else if (c.f32) reinterpret_cast<float*>(c.out)[o] = acc;
-      else reinterpret_cast<__nv_bfloat16*>(c.out)[o] = __float2bfloat16(acc);
+      // windows the weight does not use fold onto the same output
+      my[(h.oh ? kh : 0) * KKo_w + (h.ow ? kw : 0)] += x;
     }
   }
-  if (!h.dense) return;
-  // the block's outputs are one contiguous run of dW_j: write it coalesced
+  if (!h.dense) {
+    if (!live) return;
+    const int64_t obase = (int64_t)n * h.so_n + (int64_t)ci * h.so_c;
+    for (int q = 0; q < KKo; ++q) {
+      const int ah = q / KKo_w, aw = q - ah * KKo_w;
+      const int64_t o = obase + (int64_t)ah * h.so_h + (int64_t)aw * h.so_w;
+      if (c.f32) reinterpret_cast<float*>(c.out)[o] = my[q];
+      else reinterpret_cast<__nv_bfloat16*>(c.out)[o] = __float2bfloat16(my[q]);
+    }
+    return;
+  }
+  // dense [n][ci][windows] layout: the block's outputs are one contiguous run
   __syncthreads();
-  const int64_t total = (int64_t)h.N * h.C * h.so_c;
-  const int run = (int)min((int64_t)blockDim.x * h.so_c, total - blk_base);
+  const int64_t blk_base = (int64_t)blockIdx.x * blockDim.x * KKo;
+  const int64_t total = plane * KKo;
+  const int run = (int)min((int64_t)blockDim.x * KKo, total - blk_base);
   for (int e = threadIdx.x; e < run; e += blockDim.x) {
     if (c.f32) reinterpret_cast<float*>(c.out)[blk_base + e] = stage[e];
     else reinterpret_cast<__nv_bfloat16*>(c.out)[blk_base + e] = __float2bfloat16(stage[e]);
@@ -1646,7 +1658,8 @@ static void build_ws(TcPlan& tp, TcWs& w, DType dt) {
         }
       }
     const int m_tiles = (p.n_pairs + 1) / 2, n_tiles = (tp.N + bn - 1) / bn;
-    int ksplit = std::max(1, (4 * sm_count()) / std::max(1, m_tiles * n_tiles));
+    static const int waves = getenv("SYNO_TC_WG_WAVES") ? atoi(getenv("SYNO_TC_WG_WAVES")) : 1;
+    int ksplit = std::max(1, (waves * sm_count()) / std::max(1, m_tiles * n_tiles));
     ksplit = std::min(ksplit, std::max(1, p.n_cblocks / 4));
     p.ksplit = ksplit;
     p.m_ext = tp.C;
@@ -1789,7 +1802,7 @@ static void chain_fast(const TcPlan& tp, const TcWs& w, const Bindings& b, DType
                                                 (h.Kw == 1 && h.so_h == 1)
                            : h.oh ? (h.Kh == 1 || h.so_h == 1) : h.ow ? (h.Kw == 1 || h.so_w == 1) : true;
     h.dense = win_dense && h.so_c == kko && h.so_n == h.C * kko;
-    const size_t sm = h.dense ? (size_t)256 * kko * sizeof(float) : 0;
+    const size_t sm = (size_t)256 * (kko + 16) * sizeof(float);
     launch_k(chain_nc_kernel, (unsigned)((nthreads + 255) / 256), 256, sm, stream, c, h);
     cuda_check(cudaGetLastError(), "chain kernel");
     prof_end(id, stream);
