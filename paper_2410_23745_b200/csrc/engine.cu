@@ -79,6 +79,16 @@ std::atomic<bool> g_prof_on{false};
 std::vector<ProfRec> g_prof;
 }  // namespace
 
+// Inside a CUDA-graph capture the events become event-record nodes
+// (cudaEventRecordExternal), so a profiled graph replay times every launch
+// without host launch latency between them.
+static cudaError_t record_prof_event(cudaEvent_t e, cudaStream_t stream) {
+  cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(stream, &st);
+  if (st == cudaStreamCaptureStatusActive) return cudaEventRecordWithFlags(e, stream, cudaEventRecordExternal);
+  return cudaEventRecord(e, stream);
+}
+
 void prof_enable(bool on) {
   std::lock_guard<std::mutex> lock(g_prof_mu);
   for (auto& r : g_prof) {
@@ -97,7 +107,7 @@ int prof_begin(const char* name, double flops, double bytes, cudaStream_t stream
   r.bytes = bytes;
   cuda_check(cudaEventCreate(&r.a), "cudaEventCreate(prof)");
   cuda_check(cudaEventCreate(&r.b), "cudaEventCreate(prof)");
-  cuda_check(cudaEventRecord(r.a, stream), "cudaEventRecord(prof)");
+  cuda_check(record_prof_event(r.a, stream), "cudaEventRecord(prof)");
   std::lock_guard<std::mutex> lock(g_prof_mu);
   g_prof.push_back(r);
   return (int)g_prof.size() - 1;
@@ -117,7 +127,7 @@ void prof_end(int id, cudaStream_t stream) {
     if (id >= (int)g_prof.size()) return;
     b = g_prof[id].b;
   }
-  cuda_check(cudaEventRecord(b, stream), "cudaEventRecord(prof)");
+  cuda_check(record_prof_event(b, stream), "cudaEventRecord(prof)");
 }
 
 std::vector<ProfStat> prof_collect() {
