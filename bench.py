@@ -257,7 +257,7 @@ def run_layers(args, rank, world, device, peaks):
         # training-step contract: backward follows this layer's forward on the same x
         rc = _lib.lib.syno_backward_ex(s["h"].ptr, code, ctypes.c_void_p(s["x"].data_ptr()), warr, len(s["ws"]),
                                        ctypes.c_void_p(s["dy"].data_ptr()), ctypes.c_void_p(s["dx"].data_ptr()),
-                                       dwarr, _lib.SYNO_BWD_X_UNCHANGED, sp)
+                                       dwarr, _lib.SYNO_BWD_X_UNCHANGED | _lib.SYNO_BWD_W_UNCHANGED, sp)
         assert rc == 0, _lib.last_error()
 
     phases = [("fwd", call_fwd)] + ([] if fwd_only else [("bwd", call_bwd)])

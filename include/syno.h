@@ -96,12 +96,13 @@ int syno_forward(syno_op_t op, int dtype, const void* x, const void* const* w, i
 int syno_backward(syno_op_t op, int dtype, const void* x, const void* const* w, int n_w, const void* dy,
                   void* dx, void* const* dw, void* stream);
 
-/* syno_backward with flags.  SYNO_BWD_X_UNCHANGED promises that x holds the
- * same values as in the most recent syno_forward of this handle on this
- * stream (the autograd contract for a saved input): operand layouts derived
- * from x in that forward may be reused.  The library still checks that the
- * pointer matches and recomputes otherwise. */
-enum { SYNO_BWD_X_UNCHANGED = 1 };
+/* syno_backward with flags.  SYNO_BWD_X_UNCHANGED / SYNO_BWD_W_UNCHANGED
+ * promise that x / the weights hold the same values as in the most recent
+ * syno_forward of this handle on this stream (the autograd contract for
+ * saved inputs): operand layouts derived from them in that forward may be
+ * reused.  The library still checks that the pointers match and recomputes
+ * otherwise. */
+enum { SYNO_BWD_X_UNCHANGED = 1, SYNO_BWD_W_UNCHANGED = 2 };
 int syno_backward_ex(syno_op_t op, int dtype, const void* x, const void* const* w, int n_w, const void* dy,
                      void* dx, void* const* dw, int flags, void* stream);
 

@@ -26,6 +26,7 @@ SYNO_F32 = 0
 SYNO_BF16 = 1
 SYNO_F64 = 2
 SYNO_BWD_X_UNCHANGED = 1
+SYNO_BWD_W_UNCHANGED = 2
 SYNO_STAGED = 1
 SYNO_REPLAY_ONLY = 2
 

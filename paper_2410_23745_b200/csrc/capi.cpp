@@ -134,7 +134,7 @@ int syno_backward_ex(syno_op_t op, int dtype, const void* x, const void* const* 
   return guarded([&] {
     if (!op || !x || !dy || (n_w && !w)) fail(SYNO_E_INVALID, "null argument");
     if (dtype < 0 || dtype > 2) fail(SYNO_E_INVALID, "unknown dtype");
-    if (flags & ~SYNO_BWD_X_UNCHANGED) fail(SYNO_E_INVALID, "unknown backward flag");
+    if (flags & ~(SYNO_BWD_X_UNCHANGED | SYNO_BWD_W_UNCHANGED)) fail(SYNO_E_INVALID, "unknown backward flag");
     check_weights(op, w, n_w);
     cudaStream_t s = (cudaStream_t)stream;
     DevPlan& dp = dev_plan(op, s);
@@ -145,6 +145,7 @@ int syno_backward_ex(syno_op_t op, int dtype, const void* x, const void* const* 
     b.dx = dx;
     for (int j = 0; j < n_w; ++j) b.dw.push_back(dw ? dw[j] : nullptr);
     b.x_unchanged = (flags & SYNO_BWD_X_UNCHANGED) != 0;
+    b.w_unchanged = (flags & SYNO_BWD_W_UNCHANGED) != 0;
     run_backward(op->plan, dp, (DType)dtype, b, s);
   });
 }

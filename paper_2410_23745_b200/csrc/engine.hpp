@@ -100,6 +100,7 @@ struct Bindings {
   std::vector<void*> dw;
   std::vector<void*> stages;  // t_k buffers
   bool x_unchanged = false;   // syno_backward_ex(SYNO_BWD_X_UNCHANGED)
+  bool w_unchanged = false;   // syno_backward_ex(SYNO_BWD_W_UNCHANGED)
 };
 
 // Build one device stage (K1 tables) / launch it through the universal kernel.

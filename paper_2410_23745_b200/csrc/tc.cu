@@ -537,6 +537,81 @@ __global__ void __launch_bounds__(256) fold_tile_kernel(const __grid_constant__ 
   }
 }
 
+// Both B operands in one pass: Wf[k][n][ci] (forward) and Wt[k][ci][n]
+// (grad-input) from a 32 x 32 (n, ci) tile staged in shared memory for every
+// window k; reads follow the weight's memory order (k fastest, then ci),
+// both outputs are written as coalesced rows.
+struct FoldDual {
+  FoldArgs f;                 // f.out = Wf, f.Bp = Cp (ci pitch per part); ext = {Kh, Kw, N, C}
+  __nv_bfloat16* out_t;       // Wt
+  int32_t Np;                 // n pitch per part of Wt
+};
+
+__global__ void __launch_bounds__(256) fold_dual_kernel(const __grid_constant__ FoldDual d) {
+  pdl_trigger();
+  pdl_wait();
+  extern __shared__ float sv[];  // [KK][32][33]
+  __shared__ int32_t koff[MAXFW][16];
+  const FoldArgs& f = d.f;
+  const int KK = f.ext[0] * f.ext[1];
+  if ((int)threadIdx.x < KK) {
+    const int rh = threadIdx.x / f.ext[1], rw = threadIdx.x - rh * f.ext[1];
+    for (int j = 0; j < f.nw; ++j) koff[j][threadIdx.x] = (int32_t)(rh * f.s[j][0] + rw * f.s[j][1]);
+  }
+  __syncthreads();
+  const int n0 = blockIdx.x * 32, c0 = blockIdx.y * 32;
+  const int N = f.ext[2], C = f.ext[3];
+#pragma unroll 1
+  for (int i = threadIdx.x; i < 32 * 32 * KK; i += blockDim.x) {
+    const int k = i % KK;
+    const int q = i / KK;
+    const int cl = q % 32, nl = q / 32;
+    const int n = n0 + nl, ci = c0 + cl;
+    float v = 0.f;
+    if (n < N && ci < C) {
+      v = 1.f;
+      for (int j = 0; j < f.nw; ++j) {
+        const int32_t off = koff[j][k] + n * (int32_t)f.s[j][2] + ci * (int32_t)f.s[j][3];
+        v *= f.f32 ? __ldg(reinterpret_cast<const float*>(f.w[j]) + off)
+                   : __bfloat162float(__ldg(reinterpret_cast<const __nv_bfloat16*>(f.w[j]) + off));
+      }
+    }
+    sv[(k * 32 + nl) * 33 + cl] = v;
+  }
+  __syncthreads();
+  const int parts = f.split ? 3 : 1;
+  // Wf rows (k, n): ci contiguous
+#pragma unroll 1
+  for (int i = threadIdx.x; i < 32 * 32 * KK; i += blockDim.x) {
+    const int cl = i % 32, nl = (i / 32) % 32, k = i / 1024;
+    const int n = n0 + nl, ci = c0 + cl;
+    if (n >= N || ci >= f.Bp) continue;
+    const float v = sv[(k * 32 + nl) * 33 + cl];
+    __nv_bfloat16* o = f.out + ((int64_t)k * N + n) * parts * f.Bp + ci;
+    const __nv_bfloat16 hi = __float2bfloat16(v);
+    o[0] = hi;
+    if (parts == 3) {
+      o[f.Bp] = __float2bfloat16(v - __bfloat162float(hi));
+      o[2 * f.Bp] = hi;
+    }
+  }
+  // Wt rows (k, ci): n contiguous
+#pragma unroll 1
+  for (int i = threadIdx.x; i < 32 * 32 * KK; i += blockDim.x) {
+    const int nl = i % 32, cl = (i / 32) % 32, k = i / 1024;
+    const int n = n0 + nl, ci = c0 + cl;
+    if (ci >= C || n >= d.Np) continue;
+    const float v = sv[(k * 32 + nl) * 33 + cl];
+    __nv_bfloat16* o = d.out_t + ((int64_t)k * C + ci) * parts * d.Np + n;
+    const __nv_bfloat16 hi = __float2bfloat16(v);
+    o[0] = hi;
+    if (parts == 3) {
+      o[d.Np] = __float2bfloat16(v - __bfloat162float(hi));
+      o[2 * d.Np] = hi;
+    }
+  }
+}
+
 struct ChainArgs {
   float* dwf;            // [Kh][Kw][N][C] fp32
   int32_t zero_dwf;      // last reader: leave dWf zeroed for the next grad-weight (no memset)
@@ -1462,6 +1537,7 @@ struct TcWs {
   // unpadded, e.g. QKV activations) is read by TMA in place
   bool x_ident = false, xw_ident = false, dyg_ident = false, dyw_ident = false;
   const void* packed_x_src = nullptr;  // x whose packed operand xcl currently holds (last forward)
+  std::vector<const void*> wt_src;      // weights the grad-input operand wt was folded from (last forward)
   MapSpec ms_fwd_a, ms_dg_a, ms_wg_a, ms_wg_b;
   PackGeom gx{}, gxw{}, gdy_g{}, gdy_w{};
   bool share_dy = false, share_x = false;
@@ -1748,6 +1824,43 @@ static void fold_fast(const TcPlan& tp, const Bindings& b, DType dt, bool dgrad,
   prof_end(id, stream);
 }
 
+// Forward + grad-input B operands in one launch (KK <= 9).
+static bool fold_dual(const TcPlan& tp, const Bindings& b, DType dt, bool split, __nv_bfloat16* wf,
+                      __nv_bfloat16* wt, cudaStream_t stream) {
+  const int KK = tp.dh.K * tp.dw.K;
+  // measured slower than two direct folds for the ResNet shapes (few tiles,
+  // serial windows per thread); opt-in until the tiling is reworked
+  static const bool on = getenv("SYNO_TC_DUAL_FOLD") != nullptr;
+  if (KK > 9 || !on) return false;
+  if (skip_class("fold")) return true;
+  FoldDual d{};
+  FoldArgs& f = d.f;
+  f.nw = tp.nw;
+  f.f32 = dt == DT_F32;
+  for (int j = 0; j < tp.nw; ++j) {
+    f.w[j] = b.w.at(j);
+    for (int l = 0; l < 4; ++l) f.s[j][l] = tp.wstr[j][l];
+  }
+  f.ext[0] = tp.dh.K;
+  f.ext[1] = tp.dw.K;
+  f.ext[2] = tp.N;
+  f.ext[3] = tp.C;
+  f.Bp = tp.Cp;
+  f.split = split;
+  f.out = wf;
+  d.out_t = wt;
+  d.Np = tp.Np;
+  const double elems = (double)KK * tp.N * tp.C;
+  const int id = prof_begin("weight_fold", 0.0, elems * (split ? 12 : 4) + elems * tp.nw * (f.f32 ? 4 : 2), stream);
+  note_launch();
+  const int gy = (std::max(tp.C, tp.Np) + 31) / 32;
+  const int gx = (std::max(tp.N, tp.Np) + 31) / 32;
+  launch_k(fold_dual_kernel, dim3((unsigned)gx, (unsigned)gy), 256, (size_t)KK * 32 * 33 * sizeof(float), stream, d);
+  cuda_check(cudaGetLastError(), "fold_dual_kernel");
+  prof_end(id, stream);
+  return true;
+}
+
 static void chain_fast(const TcPlan& tp, const TcWs& w, const Bindings& b, DType dt, int j, bool zero_dwf,
                        cudaStream_t stream) {
   if (skip_class("chain")) return;
@@ -1916,7 +2029,9 @@ bool tc_forward(TcPlan& tp, DType dt, const Bindings& b, cudaStream_t stream) {
     pack_cl(b.x, dt, w.gx, w.xcl, stream);
     w.packed_x_src = b.x;
   }
-  if (tp.fast_fold) fold_fast(tp, b, dt, false, w.f32, w.wf, stream);
+  w.wt_src.clear();
+  if (tp.fast_fold && tp.dgrad_ok && fold_dual(tp, b, dt, w.f32, w.wf, w.wt, stream)) w.wt_src = b.w;
+  else if (tp.fast_fold) fold_fast(tp, b, dt, false, w.f32, w.wf, stream);
   else fold_into(w, tp.fold_fwd, dt, b, w.wf32, w.wf, (int64_t)tp.nwin() * tp.N, tp.Cp, stream);
   rows_gemm(p, w.bn_fwd, w.t_fwd, b.y, w.f32, w.ysc, tp.y_numel(), stream, "tc_gemm_fwd", tp.flops);
   return true;
@@ -1936,8 +2051,14 @@ bool tc_backward(TcPlan& tp, DType dt, const Bindings& b, cudaStream_t stream) {
       pack_cl(b.dy, dt, w.gdy_g, w.dycl_g, stream);
       dy_w_packed = w.share_dy;
     }
-    if (tp.fast_fold) fold_fast(tp, b, dt, true, w.f32, w.wt, stream);
-    else fold_into(w, tp.fold_dgrad, dt, b, w.wt32, w.wt, (int64_t)tp.nwin() * tp.C, tp.Np, stream);
+    const bool wt_ready = b.w_unchanged && !w.wt_src.empty() && w.wt_src == b.w;
+    if (wt_ready) {
+      // the forward folded the grad-input operand from these same weights
+    } else if (tp.fast_fold) {
+      fold_fast(tp, b, dt, true, w.f32, w.wt, stream);
+    } else {
+      fold_into(w, tp.fold_dgrad, dt, b, w.wt32, w.wt, (int64_t)tp.nwin() * tp.C, tp.Np, stream);
+    }
     rows_gemm(p, w.bn_dg, w.t_dg, b.dx, w.f32, w.dxsc, tp.x_numel(), stream, "tc_gemm_dgrad", tp.flops);
   }
   if (any_w) {

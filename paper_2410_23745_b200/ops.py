@@ -70,7 +70,7 @@ def forward(h: Handle, x: torch.Tensor, weights: Sequence[torch.Tensor], out: Op
 
 
 def backward(h: Handle, x: torch.Tensor, weights: Sequence[torch.Tensor], dy: torch.Tensor,
-             want_dx: bool = True, want_dw=True, x_unchanged: bool = False):
+             want_dx: bool = True, want_dw=True, x_unchanged: bool = False, w_unchanged: bool = False):
     x = x.contiguous()
     dy = dy.contiguous()
     weights = [w.contiguous() for w in weights]
@@ -84,7 +84,8 @@ def backward(h: Handle, x: torch.Tensor, weights: Sequence[torch.Tensor], dy: to
     dwarr = (ctypes.c_void_p * max(1, len(weights)))(*[g.data_ptr() if g is not None else 0 for g in dws])
     with torch.cuda.device(x.device):
         rc = _lib.lib.syno_backward_ex(h.ptr, code, _ptr(x), warr, len(weights), _ptr(dy), _ptr(dx), dwarr,
-                                       _lib.SYNO_BWD_X_UNCHANGED if x_unchanged else 0, _stream_ptr(x))
+                                       (_lib.SYNO_BWD_X_UNCHANGED if x_unchanged else 0)
+                                       | (_lib.SYNO_BWD_W_UNCHANGED if w_unchanged else 0), _stream_ptr(x))
     if rc:
         raise_status(rc, _lib.last_error())
     return dx, dws
@@ -114,8 +115,9 @@ class SynoFunction(torch.autograd.Function):
     def backward(ctx, dy):
         x, *weights = ctx.saved_tensors
         need = ctx.needs_input_grad
-        # autograd saved x (version-checked): the forward's packed operand is reusable
-        dx, dws = backward(ctx.h, x, weights, dy, bool(need[1]), [bool(n) for n in need[2:]], x_unchanged=True)
+        # autograd saved x and weights (version-checked): the forward's operands are reusable
+        dx, dws = backward(ctx.h, x, weights, dy, bool(need[1]), [bool(n) for n in need[2:]], x_unchanged=True,
+                           w_unchanged=True)
         return (None, dx, *dws)
 
 
