@@ -216,10 +216,9 @@ __global__ void __launch_bounds__(256) split_rows_kernel(const float* __restrict
 constexpr int PK_PIX = 128;
 
 template <typename TI, int V>
-__global__ void __launch_bounds__(256) pack_rows_kernel(const TI* __restrict__ src, __nv_bfloat16* __restrict__ dst,
-                                                        PackGeom g, int32_t rows_per_block, int64_t total_rows) {
-  pdl_trigger();
-  pdl_wait();
+__device__ __forceinline__ void pack_rows_body(const TI* __restrict__ src, __nv_bfloat16* __restrict__ dst,
+                                               const PackGeom& g, int32_t rows_per_block, int64_t total_rows,
+                                               unsigned bx, unsigned by) {
   // channel-major tile: row cl holds the block's pixels; each group of 8
   // channel rows is rotated by 8 pixels so the transposed reads of the write
   // phase spread over all banks (the rotation keeps 16-byte alignment)
@@ -228,21 +227,21 @@ __global__ void __launch_bounds__(256) pack_rows_kernel(const TI* __restrict__ s
   __shared__ int64_t s_dst[PK_PIX];    // per block pixel: destination flat pixel index (-1: not stored)
   __shared__ int32_t s_part[PK_PIX];
   const int t = threadIdx.x;
-  const int cb = blockIdx.y;
+  const int cb = (int)by;
   const int n_out = g.n_img_out();
   // rows of <= PK_PIX pixels: rows_per_block whole rows; wider rows: one PK_PIX segment per block
   int64_t row0;
   int nrows, wbeg, Win;
   if (g.Win <= PK_PIX) {
-    row0 = (int64_t)blockIdx.x * rows_per_block;
+    row0 = (int64_t)bx * rows_per_block;
     nrows = (int)min((int64_t)rows_per_block, total_rows - row0);
     wbeg = 0;
     Win = g.Win;
   } else {
     const int nseg = (g.Win + PK_PIX - 1) / PK_PIX;
-    row0 = blockIdx.x / nseg;
+    row0 = bx / nseg;
     nrows = 1;
-    wbeg = (int)(blockIdx.x % nseg) * PK_PIX;
+    wbeg = (int)(bx % nseg) * PK_PIX;
     Win = min(PK_PIX, g.Win - wbeg);
   }
   const int npix = nrows * Win;
@@ -378,6 +377,14 @@ __global__ void __launch_bounds__(256) pack_rows_kernel(const TI* __restrict__ s
   }
 }
 
+template <typename TI, int V>
+__global__ void __launch_bounds__(256) pack_rows_kernel(const TI* __restrict__ src, __nv_bfloat16* __restrict__ dst,
+                                                        PackGeom g, int32_t rows_per_block, int64_t total_rows) {
+  pdl_trigger();
+  pdl_wait();
+  pack_rows_body<TI, V>(src, dst, g, rows_per_block, total_rows, blockIdx.x, blockIdx.y);
+}
+
 // ---------------------------------------------------------------------------
 // Weight transforms (fold into the B operand, chain rule out of dWf)
 // ---------------------------------------------------------------------------
@@ -431,9 +438,7 @@ __global__ void __launch_bounds__(128) fold_kernel(const __grid_constant__ FoldA
 // (column, window phase).  Output rows are written coalesced along b; the
 // weights are read through the read-only cache (neighbouring windows of the
 // same weight element run in other iterations / threads of the block).
-__global__ void __launch_bounds__(256) fold_direct_kernel(const __grid_constant__ FoldArgs f) {
-  pdl_trigger();
-  pdl_wait();
+__device__ __forceinline__ void fold_direct_body(const FoldArgs& f, unsigned bx, unsigned by) {
   __shared__ int32_t koff[MAXFW][16];
   const int KK = f.ext[0] * f.ext[1];
   if ((int)threadIdx.x < KK) {
@@ -443,8 +448,8 @@ __global__ void __launch_bounds__(256) fold_direct_kernel(const __grid_constant_
       if (j < f.nw) koff[j][threadIdx.x] = (int32_t)(rh * f.s[j][0] + rw * f.s[j][1]);
   }
   __syncthreads();
-  const int a = blockIdx.x;
-  const int b = blockIdx.y * 64 + (threadIdx.x & 63);
+  const int a = (int)bx;
+  const int b = (int)by * 64 + (threadIdx.x & 63);
   if (b >= f.Bp) return;
   const bool inb = b < f.ext[3];
   int32_t base[MAXFW];
@@ -473,6 +478,26 @@ __global__ void __launch_bounds__(256) fold_direct_kernel(const __grid_constant_
       o[2 * f.Bp] = hi;
     }
   }
+}
+
+__global__ void __launch_bounds__(256) fold_direct_kernel(const __grid_constant__ FoldArgs f) {
+  pdl_trigger();
+  pdl_wait();
+  fold_direct_body(f, blockIdx.x, blockIdx.y);
+}
+
+// One launch for the two independent per-call operand preparations of a
+// GEMM: blocks [0, n_pack) pack the activations, the rest fold the weights.
+template <typename TI, int V>
+__global__ void __launch_bounds__(256) prep_kernel(const TI* __restrict__ src, __nv_bfloat16* __restrict__ dst,
+                                                   PackGeom g, int32_t rows_per_block, int64_t total_rows,
+                                                   uint32_t pack_gx, uint32_t n_pack, const __grid_constant__ FoldArgs f,
+                                                   uint32_t fold_gx) {
+  pdl_trigger();
+  pdl_wait();
+  const uint32_t b = blockIdx.x;
+  if (b < n_pack) pack_rows_body<TI, V>(src, dst, g, rows_per_block, total_rows, b % pack_gx, b / pack_gx);
+  else fold_direct_body(f, (b - n_pack) % fold_gx, (b - n_pack) / fold_gx);
 }
 
 template <int TA, int TB>
@@ -1387,6 +1412,35 @@ static void launch_pack_rows(const void* src, const PackGeom& g, __nv_bfloat16* 
   launch_k(pack_rows_kernel<TI, V>, grid, 256, 0, stream, static_cast<const TI*>(src), dst, g, rpb, rows);
 }
 
+// Launch geometry of a pack and its vector width (0: scalar).
+struct PackPlan {
+  dim3 grid;
+  int rpb = 1;
+  int64_t rows = 0;
+  int V = 1;
+};
+
+static PackPlan pack_plan(const void* src, DType dt, const PackGeom& g) {
+  PackPlan pp;
+  pp.rpb = std::max(1, PK_PIX / g.Win);
+  pp.rows = (int64_t)g.n_img_out() * g.Hin;
+  const int64_t blocks = g.Win <= PK_PIX ? (pp.rows + pp.rpb - 1) / pp.rpb : pp.rows * ((g.Win + PK_PIX - 1) / PK_PIX);
+  pp.grid = dim3((unsigned)blocks, (unsigned)((g.Ct() + 63) / 64));
+  const uintptr_t base = reinterpret_cast<uintptr_t>(src);
+  auto aligned = [&](int v, int es) {
+    return g.s_w == 1 && g.Win % v == 0 && (g.Win <= PK_PIX || PK_PIX % v == 0) && g.s_h % v == 0 &&
+           g.s_c % v == 0 && g.s_img % v == 0 && base % (v * es) == 0;
+  };
+  if (dt == DT_BF16) pp.V = aligned(8, 2) ? 8 : aligned(4, 2) ? 4 : 1;
+  else pp.V = aligned(4, 4) ? 4 : 1;
+  return pp;
+}
+
+static double pack_bytes(DType dt, const PackGeom& g) {
+  const double src_elems = (double)g.n_img_out() * g.C * g.Hin * g.Win;
+  return src_elems * (dt == DT_BF16 ? 2 : 4) + src_elems * (g.split == SPLIT_CH ? 3 : 1) * 2;
+}
+
 static void pack_cl(const void* src, DType dt, const PackGeom& g, __nv_bfloat16* dst, cudaStream_t stream) {
   if (skip_class("pack")) return;
   // one block = whole source rows (<= PK_PIX pixels) or one PK_PIX segment of a wider row
@@ -1784,6 +1838,62 @@ static void build_ws(TcPlan& tp, TcWs& w, DType dt) {
   }
 }
 
+static FoldArgs fold_args(const TcPlan& tp, const Bindings& b, DType dt, bool dgrad, bool split, __nv_bfloat16* dst) {
+  FoldArgs f{};
+  f.nw = tp.nw;
+  f.f32 = dt == DT_F32;
+  for (int j = 0; j < tp.nw; ++j) {
+    f.w[j] = b.w.at(j);
+    for (int l = 0; l < 4; ++l) f.s[j][l] = tp.wstr[j][l];
+  }
+  f.ext[0] = tp.dh.K;
+  f.ext[1] = tp.dw.K;
+  f.ext[2] = dgrad ? tp.C : tp.N;
+  f.ext[3] = dgrad ? tp.N : tp.C;
+  f.sl_a = dgrad ? 3 : 2;
+  f.sl_b = dgrad ? 2 : 3;
+  f.Bp = dgrad ? tp.Np : tp.Cp;
+  f.split = split;
+  f.out = dst;
+  return f;
+}
+
+template <typename TI, int V>
+static void launch_prep(const void* src, const PackGeom& g, __nv_bfloat16* dst, const PackPlan& pp,
+                        const FoldArgs& f, cudaStream_t stream) {
+  const uint32_t n_pack = pp.grid.x * pp.grid.y;
+  const uint32_t fold_gx = (uint32_t)f.ext[2];
+  const uint32_t n_fold = fold_gx * (uint32_t)((f.Bp + 63) / 64);
+  launch_k(prep_kernel<TI, V>, n_pack + n_fold, 256, 0, stream, static_cast<const TI*>(src), dst, g, pp.rpb, pp.rows,
+           pp.grid.x, n_pack, f, fold_gx);
+}
+
+// Pack the activation operand and fold the weight operand of one GEMM in a
+// single launch (they are independent); false when the fold is not of the
+// direct kind (the caller then launches them separately).
+static bool pack_and_fold(const TcPlan& tp, const Bindings& b, DType dt, const void* src, const PackGeom& g,
+                          __nv_bfloat16* packed, bool dgrad, bool split, __nv_bfloat16* folded, cudaStream_t stream) {
+  const int KK = tp.dh.K * tp.dw.K;
+  if (!tp.fast_fold || KK <= 1 || KK > 16 || getenv("SYNO_TC_NO_PREP_FUSE")) return false;
+  if (skip_class("pack") || skip_class("fold")) return false;
+  const PackPlan pp = pack_plan(src, dt, g);
+  const FoldArgs f = fold_args(tp, b, dt, dgrad, split, folded);
+  const double fold_elems = (double)KK * f.ext[2] * f.Bp;
+  const int id = prof_begin("pack_cl", 0.0, pack_bytes(dt, g) + fold_elems * (split ? 6 : 2), stream);
+  note_launch();
+  if (dt == DT_BF16) {
+    if (pp.V == 8) launch_prep<__nv_bfloat16, 8>(src, g, packed, pp, f, stream);
+    else if (pp.V == 4) launch_prep<__nv_bfloat16, 4>(src, g, packed, pp, f, stream);
+    else launch_prep<__nv_bfloat16, 1>(src, g, packed, pp, f, stream);
+  } else {
+    if (pp.V == 4) launch_prep<float, 4>(src, g, packed, pp, f, stream);
+    else launch_prep<float, 1>(src, g, packed, pp, f, stream);
+  }
+  cuda_check(cudaGetLastError(), "prep_kernel");
+  prof_end(id, stream);
+  return true;
+}
+
 static void fold_fast(const TcPlan& tp, const Bindings& b, DType dt, bool dgrad, bool split, __nv_bfloat16* dst,
                       cudaStream_t stream) {
   if (skip_class("fold")) return;
@@ -2023,16 +2133,26 @@ bool tc_forward(TcPlan& tp, DType dt, const Bindings& b, cudaStream_t stream) {
   if (!tc_dtype(dt)) return false;
   TcWs& w = workspace(tp, dt, stream);
   TcGemmParams p = w.fwd;
+  w.wt_src.clear();
+  bool fused = false;
   if (w.x_ident && aligned16(b.x)) {
     p.tma_a = make_map(b.x, w.ms_fwd_a);
+  } else if (pack_and_fold(tp, b, dt, b.x, w.gx, w.xcl, false, w.f32, w.wf, stream)) {
+    w.packed_x_src = b.x;
+    fused = true;
   } else {
     pack_cl(b.x, dt, w.gx, w.xcl, stream);
     w.packed_x_src = b.x;
   }
-  w.wt_src.clear();
-  if (tp.fast_fold && tp.dgrad_ok && fold_dual(tp, b, dt, w.f32, w.wf, w.wt, stream)) w.wt_src = b.w;
-  else if (tp.fast_fold) fold_fast(tp, b, dt, false, w.f32, w.wf, stream);
-  else fold_into(w, tp.fold_fwd, dt, b, w.wf32, w.wf, (int64_t)tp.nwin() * tp.N, tp.Cp, stream);
+  if (fused) {
+    // operand folded by the fused launch
+  } else if (tp.fast_fold && tp.dgrad_ok && fold_dual(tp, b, dt, w.f32, w.wf, w.wt, stream)) {
+    w.wt_src = b.w;
+  } else if (tp.fast_fold) {
+    fold_fast(tp, b, dt, false, w.f32, w.wf, stream);
+  } else {
+    fold_into(w, tp.fold_fwd, dt, b, w.wf32, w.wf, (int64_t)tp.nwin() * tp.N, tp.Cp, stream);
+  }
   rows_gemm(p, w.bn_fwd, w.t_fwd, b.y, w.f32, w.ysc, tp.y_numel(), stream, "tc_gemm_fwd", tp.flops);
   return true;
 }
@@ -2046,13 +2166,18 @@ bool tc_backward(TcPlan& tp, DType dt, const Bindings& b, cudaStream_t stream) {
   bool dy_w_packed = false;
   if (b.dx) {
     TcGemmParams p = w.dg;
-    if (w.dyg_ident && aligned16(b.dy)) p.tma_a = make_map(b.dy, w.ms_dg_a);
-    else {
+    const bool wt_ready = b.w_unchanged && !w.wt_src.empty() && w.wt_src == b.w;
+    bool fused = false;
+    if (w.dyg_ident && aligned16(b.dy)) {
+      p.tma_a = make_map(b.dy, w.ms_dg_a);
+    } else if (!wt_ready && pack_and_fold(tp, b, dt, b.dy, w.gdy_g, w.dycl_g, true, w.f32, w.wt, stream)) {
+      dy_w_packed = w.share_dy;
+      fused = true;
+    } else {
       pack_cl(b.dy, dt, w.gdy_g, w.dycl_g, stream);
       dy_w_packed = w.share_dy;
     }
-    const bool wt_ready = b.w_unchanged && !w.wt_src.empty() && w.wt_src == b.w;
-    if (wt_ready) {
+    if (wt_ready || fused) {
       // the forward folded the grad-input operand from these same weights
     } else if (tp.fast_fold) {
       fold_fast(tp, b, dt, true, w.f32, w.wt, stream);
