@@ -1587,6 +1587,7 @@ struct TcWs {
   float* chain_partial = nullptr;     // fast chain rule, block mode
   unsigned* chain_counter = nullptr;
   int chain_nsplit[MAXFW] = {};       // 0: thread mode
+  bool wg_fixup = false;              // grad-weight epilogue writes dW directly (no chain launch)
   // zero-copy operands: a source already in the packed layout (channels-last,
   // unpadded, e.g. QKV activations) is read by TMA in place
   bool x_ident = false, xw_ident = false, dyg_ident = false, dyw_ident = false;
@@ -1808,6 +1809,21 @@ static void build_ws(TcPlan& tp, TcWs& w, DType dt) {
     w.t_wg[0] = m_tiles;
     w.t_wg[1] = n_tiles;
     w.t_wg[2] = ksplit;
+    // single weight whose fold is a pure permutation of (rh, rw, n, ci): the
+    // last split of each tile writes dW itself
+    bool perm = tp.fast_fold && tp.nw == 1 && getenv("SYNO_TC_NO_FIXUP") == nullptr;
+    const int64_t ext[4] = {tp.dh.K, tp.dw.K, tp.N, tp.C};
+    for (int l = 0; l < 4 && perm; ++l) perm = ext[l] == 1 || tp.wstr[0][l] != 0;
+    if (perm) {
+      w.wg_fixup = true;
+      p.fix_cnt = ws_alloc<unsigned>(w, (size_t)m_tiles * n_tiles);
+      for (int rh = 0; rh < tp.dh.K; ++rh)
+        for (int rw = 0; rw < tp.dw.K; ++rw)
+          p.fix_win_off[rh * tp.dw.K + rw] = rh * tp.wstr[0][0] + rw * tp.wstr[0][1];
+      p.fix_s_co = tp.wstr[0][2];
+      p.fix_s_ci = tp.wstr[0][3];
+      p.fix_f32 = w.f32 ? 1 : 0;
+    }
   }
 
   w.x_ident = pack_identity(w.gx, dt);
@@ -2194,6 +2210,8 @@ bool tc_backward(TcPlan& tp, DType dt, const Bindings& b, cudaStream_t stream) {
     else if (!dy_w_packed) pack_cl(b.dy, dt, w.gdy_w, w.dycl_w, stream);
     // fast chain kernels leave dWf zeroed behind them (it starts zeroed)
     static const bool memset_dwf = getenv("SYNO_TC_ZERO_FILL") != nullptr;  // A/B switch
+    const bool fixup = w.wg_fixup && b.dw.size() == 1 && b.dw[0] && !memset_dwf;
+    p.fix_out = fixup ? b.dw[0] : nullptr;
     if (!tp.fast_fold || memset_dwf) zero_fill(w.dwf, (size_t)tp.nwin() * tp.N * tp.C * sizeof(float), stream);
     gemm(p, w.bn_wg, w.t_wg[0], w.t_wg[1], w.t_wg[2], stream, "tc_gemm_wgrad", tp.flops);
     // chain rule through the fold, into each requested weight gradient
@@ -2202,6 +2220,7 @@ bool tc_backward(TcPlan& tp, DType dt, const Bindings& b, cudaStream_t stream) {
     int last = -1;
     for (size_t j = 0; j < tp.chain.size(); ++j)
       if (j < b.dw.size() && b.dw[j]) last = (int)j;
+    if (fixup) return true;  // the grad-weight epilogue wrote dW
     for (size_t j = 0; j < tp.chain.size(); ++j) {
       if (j >= b.dw.size() || !b.dw[j]) continue;
       if (tp.fast_fold) chain_fast(tp, w, b, dt, (int)j, (int)j == last && !memset_dwf, stream);

@@ -98,6 +98,15 @@ struct alignas(64) TcGemmParams {
   int32_t Hp, Wp, lo_h, lo_w, H, W, n_img;
   int64_t o_img, o_h, o_w, o_n, o_m;
   int32_t m_ext, n_ext;
+  // MODE_WGRAD split-K fixup: the last split to finish an output tile turns
+  // the tile's fp32 sums into the weight gradient itself (single-weight
+  // operators whose fold is a pure permutation), replacing the chain-rule
+  // launch; it also re-zeroes the tile's accumulator for the next call
+  void* fix_out;                // dW (null: off)
+  unsigned* fix_cnt;            // per (m_tile, n_tile) arrival counters, zero between calls
+  int64_t fix_win_off[MAXWIN];  // dW offset of window w
+  int64_t fix_s_ci, fix_s_co;   // dW strides of ci and co
+  int32_t fix_f32;
   int32_t out_kind;
   float scale;
   void* out;
@@ -308,6 +317,7 @@ __global__ void __launch_bounds__(THREADS, 1) tc_gemm_kernel(const __grid_consta
   uint64_t* tfull = b_empty + BSTAGES;  // [2]
   uint64_t* tempty = tfull + 2;         // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  volatile uint32_t* fix_last = tmem_slot + 1;  // MODE_WGRAD fixup: this CTA finished the tile last
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -607,6 +617,45 @@ __global__ void __launch_bounds__(THREADS, 1) tc_gemm_kernel(const __grid_consta
       __syncwarp();
       if (warp == 2 && lane == 0 && tcount < 14) stamp(2 + tcount * 4 + 3);
       if (lane == 0) mbar_arrive(&tempty[acc]);
+      if constexpr (MODE == MODE_WGRAD) {
+        if (p.fix_out) {
+          // every epilogue warp's atomics for this tile are issued
+          asm volatile("bar.sync 1, %0;" ::"n"(EPI_WARPS * 32) : "memory");
+          if (warp == 2 && lane == 0) {
+            __threadfence();
+            const int tile_mn = ti.mt * p.n_tiles + ti.nt;
+            const unsigned prev = atomicAdd(p.fix_cnt + tile_mn, 1u);
+            *fix_last = prev == (unsigned)(p.ksplit - 1) ? 1u : 0u;
+            if (*fix_last) p.fix_cnt[tile_mn] = 0u;  // ready for the next call (stream order)
+          }
+          asm volatile("bar.sync 1, %0;" ::"n"(EPI_WARPS * 32) : "memory");
+          if (*fix_last) {
+            __threadfence();
+            const int pr = ti.mt * 2 + (r >> 6);
+            const int ci = pr < p.n_pairs ? p.pair_cb[pr] * 64 + (r & 63) : p.m_ext;
+            if (ci < p.m_ext) {
+              const int w = p.pair_win[pr];
+              float* src = reinterpret_cast<float*>(p.out) + p.g_out_off[w] + (int64_t)ci * p.o_m;
+              const int64_t dst = p.fix_win_off[w] + (int64_t)ci * p.fix_s_ci;
+#pragma unroll 1
+              for (int c = half * 32; c < BN; c += 64) {
+                const int n0 = ti.nt * BN + c;
+                if (n0 >= p.n_ext) break;
+                const int nlim = min(32, p.n_ext - n0);
+#pragma unroll 4
+                for (int j = 0; j < nlim; ++j) {
+                  float* e = src + (int64_t)(n0 + j) * p.o_n;
+                  const float v = __ldcg(e);
+                  *e = 0.f;
+                  const int64_t o = dst + (int64_t)(n0 + j) * p.fix_s_co;
+                  if (p.fix_f32) reinterpret_cast<float*>(p.fix_out)[o] = v;
+                  else reinterpret_cast<__nv_bfloat16*>(p.fix_out)[o] = __float2bfloat16(v);
+                }
+              }
+            }
+          }
+        }
+      }
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
