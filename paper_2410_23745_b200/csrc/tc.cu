@@ -1811,7 +1811,9 @@ static void build_ws(TcPlan& tp, TcWs& w, DType dt) {
     w.t_wg[2] = ksplit;
     // single weight whose fold is a pure permutation of (rh, rw, n, ci): the
     // last split of each tile writes dW itself
-    bool perm = tp.fast_fold && tp.nw == 1 && getenv("SYNO_TC_NO_FIXUP") == nullptr;
+    // measured slower than the separate chain-rule kernel (the last split's
+    // strided dW writes serialise in the GEMM tail): opt-in only
+    bool perm = tp.fast_fold && tp.nw == 1 && getenv("SYNO_TC_FIXUP") != nullptr;
     const int64_t ext[4] = {tp.dh.K, tp.dw.K, tp.N, tp.C};
     for (int l = 0; l < 4 && perm; ++l) perm = ext[l] == 1 || tp.wstr[0][l] != 0;
     if (perm) {
