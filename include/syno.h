@@ -123,6 +123,14 @@ void syno_destroy(syno_op_t op);
 const char* syno_last_error(void);
 const char* syno_version(void);
 
+/* The reference's tensor file format (codegen.save_tensor / load_tensor,
+ * codegen.py:950-976): rank, then dims, as little-endian int64; float64
+ * row-major payload.  syno_tensor_read fills dims (up to SYNO_MAX_RANK) and,
+ * when data is non-null and cap >= the element count, the payload; a short
+ * or inconsistent file is SYNO_E_SHAPE (ShapeMismatch in the reference). */
+int syno_tensor_write(const char* path, int rank, const int64_t* dims, const double* data);
+int syno_tensor_read(const char* path, int* rank, int64_t* dims, double* data, int64_t cap, int64_t* count);
+
 /* Kernels this library has launched in this process (all handles, all
  * devices); bench.py reports the difference across its timed region. */
 uint64_t syno_launch_count(void);

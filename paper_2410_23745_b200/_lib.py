@@ -38,7 +38,7 @@ EXPORTS = (
     "syno_compile", "syno_forward", "syno_backward", "syno_query",
     "syno_emit_loop_nest", "syno_print_operator", "syno_describe_plan",
     "syno_index_map", "syno_destroy", "syno_last_error", "syno_version", "syno_launch_count",
-    "syno_profile_begin", "syno_profile_end", "syno_backward_ex",
+    "syno_profile_begin", "syno_profile_end", "syno_backward_ex", "syno_tensor_write", "syno_tensor_read",
 )
 
 
@@ -89,6 +89,10 @@ def _load():
                                   ctypes.POINTER(vp), vp]
     lib.syno_backward_ex.argtypes = [vp, ctypes.c_int, vp, ctypes.POINTER(vp), ctypes.c_int, vp, vp,
                                      ctypes.POINTER(vp), ctypes.c_int, vp]
+    lib.syno_tensor_write.argtypes = [ctypes.c_char_p, ctypes.c_int, ctypes.POINTER(ctypes.c_int64),
+                                      ctypes.POINTER(ctypes.c_double)]
+    lib.syno_tensor_read.argtypes = [ctypes.c_char_p, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int64),
+                                     ctypes.POINTER(ctypes.c_double), ctypes.c_int64, ctypes.POINTER(ctypes.c_int64)]
     lib.syno_query.argtypes = [vp, ctypes.POINTER(SynoInfo)]
     for name in ("syno_emit_loop_nest",):
         getattr(lib, name).argtypes = [vp, ctypes.c_int, ctypes.c_char_p, ctypes.c_size_t,

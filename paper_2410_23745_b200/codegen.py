@@ -148,4 +148,42 @@ def gradients(graph, x, upstream, weights: Sequence = (), assignment: Optional[M
     return _grads(graph, x, upstream, weights, assignment, True, True)
 
 
-__all__ += ["gradients", "PGraph", "operator_document"]
+# ---------------------------------------------------------------------------
+# Tensor file format (codegen.save_tensor / load_tensor, codegen.py:950-976),
+# implemented by the native library (syno_tensor_write / syno_tensor_read)
+# ---------------------------------------------------------------------------
+
+def save_tensor(path, array) -> None:
+    """rank, then dims, as little-endian int64; float64 row-major payload."""
+    import ctypes
+
+    from . import _lib
+    from .errors import raise_status
+    arr = np.array(array, dtype="<f8", order="C", copy=True)  # keeps 0-d arrays 0-d
+    dims = (ctypes.c_int64 * max(1, arr.ndim))(*arr.shape)
+    rc = _lib.lib.syno_tensor_write(str(path).encode(), arr.ndim, dims,
+                                    arr.ctypes.data_as(ctypes.POINTER(ctypes.c_double)))
+    if rc:
+        raise_status(rc, _lib.last_error())
+
+
+def load_tensor(path) -> np.ndarray:
+    import ctypes
+
+    from . import _lib
+    from .errors import raise_status
+    rank, count = ctypes.c_int(0), ctypes.c_int64(0)
+    dims = (ctypes.c_int64 * _lib.MAX_RANK)()
+    rc = _lib.lib.syno_tensor_read(str(path).encode(), ctypes.byref(rank), dims, None, 0, ctypes.byref(count))
+    if rc:
+        raise_status(rc, _lib.last_error())
+    out = np.empty(tuple(dims[k] for k in range(rank.value)), dtype="<f8")
+    rc = _lib.lib.syno_tensor_read(str(path).encode(), ctypes.byref(rank), dims,
+                                   out.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), out.size,
+                                   ctypes.byref(count))
+    if rc:
+        raise_status(rc, _lib.last_error())
+    return out
+
+
+__all__ += ["gradients", "PGraph", "operator_document", "save_tensor", "load_tensor"]

@@ -3,6 +3,7 @@
 
 #include <cuda_runtime.h>
 
+#include <cstdio>
 #include <cstring>
 #include <functional>
 #include <map>
@@ -286,6 +287,62 @@ int syno_profile_end(syno_kernel_stat* out, int cap, int* n) {
       out[i].ms = stats[i].ms;
       out[i].flops = stats[i].flops;
       out[i].bytes = stats[i].bytes;
+    }
+  });
+}
+
+}  // extern "C"
+
+extern "C" {
+
+int syno_tensor_write(const char* path, int rank, const int64_t* dims, const double* data) {
+  return guarded([&] {
+    if (!path || rank < 0 || (rank && !dims)) fail(SYNO_E_INVALID, "null argument");
+    int64_t count = 1;
+    for (int k = 0; k < rank; ++k) {
+      if (dims[k] < 0) fail(SYNO_E_VALUE, "negative tensor dimension");
+      count *= dims[k];
+    }
+    if (count && !data) fail(SYNO_E_INVALID, "null payload");
+    std::unique_ptr<FILE, int (*)(FILE*)> f(fopen(path, "wb"), fclose);
+    if (!f) fail(SYNO_E_INVALID, std::string("cannot open ") + path);
+    // the format is little-endian; this library only builds for little-endian hosts
+    const int64_t r = rank;
+    bool ok = fwrite(&r, 8, 1, f.get()) == 1;
+    if (rank) ok = ok && fwrite(dims, 8, (size_t)rank, f.get()) == (size_t)rank;
+    if (count) ok = ok && fwrite(data, 8, (size_t)count, f.get()) == (size_t)count;
+    if (!ok) fail(SYNO_E_INVALID, std::string("short write to ") + path);
+  });
+}
+
+int syno_tensor_read(const char* path, int* rank, int64_t* dims, double* data, int64_t cap, int64_t* count) {
+  return guarded([&] {
+    if (!path || !rank || !count) fail(SYNO_E_INVALID, "null argument");
+    std::unique_ptr<FILE, int (*)(FILE*)> f(fopen(path, "rb"), fclose);
+    if (!f) fail(SYNO_E_INVALID, std::string("cannot open ") + path);
+    fseek(f.get(), 0, SEEK_END);
+    const long size = ftell(f.get());
+    fseek(f.get(), 0, SEEK_SET);
+    if (size < 8) fail(SYNO_E_SHAPE, "tensor file too short for a header");
+    int64_t r = 0;
+    if (fread(&r, 8, 1, f.get()) != 1) fail(SYNO_E_SHAPE, "tensor file too short for a header");
+    if (r < 0 || size < 8 + 8 * r) fail(SYNO_E_SHAPE, "tensor file header truncated");
+    if (r > SYNO_MAX_RANK) fail(SYNO_E_UNSUPPORTED, "tensor rank exceeds SYNO_MAX_RANK");
+    int64_t d[SYNO_MAX_RANK];
+    if (r && fread(d, 8, (size_t)r, f.get()) != (size_t)r) fail(SYNO_E_SHAPE, "tensor file header truncated");
+    int64_t n = 1;
+    for (int64_t k = 0; k < r; ++k) n *= d[k];
+    const long payload = size - 8 - 8 * r;
+    if (payload != 8 * n)
+      fail(SYNO_E_SHAPE, "tensor payload holds " + std::to_string(payload / 8) + " values, header says " +
+                             std::to_string(n));
+    *rank = (int)r;
+    *count = n;
+    if (dims)
+      for (int64_t k = 0; k < r; ++k) dims[k] = d[k];
+    if (data) {
+      if (cap < n) fail(SYNO_E_INVALID, "payload buffer too small");
+      if (n && fread(data, 8, (size_t)n, f.get()) != (size_t)n) fail(SYNO_E_SHAPE, "tensor payload truncated");
     }
   });
 }

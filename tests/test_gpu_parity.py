@@ -219,3 +219,34 @@ def test_program_fallback_matches_oracle(cuda, name, monkeypatch):
     assert O.rel_err(f(gdx), O.input_gradient(case["nest"], env, x, up, ws, bs)) < 1e-10
     for a, b in zip(gdw, dws):
         assert O.rel_err(f(a), b) < 1e-10
+
+
+def test_cli_eval_against_reference_golden(cuda, tmp_path):
+    """`python -m paper_2410_23745_b200 eval` on tensors in the
+    reference's file format, compared with the reference's own outputs."""
+    import subprocess
+    import sys
+
+    from paper_2410_23745_b200.codegen import load_tensor, save_tensor
+    from conftest import ROOT
+    case = next(c for c in CASES if c["name"] == "sep_shared")
+    x, ws, up, y, _, dws = case_tensors(case)
+    (tmp_path / "op.txt").write_text(case["document"])
+    save_tensor(tmp_path / "x.tensor", x)
+    save_tensor(tmp_path / "up.tensor", up)
+    wpaths = []
+    for j, w in enumerate(ws):
+        save_tensor(tmp_path / f"w{j}.tensor", w)
+        wpaths.append(str(tmp_path / f"w{j}.tensor"))
+    gpaths = [str(tmp_path / f"dw{j}.tensor") for j in range(len(ws))]
+    cmd = [sys.executable, "-m", "paper_2410_23745_b200", "eval", "--op", str(tmp_path / "op.txt"),
+           "--input", str(tmp_path / "x.tensor"), "--weights", *wpaths, "--output", str(tmp_path / "y.tensor"),
+           "--upstream", str(tmp_path / "up.tensor"), "--grad-input", str(tmp_path / "dx.tensor"),
+           "--grad-weights", *gpaths]
+    r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stderr
+    assert O.rel_err(load_tensor(tmp_path / "y.tensor"), y) < 1e-10
+    for p, want in zip(gpaths, dws):
+        assert O.rel_err(load_tensor(p), want) < 1e-10
+    dx_want = O.input_gradient(case["nest"], case["env"], x, up, ws, case["batch_shape"])
+    assert O.rel_err(load_tensor(tmp_path / "dx.tensor"), dx_want) < 1e-10
