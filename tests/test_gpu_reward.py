@@ -66,3 +66,25 @@ def test_reward_fn_memoises(target):
     g = parse_steps(G["cases"][0]["steps"], spec)
     assert fn(g) == fn(g)
     assert len(calls) == 1
+
+
+@pytest.mark.parametrize("name", ["self", "partial"])
+def test_external_protocol_child(cuda, name):
+    """The GPU reward child speaks the reference's external-reward protocol
+    (reward.py:179-222): operator document on stdin, `reward <float>` and
+    `diag k v` lines on stdout."""
+    import subprocess
+    import sys
+
+    from conftest import ROOT
+    from paper_2410_23745_b200.pgraph import build_spec, parse_steps
+    case = next(c for c in G["cases"] if c["name"] == name and c["seed"] == 0)
+    spec = build_spec(**G["spec"])
+    doc = parse_steps(case["steps"], spec).document
+    r = subprocess.run([sys.executable, "-m", "paper_2410_23745_b200.reward_child", "--target", G["target"],
+                        "--seed", "0"], input=doc, cwd=ROOT, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr
+    lines = r.stdout.splitlines()
+    head = lines[0].split()
+    assert head[0] == "reward" and float(head[1]) == pytest.approx(case["reward"], abs=1e-6)
+    assert any(ln.startswith("diag residual ") for ln in lines[1:])
