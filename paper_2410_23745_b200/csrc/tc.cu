@@ -1588,6 +1588,10 @@ struct TcWs {
   unsigned* chain_counter = nullptr;
   int chain_nsplit[MAXFW] = {};       // 0: thread mode
   bool wg_fixup = false;              // grad-weight epilogue writes dW directly (no chain launch)
+  // grad-weight runs on a side stream concurrently with grad-input (fork /
+  // join by events; graph-capturable), so one GEMM's tail overlaps the other
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   // zero-copy operands: a source already in the packed layout (channels-last,
   // unpadded, e.g. QKV activations) is read by TMA in place
   bool x_ident = false, xw_ident = false, dyg_ident = false, dyw_ident = false;
@@ -1602,6 +1606,9 @@ struct TcWs {
   std::vector<void*> owned;
   ~TcWs() {
     for (void* q : owned) cudaFree(q);
+    if (ev_fork) cudaEventDestroy(ev_fork);
+    if (ev_join) cudaEventDestroy(ev_join);
+    if (side) cudaStreamDestroy(side);
   }
 };
 
@@ -2182,6 +2189,9 @@ bool tc_backward(TcPlan& tp, DType dt, const Bindings& b, cudaStream_t stream) {
   bool any_w = false;
   for (auto* q : b.dw) any_w = any_w || q;
   bool dy_w_packed = false;
+  static const bool concurrent = getenv("SYNO_TC_SERIAL_BWD") == nullptr;
+  const bool fork = concurrent && b.dx && any_w;
+  cudaStream_t wstream = stream;
   if (b.dx) {
     TcGemmParams p = w.dg;
     const bool wt_ready = b.w_unchanged && !w.wt_src.empty() && w.wt_src == b.w;
@@ -2202,9 +2212,21 @@ bool tc_backward(TcPlan& tp, DType dt, const Bindings& b, cudaStream_t stream) {
     } else {
       fold_into(w, tp.fold_dgrad, dt, b, w.wt32, w.wt, (int64_t)tp.nwin() * tp.C, tp.Np, stream);
     }
+    if (fork) {
+      if (!w.side) {
+        cuda_check(cudaStreamCreateWithFlags(&w.side, cudaStreamNonBlocking), "cudaStreamCreate(side)");
+        cuda_check(cudaEventCreateWithFlags(&w.ev_fork, cudaEventDisableTiming), "cudaEventCreate(fork)");
+        cuda_check(cudaEventCreateWithFlags(&w.ev_join, cudaEventDisableTiming), "cudaEventCreate(join)");
+      }
+      // the packed dy (and the rest of the stream's prior work) is ready for grad-weight
+      cuda_check(cudaEventRecord(w.ev_fork, stream), "cudaEventRecord(fork)");
+      cuda_check(cudaStreamWaitEvent(w.side, w.ev_fork, 0), "cudaStreamWaitEvent(fork)");
+      wstream = w.side;
+    }
     rows_gemm(p, w.bn_dg, w.t_dg, b.dx, w.f32, w.dxsc, tp.x_numel(), stream, "tc_gemm_dgrad", tp.flops);
   }
   if (any_w) {
+    cudaStream_t stream = wstream;  // grad-weight work: the side stream when forked
     TcGemmParams p = w.wg;
     if (w.xw_ident && aligned16(b.x)) p.tma_a = make_map(b.x, w.ms_wg_a);
     else if (!(b.x_unchanged && w.share_x && w.packed_x_src == b.x)) pack_cl(b.x, dt, w.gxw, w.xclw, stream);
@@ -2222,12 +2244,17 @@ bool tc_backward(TcPlan& tp, DType dt, const Bindings& b, cudaStream_t stream) {
     int last = -1;
     for (size_t j = 0; j < tp.chain.size(); ++j)
       if (j < b.dw.size() && b.dw[j]) last = (int)j;
-    if (fixup) return true;  // the grad-weight epilogue wrote dW
-    for (size_t j = 0; j < tp.chain.size(); ++j) {
-      if (j >= b.dw.size() || !b.dw[j]) continue;
-      if (tp.fast_fold) chain_fast(tp, w, b, dt, (int)j, (int)j == last && !memset_dwf, stream);
-      else run_stage(dt, tp.chain[j], cb, b.dw[j], false, stream);
+    if (!fixup) {
+      for (size_t j = 0; j < tp.chain.size(); ++j) {
+        if (j >= b.dw.size() || !b.dw[j]) continue;
+        if (tp.fast_fold) chain_fast(tp, w, b, dt, (int)j, (int)j == last && !memset_dwf, stream);
+        else run_stage(dt, tp.chain[j], cb, b.dw[j], false, stream);
+      }
     }
+  }
+  if (fork) {
+    cuda_check(cudaEventRecord(w.ev_join, w.side), "cudaEventRecord(join)");
+    cuda_check(cudaStreamWaitEvent(stream, w.ev_join, 0), "cudaStreamWaitEvent(join)");
   }
   return true;
 }
