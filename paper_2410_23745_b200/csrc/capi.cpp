@@ -223,6 +223,7 @@ int syno_describe_plan(syno_op_t op, char* buf, size_t cap, size_t* len) {
   for (auto& st : op->plan.grad_x) s += "grad_x: " + st.describe() + "\n";
   for (size_t j = 0; j < op->plan.grad_w.size(); ++j)
     for (auto& st : op->plan.grad_w[j]) s += "grad_w" + std::to_string(j) + ": " + st.describe() + "\n";
+  for (auto& st : op->plan.bwd_staged) s += "staged_bwd: " + st.describe() + "\n";
   return put_text(s, buf, cap, len);
 }
 

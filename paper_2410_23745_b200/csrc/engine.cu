@@ -355,7 +355,7 @@ static void build_kterm(const CStage& s, const CTerm& t, KTerm* k, std::vector<T
   memset(k, 0, sizeof(KTerm));
   const int A = (int)s.axis_ext.size();
   const int L = s.nloops();
-  k->kind = t.t.kind == TK_PHANTOM ? 2 : (t.t.kind == TK_STAGE ? 1 : 0);
+  k->kind = t.t.kind == TK_PHANTOM ? 2 : (t.t.kind == TK_STAGE || t.t.kind == TK_DSTAGE ? 1 : 0);
   if (t.t.numel() >= (int64_t)INT32_MAX) fail(SYNO_E_UNSUPPORTED, "tensor has 2^31 or more elements");
   auto strides = row_major_strides(t.t.extents);
   if (t.coords.size() != t.t.extents.size()) fail(SYNO_E_SHAPE, "access rank does not match tensor rank");
@@ -491,7 +491,7 @@ static void build_prog_stage(const CStage& cs, DevStage* ds) {
     KTerm& kt = k.terms[t];
     memset(&kt, 0, sizeof(KTerm));
     const int tk = cs.terms[t].t.kind;
-    kt.kind = tk == TK_PHANTOM ? 2 : (tk == TK_STAGE ? 1 : 0);
+    kt.kind = tk == TK_PHANTOM ? 2 : (tk == TK_STAGE || tk == TK_DSTAGE ? 1 : 0);
   }
   memset(&k.target, 0, sizeof(KTerm));
 }
@@ -555,6 +555,7 @@ DevPlan::~DevPlan() {
   };
   rel(forward);
   rel(grad_x);
+  rel(bwd_staged);
   for (auto& g : grad_w) rel(g);
   tc.reset();
   if (device >= 0 && device != cur && cur >= 0) cudaSetDevice(cur);
@@ -575,6 +576,15 @@ static void ensure_forward(const Plan& plan, DevPlan& dp, cudaStream_t stream) {
 static void ensure_backward(const Plan& plan, DevPlan& dp, cudaStream_t stream) {
   std::lock_guard<std::mutex> lock(dp.mu);
   if (dp.have_backward) return;
+  if (!plan.bwd_staged.empty()) {
+    for (auto& s : plan.bwd_staged) {
+      dp.bwd_staged.emplace_back();
+      build_dev_stage(s, &dp.bwd_staged.back(), stream);
+    }
+    cuda_check(cudaStreamSynchronize(stream), "ensure_backward");
+    dp.have_backward = true;
+    return;
+  }
   for (auto& s : plan.grad_x) {
     dp.grad_x.emplace_back();
     build_dev_stage(s, &dp.grad_x.back(), stream);
@@ -946,6 +956,7 @@ static const void* bind_ptr(const CTensor& t, const Bindings& b) {
     case TK_DY: return b.dy;
     case TK_DX: return b.dx;
     case TK_DW: return b.dw.at(t.index);
+    case TK_DSTAGE: return b.dstages.at(t.index);
     default: return nullptr;
   }
 }
@@ -1132,8 +1143,63 @@ static void run_grad(DType dt, const DevStage& ds, const Bindings& b, void* out,
   cuda_check(cudaFreeAsync(acc, stream), "free grad acc");
 }
 
+static int64_t numel_of(const std::vector<int64_t>& e) {
+  int64_t n = 1;
+  for (auto v : e) n *= v;
+  return n;
+}
+
+// Reverse-mode through the rfactored stages (Plan::bwd_staged): recompute
+// the forward intermediates, then run each gradient stage into dx, dw_j or
+// the gradient buffer of an intermediate.
+static void run_backward_staged(const Plan& plan, DevPlan& dp, DType dt, const Bindings& b_in, cudaStream_t stream) {
+  ensure_forward(plan, dp, stream);
+  ensure_backward(plan, dp, stream);
+  Bindings b = b_in;
+  const size_t nst = plan.stage_ext.size();
+  std::vector<void*> owned;
+  auto acc_alloc = [&](int64_t n) {
+    void* p = nullptr;
+    cuda_check(cudaMallocAsync(&p, std::max<int64_t>(n, 1) * acc_size(dt), stream), "alloc stage buffer");
+    owned.push_back(p);
+    return p;
+  };
+  b.stages.assign(nst, nullptr);
+  b.dstages.assign(nst, nullptr);
+  for (size_t k = 0; k < nst; ++k) {
+    b.stages[k] = acc_alloc(numel_of(plan.stage_ext[k]));
+    b.dstages[k] = acc_alloc(numel_of(plan.stage_ext[k]));
+  }
+  for (auto& ds : dp.forward) {
+    if (ds.cs.out.kind != TK_STAGE) continue;  // the output y is not needed
+    run_stage(dt, ds, b, b.stages[ds.cs.out.index], true, stream);
+  }
+  for (auto& ds : dp.bwd_staged) {
+    const CTensor& o = ds.cs.out;
+    if (o.kind == TK_DX) {
+      run_grad(dt, ds, b, b.dx, numel_of(plan.x_ext), stream);
+    } else if (o.kind == TK_DW) {
+      run_grad(dt, ds, b, o.index < (int)b.dw.size() ? b.dw[o.index] : nullptr, numel_of(plan.w_ext.at(o.index)),
+               stream);
+    } else {
+      void* out = b.dstages.at(o.index);
+      if (ds.cs.scatter) {
+        zero_fill(out, numel_of(o.extents) * acc_size(dt), stream);
+        if (!ds.dead) run_stage(dt, ds, b, out, true, stream);
+      } else {
+        run_stage(dt, ds, b, out, true, stream);
+      }
+    }
+  }
+  for (void* p : owned) cuda_check(cudaFreeAsync(p, stream), "free stage buffer");
+}
+
 void run_backward(const Plan& plan, DevPlan& dp, DType dt, const Bindings& b, cudaStream_t stream) {
   if (dp.tc && tc_backward(*dp.tc, dt, b, stream)) return;
+  if (!plan.bwd_staged.empty()) {
+    run_backward_staged(plan, dp, dt, b, stream);
+    return;
+  }
   ensure_backward(plan, dp, stream);
   int64_t nx = 1;
   for (auto e : plan.x_ext) nx *= e;

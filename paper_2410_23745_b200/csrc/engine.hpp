@@ -83,7 +83,7 @@ struct DevPlan {
   // usually makes them unnecessary); guarded by `mu`.
   std::mutex mu;
   bool have_forward = false, have_backward = false;
-  std::vector<DevStage> forward, grad_x;
+  std::vector<DevStage> forward, grad_x, bwd_staged;
   std::vector<std::vector<DevStage>> grad_w;
   TcPlanPtr tc;  // null when the operator is not contraction-shaped
   ~DevPlan();
@@ -99,6 +99,7 @@ struct Bindings {
   void* dx = nullptr;
   std::vector<void*> dw;
   std::vector<void*> stages;  // t_k buffers
+  std::vector<void*> dstages; // gradients of t_k (staged backward)
   bool x_unchanged = false;   // syno_backward_ex(SYNO_BWD_X_UNCHANGED)
   bool w_unchanged = false;   // syno_backward_ex(SYNO_BWD_W_UNCHANGED)
 };

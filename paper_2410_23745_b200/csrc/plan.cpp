@@ -3,6 +3,7 @@
 
 #include <algorithm>
 #include <functional>
+#include <map>
 #include <set>
 #include <sstream>
 
@@ -80,7 +81,7 @@ double CStage::grid_points() const {
 
 std::string CStage::describe() const {
   std::ostringstream o;
-  static const char* kn[] = {"x", "w", "t", "y", "dy", "dx", "dw", "phantom"};
+  static const char* kn[] = {"x", "w", "t", "y", "dy", "dx", "dw", "phantom", "dt"};
   o << (scatter ? "scatter" : "gather") << " out=" << kn[out.kind] << out.index << " axes=[";
   for (size_t k = 0; k < axis_ext.size(); ++k) o << (k ? "," : "") << axis_ext[k];
   o << "] reduces=[";
@@ -202,13 +203,19 @@ static CStage remap_stage_loops(CStage s, const std::map<int, int>& m) {
 
 // Gradient of <dy, out> with respect to term j of the unstaged stage S.
 CStage derive_gradient(const CStage& S, int j, const CTensor& grad) {
+  CTensor up;
+  up.kind = TK_DY;
+  up.extents = S.out.extents;
+  return derive_gradient(S, j, grad, up);
+}
+
+CStage derive_gradient(const CStage& S, int j, const CTensor& grad, const CTensor& upstream) {
   const int L = S.nloops();
   const int A = (int)S.axis_ext.size();
   const CTerm& tj = S.terms[j];
   const int D = (int)tj.coords.size();
   CTerm up;
-  up.t.kind = TK_DY;
-  up.t.extents = S.out.extents;
+  up.t = upstream;
   for (int a = 0; a < A; ++a) up.coords.push_back(c_loop(a));
 
   // --- scatter form: the reference algorithm (codegen.py:727-742) ---------
@@ -398,6 +405,46 @@ Plan build_plan(const LoopNest& unstaged, const LoopNest& staged, const std::vec
     gw.index = (int)j;
     gw.extents = p.w_ext[j];
     p.grad_w.push_back({derive_gradient(S, (int)j + 1, gw)});
+  }
+
+  // Staged backward: reverse-mode through the rfactored stages when every
+  // tensor is read by exactly one term (no gradient accumulation needed).
+  if (p.forward.size() > 1 && &staged != &unstaged) {
+    std::map<std::pair<int, int>, int> reads;  // (kind, index) -> count
+    for (auto& st : p.forward)
+      for (auto& t : st.terms) ++reads[{t.t.kind, t.t.index}];
+    bool unique = true;
+    for (auto& kv : reads) unique = unique && kv.second == 1 && kv.first.first != TK_PHANTOM;
+    const int S = (int)p.forward.size();
+    for (int k = 0; k + 1 < S && unique; ++k) unique = reads.count({TK_STAGE, k}) == 1;
+    if (unique) {
+      for (int k = S - 1; k >= 0; --k) {
+        const CStage& F = p.forward[k];
+        CTensor up;
+        if (k == S - 1) {
+          up.kind = TK_DY;
+        } else {
+          up.kind = TK_DSTAGE;
+          up.index = k;
+        }
+        up.extents = F.out.extents;
+        for (size_t j = 0; j < F.terms.size(); ++j) {
+          const CTensor& t = F.terms[j].t;
+          CTensor g;
+          g.extents = t.extents;
+          if (t.kind == TK_X) {
+            g.kind = TK_DX;
+          } else if (t.kind == TK_W) {
+            g.kind = TK_DW;
+            g.index = t.index;
+          } else {
+            g.kind = TK_DSTAGE;
+            g.index = t.index;
+          }
+          p.bwd_staged.push_back(derive_gradient(F, (int)j, g, up));
+        }
+      }
+    }
   }
   return p;
 }

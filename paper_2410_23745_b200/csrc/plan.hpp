@@ -50,6 +50,7 @@ enum TensorKind : int {
   TK_DX = 5,      // input gradient
   TK_DW = 6,      // weight gradient j
   TK_PHANTOM = 7, // validity-only term (value 1 when in range)
+  TK_DSTAGE = 8,  // gradient of intermediate t_k (workspace, accumulator precision)
 };
 
 struct CTensor {
@@ -94,12 +95,19 @@ struct Plan {
   CStage unstaged;                                // batch-explicit unstaged stage (backward source)
   std::vector<CStage> grad_x;                     // stages producing dX (one)
   std::vector<std::vector<CStage>> grad_w;        // per weight
+  // Staged backward (SYNO_STAGED handles whose rfactored nest has several
+  // stages and reads every tensor in exactly one term): reverse-mode through
+  // the forward stages; outputs are TK_DX, TK_DW j or TK_DSTAGE k.  The
+  // forward intermediates are recomputed first.  Empty: unstaged backward.
+  std::vector<CStage> bwd_staged;
   int64_t flops_unstaged = 0, flops_staged = 0;   // codegen.flops, batch included
 };
 
 // Gradient of <dy, out> with respect to term j of stage S (gather form when
 // the target's coordinates invert at acceptable cost, else scatter form).
 CStage derive_gradient(const CStage& S, int j, const CTensor& grad);
+// Same, with an explicit upstream tensor (dy, or the gradient of an intermediate).
+CStage derive_gradient(const CStage& S, int j, const CTensor& grad, const CTensor& upstream);
 
 Plan build_plan(const LoopNest& unstaged, const LoopNest& staged_or_same, const std::vector<Size>& batch_dims,
                 const Assignment& env);

@@ -1358,7 +1358,9 @@ static RowsTiling rows_tiling(int64_t F, int n_tiles, int groups, int bn, int n_
   const bool no_split = getenv("SYNO_TC_NO_RSPLIT") != nullptr;
   RowsTiling best{mgroup_of(bn), 1, mt(mgroup_of(bn))};
   double best_cost = 1e300;
+  static const int force_g = getenv("SYNO_TC_G") ? atoi(getenv("SYNO_TC_G")) : 0;  // experiments
   for (int G = mgroup_of(bn); G >= 1; G /= 2) {
+    if (force_g && G != force_g && force_g <= mgroup_of(bn)) continue;
     for (int rs = 1; rs <= (no_split ? 1 : n_cblocks); ++rs) {
       const int per = (n_cblocks + rs - 1) / rs;
       if (rs > 1 && (n_cblocks + per - 1) / per != rs) continue;  // an empty split: same as fewer splits

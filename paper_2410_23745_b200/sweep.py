@@ -106,7 +106,9 @@ def evaluate(graph, sample_id: int, seed: int, dtype=None, device=None,
 
     dtype = dtype or torch.float32
     device = device or torch.device("cuda", torch.cuda.current_device())
-    h = handle_for(graph)
+    # the rfactored nest (the reference's interpret(staged=True) path, same
+    # values): forward runs its stages, backward reverse-mode through them
+    h = handle_for(graph, None, True)
     op = print_steps(graph)
     if not within_budget(h.flops_unstaged, h.params, flops_cap, params_cap):
         return EvalRecord(sample_id, seed, h.flops_unstaged, h.params, "over_budget", op)
@@ -141,10 +143,10 @@ def candidate_costs(graphs) -> List[float]:
     from .pgraph import handle_for
     out = []
     for g in graphs:
-        h = handle_for(g)
+        h = handle_for(g, None, True)
         nbytes = 4 * (2 * math.prod(h.x_shape) + 2 * math.prod(h.y_shape)
                       + 2 * sum(math.prod(s) for s in h.w_shapes))
-        out.append(predicted_seconds(h.flops_unstaged, nbytes))
+        out.append(predicted_seconds(h.flops_staged, nbytes))
     return out
 
 

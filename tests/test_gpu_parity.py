@@ -250,3 +250,61 @@ def test_cli_eval_against_reference_golden(cuda, tmp_path):
         assert O.rel_err(load_tensor(p), want) < 1e-10
     dx_want = O.input_gradient(case["nest"], case["env"], x, up, ws, case["batch_shape"])
     assert O.rel_err(load_tensor(tmp_path / "dx.tensor"), dx_want) < 1e-10
+
+
+@pytest.mark.parametrize("dtype", ["float64", "float32"])
+@pytest.mark.parametrize("case", CASES, ids=CASE_IDS)
+def test_staged_handles_forward_backward(cuda, case, dtype):
+    """SYNO_STAGED handles run the rfactored nest forward and, where every
+    tensor is read once, reverse-mode through its stages backward; the math
+    is the unstaged operator's (reference weight_gradient differentiates the
+    unstaged nest, codegen.py:680), so the same oracle values apply."""
+    x, ws, up, y, ys, dws = case_tensors(case)
+    env, bs = case["env"], case["batch_shape"]
+    if dtype != "float64":
+        x, up = _rounded(x, dtype), _rounded(up, dtype)
+        ws = [_rounded(w, dtype) for w in ws]
+        y = O.interpret(case["nest"], env, x, ws, bs)
+        dws = O.weight_gradient(case["nest"], env, x, up, ws, bs) if ws else []
+    dx_want = O.input_gradient(case["nest"], env, x, up, ws, bs)
+    gy, gdx, gdw = _run(case, x, ws, up, dtype, staged=True)
+    tol = TOL[dtype]
+    assert O.rel_err(gy, y) < tol
+    assert O.rel_err(gdx, dx_want) < tol
+    for a, b in zip(gdw, dws):
+        assert O.rel_err(a, b) < tol
+
+
+@pytest.mark.parametrize("chunk", range(4))
+def test_corpus_reduced_staged_fp32(cuda, chunk):
+    """Corpus operators through staged handles (rfactored forward, staged
+    backward where it applies) at reduced sizes, fp32, against the oracle."""
+    from paper_2410_23745_b200 import codegen as C
+    from paper_2410_23745_b200 import ops
+    from paper_2410_23745_b200 import pgraph as P
+    torch = _torch()
+    ops_ = _corpus()[chunk::4][:96]
+    checked = 0
+    for op in ops_:
+        g, red = reduced_case(op)
+        if red is None:
+            continue
+        h = P.handle_for(g, red, True)
+        text = C.emit_loop_nest(g, red)
+        rng = np.random.default_rng(1000 + checked)
+        xr = _rounded(rng.standard_normal(h.x_shape), "float32")
+        wr = [_rounded(rng.standard_normal(s), "float32") for s in h.w_shapes]
+        upr = _rounded(rng.standard_normal(h.y_shape), "float32")
+        xd, ud = ops.to_device(xr, "float32"), ops.to_device(upr, "float32")
+        wd = [ops.to_device(w, "float32") for w in wr]
+        gy = ops.forward(h, xd, wd)
+        gdx, gdw = ops.backward(h, xd, wd, ud)
+        torch.cuda.synchronize()
+        bs = h.x_shape[:1]
+        f = lambda t: t.double().cpu().numpy()  # noqa: E731
+        assert O.rel_err(f(gy), O.interpret(text, red, xr, wr, bs)) < 1e-4, op
+        assert O.rel_err(f(gdx), O.input_gradient(text, red, xr, upr, wr, bs)) < 1e-4, op
+        for a, b in zip(gdw, O.weight_gradient(text, red, xr, upr, wr, bs) if wr else []):
+            assert O.rel_err(f(a), b) < 1e-4, op
+        checked += 1
+    assert checked >= len(ops_) // 2
