@@ -1260,15 +1260,15 @@ std::string tc_describe(const TcPlan* tp) {
 // Launch helpers
 // ---------------------------------------------------------------------------
 
-template <int BN, int MODE>
+template <int BN, int MODE, int CFG>
 static void launch_gemm(const TcGemmParams& p, unsigned grid, cudaStream_t stream) {
   static std::atomic<uint64_t> configured{0};  // per-device bit
-  constexpr int smem = smem_bytes<BN>();
+  constexpr int smem = smem_bytes<BN, CFG>();
   int dev = 0;
   cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
   const uint64_t bit = 1ull << (dev & 63);
   if (!(configured.load() & bit)) {
-    cuda_check(cudaFuncSetAttribute(tc_gemm_kernel<BN, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
+    cuda_check(cudaFuncSetAttribute(tc_gemm_kernel<BN, MODE, CFG>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
                "cudaFuncSetAttribute(tc_gemm)");
     configured.fetch_or(bit);
   }
@@ -1277,12 +1277,12 @@ static void launch_gemm(const TcGemmParams& p, unsigned grid, cudaStream_t strea
   const bool want_trace = getenv("SYNO_TC_TRACE") != nullptr;
   if (want_trace && !trace_buf) cuda_check(cudaMalloc(&trace_buf, 64 * sizeof(unsigned long long)), "trace");
   if (!want_trace) {
-    launch_k(tc_gemm_kernel<BN, MODE>, grid, THREADS, smem, stream, p);
+    launch_k(tc_gemm_kernel<BN, MODE, CFG>, grid, THREADS, smem, stream, p);
   } else {
     TcGemmParams q = p;
     q.trace = trace_buf;
     cuda_check(cudaMemsetAsync(trace_buf, 0, 64 * sizeof(unsigned long long), stream), "trace memset");
-    launch_k(tc_gemm_kernel<BN, MODE>, grid, THREADS, smem, stream, q);
+    launch_k(tc_gemm_kernel<BN, MODE, CFG>, grid, THREADS, smem, stream, q);
     unsigned long long h[64];
     cuda_check(cudaMemcpyAsync(h, trace_buf, sizeof(h), cudaMemcpyDeviceToHost, stream), "trace copy");
     cuda_check(cudaStreamSynchronize(stream), "trace sync");
@@ -1318,20 +1318,28 @@ static void gemm(TcGemmParams& p, int bn, int m_tiles, int n_tiles, int z_tiles,
   p.m_tiles = m_tiles;
   p.n_tiles = n_tiles;
   p.z_tiles = z_tiles;
-  const int a_region = bn == 64 ? a_region_bytes<64>() : bn == 128 ? a_region_bytes<128>() : a_region_bytes<256>();
+  const bool small = p.cfg == 1 && bn <= 128;
+  const int a_region = small ? (bn == 64 ? a_region_bytes<64, 1>() : a_region_bytes<128, 1>())
+                             : (bn == 64 ? a_region_bytes<64>() : bn == 128 ? a_region_bytes<128>() : a_region_bytes<256>());
   p.a_stages = std::max(1, std::min(8, a_region / p.a_stage_bytes));
   const int64_t tiles = (int64_t)m_tiles * n_tiles * z_tiles;
   if (tiles <= 0) return;
-  const unsigned grid = (unsigned)std::min<int64_t>(tiles, sm_count());
+  const unsigned grid = (unsigned)std::min<int64_t>(tiles, (int64_t)sm_count() * (small ? 2 : 1));
   const int id = prof_begin(name, flops, 0.0, stream);
   if (p.mode == MODE_ROWS) {
-    if (bn == 64) launch_gemm<64, MODE_ROWS>(p, grid, stream);
-    else if (bn == 128) launch_gemm<128, MODE_ROWS>(p, grid, stream);
-    else launch_gemm<256, MODE_ROWS>(p, grid, stream);
+    if (small) {
+      if (bn == 64) launch_gemm<64, MODE_ROWS, 1>(p, grid, stream);
+      else launch_gemm<128, MODE_ROWS, 1>(p, grid, stream);
+    } else if (bn == 64) launch_gemm<64, MODE_ROWS, 0>(p, grid, stream);
+    else if (bn == 128) launch_gemm<128, MODE_ROWS, 0>(p, grid, stream);
+    else launch_gemm<256, MODE_ROWS, 0>(p, grid, stream);
   } else {
-    if (bn == 64) launch_gemm<64, MODE_WGRAD>(p, grid, stream);
-    else if (bn == 128) launch_gemm<128, MODE_WGRAD>(p, grid, stream);
-    else launch_gemm<256, MODE_WGRAD>(p, grid, stream);
+    if (small) {
+      if (bn == 64) launch_gemm<64, MODE_WGRAD, 1>(p, grid, stream);
+      else launch_gemm<128, MODE_WGRAD, 1>(p, grid, stream);
+    } else if (bn == 64) launch_gemm<64, MODE_WGRAD, 0>(p, grid, stream);
+    else if (bn == 128) launch_gemm<128, MODE_WGRAD, 0>(p, grid, stream);
+    else launch_gemm<256, MODE_WGRAD, 0>(p, grid, stream);
   }
   prof_end(id, stream);
 }
@@ -1346,21 +1354,29 @@ struct RowsTiling {
   int64_t m_tiles;
 };
 
+// Two-CTA-per-SM configuration for BN <= 128 (SYNO_TC_SMALL=0 disables).
+static bool use_small_cfg(int bn) {
+  static const bool on = !(getenv("SYNO_TC_SMALL") && atoi(getenv("SYNO_TC_SMALL")) == 0);
+  return on && bn <= 128;
+}
+
 static RowsTiling rows_tiling(int64_t F, int n_tiles, int groups, int bn, int n_cblocks, int nwin) {
   // Cost model (measured on B200, profiles/r01_gemm_trace_dbg.txt): a
   // 128 x BN x 16 MMA from shared memory takes ~80 cycles for BN <= 128 and
   // ~160 for BN = 256; the epilogue of a 128-row sub-tile costs about as
   // much as 16 such MMAs (more with split-K atomics).  A CTA's time is the
   // number of waves times one tile; pick the (G, split) with the least.
-  const int sms = sm_count();
+  const bool small = use_small_cfg(bn);
+  const int sms = sm_count() * (small ? 2 : 1);
+  const int gm = small ? 1 : mgroup_of(bn);
   auto mt = [&](int g) { return (F + (int64_t)g * BM - 1) / ((int64_t)g * BM); };
   const double mma = bn >= 256 ? 2.0 : 1.0;
   const bool no_split = getenv("SYNO_TC_NO_RSPLIT") != nullptr;
-  RowsTiling best{mgroup_of(bn), 1, mt(mgroup_of(bn))};
+  RowsTiling best{gm, 1, mt(gm)};
   double best_cost = 1e300;
   static const int force_g = getenv("SYNO_TC_G") ? atoi(getenv("SYNO_TC_G")) : 0;  // experiments
-  for (int G = mgroup_of(bn); G >= 1; G /= 2) {
-    if (force_g && G != force_g && force_g <= mgroup_of(bn)) continue;
+  for (int G = gm; G >= 1; G /= 2) {
+    if (force_g && G != force_g && force_g <= gm) continue;
     for (int rs = 1; rs <= (no_split ? 1 : n_cblocks); ++rs) {
       const int per = (n_cblocks + rs - 1) / rs;
       if (rs > 1 && (n_cblocks + per - 1) / per != rs) continue;  // an empty split: same as fewer splits
@@ -1674,6 +1690,7 @@ static void build_ws(TcPlan& tp, TcWs& w, DType dt) {
         groups[0].push_back({tp.dh.delta(rh) * w.gx.Wp + tp.dw.delta(rw), tp.dh.phi(rh) * w.gx.Sw + tp.dw.phi(rw),
                              rh * tp.dw.K + rw});
     const RowsTiling rt = rows_tiling(F, (tp.N + bn - 1) / bn, 1, bn, p.n_cblocks, tp.nwin());
+    p.cfg = use_small_cfg(bn) ? 1 : 0;
     rows_schedule(p, groups, bn, rt.G);
     p.rsplit = rt.rs;
     w.ms_fwd_a = map_spec(Ck, F, planes, Ck, F * Ck, 64);
@@ -1744,6 +1761,7 @@ static void build_ws(TcPlan& tp, TcWs& w, DType dt) {
         p.g_out_off[grp] = ph * tp.dh.xs + pw * tp.dw.xs;
       }
     const RowsTiling rt = rows_tiling(Fg, (tp.C + bn - 1) / bn, Sh * Sw, bn, p.n_cblocks, tp.nwin() / (Sh * Sw));
+    p.cfg = use_small_cfg(bn) ? 1 : 0;
     rows_schedule(p, groups, bn, rt.G);
     p.rsplit = rt.rs;
     w.ms_dg_a = map_spec(Nk, Fg, 1, Nk, Fg * Nk, 64);
@@ -1799,7 +1817,8 @@ static void build_ws(TcPlan& tp, TcWs& w, DType dt) {
       }
     const int m_tiles = (p.n_pairs + 1) / 2, n_tiles = (tp.N + bn - 1) / bn;
     static const int waves = getenv("SYNO_TC_WG_WAVES") ? atoi(getenv("SYNO_TC_WG_WAVES")) : 1;
-    int ksplit = std::max(1, (waves * sm_count()) / std::max(1, m_tiles * n_tiles));
+    p.cfg = use_small_cfg(bn) ? 1 : 0;
+    int ksplit = std::max(1, (waves * sm_count() * (p.cfg ? 2 : 1)) / std::max(1, m_tiles * n_tiles));
     ksplit = std::min(ksplit, std::max(1, p.n_cblocks / 4));
     p.ksplit = ksplit;
     p.m_ext = tp.C;

@@ -42,13 +42,25 @@ template <int BN>
 __host__ __device__ constexpr int mgroup() {
   return BN >= 256 ? 1 : 256 / BN;
 }
-template <int BN>
-__host__ __device__ constexpr int b_stages() {
-  return 4;
+// CFG 0: one CTA per SM (192 KB ring, 512 TMEM columns, G up to mgroup).
+// CFG 1: two CTAs per SM (96 KB ring, <= 256 TMEM columns, G = 1): the
+// second CTA hides the first one's fixed costs (setup, first loads,
+// epilogue tail) and the next kernel's CTAs can start beside a tail CTA.
+template <int CFG>
+__host__ __device__ constexpr int ring_bytes() {
+  return CFG ? 96 * 1024 : RING_BYTES;
 }
-template <int BN>
+template <int BN, int CFG>
+__host__ __device__ constexpr int gmax() {
+  return CFG ? 1 : mgroup<BN>();
+}
+template <int BN, int CFG = 0>
+__host__ __device__ constexpr int b_stages() {
+  return CFG && BN >= 128 ? 2 : 4;
+}
+template <int BN, int CFG = 0>
 __host__ __device__ constexpr int a_region_bytes() {
-  return RING_BYTES - b_stages<BN>() * BN * BK * 2;
+  return ring_bytes<CFG>() - b_stages<BN, CFG>() * BN * BK * 2;
 }
 
 enum Mode : int32_t {
@@ -72,7 +84,8 @@ struct alignas(64) TcGemmParams {
   int32_t n_win;
   int32_t ksplit;      // MODE_WGRAD split of the pixel blocks
   int32_t rsplit;      // MODE_ROWS split of the channel blocks (>1: fp32 atomic output)
-  int32_t G;           // MODE_ROWS M tiles per step (<= mgroup<BN>(); fewer for small problems)
+  int32_t G;           // MODE_ROWS M tiles per step (<= gmax<BN, CFG>(); fewer for small problems)
+  int32_t cfg;         // host-side: kernel configuration (CFG template argument) to launch
   int32_t a_shift[MAXWIN];   // MODE_ROWS: row shift of A per window; MODE_WGRAD: B row (pixel) shift
   int32_t a_plane[MAXWIN];   // MODE_WGRAD: plane (phase) of x per window
   int32_t b_plane[MAXWIN];   // MODE_ROWS: B plane (packed weight window) per window
@@ -298,19 +311,19 @@ struct Ring {
   __device__ __forceinline__ uint32_t phase(int n) const { return (i / (uint32_t)n) & 1u; }
 };
 
-template <int BN, int MODE>
-__global__ void __launch_bounds__(THREADS, 1) tc_gemm_kernel(const __grid_constant__ TcGemmParams p) {
+template <int BN, int MODE, int CFG>
+__global__ void __launch_bounds__(THREADS, CFG ? 2 : 1) tc_gemm_kernel(const __grid_constant__ TcGemmParams p) {
   pdl_trigger();
-  constexpr int BSTAGES = b_stages<BN>();
+  constexpr int BSTAGES = b_stages<BN, CFG>();
   constexpr int B_BYTES = BN * BK * 2;
-  constexpr int G = mgroup<BN>();
+  constexpr int G = gmax<BN, CFG>();
   constexpr uint32_t ACC_COLS = G * BN;          // one accumulator buffer: G sub-tiles
-  constexpr uint32_t TMEM_COLS = 2 * ACC_COLS;   // double-buffered (= 512)
+  constexpr uint32_t TMEM_COLS = 2 * ACC_COLS;   // double-buffered (512 for CFG 0)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sa = smem;
-  uint8_t* sb = smem + a_region_bytes<BN>();
-  uint64_t* a_full = reinterpret_cast<uint64_t*>(smem + RING_BYTES);
+  uint8_t* sb = smem + a_region_bytes<BN, CFG>();
+  uint64_t* a_full = reinterpret_cast<uint64_t*>(smem + ring_bytes<CFG>());
   uint64_t* a_empty = a_full + 8;
   uint64_t* b_full = a_empty + 8;
   uint64_t* b_empty = b_full + BSTAGES;
@@ -666,9 +679,9 @@ __global__ void __launch_bounds__(THREADS, 1) tc_gemm_kernel(const __grid_consta
   }
 }
 
-template <int BN>
+template <int BN, int CFG = 0>
 constexpr int smem_bytes() {
-  return 1024 + RING_BYTES + 512;
+  return 1024 + ring_bytes<CFG>() + 512;
 }
 
 }  // namespace tc
