@@ -1422,7 +1422,13 @@ static void cast_to_bf16(float* in, void* out, int64_t n, cudaStream_t stream) {
   prof_end(id, stream);
 }
 
-static int pick_bn(int n) { return n <= 64 ? 64 : n <= 128 ? 128 : 256; }
+static int pick_bn(int n) {
+  // BN = 128 costs the same cycles per 128x128x16 as BN = 256 does per half of
+  // its tile (shared-memory bound), and it allows two CTAs per SM
+  static const int cap = getenv("SYNO_TC_MAXBN") ? atoi(getenv("SYNO_TC_MAXBN")) : 256;
+  const int bn = n <= 64 ? 64 : n <= 128 ? 128 : 256;
+  return std::min(bn, std::max(64, cap));
+}
 
 template <typename TI, int V>
 static void launch_pack_rows(const void* src, const PackGeom& g, __nv_bfloat16* dst, dim3 grid, int rpb,
