@@ -815,6 +815,16 @@ struct ChainNC {
   int32_t oh, ow;                  // rh / rw is an output loop
   int32_t sw[MAXFW][4];            // other weights' strides (0 for the differentiated one)
   int32_t dense;                   // dW_j is [n][ci][window outputs] dense: stage the block's outputs in smem
+  // Side output: a second weight j2 that uses only window loops (sep_shared's
+  // shared [K] weight) takes its gradient from the same pass over dWf:
+  // dW_j2[win] = sum_{n, ci} dWf * prod_{q != j2} w_q, reduced per block into
+  // `partial` and combined in block order by the last block (deterministic).
+  int32_t side_j;                  // -1: none
+  int32_t side_sw[MAXFW][4];       // strides of every weight except j2 (0 for j2)
+  int32_t side_oh, side_ow, side_so_h, side_so_w;
+  void* side_out;
+  float* partial;                  // [gridDim.x][KK]
+  unsigned* counter;               // zero between calls
 };
 
 __global__ void __launch_bounds__(256) chain_nc_kernel(const __grid_constant__ ChainArgs c, const __grid_constant__ ChainNC h) {
@@ -842,14 +852,15 @@ __global__ void __launch_bounds__(256) chain_nc_kernel(const __grid_constant__ C
       for (int k = 0; k < 16; ++k)
         if (k < KK) src[k * plane] = 0.f;
     }
-    float* vs = stage + blockDim.x * KKo + threadIdx.x * 16;  // per-thread window values
+    float* vs = stage + blockDim.x * KKo + threadIdx.x * 17;  // per-thread window values (odd stride)
 #pragma unroll
     for (int k = 0; k < 16; ++k)
       if (k < KK) vs[k] = v[k];
 #pragma unroll 1
     for (int k = 0; k < KK; ++k) {
       const int kh = k / h.Kw, kw = k - kh * h.Kw;
-      float x = vs[k];
+      const float d = vs[k];
+      float x = d;
 #pragma unroll 1
       for (int q = 0; q < c.nw; ++q) {
         if (q == c.j) continue;
@@ -859,6 +870,72 @@ __global__ void __launch_bounds__(256) chain_nc_kernel(const __grid_constant__ C
       }
       // windows the weight does not use fold onto the same output
       my[(h.oh ? kh : 0) * KKo_w + (h.ow ? kw : 0)] += x;
+      if (h.side_j >= 0) {
+        float z = d;
+#pragma unroll 1
+        for (int q = 0; q < c.nw; ++q) {
+          if (q == h.side_j) continue;
+          const int32_t off = kh * h.side_sw[q][0] + kw * h.side_sw[q][1] + n * h.side_sw[q][2] + ci * h.side_sw[q][3];
+          z *= c.f32 ? __ldg(reinterpret_cast<const float*>(c.w[q]) + off)
+                     : __bfloat162float(__ldg(reinterpret_cast<const __nv_bfloat16*>(c.w[q]) + off));
+        }
+        vs[k] = z;
+      }
+    }
+  } else if (h.side_j >= 0) {
+    float* vs = stage + blockDim.x * KKo + threadIdx.x * 17;
+    for (int k = 0; k < KK; ++k) vs[k] = 0.f;
+  }
+  if (h.side_j >= 0) {
+    // block sums of the side products per window, then the last block combines
+    __syncthreads();
+    const float* vall = stage + blockDim.x * KKo;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    __shared__ float wsum[8][16];
+    for (int k = 0; k < KK; ++k) {
+      float t = 0.f;
+      t = vall[(warp * 32 + lane) * 17 + k];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+      if (lane == 0) wsum[warp][k] = t;
+    }
+    __syncthreads();
+    __shared__ bool last;
+    if (threadIdx.x < KK) {
+      float t = 0.f;
+      for (int q = 0; q < (int)(blockDim.x >> 5); ++q) t += wsum[q][threadIdx.x];
+      h.partial[(size_t)blockIdx.x * KK + threadIdx.x] = t;
+      __threadfence();
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) last = atomicAdd(h.counter, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (last) {
+      __threadfence();
+      __shared__ float tot[16];
+      if (threadIdx.x < KK) {
+        float t = 0.f;
+        for (unsigned b = 0; b < gridDim.x; ++b) t += *((volatile float*)h.partial + (size_t)b * KK + threadIdx.x);
+        tot[threadIdx.x] = t;
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        const int ow2 = h.side_ow ? h.Kw : 1;
+        const int no = (h.side_oh ? h.Kh : 1) * ow2;
+        float acc[16];
+        for (int q = 0; q < no; ++q) acc[q] = 0.f;
+        for (int k = 0; k < KK; ++k) {
+          const int kh = k / h.Kw, kw = k - kh * h.Kw;
+          acc[(h.side_oh ? kh : 0) * ow2 + (h.side_ow ? kw : 0)] += tot[k];
+        }
+        for (int q = 0; q < no; ++q) {
+          const int ah = q / ow2, aw = q - ah * ow2;
+          const int64_t o = (int64_t)ah * h.side_so_h + (int64_t)aw * h.side_so_w;
+          if (c.f32) reinterpret_cast<float*>(h.side_out)[o] = acc[q];
+          else reinterpret_cast<__nv_bfloat16*>(h.side_out)[o] = __float2bfloat16(acc[q]);
+        }
+        *h.counter = 0;  // ready for the next call (stream order)
+      }
     }
   }
   if (!h.dense) {
@@ -1882,6 +1959,9 @@ static void build_ws(TcPlan& tp, TcWs& w, DType dt) {
         outs = std::max(outs, oc);
       }
     }
+    // fused side chains (chain_side_ok): one partial per (block, window)
+    need = std::max(need, ((int64_t)tp.N * tp.C + 255) / 256 * 16);
+    outs = std::max<int64_t>(outs, 1);
     if (need) {
       w.chain_partial = ws_alloc<float>(w, (size_t)need);
       w.chain_counter = ws_alloc<unsigned>(w, (size_t)outs);
@@ -2023,8 +2103,15 @@ static bool fold_dual(const TcPlan& tp, const Bindings& b, DType dt, bool split,
   return true;
 }
 
+// Whether weight j2's gradient can ride along j's chain_nc pass (side output).
+static bool chain_side_ok(const TcPlan& tp, int j, int j2) {
+  if (j2 == j || tp.dh.K * tp.dw.K > 16) return false;
+  if (!(tp.wstr[j][2] != 0 && tp.wstr[j][3] != 0)) return false;
+  return tp.wstr[j2][2] == 0 && tp.wstr[j2][3] == 0;
+}
+
 static void chain_fast(const TcPlan& tp, const TcWs& w, const Bindings& b, DType dt, int j, bool zero_dwf,
-                       cudaStream_t stream) {
+                       cudaStream_t stream, int side = -1) {
   if (skip_class("chain")) return;
   ChainArgs c{};
   c.dwf = w.dwf;
@@ -2077,7 +2164,20 @@ static void chain_fast(const TcPlan& tp, const TcWs& w, const Bindings& b, DType
                                                 (h.Kw == 1 && h.so_h == 1)
                            : h.oh ? (h.Kh == 1 || h.so_h == 1) : h.ow ? (h.Kw == 1 || h.so_w == 1) : true;
     h.dense = win_dense && h.so_c == kko && h.so_n == h.C * kko;
-    const size_t sm = (size_t)256 * (kko + 16) * sizeof(float);
+    h.side_j = -1;
+    if (side >= 0) {
+      h.side_j = side;
+      for (int k = 0; k < tp.nw; ++k)
+        for (int l = 0; l < 4; ++l) h.side_sw[k][l] = k == side ? 0 : (int32_t)tp.wstr[k][l];
+      h.side_oh = tp.wstr[side][0] != 0 || h.Kh == 1;
+      h.side_ow = tp.wstr[side][1] != 0 || h.Kw == 1;
+      h.side_so_h = (int32_t)tp.wstr[side][0];
+      h.side_so_w = (int32_t)tp.wstr[side][1];
+      h.side_out = b.dw.at(side);
+      h.partial = w.chain_partial;
+      h.counter = w.chain_counter;
+    }
+    const size_t sm = (size_t)256 * (kko + 17) * sizeof(float);
     launch_k(chain_nc_kernel, (unsigned)((nthreads + 255) / 256), 256, sm, stream, c, h);
     cuda_check(cudaGetLastError(), "chain kernel");
     prof_end(id, stream);
@@ -2268,14 +2368,24 @@ bool tc_backward(TcPlan& tp, DType dt, const Bindings& b, cudaStream_t stream) {
     // chain rule through the fold, into each requested weight gradient
     Bindings cb = b;
     cb.stages = {w.dwf};
-    int last = -1;
-    for (size_t j = 0; j < tp.chain.size(); ++j)
-      if (j < b.dw.size() && b.dw[j]) last = (int)j;
     if (!fixup) {
+      static const bool fuse_side = getenv("SYNO_TC_NO_SIDE_CHAIN") == nullptr;
+      std::vector<int> done(tp.chain.size(), 0);
       for (size_t j = 0; j < tp.chain.size(); ++j) {
-        if (j >= b.dw.size() || !b.dw[j]) continue;
-        if (tp.fast_fold) chain_fast(tp, w, b, dt, (int)j, (int)j == last && !memset_dwf, stream);
-        else run_stage(dt, tp.chain[j], cb, b.dw[j], false, stream);
+        if (j >= b.dw.size() || !b.dw[j] || done[j]) continue;
+        if (!tp.fast_fold) {
+          run_stage(dt, tp.chain[j], cb, b.dw[j], false, stream);
+          continue;
+        }
+        int side = -1;
+        for (size_t j2 = 0; fuse_side && side < 0 && j2 < tp.chain.size(); ++j2)
+          if (j2 < b.dw.size() && b.dw[j2] && !done[j2] && chain_side_ok(tp, (int)j, (int)j2)) side = (int)j2;
+        done[j] = 1;
+        if (side >= 0) done[side] = 1;
+        bool zero = true;  // the last pass over dWf leaves it zeroed
+        for (size_t j2 = 0; j2 < tp.chain.size(); ++j2)
+          if (j2 < b.dw.size() && b.dw[j2] && !done[j2]) zero = false;
+        chain_fast(tp, w, b, dt, (int)j, zero && !memset_dwf, stream, side);
       }
     }
   }

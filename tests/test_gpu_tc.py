@@ -126,3 +126,35 @@ def test_backward_reuse_flags_match(cuda, op, c_in, c_out, h, batch, dtype):
     assert _rel(dx1, dx0) < 1e-6
     for a, b in zip(dw0, dw1):
         assert _rel(a, b) < 1e-6
+
+
+@pytest.mark.parametrize("want", [(True, True), (True, False), (False, True)], ids=["both", "w0", "w1"])
+@pytest.mark.parametrize("dtype", ["bfloat16", "float32"])
+def test_sep_shared_weight_gradient_subsets(cuda, want, dtype):
+    """sep_shared's [K] weight takes its gradient from the main weight's chain
+    pass (side output, block partials combined by the last block); any subset
+    of weight gradients, called repeatedly (dWf and the block counter are left
+    zeroed for the next call), matches autograd."""
+    import torch
+    from paper_2410_23745_b200 import ops
+    from paper_2410_23745_b200 import pgraph as P
+    dt = getattr(torch, dtype)
+    L = _layer("sep_shared", 128, 128, 16, 2)
+    hd = P.handle_for(L.graph)
+    g = torch.Generator(device="cpu").manual_seed(6)
+    x = torch.randn(hd.x_shape, generator=g).to("cuda", dt)
+    ws = [(torch.randn(s, generator=g) * 0.2).to("cuda", dt) for s in hd.w_shapes]
+    xf = x.float().requires_grad_(True)
+    wf = [w.float().requires_grad_(True) for w in ws]
+    yr = _torch_ref("sep_shared", xf, wf, 128, 128)
+    for it in range(3):
+        dy = torch.randn(hd.y_shape, generator=g).to("cuda", dt)
+        _, dws = ops.backward(hd, x, ws, dy, want_dx=False, want_dw=list(want))
+        torch.cuda.synchronize()
+        refs = torch.autograd.grad(yr, wf, dy.float(), retain_graph=True)
+        tol = 2e-2 if dtype == "bfloat16" else 1e-4
+        for j in range(2):
+            if want[j]:
+                assert _rel(dws[j], refs[j]) < tol, (it, j)
+            else:
+                assert dws[j] is None
