@@ -484,7 +484,20 @@ __global__ void __launch_bounds__(THREADS, CFG ? 2 : 1) tc_gemm_kernel(const __g
               const uint64_t db = sw128_desc(sb + bs * B_BYTES);
               // profiling switch 32: every window reads the aligned halo start (wrong values, timing only)
               const uint32_t arow = abase + ((p.dbg & 32) ? 0u : (uint32_t)(p.a_shift[w] - p.chunk_pmin[c]) * 128u);
-              if (!(p.dbg & 2)) {
+              if (G > 1 && (p.dbg & 128)) {
+                // profiling switch 128: k outer, tiles inner (independent accumulators back to back)
+#pragma unroll
+                for (int k = 0; k < BK / 16; ++k) {
+#pragma unroll
+                  for (int g = 0; g < G; ++g) {
+                    if (g >= p.G) break;
+                    const uint64_t da = (((uint64_t)((arow + g * BM * 128u) >> 4)) & 0x3FFF) | (1ull << 16) |
+                                        ((uint64_t)(1024 >> 4) << 32) | (1ull << 46) | (2ull << 61);
+                    mma_bf16(dst + g * BN, da + (uint64_t)(k * 2), db + (uint64_t)(k * 2), idesc,
+                             (accumulate || k > 0) ? 1u : 0u);
+                  }
+                }
+              } else if (!(p.dbg & 2)) {
 #pragma unroll
                 for (int g = 0; g < G; ++g) {
                   if (g >= p.G) break;
