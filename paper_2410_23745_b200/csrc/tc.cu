@@ -1542,8 +1542,20 @@ static double pack_bytes(DType dt, const PackGeom& g) {
   return src_elems * (dt == DT_BF16 ? 2 : 4) + src_elems * (g.split == SPLIT_CH ? 3 : 1) * 2;
 }
 
+static bool tc_log() {
+  static const bool on = getenv("SYNO_TC_LOG") != nullptr;
+  return on;
+}
+
+static void log_pack(const char* what, const void* src, const PackGeom& g) {
+  if (tc_log())
+    fprintf(stderr, "[tc] %s src=%p C=%d in=%dx%d S=%dx%d lo=%d,%d grid=%dx%d split=%d imgs=%d\n", what, src, g.C, g.Hin,
+            g.Win, g.Sh, g.Sw, g.lo_h, g.lo_w, g.Hp, g.Wp, g.split, g.n_img);
+}
+
 static void pack_cl(const void* src, DType dt, const PackGeom& g, __nv_bfloat16* dst, cudaStream_t stream) {
   if (skip_class("pack")) return;
+  log_pack("pack", src, g);
   // one block = whole source rows (<= PK_PIX pixels) or one PK_PIX segment of a wider row
   const int rpb = std::max(1, PK_PIX / g.Win);
   const int64_t rows = (int64_t)g.n_img_out() * g.Hin;
@@ -1939,6 +1951,13 @@ static void build_ws(TcPlan& tp, TcWs& w, DType dt) {
     }
   }
 
+  if (tc_log()) {
+    log_pack("ws x", nullptr, w.gx);
+    log_pack("ws xw", nullptr, w.gxw);
+    log_pack("ws dy_g", nullptr, w.gdy_g);
+    log_pack("ws dy_w", nullptr, w.gdy_w);
+    fprintf(stderr, "[tc] ws share_x=%d share_dy=%d\n", (int)w.share_x, (int)w.share_dy);
+  }
   w.x_ident = pack_identity(w.gx, dt);
   w.xw_ident = pack_identity(w.gxw, dt);
   w.dyg_ident = tp.dgrad_ok && pack_identity(w.gdy_g, dt);
@@ -2009,6 +2028,7 @@ static bool pack_and_fold(const TcPlan& tp, const Bindings& b, DType dt, const v
   if (!tp.fast_fold || KK <= 1 || KK > 16 || getenv("SYNO_TC_NO_PREP_FUSE")) return false;
   if (skip_class("pack") || skip_class("fold")) return false;
   const PackPlan pp = pack_plan(src, dt, g);
+  log_pack(dgrad ? "prep(dgrad)" : "prep(fwd)", src, g);
   const FoldArgs f = fold_args(tp, b, dt, dgrad, split, folded);
   const double fold_elems = (double)KK * f.ext[2] * f.Bp;
   const int id = prof_begin("pack_cl", 0.0, pack_bytes(dt, g) + fold_elems * (split ? 6 : 2), stream);

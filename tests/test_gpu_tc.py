@@ -144,14 +144,15 @@ def test_sep_shared_weight_gradient_subsets(cuda, want, dtype):
     g = torch.Generator(device="cpu").manual_seed(6)
     x = torch.randn(hd.x_shape, generator=g).to("cuda", dt)
     ws = [(torch.randn(s, generator=g) * 0.2).to("cuda", dt) for s in hd.w_shapes]
-    xf = x.float().requires_grad_(True)
-    wf = [w.float().requires_grad_(True) for w in ws]
+    # float64 reference (a float32 torch conv may run in TF32)
+    xf = x.double().requires_grad_(True)
+    wf = [w.double().requires_grad_(True) for w in ws]
     yr = _torch_ref("sep_shared", xf, wf, 128, 128)
     for it in range(3):
         dy = torch.randn(hd.y_shape, generator=g).to("cuda", dt)
         _, dws = ops.backward(hd, x, ws, dy, want_dx=False, want_dw=list(want))
         torch.cuda.synchronize()
-        refs = torch.autograd.grad(yr, wf, dy.float(), retain_graph=True)
+        refs = torch.autograd.grad(yr, wf, dy.double(), retain_graph=True)
         tol = 2e-2 if dtype == "bfloat16" else 1e-4
         for j in range(2):
             if want[j]:
