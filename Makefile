@@ -2,6 +2,10 @@
 NVCC ?= /usr/local/cuda/bin/nvcc
 ARCH := -gencode arch=compute_100a,code=sm_100a
 CXXFLAGS := -O3 -std=c++17 -Xcompiler -fPIC -Xcompiler -Wall -lineinfo
+# `make TRACE=1` (after touching csrc/tc.cu) compiles the GEMM event log in (SYNO_TC_TRACE=<file>)
+ifdef TRACE
+CXXFLAGS += -DSYNO_TC_TRACE_EVENTS
+endif
 PKG := paper_2410_23745_b200
 SRC := $(PKG)/csrc
 OBJ := build/obj

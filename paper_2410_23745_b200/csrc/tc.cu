@@ -1350,33 +1350,32 @@ static void launch_gemm(const TcGemmParams& p, unsigned grid, cudaStream_t strea
     configured.fetch_or(bit);
   }
   note_launch();
+  // SYNO_TC_TRACE=<file>: append the SM-0 event log of every launch to <file>
+  static const char* trace_path = getenv("SYNO_TC_TRACE");
   static unsigned long long* trace_buf = nullptr;
-  const bool want_trace = getenv("SYNO_TC_TRACE") != nullptr;
-  if (want_trace && !trace_buf) cuda_check(cudaMalloc(&trace_buf, 64 * sizeof(unsigned long long)), "trace");
-  if (!want_trace) {
+  if (trace_path && !trace_buf) cuda_check(cudaMalloc(&trace_buf, 8192 * sizeof(unsigned long long)), "trace");
+  if (!trace_path) {
     launch_k(tc_gemm_kernel<BN, MODE, CFG>, grid, THREADS, smem, stream, p);
   } else {
     TcGemmParams q = p;
     q.trace = trace_buf;
-    cuda_check(cudaMemsetAsync(trace_buf, 0, 64 * sizeof(unsigned long long), stream), "trace memset");
+    cuda_check(cudaMemsetAsync(trace_buf, 0, 8192 * sizeof(unsigned long long), stream), "trace memset");
     launch_k(tc_gemm_kernel<BN, MODE, CFG>, grid, THREADS, smem, stream, q);
-    unsigned long long h[64];
-    cuda_check(cudaMemcpyAsync(h, trace_buf, sizeof(h), cudaMemcpyDeviceToHost, stream), "trace copy");
+    std::vector<unsigned long long> h(8192);
+    cuda_check(cudaMemcpyAsync(h.data(), trace_buf, 8192 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, stream),
+               "trace copy");
     cuda_check(cudaStreamSynchronize(stream), "trace sync");
-    fprintf(stderr, "[tc trace BN=%d mode=%d tiles=%d grid=%u] setup %.2f us |", BN, p.mode,
-            p.m_tiles * p.n_tiles * p.z_tiles, grid, (h[1] - h[0]) / 1e3);
-    for (int i = 0; i < 14 && h[2 + i * 4]; ++i)
-      fprintf(stderr, " t%d: prod %.2f mma %.2f epi %.2f-%.2f |", i, (h[2 + i * 4] - h[0]) / 1e3,
-              h[3 + i * 4] ? (h[3 + i * 4] - h[0]) / 1e3 : -1.0, h[4 + i * 4] ? (h[4 + i * 4] - h[0]) / 1e3 : -1.0,
-              h[5 + i * 4] ? (h[5 + i * 4] - h[0]) / 1e3 : -1.0);
-    fprintf(stderr, "\n   tile0 windows: b_full seen at");
-    for (int i = 40; i < 49; ++i) fprintf(stderr, " %.2f", h[i] ? (h[i] - h[0]) / 1e3 : -1.0);
-    fprintf(stderr, "\n   tile0 windows: b_empty free at");
-    for (int i = 50; i < 59; ++i) fprintf(stderr, " %.2f", h[i] ? (h[i] - h[0]) / 1e3 : -1.0);
-    fprintf(stderr, "\n   tile1 windows 1-4 cycles (wait, issue, commit):");
-    for (int i = 59; i < 63; ++i)
-      fprintf(stderr, " (%llu, %llu, %llu)", h[i] & 0xFFFFF, (h[i] >> 20) & 0xFFFFF, (h[i] >> 40) & 0xFFFFF);
-    fprintf(stderr, "\n");
+    if (FILE* f = fopen(trace_path, "a")) {
+      fprintf(f, "launch BN=%d mode=%d cfg=%d tiles=%d grid=%u G=%d\n", BN, p.mode, CFG, p.m_tiles * p.n_tiles * p.z_tiles,
+              grid, p.G);
+      const unsigned long long nc = std::min<unsigned long long>(h[0], 7);
+      for (unsigned long long c = 0; c < nc; ++c)
+        for (int i = 0; i < 512; ++i) {
+          const unsigned long long t = h[64 + c * 1024 + 2 * i], v = h[64 + c * 1024 + 2 * i + 1];
+          if (t) fprintf(f, "%llu %llu %llu %llu %llu\n", t, v & 0xFF, (v >> 8) & 0xFFFF, (v >> 24) & 0xFFFF, v >> 40);
+        }
+      fclose(f);
+    }
   }
   cuda_check(cudaGetLastError(), "tc_gemm_kernel");
 }
@@ -1398,7 +1397,9 @@ static void gemm(TcGemmParams& p, int bn, int m_tiles, int n_tiles, int z_tiles,
   const bool small = p.cfg == 1 && bn <= 128;
   const int a_region = small ? (bn == 64 ? a_region_bytes<64, 1>() : a_region_bytes<128, 1>())
                              : (bn == 64 ? a_region_bytes<64>() : bn == 128 ? a_region_bytes<128>() : a_region_bytes<256>());
-  p.a_stages = std::max(1, std::min(8, a_region / p.a_stage_bytes));
+  const int ring = small ? ring_bytes<1>() : ring_bytes<0>();
+  p.a_stages = std::max(1, std::min(8, (p.mode == MODE_ROWS && p.b_res ? ring - p.b_res * bn * BK * 2 : a_region) /
+                                           p.a_stage_bytes));
   const int64_t tiles = (int64_t)m_tiles * n_tiles * z_tiles;
   if (tiles <= 0) return;
   const unsigned grid = (unsigned)std::min<int64_t>(tiles, (int64_t)sm_count() * (small ? 2 : 1));
@@ -1435,6 +1436,16 @@ struct RowsTiling {
 static bool use_small_cfg(int bn) {
   static const bool on = !(getenv("SYNO_TC_SMALL") && atoi(getenv("SYNO_TC_SMALL")) == 0);
   return on && bn <= 128;
+}
+
+// Resident B (TcGemmParams::b_res) when the whole weight operand of the
+// launch (one N tile, one channel block) fits beside one A stage.
+static void set_b_res(TcGemmParams& p, int bn, int n_tiles) {
+  static const bool off = getenv("SYNO_TC_NO_BRES") != nullptr;
+  p.b_res = 0;
+  if (off || n_tiles != 1 || p.n_cblocks != 1 || p.rsplit > 1) return;
+  const int ring = (p.cfg == 1 && bn <= 128) ? ring_bytes<1>() : ring_bytes<0>();
+  if (p.n_win * bn * BK * 2 + p.a_stage_bytes <= ring) p.b_res = p.n_win;
 }
 
 static RowsTiling rows_tiling(int64_t F, int n_tiles, int groups, int bn, int n_cblocks, int nwin) {
@@ -1788,6 +1799,7 @@ static void build_ws(TcPlan& tp, TcWs& w, DType dt) {
     p.cfg = use_small_cfg(bn) ? 1 : 0;
     rows_schedule(p, groups, bn, rt.G);
     p.rsplit = rt.rs;
+    set_b_res(p, bn, (tp.N + bn - 1) / bn);
     w.ms_fwd_a = map_spec(Ck, F, planes, Ck, F * Ck, 64);
     p.tma_a = make_map(w.xcl, w.ms_fwd_a);
     p.tma_b = make_map(w.wf, Ck, tp.N, tp.nwin(), Ck, (int64_t)tp.N * Ck, bn);
@@ -1859,6 +1871,7 @@ static void build_ws(TcPlan& tp, TcWs& w, DType dt) {
     p.cfg = use_small_cfg(bn) ? 1 : 0;
     rows_schedule(p, groups, bn, rt.G);
     p.rsplit = rt.rs;
+    set_b_res(p, bn, (tp.C + bn - 1) / bn);
     w.ms_dg_a = map_spec(Nk, Fg, 1, Nk, Fg * Nk, 64);
     p.tma_a = make_map(w.dycl_g, w.ms_dg_a);
     p.tma_b = make_map(w.wt, Nk, tp.C, tp.nwin(), Nk, (int64_t)tp.C * Nk, bn);

@@ -43,12 +43,12 @@ __host__ __device__ constexpr int mgroup() {
   return BN >= 256 ? 1 : 256 / BN;
 }
 // CFG 0: one CTA per SM (192 KB ring, 512 TMEM columns, G up to mgroup).
-// CFG 1: two CTAs per SM (96 KB ring, <= 256 TMEM columns, G = 1): the
+// CFG 1: two CTAs per SM (104 KB ring, <= 256 TMEM columns, G = 1): the
 // second CTA hides the first one's fixed costs (setup, first loads,
 // epilogue tail) and the next kernel's CTAs can start beside a tail CTA.
 template <int CFG>
 __host__ __device__ constexpr int ring_bytes() {
-  return CFG ? 96 * 1024 : RING_BYTES;
+  return CFG ? 104 * 1024 : RING_BYTES;
 }
 template <int BN, int CFG>
 __host__ __device__ constexpr int gmax() {
@@ -86,6 +86,10 @@ struct alignas(64) TcGemmParams {
   int32_t rsplit;      // MODE_ROWS split of the channel blocks (>1: fp32 atomic output)
   int32_t G;           // MODE_ROWS M tiles per step (<= gmax<BN, CFG>(); fewer for small problems)
   int32_t cfg;         // host-side: kernel configuration (CFG template argument) to launch
+  // MODE_ROWS, one N tile and one channel block: the B tiles of all b_res
+  // windows stay resident in shared memory (loaded once per CTA), so the
+  // window loop issues no B loads and no per-window commits
+  int32_t b_res;
   int32_t a_shift[MAXWIN];   // MODE_ROWS: row shift of A per window; MODE_WGRAD: B row (pixel) shift
   int32_t a_plane[MAXWIN];   // MODE_WGRAD: plane (phase) of x per window
   int32_t b_plane[MAXWIN];   // MODE_ROWS: B plane (packed weight window) per window
@@ -322,7 +326,8 @@ __global__ void __launch_bounds__(THREADS, CFG ? 2 : 1) tc_gemm_kernel(const __g
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sa = smem;
-  uint8_t* sb = smem + a_region_bytes<BN, CFG>();
+  const int b_res = MODE == MODE_ROWS ? p.b_res : 0;
+  uint8_t* sb = b_res ? smem + ring_bytes<CFG>() - b_res * B_BYTES : smem + a_region_bytes<BN, CFG>();
   uint64_t* a_full = reinterpret_cast<uint64_t*>(smem + ring_bytes<CFG>());
   uint64_t* a_empty = a_full + 8;
   uint64_t* b_full = a_empty + 8;
@@ -365,15 +370,45 @@ __global__ void __launch_bounds__(THREADS, CFG ? 2 : 1) tc_gemm_kernel(const __g
   // barrier init, TMEM allocation and the tensormap prefetch overlapped the
   // previous kernel; from here on global memory is touched
   pdl_wait();
-  const bool tr = p.trace != nullptr && blockIdx.x == 0;
-  auto stamp = [&](int i) {
-    if (tr && i < 64) {
-      unsigned long long t;
-      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-      p.trace[i] = t;
+  // profiling: event log of every CTA on SM 0.  trace[0] counts CTAs; CTA
+  // slot s owns entries [64 + s*1024, +1024): 256 per role (start, producer,
+  // MMA, epilogue), each entry (globaltimer, kind | tile << 8 | w << 24 |
+  // cta << 40); the roles write with private counters (no atomics in the loops).
+  // Compiled in only with -DSYNO_TC_TRACE_EVENTS (`make TRACE=1`): the
+  // checks cost the latency-critical issue loops ~15% otherwise.
+#ifdef SYNO_TC_TRACE_EVENTS
+  uint32_t smid;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+  const bool tr = p.trace != nullptr && smid == 0;
+  __shared__ uint32_t tr_slot;
+  if (tr && threadIdx.x == 0) tr_slot = (uint32_t)atomicAdd(p.trace, 1ull);
+  __syncthreads();
+  uint32_t tr_n = 0;
+  const int tr_role = warp == 0 ? 1 : warp == 1 ? 2 : 3;
+#else
+  constexpr bool tr = false;
+  constexpr uint32_t tr_slot = 0;
+  uint32_t tr_n = 0;
+  constexpr int tr_role = 0;
+#endif
+  auto ev = [&](int kind, int tile, int w) {
+    if (tr && tr_slot < 7) {
+      // SM cycle counter (every traced CTA runs on SM 0); the viewer converts at 1.965 GHz
+      const unsigned long long t = clock64();
+      const int role = threadIdx.x == 0 && kind == 0 ? 0 : tr_role;
+      if (tr_n < 127) {
+        unsigned long long* e = p.trace + 64 + tr_slot * 1024 + role * 256 + tr_n * 2;
+        e[0] = t;
+        e[1] = (unsigned long long)kind | ((unsigned long long)(tile & 0xFFFF) << 8) |
+               ((unsigned long long)(w & 0xFFFF) << 24) | ((unsigned long long)blockIdx.x << 40);
+        ++tr_n;
+      }
     }
   };
-  if (threadIdx.x == 0) stamp(0);
+  if (threadIdx.x == 0) {
+    ev(0, 0, 0);
+    tr_n = 0;
+  }
 
   if (warp == 0) {
     // ---------------- TMA producer: the whole warp walks the schedule, one
@@ -384,17 +419,27 @@ __global__ void __launch_bounds__(THREADS, CFG ? 2 : 1) tc_gemm_kernel(const __g
     }
     __syncwarp();
     Ring ra, rb;
-    if (lane == 0) stamp(1);
     uint32_t pcount = 0;
+    if (b_res && blockIdx.x < n_tiles_total) {
+      if (elect_one()) {
+        if (p.dbg & 8) {
+          mbar_arrive(&b_full[0]);
+        } else {
+          mbar_expect_tx(&b_full[0], p.b_tx * (uint32_t)b_res);
+          for (int w = 0; w < b_res; ++w) tma_load_3d(sb + w * B_BYTES, &p.tma_b, &b_full[0], 0, 0, p.b_plane[w]);
+        }
+      }
+      __syncwarp();
+    }
     for (int t = blockIdx.x; t < n_tiles_total; t += gridDim.x, ++pcount) {
       const TileInfo ti = tile_info(p, t);
-      if (lane == 0 && pcount < 14) stamp(2 + pcount * 4);
       if constexpr (MODE == MODE_ROWS) {
         for (int c = p.g_chunk0[ti.g]; c < p.g_chunk1[ti.g]; ++c) {
           for (int cb = ti.cb0; cb < ti.cb1; ++cb) {
             // one halo tile of A for this plane and channel block
             const int as = ra.slot(AST);
             mbar_wait(&a_empty[as], ra.phase(AST) ^ 1u);
+            if (lane == 0) ev(1, (int)pcount, c * 64 + cb);  // A slot free, load issued
             const int row0 = ti.mt * p.G * BM + p.chunk_pmin[c];
             const int nbox = p.a_rows / 64;
             if (elect_one()) {
@@ -409,10 +454,10 @@ __global__ void __launch_bounds__(THREADS, CFG ? 2 : 1) tc_gemm_kernel(const __g
             }
             __syncwarp();
             ++ra.i;
-            for (int w = p.chunk_w0[c]; w < p.chunk_w1[c]; ++w) {
+            for (int w = p.chunk_w0[c]; w < p.chunk_w1[c] && !b_res; ++w) {
               const int bs = rb.slot(BSTAGES);
               mbar_wait(&b_empty[bs], rb.phase(BSTAGES) ^ 1u);
-              if (lane == 0 && pcount == 0 && w < 9) stamp(50 + w);
+              if (lane == 0) ev(2, (int)pcount, w);  // B slot free, load issued
               if (elect_one()) {
                 if (p.dbg & 8) {
                   mbar_arrive(&b_full[bs]);
@@ -463,10 +508,13 @@ __global__ void __launch_bounds__(THREADS, CFG ? 2 : 1) tc_gemm_kernel(const __g
     const uint32_t idesc = mn ? idesc_bf16(BM, BN, 1, 1) : idesc_bf16(BM, BN);
     Ring ra, rb;
     uint32_t tcount = 0;
+    if (b_res && blockIdx.x < n_tiles_total) mbar_wait(&b_full[0], 0);  // resident B tiles landed
     for (int t = blockIdx.x; t < n_tiles_total; t += gridDim.x, ++tcount) {
       const TileInfo ti = tile_info(p, t);
       const uint32_t acc = tcount & 1u;
+      if (lane == 0) ev(9, (int)tcount, 0);  // MMA warp: next tile decoded
       mbar_wait(&tempty[acc], ((tcount >> 1) & 1u) ^ 1u);  // epilogue drained this buffer
+      if (lane == 0) ev(5, (int)tcount, 0);  // MMA warp: accumulator free
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const uint32_t dst = tmem + acc * ACC_COLS;
       uint32_t accumulate = 0;
@@ -475,13 +523,17 @@ __global__ void __launch_bounds__(THREADS, CFG ? 2 : 1) tc_gemm_kernel(const __g
           for (int cb = ti.cb0; cb < ti.cb1; ++cb) {
             const int as = ra.slot(AST);
             mbar_wait(&a_full[as], ra.phase(AST));
+            if (lane == 0) ev(3, (int)tcount, c * 64 + cb);  // MMA warp: A halo ready
             const uint32_t abase = smem_u32(sa + as * p.a_stage_bytes);
+            if (b_res) asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
             for (int w = p.chunk_w0[c]; w < p.chunk_w1[c]; ++w) {
               const int bs = rb.slot(BSTAGES);
-              mbar_wait(&b_full[bs], rb.phase(BSTAGES));
-              if (lane == 0 && tcount == 0 && w < 9) stamp(40 + w);
-              asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-              const uint64_t db = sw128_desc(sb + bs * B_BYTES);
+              if (!b_res) {
+                mbar_wait(&b_full[bs], rb.phase(BSTAGES));
+                if (lane == 0) ev(4, (int)tcount, w);  // MMA warp: B window ready
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+              }
+              const uint64_t db = sw128_desc(sb + (b_res ? w : bs) * B_BYTES);
               // profiling switch 32: every window reads the aligned halo start (wrong values, timing only)
               const uint32_t arow = abase + ((p.dbg & 32) ? 0u : (uint32_t)(p.a_shift[w] - p.chunk_pmin[c]) * 128u);
               if (G > 1 && (p.dbg & 128)) {
@@ -511,7 +563,10 @@ __global__ void __launch_bounds__(THREADS, CFG ? 2 : 1) tc_gemm_kernel(const __g
                 }
               }
               accumulate = 1;
-              if (p.dbg & 16) {
+              if (lane == 0) ev(11, (int)tcount, w);  // MMA warp: window issued
+              if (b_res) {
+                // resident B: nothing to release
+              } else if (p.dbg & 16) {
                 if (elect_one()) mbar_arrive(&b_empty[bs]);  // profiling only: no MMA reads B
                 __syncwarp();
               } else {
@@ -543,13 +598,14 @@ __global__ void __launch_bounds__(THREADS, CFG ? 2 : 1) tc_gemm_kernel(const __g
           ++rb.i;
         }
       }
-      if (lane == 0 && tcount < 14) stamp(2 + tcount * 4 + 1);
+      if (lane == 0) ev(6, (int)tcount, 0);  // MMA warp: tile issued
       if (accumulate) {
         mma_commit(&tfull[acc]);
       } else {
         if (elect_one()) mbar_arrive(&tfull[acc]);
         __syncwarp();
       }
+      if (lane == 0) ev(10, (int)tcount, 0);  // MMA warp: tile committed
     }
   } else {
     // epilogue warps: TMEM lane quarter = warp % 4, column-chunk parity = (warp - 2) / 4
@@ -562,9 +618,10 @@ __global__ void __launch_bounds__(THREADS, CFG ? 2 : 1) tc_gemm_kernel(const __g
       const uint32_t acc = tcount & 1u;
       if (p.dbg & 64) mbar_wait(&tfull[acc], (tcount >> 1) & 1u);
       else mbar_wait_sleep(&tfull[acc], (tcount >> 1) & 1u);
-      if (warp == 2 && lane == 0 && tcount < 14) stamp(2 + tcount * 4 + 2);
+      if (warp == 2 && lane == 0) ev(7, (int)tcount, 0);  // epilogue: accumulator full
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const int nsub = MODE == MODE_ROWS ? p.G : 1;
+      // profiling switch 256: no TMEM reads or stores (release the buffer at once)
+      const int nsub = (p.dbg & 256) ? 0 : MODE == MODE_ROWS ? p.G : 1;
       const bool have = ti.nkb > 0;
       const float scale = p.scale;
 #pragma unroll 1
@@ -641,7 +698,7 @@ __global__ void __launch_bounds__(THREADS, CFG ? 2 : 1) tc_gemm_kernel(const __g
       // release the accumulator buffer to the MMA warp (one arrive per warp)
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       __syncwarp();
-      if (warp == 2 && lane == 0 && tcount < 14) stamp(2 + tcount * 4 + 3);
+      if (warp == 2 && lane == 0) ev(8, (int)tcount, 0);  // epilogue: drained
       if (lane == 0) mbar_arrive(&tempty[acc]);
       if constexpr (MODE == MODE_WGRAD) {
         if (p.fix_out) {
