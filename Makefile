@@ -6,6 +6,10 @@ CXXFLAGS := -O3 -std=c++17 -Xcompiler -fPIC -Xcompiler -Wall -lineinfo
 ifdef TRACE
 CXXFLAGS += -DSYNO_TC_TRACE_EVENTS
 endif
+# `make DBG=1` (after touching csrc/tc.cu) compiles the SYNO_TC_DEBUG switches in
+ifdef DBG
+CXXFLAGS += -DSYNO_TC_DBG_SWITCHES
+endif
 PKG := paper_2410_23745_b200
 SRC := $(PKG)/csrc
 OBJ := build/obj

@@ -1337,6 +1337,27 @@ std::string tc_describe(const TcPlan* tp) {
 // Launch helpers
 // ---------------------------------------------------------------------------
 
+// PDL launch of a GEMM kernel; `pair`: clusters of two CTAs (one TPC) for
+// the cta_group::2 configuration.
+static void launch_tc(void (*kernel)(TcGemmParams), bool pair, unsigned grid, int smem, cudaStream_t stream,
+                      const TcGemmParams& p) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(THREADS);
+  cfg.dynamicSmemBytes = (size_t)smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  attr[1].id = cudaLaunchAttributeClusterDimension;
+  attr[1].val.clusterDim.x = pair ? 2 : 1;
+  attr[1].val.clusterDim.y = 1;
+  attr[1].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pair ? 2 : 1;
+  cuda_check(cudaLaunchKernelEx(&cfg, kernel, p), "cudaLaunchKernelEx(tc_gemm)");
+}
+
 template <int BN, int MODE, int CFG>
 static void launch_gemm(const TcGemmParams& p, unsigned grid, cudaStream_t stream) {
   static std::atomic<uint64_t> configured{0};  // per-device bit
@@ -1355,12 +1376,12 @@ static void launch_gemm(const TcGemmParams& p, unsigned grid, cudaStream_t strea
   static unsigned long long* trace_buf = nullptr;
   if (trace_path && !trace_buf) cuda_check(cudaMalloc(&trace_buf, 8192 * sizeof(unsigned long long)), "trace");
   if (!trace_path) {
-    launch_k(tc_gemm_kernel<BN, MODE, CFG>, grid, THREADS, smem, stream, p);
+    launch_tc(tc_gemm_kernel<BN, MODE, CFG>, CFG == CFG_PAIR, grid, smem, stream, p);
   } else {
     TcGemmParams q = p;
     q.trace = trace_buf;
     cuda_check(cudaMemsetAsync(trace_buf, 0, 8192 * sizeof(unsigned long long), stream), "trace memset");
-    launch_k(tc_gemm_kernel<BN, MODE, CFG>, grid, THREADS, smem, stream, q);
+    launch_tc(tc_gemm_kernel<BN, MODE, CFG>, CFG == CFG_PAIR, grid, smem, stream, q);
     std::vector<unsigned long long> h(8192);
     cuda_check(cudaMemcpyAsync(h.data(), trace_buf, 8192 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, stream),
                "trace copy");
@@ -1387,25 +1408,36 @@ static int sm_count() {
   return n;
 }
 
+static bool tc_log();
+
 // Persistent launch: one CTA per SM walks the (n fastest, m, z) tile grid.
 static void gemm(TcGemmParams& p, int bn, int m_tiles, int n_tiles, int z_tiles, cudaStream_t stream,
                  const char* name, double flops) {
   if (skip_class("gemm")) return;
-  p.m_tiles = m_tiles;
+  const bool pair = p.cfg == CFG_PAIR;
+  // pair: the kernel's M tiles are pairs of 128-row tiles
+  p.m_tiles = pair ? (m_tiles + 1) / 2 : m_tiles;
   p.n_tiles = n_tiles;
   p.z_tiles = z_tiles;
   const bool small = p.cfg == 1 && bn <= 128;
-  const int a_region = small ? (bn == 64 ? a_region_bytes<64, 1>() : a_region_bytes<128, 1>())
-                             : (bn == 64 ? a_region_bytes<64>() : bn == 128 ? a_region_bytes<128>() : a_region_bytes<256>());
+  const int a_region = pair ? a_region_bytes<256, CFG_PAIR>()
+                       : small ? (bn == 64 ? a_region_bytes<64, 1>() : a_region_bytes<128, 1>())
+                               : (bn == 64 ? a_region_bytes<64>() : bn == 128 ? a_region_bytes<128>() : a_region_bytes<256>());
   const int ring = small ? ring_bytes<1>() : ring_bytes<0>();
   p.a_stages = std::max(1, std::min(8, (p.mode == MODE_ROWS && p.b_res ? ring - p.b_res * bn * BK * 2 : a_region) /
                                            p.a_stage_bytes));
-  const int64_t tiles = (int64_t)m_tiles * n_tiles * z_tiles;
+  const int64_t tiles = (int64_t)p.m_tiles * n_tiles * z_tiles;
   if (tiles <= 0) return;
-  const unsigned grid = (unsigned)std::min<int64_t>(tiles, (int64_t)sm_count() * (small ? 2 : 1));
+  const unsigned grid = pair ? (unsigned)std::min<int64_t>(tiles, sm_count() / 2) * 2
+                             : (unsigned)std::min<int64_t>(tiles, (int64_t)sm_count() * (small ? 2 : 1));
+  if (tc_log())
+    fprintf(stderr, "[tc] gemm %s bn=%d cfg=%d tiles=%lld grid=%u G=%d rsplit=%d a_stages=%d\n", name, bn, p.cfg,
+            (long long)tiles, grid, p.G, p.rsplit, p.a_stages);
   const int id = prof_begin(name, flops, 0.0, stream);
   if (p.mode == MODE_ROWS) {
-    if (small) {
+    if (pair) {
+      launch_gemm<256, MODE_ROWS, CFG_PAIR>(p, grid, stream);
+    } else if (small) {
       if (bn == 64) launch_gemm<64, MODE_ROWS, 1>(p, grid, stream);
       else launch_gemm<128, MODE_ROWS, 1>(p, grid, stream);
     } else if (bn == 64) launch_gemm<64, MODE_ROWS, 0>(p, grid, stream);
@@ -1446,6 +1478,17 @@ static void set_b_res(TcGemmParams& p, int bn, int n_tiles) {
   if (off || n_tiles != 1 || p.n_cblocks != 1 || p.rsplit > 1) return;
   const int ring = (p.cfg == 1 && bn <= 128) ? ring_bytes<1>() : ring_bytes<0>();
   if (p.n_win * bn * BK * 2 + p.a_stage_bytes <= ring) p.b_res = p.n_win;
+}
+
+// CTA-pair configuration (CFG_PAIR, SYNO_TC_PAIR=0 disables): BN = 256
+// launches without a channel split or resident B and with two or more M
+// tiles.  Returns the B box rows of one CTA.
+static int set_pair(TcGemmParams& p, int bn, const RowsTiling& rt) {
+  static const bool on = !(getenv("SYNO_TC_PAIR") && atoi(getenv("SYNO_TC_PAIR")) == 0);
+  if (!on || bn != 256 || rt.G != 1 || rt.rs != 1 || p.b_res || rt.m_tiles < 2) return bn;
+  p.cfg = CFG_PAIR;
+  p.b_tx = (uint32_t)(bn / 2) * BK * 2;
+  return bn / 2;
 }
 
 static RowsTiling rows_tiling(int64_t F, int n_tiles, int groups, int bn, int n_cblocks, int nwin) {
@@ -1800,9 +1843,10 @@ static void build_ws(TcPlan& tp, TcWs& w, DType dt) {
     rows_schedule(p, groups, bn, rt.G);
     p.rsplit = rt.rs;
     set_b_res(p, bn, (tp.N + bn - 1) / bn);
+    const int b_box = set_pair(p, bn, rt);
     w.ms_fwd_a = map_spec(Ck, F, planes, Ck, F * Ck, 64);
     p.tma_a = make_map(w.xcl, w.ms_fwd_a);
-    p.tma_b = make_map(w.wf, Ck, tp.N, tp.nwin(), Ck, (int64_t)tp.N * Ck, bn);
+    p.tma_b = make_map(w.wf, Ck, tp.N, tp.nwin(), Ck, (int64_t)tp.N * Ck, b_box);
     p.Hp = w.gx.Hp;
     p.Wp = w.gx.Wp;
     p.lo_h = w.gx.lo_h;
@@ -1872,9 +1916,10 @@ static void build_ws(TcPlan& tp, TcWs& w, DType dt) {
     rows_schedule(p, groups, bn, rt.G);
     p.rsplit = rt.rs;
     set_b_res(p, bn, (tp.C + bn - 1) / bn);
+    const int b_box = set_pair(p, bn, rt);
     w.ms_dg_a = map_spec(Nk, Fg, 1, Nk, Fg * Nk, 64);
     p.tma_a = make_map(w.dycl_g, w.ms_dg_a);
-    p.tma_b = make_map(w.wt, Nk, tp.C, tp.nwin(), Nk, (int64_t)tp.C * Nk, bn);
+    p.tma_b = make_map(w.wt, Nk, tp.C, tp.nwin(), Nk, (int64_t)tp.C * Nk, b_box);
     p.Hp = w.gdy_g.Hp;
     p.Wp = w.gdy_g.Wp;
     p.lo_h = w.gdy_g.lo_h;

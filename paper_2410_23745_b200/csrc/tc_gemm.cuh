@@ -46,9 +46,16 @@ __host__ __device__ constexpr int mgroup() {
 // CFG 1: two CTAs per SM (104 KB ring, <= 256 TMEM columns, G = 1): the
 // second CTA hides the first one's fixed costs (setup, first loads,
 // epilogue tail) and the next kernel's CTAs can start beside a tail CTA.
+// CFG 2 (CTA pair, BN = 256, MODE_ROWS): a cluster of two CTAs on one TPC
+// computes a 256 x 256 tile with tcgen05.mma.cta_group::2 issued by the
+// leader.  Each CTA stages its own 128-row A halo tile and HALF of the B
+// tile (128 of the 256 N rows), so one 256 x 256 x 64 k-step moves 32 KB
+// per SM from L2 instead of 48 KB for a 128 x 256 tile, and the ring holds
+// six k-steps instead of four.  Each CTA's TMEM holds its own 128 rows.
+constexpr int CFG_PAIR = 2;
 template <int CFG>
 __host__ __device__ constexpr int ring_bytes() {
-  return CFG ? 104 * 1024 : RING_BYTES;
+  return CFG == 1 ? 104 * 1024 : RING_BYTES;
 }
 template <int BN, int CFG>
 __host__ __device__ constexpr int gmax() {
@@ -56,11 +63,16 @@ __host__ __device__ constexpr int gmax() {
 }
 template <int BN, int CFG = 0>
 __host__ __device__ constexpr int b_stages() {
-  return CFG && BN >= 128 ? 2 : 4;
+  return CFG == CFG_PAIR ? 6 : CFG && BN >= 128 ? 2 : 4;
+}
+// B rows one CTA stages per k-step (the pair splits N)
+template <int BN, int CFG = 0>
+__host__ __device__ constexpr int b_rows() {
+  return CFG == CFG_PAIR ? BN / 2 : BN;
 }
 template <int BN, int CFG = 0>
 __host__ __device__ constexpr int a_region_bytes() {
-  return ring_bytes<CFG>() - b_stages<BN, CFG>() * BN * BK * 2;
+  return ring_bytes<CFG>() - b_stages<BN, CFG>() * b_rows<BN, CFG>() * BK * 2;
 }
 
 enum Mode : int32_t {
@@ -191,6 +203,63 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, u
       : "memory");
 }
 
+// CTA-pair helpers (CFG_PAIR)
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t cluster_id_x() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%clusterid.x;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t n_clusters_x() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%nclusterid.x;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// shared::cluster address of `p` (same offset) in CTA `rank` of the cluster
+__device__ __forceinline__ uint32_t peer_addr(const void* p, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_bar) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_bar) : "memory");
+}
+// TMA load into this CTA's shared memory whose completion is signalled on an
+// mbarrier of either CTA of the pair (the leader's full barrier)
+__device__ __forceinline__ void tma_load_3d_pair(void* dst, const CUtensorMap* map, uint32_t cluster_bar, int c0,
+                                                 int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];" ::
+          "r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(cluster_bar), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+__device__ __forceinline__ void mma_bf16_pair(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+// commit the leader's MMAs to the same barrier in both CTAs of the pair
+__device__ __forceinline__ void mma_commit_pair(uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n\t}" ::"r"(
+          smem_u32(bar)),
+      "h"((uint16_t)3)
+      : "memory");
+}
+
 // K-major, 128-byte swizzle smem descriptor (canonical ((8,m),(T,2)) : ((8T,SBO),(1,T))),
 // starting `row` 128-byte rows into a 1024-byte aligned tile.
 __device__ __forceinline__ uint64_t sw128_desc(const void* smem, int row = 0, int base_mode = 0) {
@@ -308,18 +377,29 @@ __device__ __forceinline__ TileInfo tile_info(const TcGemmParams& p, int t) {
   return ti;
 }
 
-// Ring position helper: slot index and phase parity of the i-th use.
+// Ring position: slot index and phase parity, advanced incrementally (a
+// runtime-sized ring would otherwise cost an integer division per k-step on
+// the latency-critical producer / MMA loops).
 struct Ring {
-  uint32_t i = 0;
-  __device__ __forceinline__ int slot(int n) const { return (int)(i % (uint32_t)n); }
-  __device__ __forceinline__ uint32_t phase(int n) const { return (i / (uint32_t)n) & 1u; }
+  int s = 0;
+  uint32_t ph = 0;
+  __device__ __forceinline__ int slot(int) const { return s; }
+  __device__ __forceinline__ uint32_t phase(int) const { return ph; }
+  __device__ __forceinline__ void next(int n) {
+    if (++s == n) {
+      s = 0;
+      ph ^= 1u;
+    }
+  }
 };
 
 template <int BN, int MODE, int CFG>
-__global__ void __launch_bounds__(THREADS, CFG ? 2 : 1) tc_gemm_kernel(const __grid_constant__ TcGemmParams p) {
+__global__ void __launch_bounds__(THREADS, CFG == 1 ? 2 : 1) tc_gemm_kernel(const __grid_constant__ TcGemmParams p) {
   pdl_trigger();
+  constexpr bool PAIR = CFG == CFG_PAIR;
+  static_assert(!PAIR || (MODE == MODE_ROWS && BN == 256), "CTA pair: MODE_ROWS, BN = 256");
   constexpr int BSTAGES = b_stages<BN, CFG>();
-  constexpr int B_BYTES = BN * BK * 2;
+  constexpr int B_BYTES = b_rows<BN, CFG>() * BK * 2;
   constexpr int G = gmax<BN, CFG>();
   constexpr uint32_t ACC_COLS = G * BN;          // one accumulator buffer: G sub-tiles
   constexpr uint32_t TMEM_COLS = 2 * ACC_COLS;   // double-buffered (512 for CFG 0)
@@ -341,6 +421,23 @@ __global__ void __launch_bounds__(THREADS, CFG ? 2 : 1) tc_gemm_kernel(const __g
   const int lane = threadIdx.x & 31;
   const int n_tiles_total = p.m_tiles * p.n_tiles * p.z_tiles;
   const int AST = p.a_stages;
+  // profiling switches (SYNO_TC_DEBUG) are compiled in only with `make DBG=1`:
+  // their runtime tests cost the issue loops measurably
+#ifdef SYNO_TC_DBG_SWITCHES
+  const int dbg = dbg;
+#else
+  constexpr int dbg = 0;
+#endif
+  // CTA pair: both CTAs walk the same pair tiles (m_tiles counts pairs of
+  // 128-row M tiles; this CTA takes M tile 2 * pair + rank)
+  const uint32_t rank = PAIR ? cluster_rank() : 0u;
+  const int t_first = PAIR ? (int)cluster_id_x() : (int)blockIdx.x;
+  const int t_step = PAIR ? (int)n_clusters_x() : (int)gridDim.x;
+  auto tinfo = [&](int t) {
+    TileInfo ti = tile_info(p, t);
+    if (PAIR) ti.mt = 2 * ti.mt + (int)rank;
+    return ti;
+  };
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < AST; ++s) {
@@ -353,18 +450,25 @@ __global__ void __launch_bounds__(THREADS, CFG ? 2 : 1) tc_gemm_kernel(const __g
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], EPI_WARPS);
+      mbar_init(&tempty[a], PAIR ? 2 * EPI_WARPS : EPI_WARPS);  // pair: both CTAs' epilogues arrive at the leader
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
   if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                 "r"(TMEM_COLS));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    if constexpr (PAIR) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                   "r"(TMEM_COLS));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                   "r"(TMEM_COLS));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
+  if constexpr (PAIR) cluster_sync_all();  // the peer's barriers are initialised before any remote signal
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
   // barrier init, TMEM allocation and the tensormap prefetch overlapped the
@@ -422,7 +526,7 @@ __global__ void __launch_bounds__(THREADS, CFG ? 2 : 1) tc_gemm_kernel(const __g
     uint32_t pcount = 0;
     if (b_res && blockIdx.x < n_tiles_total) {
       if (elect_one()) {
-        if (p.dbg & 8) {
+        if (dbg & 8) {
           mbar_arrive(&b_full[0]);
         } else {
           mbar_expect_tx(&b_full[0], p.b_tx * (uint32_t)b_res);
@@ -431,8 +535,8 @@ __global__ void __launch_bounds__(THREADS, CFG ? 2 : 1) tc_gemm_kernel(const __g
       }
       __syncwarp();
     }
-    for (int t = blockIdx.x; t < n_tiles_total; t += gridDim.x, ++pcount) {
-      const TileInfo ti = tile_info(p, t);
+    for (int t = t_first; t < n_tiles_total; t += t_step, ++pcount) {
+      const TileInfo ti = tinfo(t);
       if constexpr (MODE == MODE_ROWS) {
         for (int c = p.g_chunk0[ti.g]; c < p.g_chunk1[ti.g]; ++c) {
           for (int cb = ti.cb0; cb < ti.cb1; ++cb) {
@@ -443,7 +547,14 @@ __global__ void __launch_bounds__(THREADS, CFG ? 2 : 1) tc_gemm_kernel(const __g
             const int row0 = ti.mt * p.G * BM + p.chunk_pmin[c];
             const int nbox = p.a_rows / 64;
             if (elect_one()) {
-              if (p.dbg & 4) {
+              if constexpr (PAIR) {
+                // both halves land on the leader's barrier
+                if (rank == 0) mbar_expect_tx(&a_full[as], 2 * p.a_tx);
+                const uint32_t bar = peer_addr(&a_full[as], 0);
+                for (int j = 0; j < nbox; ++j)
+                  tma_load_3d_pair(sa + as * p.a_stage_bytes + j * 8192, &p.tma_a, bar, cb * BK, row0 + 64 * j,
+                                   p.chunk_plane[c]);
+              } else if (dbg & 4) {
                 mbar_arrive(&a_full[as]);
               } else {
                 mbar_expect_tx(&a_full[as], p.a_tx);
@@ -453,13 +564,18 @@ __global__ void __launch_bounds__(THREADS, CFG ? 2 : 1) tc_gemm_kernel(const __g
               }
             }
             __syncwarp();
-            ++ra.i;
+            ra.next(AST);
             for (int w = p.chunk_w0[c]; w < p.chunk_w1[c] && !b_res; ++w) {
               const int bs = rb.slot(BSTAGES);
               mbar_wait(&b_empty[bs], rb.phase(BSTAGES) ^ 1u);
               if (lane == 0) ev(2, (int)pcount, w);  // B slot free, load issued
               if (elect_one()) {
-                if (p.dbg & 8) {
+                if constexpr (PAIR) {
+                  // this CTA's half of the N rows
+                  if (rank == 0) mbar_expect_tx(&b_full[bs], 2 * p.b_tx);
+                  tma_load_3d_pair(sb + bs * B_BYTES, &p.tma_b, peer_addr(&b_full[bs], 0), cb * BK,
+                                   ti.nt * BN + (int)rank * (BN / 2), p.b_plane[w]);
+                } else if (dbg & 8) {
                   mbar_arrive(&b_full[bs]);
                 } else {
                   mbar_expect_tx(&b_full[bs], p.b_tx);
@@ -467,7 +583,7 @@ __global__ void __launch_bounds__(THREADS, CFG ? 2 : 1) tc_gemm_kernel(const __g
                 }
               }
               __syncwarp();
-              ++rb.i;
+              rb.next(BSTAGES);
             }
           }
         }
@@ -488,7 +604,7 @@ __global__ void __launch_bounds__(THREADS, CFG ? 2 : 1) tc_gemm_kernel(const __g
             }
           }
           __syncwarp();
-          ++ra.i;
+          ra.next(AST);
           const int bs = rb.slot(BSTAGES);
           mbar_wait(&b_empty[bs], rb.phase(BSTAGES) ^ 1u);
           if (elect_one()) {
@@ -498,19 +614,21 @@ __global__ void __launch_bounds__(THREADS, CFG ? 2 : 1) tc_gemm_kernel(const __g
               tma_load_3d(sb + bs * B_BYTES + h * 8192, &p.tma_b, &b_full[bs], ti.nt * BN + h * 64, kb * BK, 0);
           }
           __syncwarp();
-          ++rb.i;
+          rb.next(BSTAGES);
         }
       }
     }
   } else if (warp == 1) {
+   // CTA pair: the leader issues every MMA of the pair; the peer's warp 1 only owns its TMEM allocation
+   if (!PAIR || rank == 0) {
     // ---------------- MMA issuer: warp-wide loop, elected-lane issue
     constexpr bool mn = MODE == MODE_WGRAD;
-    const uint32_t idesc = mn ? idesc_bf16(BM, BN, 1, 1) : idesc_bf16(BM, BN);
+    const uint32_t idesc = mn ? idesc_bf16(BM, BN, 1, 1) : idesc_bf16(PAIR ? 2 * BM : BM, BN);
     Ring ra, rb;
     uint32_t tcount = 0;
     if (b_res && blockIdx.x < n_tiles_total) mbar_wait(&b_full[0], 0);  // resident B tiles landed
-    for (int t = blockIdx.x; t < n_tiles_total; t += gridDim.x, ++tcount) {
-      const TileInfo ti = tile_info(p, t);
+    for (int t = t_first; t < n_tiles_total; t += t_step, ++tcount) {
+      const TileInfo ti = tinfo(t);
       const uint32_t acc = tcount & 1u;
       if (lane == 0) ev(9, (int)tcount, 0);  // MMA warp: next tile decoded
       mbar_wait(&tempty[acc], ((tcount >> 1) & 1u) ^ 1u);  // epilogue drained this buffer
@@ -535,8 +653,8 @@ __global__ void __launch_bounds__(THREADS, CFG ? 2 : 1) tc_gemm_kernel(const __g
               }
               const uint64_t db = sw128_desc(sb + (b_res ? w : bs) * B_BYTES);
               // profiling switch 32: every window reads the aligned halo start (wrong values, timing only)
-              const uint32_t arow = abase + ((p.dbg & 32) ? 0u : (uint32_t)(p.a_shift[w] - p.chunk_pmin[c]) * 128u);
-              if (G > 1 && (p.dbg & 128)) {
+              const uint32_t arow = abase + ((dbg & 32) ? 0u : (uint32_t)(p.a_shift[w] - p.chunk_pmin[c]) * 128u);
+              if (G > 1 && (dbg & 128)) {
                 // profiling switch 128: k outer, tiles inner (independent accumulators back to back)
 #pragma unroll
                 for (int k = 0; k < BK / 16; ++k) {
@@ -549,7 +667,7 @@ __global__ void __launch_bounds__(THREADS, CFG ? 2 : 1) tc_gemm_kernel(const __g
                              (accumulate || k > 0) ? 1u : 0u);
                   }
                 }
-              } else if (!(p.dbg & 2)) {
+              } else if (!(dbg & 2)) {
 #pragma unroll
                 for (int g = 0; g < G; ++g) {
                   if (g >= p.G) break;
@@ -557,25 +675,34 @@ __global__ void __launch_bounds__(THREADS, CFG ? 2 : 1) tc_gemm_kernel(const __g
                   const uint64_t da = (((uint64_t)((arow + g * BM * 128u) >> 4)) & 0x3FFF) | (1ull << 16) |
                                       ((uint64_t)(1024 >> 4) << 32) | (1ull << 46) | (2ull << 61);
 #pragma unroll
-                  for (int k = 0; k < BK / 16; ++k)
-                    mma_bf16(dst + g * BN, da + (uint64_t)(k * 2), db + (uint64_t)(k * 2), idesc,
-                             (accumulate || k > 0) ? 1u : 0u);
+                  for (int k = 0; k < BK / 16; ++k) {
+                    if constexpr (PAIR)
+                      mma_bf16_pair(dst + g * BN, da + (uint64_t)(k * 2), db + (uint64_t)(k * 2), idesc,
+                                    (accumulate || k > 0) ? 1u : 0u);
+                    else
+                      mma_bf16(dst + g * BN, da + (uint64_t)(k * 2), db + (uint64_t)(k * 2), idesc,
+                               (accumulate || k > 0) ? 1u : 0u);
+                  }
                 }
               }
               accumulate = 1;
               if (lane == 0) ev(11, (int)tcount, w);  // MMA warp: window issued
               if (b_res) {
                 // resident B: nothing to release
-              } else if (p.dbg & 16) {
+              } else if (dbg & 16) {
                 if (elect_one()) mbar_arrive(&b_empty[bs]);  // profiling only: no MMA reads B
                 __syncwarp();
+              } else if constexpr (PAIR) {
+                mma_commit_pair(&b_empty[bs]);
               } else {
                 mma_commit(&b_empty[bs]);
               }
-              ++rb.i;
+              rb.next(BSTAGES);
             }
-            mma_commit(&a_empty[as]);  // halo tile free once its windows' MMAs finish
-            ++ra.i;
+            // halo tile free once its windows' MMAs finish
+            if constexpr (PAIR) mma_commit_pair(&a_empty[as]);
+            else mma_commit(&a_empty[as]);
+            ra.next(AST);
           }
         }
       } else {
@@ -594,34 +721,39 @@ __global__ void __launch_bounds__(THREADS, CFG ? 2 : 1) tc_gemm_kernel(const __g
           }
           mma_commit(&a_empty[as]);
           mma_commit(&b_empty[bs]);
-          ++ra.i;
-          ++rb.i;
+          ra.next(AST);
+          rb.next(BSTAGES);
         }
       }
       if (lane == 0) ev(6, (int)tcount, 0);  // MMA warp: tile issued
       if (accumulate) {
-        mma_commit(&tfull[acc]);
+        if constexpr (PAIR) mma_commit_pair(&tfull[acc]);
+        else mma_commit(&tfull[acc]);
       } else {
-        if (elect_one()) mbar_arrive(&tfull[acc]);
+        if (elect_one()) {
+          mbar_arrive(&tfull[acc]);
+          if constexpr (PAIR) mbar_arrive_cluster(peer_addr(&tfull[acc], 1));
+        }
         __syncwarp();
       }
       if (lane == 0) ev(10, (int)tcount, 0);  // MMA warp: tile committed
     }
+   }
   } else {
     // epilogue warps: TMEM lane quarter = warp % 4, column-chunk parity = (warp - 2) / 4
     const int q = warp & 3;
     const int half = (warp - 2) >> 2;
     const int r = q * 32 + lane;
     uint32_t tcount = 0;
-    for (int t = blockIdx.x; t < n_tiles_total; t += gridDim.x, ++tcount) {
-      const TileInfo ti = tile_info(p, t);
+    for (int t = t_first; t < n_tiles_total; t += t_step, ++tcount) {
+      const TileInfo ti = tinfo(t);
       const uint32_t acc = tcount & 1u;
-      if (p.dbg & 64) mbar_wait(&tfull[acc], (tcount >> 1) & 1u);
+      if (dbg & 64) mbar_wait(&tfull[acc], (tcount >> 1) & 1u);
       else mbar_wait_sleep(&tfull[acc], (tcount >> 1) & 1u);
       if (warp == 2 && lane == 0) ev(7, (int)tcount, 0);  // epilogue: accumulator full
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       // profiling switch 256: no TMEM reads or stores (release the buffer at once)
-      const int nsub = (p.dbg & 256) ? 0 : MODE == MODE_ROWS ? p.G : 1;
+      const int nsub = (dbg & 256) ? 0 : MODE == MODE_ROWS ? p.G : 1;
       const bool have = ti.nkb > 0;
       const float scale = p.scale;
 #pragma unroll 1
@@ -652,7 +784,7 @@ __global__ void __launch_bounds__(THREADS, CFG ? 2 : 1) tc_gemm_kernel(const __g
           tmem_ld32(tmem + acc * ACC_COLS + (uint32_t)(g * BN) + ((uint32_t)(q * 32) << 16) + (uint32_t)c, v);
           const int nlim = min(32, p.n_ext - n0);
           const int64_t os = p.o_n;
-          if (!ok || (p.dbg & 1)) {
+          if (!ok || (dbg & 1)) {
             // masked row (pad pixel / beyond the extent): nothing to store
           } else if (MODE == MODE_WGRAD || p.out_kind == OUT_F32_ATOMIC) {
             float* o = reinterpret_cast<float*>(p.out) + off + (int64_t)n0 * os;
@@ -699,7 +831,10 @@ __global__ void __launch_bounds__(THREADS, CFG ? 2 : 1) tc_gemm_kernel(const __g
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       __syncwarp();
       if (warp == 2 && lane == 0) ev(8, (int)tcount, 0);  // epilogue: drained
-      if (lane == 0) mbar_arrive(&tempty[acc]);
+      if (lane == 0) {
+        if constexpr (PAIR) mbar_arrive_cluster(peer_addr(&tempty[acc], 0));  // the leader's MMA warp waits
+        else mbar_arrive(&tempty[acc]);
+      }
       if constexpr (MODE == MODE_WGRAD) {
         if (p.fix_out) {
           // every epilogue warp's atomics for this tile are issued
@@ -743,9 +878,14 @@ __global__ void __launch_bounds__(THREADS, CFG ? 2 : 1) tc_gemm_kernel(const __g
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
+  // pair: neither CTA leaves (or frees TMEM) while the other may still signal it
+  if constexpr (PAIR) cluster_sync_all();
   if (warp == 1) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
+    if constexpr (PAIR)
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
+    else
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
   }
 }
 

@@ -1,0 +1,219 @@
+// Producer -> MMA-warp hand-off cost (no TMA, optional MMAs): cycles per
+// k-step of the ring protocol tc_gemm_kernel uses, under variants.
+//
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I paper_2410_23745_b200/csrc \
+//        scripts/sync_bench.cu -o /tmp/sync_bench -lcuda && /tmp/sync_bench
+//
+// Warp 0 (producer): per step wait empty[s], arrive full[s].  Warp 1 (consumer):
+// wait full[s], fence, [n_mma MMAs 128x256x16], commit empty[s] (tcgen05.commit)
+// or a plain arrive.  Flags: bit0 consumer uses try_wait, bit1 producer uses
+// try_wait, bit2 plain arrive instead of tcgen05.commit (no MMAs), bit3 no fence,
+// bit4 second commit per step (as the A + B rings do), bit5 consumer alone
+// (no producer: waits on a pre-completed phase), bit6 producer alone,
+// bit7 relaxed try_wait, bit8 consumer does not wait, bit9 consumer does not release.
+#include <cstdio>
+#include <cstdint>
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include "engine.hpp"
+#include "tc_gemm.cuh"
+
+using namespace syno::tc;
+
+__device__ __forceinline__ void wait_try(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void wait_relaxed(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.relaxed.cta.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+__global__ void sync_kernel(int steps, int stages, int n_mma, int flags, unsigned long long* out) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  __shared__ __align__(8) uint64_t full[8], empty[8], empty2[8];
+  __shared__ uint32_t tslot;
+  const int warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < 8; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+      mbar_init(&empty2[s], 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tslot)), "r"(256));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = tslot;
+  unsigned long long c0 = clock64();
+  if (warp == 0 && !(flags & 32)) {
+    for (int i = 0; i < steps; ++i) {
+      const int s = i % stages;
+      const uint32_t ph = (flags & 64) ? 1u : ((i / stages) & 1) ^ 1;
+      if (flags & 2) wait_try(&empty[s], ph);
+      else mbar_wait(&empty[s], ph);
+      if (flags & 16) {
+        if (flags & 2) wait_try(&empty2[s], ph);
+        else mbar_wait(&empty2[s], ph);
+      }
+      if (elect_one()) mbar_arrive(&full[s]);
+      __syncwarp();
+    }
+  } else if (warp == 1 && !(flags & 64)) {
+    const uint32_t idesc = idesc_bf16(128, 256);
+    const uint64_t da = sw128_desc(smem), db = sw128_desc(smem + 32768);
+    for (int i = 0; i < steps; ++i) {
+      const int s = i % stages;
+      const uint32_t ph = (flags & 32) ? 1u : (i / stages) & 1;  // alone: parity 1 of a fresh barrier completes at once
+      if (flags & 256) {
+        // no wait
+      } else if (flags & 128) wait_relaxed(&full[s], ph);
+      else if (flags & 1) wait_try(&full[s], ph);
+      else mbar_wait(&full[s], ph);
+      if (!(flags & 8)) asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      for (int k = 0; k < n_mma; ++k) mma_bf16(tmem, da + (uint64_t)((k & 3) * 2), db + (uint64_t)((k & 3) * 2), idesc, 1u);
+      if (flags & 512) {
+        // no release
+      } else if (flags & 4) {
+        if (elect_one()) {
+          mbar_arrive(&empty[s]);
+          if (flags & 16) mbar_arrive(&empty2[s]);
+        }
+        __syncwarp();
+      } else {
+        mma_commit(&empty[s]);
+        if (flags & 16) mma_commit(&empty2[s]);
+      }
+    }
+  }
+  unsigned long long c1 = clock64();
+  __syncthreads();
+  if (threadIdx.x == 32) out[blockIdx.x] = c1 - c0;
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(256));
+}
+
+// Compile-time variants of the consumer loop alone (no producer): W wait
+// (0 none, 1 test_wait, 2 try_wait), R release (0 none, 1 tcgen05.commit,
+// 2 plain arrive), M MMAs per step; stages fixed at 4 (masking, no division).
+template <int W, int R, int M>
+__global__ void cons_kernel(int steps, unsigned long long* out) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  __shared__ __align__(8) uint64_t full[4], empty[4];
+  __shared__ uint32_t tslot;
+  const int warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < 4; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tslot)), "r"(256));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = tslot;
+  const uint32_t idesc = idesc_bf16(128, 256);
+  const uint64_t da = sw128_desc(smem), db = sw128_desc(smem + 32768);
+  unsigned long long c0 = clock64();
+  for (int i = 0; i < steps; ++i) {
+    const int s = i & 3;
+    if (W == 1) mbar_wait(&full[s], 1u);
+    if (W == 2) wait_try(&full[s], 1u);
+#pragma unroll
+    for (int k = 0; k < M; ++k) mma_bf16(tmem, da + (uint64_t)((k & 3) * 2), db + (uint64_t)((k & 3) * 2), idesc, 1u);
+    if (R == 1) mma_commit(&empty[s]);
+    if (R == 2) {
+      if (elect_one()) mbar_arrive(&empty[s]);
+      __syncwarp();
+    }
+  }
+  unsigned long long c1 = clock64();
+  if (threadIdx.x == 0) out[blockIdx.x] = c1 - c0;
+  mma_commit(&empty[0]);
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(256));
+}
+
+template <int W, int R, int M>
+static void run_cons(unsigned long long* d_out) {
+  const int steps = 2048, grid = 148;
+  cudaFuncSetAttribute(cons_kernel<W, R, M>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+  for (int rep = 0; rep < 2; ++rep) cons_kernel<W, R, M><<<grid, 32, 100 * 1024>>>(steps, d_out);
+  cudaDeviceSynchronize();
+  static unsigned long long h[4096];
+  cudaMemcpy(h, d_out, grid * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+  double mean = 0;
+  for (int i = 0; i < grid; ++i) mean += (double)h[i];
+  printf("cons wait=%d release=%d mma=%2d | %8.1f cycles/step\n", W, R, M, mean / grid / steps);
+}
+
+int main() {
+  unsigned long long* d_out;
+  cudaMalloc(&d_out, 4096 * sizeof(unsigned long long));
+  static unsigned long long h[4096];
+  const size_t smem = 100 * 1024;
+  cudaFuncSetAttribute(sync_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  struct Cfg {
+    int stages, n_mma, flags, threads;
+  };
+  const Cfg cfgs[] = {
+      {4, 0, 32, 64},        {4, 0, 32 | 256, 64},  {4, 0, 32 | 512, 64}, {4, 0, 32 | 256 | 512, 64},
+      {4, 0, 32 | 128, 64},  {4, 0, 32 | 128 | 512, 64}, {4, 0, 32 | 256 | 4, 64}, {4, 0, 32 | 1 | 512, 64},
+      {4, 0, 32 | 8 | 256 | 512, 64}, {4, 4, 32 | 256 | 512, 64}, {4, 4, 32 | 256, 64}, {4, 4, 128, 64},
+      {4, 8, 128, 64},
+  };
+  printf("stages n_mma flags threads | cycles/step  (flags: 1 cons try_wait, 2 prod try_wait, 4 plain arrive, 8 no fence, 16 two commits)\n");
+  for (const Cfg& c : cfgs) {
+    const int steps = 2048, grid = 148;
+    for (int rep = 0; rep < 2; ++rep) sync_kernel<<<grid, c.threads, smem>>>(steps, c.stages, c.n_mma, c.flags, d_out);
+    cudaError_t e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) {
+      printf("error %s\n", cudaGetErrorString(e));
+      return 1;
+    }
+    cudaMemcpy(h, d_out, grid * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+    double mean = 0;
+    for (int i = 0; i < grid; ++i) mean += (double)h[i];
+    mean /= grid;
+    printf("%6d %5d %5d %7d | %8.1f\n", c.stages, c.n_mma, c.flags, c.threads, mean / steps);
+  }
+  run_cons<0, 0, 0>(d_out);
+  run_cons<1, 0, 0>(d_out);
+  run_cons<2, 0, 0>(d_out);
+  run_cons<0, 1, 0>(d_out);
+  run_cons<0, 2, 0>(d_out);
+  run_cons<1, 1, 0>(d_out);
+  run_cons<2, 1, 0>(d_out);
+  run_cons<0, 0, 4>(d_out);
+  run_cons<0, 1, 4>(d_out);
+  run_cons<2, 1, 4>(d_out);
+  run_cons<2, 1, 8>(d_out);
+  run_cons<2, 1, 16>(d_out);
+  return 0;
+}

@@ -50,6 +50,10 @@ CASES = [
     ("shortcut_s2", 64, 128, 16, 2),
     ("sep_shared", 64, 64, 32, 2),
     ("pointwise", 64, 128, 32, 2),
+    # BN = 256 with many M tiles: the CTA-pair (cta_group::2) configuration
+    ("conv3x3", 256, 256, 14, 8),
+    ("conv3x3_s2", 128, 256, 14, 8),
+    ("conv3x3", 512, 512, 7, 16),
 ]
 
 
@@ -79,12 +83,13 @@ def test_tc_conv_family_fwd_bwd(cuda, op, c_in, c_out, h, batch):
         assert _rel(a, b.grad) < 2e-2
 
 
-def test_tc_qkv_projection(cuda):
+@pytest.mark.parametrize("batch,t", [(2, 256), (4, 512)])  # (4, 512): CTA-pair forward / grad-input
+def test_tc_qkv_projection(cuda, batch, t):
     import torch
     from paper_2410_23745_b200 import ops
     from paper_2410_23745_b200 import pgraph as P
     from paper_2410_23745_b200 import workloads as WL
-    L = WL.qkv(batch=2, t=256)
+    L = WL.qkv(batch=batch, t=t)
     hd = P.handle_for(L.graph)
     assert hd.info.tc_path == 1
     g = torch.Generator(device="cpu").manual_seed(4)
