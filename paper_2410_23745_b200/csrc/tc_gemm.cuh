@@ -417,7 +417,10 @@ __global__ void __launch_bounds__(THREADS, CFG == 1 ? 2 : 1) tc_gemm_kernel(cons
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
   volatile uint32_t* fix_last = tmem_slot + 1;  // MODE_WGRAD fixup: this CTA finished the tile last
 
-  const int warp = threadIdx.x >> 5;
+  // warp index through a shuffle: the compiler then knows it is warp-uniform,
+  // so each role's loops run on the uniform datapath (descriptors, ring
+  // counters and parameter reads in uniform registers, no R2UR per MMA)
+  const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0);
   const int lane = threadIdx.x & 31;
   const int n_tiles_total = p.m_tiles * p.n_tiles * p.z_tiles;
   const int AST = p.a_stages;

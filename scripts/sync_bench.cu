@@ -115,8 +115,15 @@ __global__ void sync_kernel(int steps, int stages, int n_mma, int flags, unsigne
 // Compile-time variants of the consumer loop alone (no producer): W wait
 // (0 none, 1 test_wait, 2 try_wait), R release (0 none, 1 tcgen05.commit,
 // 2 plain arrive), M MMAs per step; stages fixed at 4 (masking, no division).
-template <int W, int R, int M>
-__global__ void cons_kernel(int steps, unsigned long long* out) {
+struct Tab {
+  int v[64];
+};
+
+// X: 0 none, 1 per-step indexed read of a __grid_constant__ array feeding the
+// wait address, 2 the same array staged in shared memory, 3 runtime-bound
+// inner loop over array entries (as the window loop), 4 = 3 with smem.
+template <int W, int R, int M, int X = 0>
+__global__ void cons_kernel(int steps, unsigned long long* out, const __grid_constant__ Tab tab) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   __shared__ __align__(8) uint64_t full[4], empty[4];
@@ -136,12 +143,21 @@ __global__ void cons_kernel(int steps, unsigned long long* out) {
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  __shared__ int stab[64];
+  if (threadIdx.x < 64) stab[threadIdx.x] = tab.v[threadIdx.x];
+  __syncthreads();
   const uint32_t tmem = tslot;
   const uint32_t idesc = idesc_bf16(128, 256);
   const uint64_t da = sw128_desc(smem), db = sw128_desc(smem + 32768);
   unsigned long long c0 = clock64();
   for (int i = 0; i < steps; ++i) {
-    const int s = i & 3;
+    int s = i & 3;
+    if (X == 1) s = tab.v[i & 63];
+    if (X == 2) s = stab[i & 63];
+    if (X == 3 || X == 4) {
+      const int lo = X == 3 ? tab.v[(i & 31)] : stab[i & 31], hi = X == 3 ? tab.v[32 + (i & 31)] : stab[32 + (i & 31)];
+      for (int j = lo; j < hi; ++j) s = (s + j) & 3;
+    }
     if (W == 1) mbar_wait(&full[s], 1u);
     if (W == 2) wait_try(&full[s], 1u);
 #pragma unroll
@@ -160,17 +176,20 @@ __global__ void cons_kernel(int steps, unsigned long long* out) {
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(256));
 }
 
-template <int W, int R, int M>
+template <int W, int R, int M, int X = 0>
 static void run_cons(unsigned long long* d_out) {
   const int steps = 2048, grid = 148;
-  cudaFuncSetAttribute(cons_kernel<W, R, M>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
-  for (int rep = 0; rep < 2; ++rep) cons_kernel<W, R, M><<<grid, 32, 100 * 1024>>>(steps, d_out);
+  Tab tab;
+  for (int i = 0; i < 64; ++i) tab.v[i] = i < 32 ? 0 : 1;  // X 1/2: slot 0..; X 3/4: one inner iteration
+  for (int i = 0; i < 32; ++i) tab.v[i] = 0;
+  cudaFuncSetAttribute(cons_kernel<W, R, M, X>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+  for (int rep = 0; rep < 2; ++rep) cons_kernel<W, R, M, X><<<grid, 32, 100 * 1024>>>(steps, d_out, tab);
   cudaDeviceSynchronize();
   static unsigned long long h[4096];
   cudaMemcpy(h, d_out, grid * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
   double mean = 0;
   for (int i = 0; i < grid; ++i) mean += (double)h[i];
-  printf("cons wait=%d release=%d mma=%2d | %8.1f cycles/step\n", W, R, M, mean / grid / steps);
+  printf("cons wait=%d release=%d mma=%2d x=%d | %8.1f cycles/step\n", W, R, M, X, mean / grid / steps);
 }
 
 int main() {
@@ -215,5 +234,12 @@ int main() {
   run_cons<2, 1, 4>(d_out);
   run_cons<2, 1, 8>(d_out);
   run_cons<2, 1, 16>(d_out);
+  run_cons<1, 1, 0, 1>(d_out);
+  run_cons<1, 1, 0, 2>(d_out);
+  run_cons<1, 1, 0, 3>(d_out);
+  run_cons<1, 1, 0, 4>(d_out);
+  run_cons<1, 1, 4, 1>(d_out);
+  run_cons<1, 1, 4, 3>(d_out);
+  run_cons<1, 1, 4, 4>(d_out);
   return 0;
 }
