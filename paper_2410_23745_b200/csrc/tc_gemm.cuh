@@ -249,6 +249,31 @@ __device__ __forceinline__ void mma_bf16_pair(uint32_t tmem_d, uint64_t a, uint6
       "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
       "l"(a), "l"(b), "r"(idesc), "r"(acc));
 }
+// MMA from the low words of two K-major SWIZZLE_128B descriptors (start
+// address >> 4 | LBO 1 << 16); the high word (SBO 1024 B, version, swizzle)
+// is the constant DESC_HI, so the issue loop advances 32-bit words only.
+constexpr uint32_t DESC_HI = (1024u >> 4) | (1u << 14) | (2u << 29);
+__device__ __forceinline__ uint32_t desc_lo(uint32_t smem_addr) { return (smem_addr >> 4) | (1u << 16); }
+template <bool PAIR>
+__device__ __forceinline__ void mma_lo(uint32_t tmem_d, uint32_t a_lo, uint32_t b_lo, uint32_t idesc, uint32_t acc) {
+  if constexpr (PAIR)
+    asm volatile(
+        "{\n\t.reg .pred p, e;\n\t.reg .b64 da, db;\n\t"
+        "mov.b64 da, {%1, %5};\n\tmov.b64 db, {%2, %5};\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "@e tcgen05.mma.cta_group::2.kind::f16 [%0], da, db, %3, p;\n\t}" ::"r"(tmem_d),
+        "r"(a_lo), "r"(b_lo), "r"(idesc), "r"(acc), "n"(DESC_HI));
+  else
+    asm volatile(
+        "{\n\t.reg .pred p, e;\n\t.reg .b64 da, db;\n\t"
+        "mov.b64 da, {%1, %5};\n\tmov.b64 db, {%2, %5};\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], da, db, %3, p;\n\t}" ::"r"(tmem_d),
+        "r"(a_lo), "r"(b_lo), "r"(idesc), "r"(acc), "n"(DESC_HI));
+}
+
 // commit the leader's MMAs to the same barrier in both CTAs of the pair
 __device__ __forceinline__ void mma_commit_pair(uint64_t* bar) {
   asm volatile(
@@ -427,7 +452,7 @@ __global__ void __launch_bounds__(THREADS, CFG == 1 ? 2 : 1) tc_gemm_kernel(cons
   // profiling switches (SYNO_TC_DEBUG) are compiled in only with `make DBG=1`:
   // their runtime tests cost the issue loops measurably
 #ifdef SYNO_TC_DBG_SWITCHES
-  const int dbg = dbg;
+  const int dbg = p.dbg;
 #else
   constexpr int dbg = 0;
 #endif
@@ -554,6 +579,7 @@ __global__ void __launch_bounds__(THREADS, CFG == 1 ? 2 : 1) tc_gemm_kernel(cons
                 // both halves land on the leader's barrier
                 if (rank == 0) mbar_expect_tx(&a_full[as], 2 * p.a_tx);
                 const uint32_t bar = peer_addr(&a_full[as], 0);
+                #pragma unroll 1
                 for (int j = 0; j < nbox; ++j)
                   tma_load_3d_pair(sa + as * p.a_stage_bytes + j * 8192, &p.tma_a, bar, cb * BK, row0 + 64 * j,
                                    p.chunk_plane[c]);
@@ -561,6 +587,7 @@ __global__ void __launch_bounds__(THREADS, CFG == 1 ? 2 : 1) tc_gemm_kernel(cons
                 mbar_arrive(&a_full[as]);
               } else {
                 mbar_expect_tx(&a_full[as], p.a_tx);
+                #pragma unroll 1
                 for (int j = 0; j < nbox; ++j)
                   tma_load_3d(sa + as * p.a_stage_bytes + j * 8192, &p.tma_a, &a_full[as], cb * BK, row0 + 64 * j,
                               p.chunk_plane[c]);
@@ -629,6 +656,8 @@ __global__ void __launch_bounds__(THREADS, CFG == 1 ? 2 : 1) tc_gemm_kernel(cons
     const uint32_t idesc = mn ? idesc_bf16(BM, BN, 1, 1) : idesc_bf16(PAIR ? 2 * BM : BM, BN);
     Ring ra, rb;
     uint32_t tcount = 0;
+    const uint32_t sa_u = smem_u32(sa), sb_u = smem_u32(sb);
+    const int a_stage_bytes = p.a_stage_bytes, Gr = p.G;
     if (b_res && blockIdx.x < n_tiles_total) mbar_wait(&b_full[0], 0);  // resident B tiles landed
     for (int t = t_first; t < n_tiles_total; t += t_step, ++tcount) {
       const TileInfo ti = tinfo(t);
@@ -640,52 +669,33 @@ __global__ void __launch_bounds__(THREADS, CFG == 1 ? 2 : 1) tc_gemm_kernel(cons
       const uint32_t dst = tmem + acc * ACC_COLS;
       uint32_t accumulate = 0;
       if constexpr (!mn) {
-        for (int c = p.g_chunk0[ti.g]; c < p.g_chunk1[ti.g]; ++c) {
+        // descriptor low words advance by 16-byte units: a row of the
+        // swizzled tile is 8, a 16-element K step 2
+        const int c1 = p.g_chunk1[ti.g];
+        for (int c = p.g_chunk0[ti.g]; c < c1; ++c) {
+          const int w0 = p.chunk_w0[c], w1 = p.chunk_w1[c], pmin = p.chunk_pmin[c];
           for (int cb = ti.cb0; cb < ti.cb1; ++cb) {
-            const int as = ra.slot(AST);
-            mbar_wait(&a_full[as], ra.phase(AST));
+            mbar_wait(&a_full[ra.s], ra.ph);
             if (lane == 0) ev(3, (int)tcount, c * 64 + cb);  // MMA warp: A halo ready
-            const uint32_t abase = smem_u32(sa + as * p.a_stage_bytes);
+            const uint32_t a_lo0 = desc_lo(sa_u + (uint32_t)(ra.s * a_stage_bytes)) - (uint32_t)pmin * 8u;
             if (b_res) asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-            for (int w = p.chunk_w0[c]; w < p.chunk_w1[c]; ++w) {
-              const int bs = rb.slot(BSTAGES);
+            for (int w = w0; w < w1; ++w) {
               if (!b_res) {
-                mbar_wait(&b_full[bs], rb.phase(BSTAGES));
+                mbar_wait(&b_full[rb.s], rb.ph);
                 if (lane == 0) ev(4, (int)tcount, w);  // MMA warp: B window ready
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
               }
-              const uint64_t db = sw128_desc(sb + (b_res ? w : bs) * B_BYTES);
+              const uint32_t b_lo = desc_lo(sb_u + (uint32_t)((b_res ? w : rb.s) * B_BYTES));
               // profiling switch 32: every window reads the aligned halo start (wrong values, timing only)
-              const uint32_t arow = abase + ((dbg & 32) ? 0u : (uint32_t)(p.a_shift[w] - p.chunk_pmin[c]) * 128u);
-              if (G > 1 && (dbg & 128)) {
-                // profiling switch 128: k outer, tiles inner (independent accumulators back to back)
-#pragma unroll
-                for (int k = 0; k < BK / 16; ++k) {
-#pragma unroll
-                  for (int g = 0; g < G; ++g) {
-                    if (g >= p.G) break;
-                    const uint64_t da = (((uint64_t)((arow + g * BM * 128u) >> 4)) & 0x3FFF) | (1ull << 16) |
-                                        ((uint64_t)(1024 >> 4) << 32) | (1ull << 46) | (2ull << 61);
-                    mma_bf16(dst + g * BN, da + (uint64_t)(k * 2), db + (uint64_t)(k * 2), idesc,
-                             (accumulate || k > 0) ? 1u : 0u);
-                  }
-                }
-              } else if (!(dbg & 2)) {
+              const uint32_t a_lo = (dbg & 32) ? a_lo0 + (uint32_t)pmin * 8u : a_lo0 + (uint32_t)p.a_shift[w] * 8u;
+              if (!(dbg & 2)) {
 #pragma unroll
                 for (int g = 0; g < G; ++g) {
-                  if (g >= p.G) break;
-                  // start = halo + (g*128 + shift) rows; K advance: 32 B inside the swizzled row
-                  const uint64_t da = (((uint64_t)((arow + g * BM * 128u) >> 4)) & 0x3FFF) | (1ull << 16) |
-                                      ((uint64_t)(1024 >> 4) << 32) | (1ull << 46) | (2ull << 61);
+                  if (g >= Gr) break;
 #pragma unroll
-                  for (int k = 0; k < BK / 16; ++k) {
-                    if constexpr (PAIR)
-                      mma_bf16_pair(dst + g * BN, da + (uint64_t)(k * 2), db + (uint64_t)(k * 2), idesc,
-                                    (accumulate || k > 0) ? 1u : 0u);
-                    else
-                      mma_bf16(dst + g * BN, da + (uint64_t)(k * 2), db + (uint64_t)(k * 2), idesc,
-                               (accumulate || k > 0) ? 1u : 0u);
-                  }
+                  for (int k = 0; k < BK / 16; ++k)
+                    mma_lo<PAIR>(dst + g * BN, a_lo + (uint32_t)(g * BM * 8 + k * 2), b_lo + (uint32_t)(k * 2), idesc,
+                                 (accumulate || k > 0) ? 1u : 0u);
                 }
               }
               accumulate = 1;
@@ -693,18 +703,18 @@ __global__ void __launch_bounds__(THREADS, CFG == 1 ? 2 : 1) tc_gemm_kernel(cons
               if (b_res) {
                 // resident B: nothing to release
               } else if (dbg & 16) {
-                if (elect_one()) mbar_arrive(&b_empty[bs]);  // profiling only: no MMA reads B
+                if (elect_one()) mbar_arrive(&b_empty[rb.s]);  // profiling only: no MMA reads B
                 __syncwarp();
               } else if constexpr (PAIR) {
-                mma_commit_pair(&b_empty[bs]);
+                mma_commit_pair(&b_empty[rb.s]);
               } else {
-                mma_commit(&b_empty[bs]);
+                mma_commit(&b_empty[rb.s]);
               }
               rb.next(BSTAGES);
             }
             // halo tile free once its windows' MMAs finish
-            if constexpr (PAIR) mma_commit_pair(&a_empty[as]);
-            else mma_commit(&a_empty[as]);
+            if constexpr (PAIR) mma_commit_pair(&a_empty[ra.s]);
+            else mma_commit(&a_empty[ra.s]);
             ra.next(AST);
           }
         }

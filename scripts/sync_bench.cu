@@ -176,6 +176,83 @@ __global__ void cons_kernel(int steps, unsigned long long* out, const __grid_con
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(256));
 }
 
+// Compile-time producer/consumer ping-pong over a 4-stage ring: R release
+// (1 tcgen05.commit, 2 plain arrive), M MMAs per step, D data-ring pairs per
+// step (1: one full/empty pair as one ring; 2: A and B rings as tc_gemm has).
+template <int R, int M, int D>
+__global__ void pp_kernel(int steps, unsigned long long* out) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  __shared__ __align__(8) uint64_t full[2][4], empty[2][4];
+  __shared__ uint32_t tslot;
+  const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0);
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < 4; ++s)
+      for (int d = 0; d < 2; ++d) {
+        mbar_init(&full[d][s], 1);
+        mbar_init(&empty[d][s], 1);
+      }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tslot)), "r"(256));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = tslot;
+  unsigned long long c0 = clock64();
+  if (warp == 0) {
+    for (int i = 0; i < steps; ++i) {
+      const int s = i & 3;
+      const uint32_t ph = ((i >> 2) & 1) ^ 1;
+      for (int d = 0; d < D; ++d) {
+        mbar_wait(&empty[d][s], ph);
+        if (elect_one()) mbar_arrive(&full[d][s]);
+        __syncwarp();
+      }
+    }
+  } else if (warp == 1) {
+    const uint32_t idesc = idesc_bf16(128, 256);
+    const uint64_t da = sw128_desc(smem), db = sw128_desc(smem + 32768);
+    for (int i = 0; i < steps; ++i) {
+      const int s = i & 3;
+      const uint32_t ph = (i >> 2) & 1;
+      for (int d = 0; d < D; ++d) mbar_wait(&full[d][s], ph);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+#pragma unroll
+      for (int k = 0; k < M; ++k) mma_bf16(tmem, da + (uint64_t)((k & 3) * 2), db + (uint64_t)((k & 3) * 2), idesc, 1u);
+      for (int d = 0; d < D; ++d) {
+        if (R == 1) mma_commit(&empty[d][s]);
+        if (R == 2) {
+          if (elect_one()) mbar_arrive(&empty[d][s]);
+          __syncwarp();
+        }
+      }
+    }
+  }
+  unsigned long long c1 = clock64();
+  __syncthreads();
+  if (threadIdx.x == 32) out[blockIdx.x] = c1 - c0;
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(256));
+}
+
+template <int R, int M, int D>
+static void run_pp(unsigned long long* d_out) {
+  const int steps = 2048, grid = 148;
+  cudaFuncSetAttribute(pp_kernel<R, M, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+  for (int rep = 0; rep < 2; ++rep) pp_kernel<R, M, D><<<grid, 64, 100 * 1024>>>(steps, d_out);
+  cudaDeviceSynchronize();
+  static unsigned long long h[4096];
+  cudaMemcpy(h, d_out, grid * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+  double mean = 0;
+  for (int i = 0; i < grid; ++i) mean += (double)h[i];
+  printf("pingpong release=%d mma=%2d rings=%d | %8.1f cycles/step\n", R, M, D, mean / grid / steps);
+}
+
 template <int W, int R, int M, int X = 0>
 static void run_cons(unsigned long long* d_out) {
   const int steps = 2048, grid = 148;
@@ -241,5 +318,11 @@ int main() {
   run_cons<1, 1, 4, 1>(d_out);
   run_cons<1, 1, 4, 3>(d_out);
   run_cons<1, 1, 4, 4>(d_out);
+  run_pp<1, 0, 1>(d_out);
+  run_pp<2, 0, 1>(d_out);
+  run_pp<1, 0, 2>(d_out);
+  run_pp<1, 4, 1>(d_out);
+  run_pp<1, 4, 2>(d_out);
+  run_pp<1, 8, 2>(d_out);
   return 0;
 }
