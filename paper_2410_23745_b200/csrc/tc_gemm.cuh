@@ -33,6 +33,14 @@ constexpr int MAXCHUNK = 32;
 constexpr int EPI_WARPS = 8;  // two per TMEM lane quarter, splitting the column chunks
 constexpr int THREADS = 64 + 32 * EPI_WARPS;
 constexpr int RING_BYTES = 192 * 1024;  // A ring (halo / dy tiles) + B ring
+// Epilogue staging (CFG 0 / pair): per epilogue warp a 32-row x 32-column
+// bf16 block with an 80-byte row pitch.  Outputs whose N dim is contiguous
+// (QKV-like) are transposed through it so that each warp store writes
+// 8 rows x 64 contiguous bytes instead of 32 rows x 16 bytes: the per-lane
+// row stores cost 32 L1 wavefronts per instruction and made the epilogue,
+// not the MMAs, the limit of such GEMMs (1x1 K=64 launches: 48 us store-bound).
+constexpr int EPI_ROW_WORDS = 20;
+constexpr int EPI_STAGE_BYTES = 8 * 32 * EPI_ROW_WORDS * 4;
 
 // MODE_ROWS processes G = 256/BN consecutive 128-row M tiles per step: one
 // contiguous A halo and one B tile per window feed G accumulators, cutting
@@ -151,11 +159,11 @@ __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
 
 __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
-               : "memory");
+              );
 }
 
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)));
 }
 
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
@@ -166,7 +174,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
       "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
       "r"(parity), "r"(0x989680)
-      : "memory");
+     );
 #else
   // spin on the non-suspending probe: the wait is on the critical path of
   // the producer -> MMA -> epilogue hand-offs
@@ -175,11 +183,16 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "WAIT_%=:\n\t"
       "mbarrier.test_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
       "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
-      "r"(parity)
-      : "memory");
+      "r"(parity));
 #endif
 }
 
+// The issue-path helpers (waits, arrives, TMA, commits) carry no "memory"
+// clobber: they are ordered among themselves as volatile asm, the producer
+// and MMA warps touch memory only through them, and a clobber would force
+// every kernel parameter to be re-read from the constant bank after each
+// one (measured: dependent LDCU chains in the per-k-step loops).
+//
 // Long waits (the epilogue warps waiting a whole tile for the accumulator):
 // the suspending probe with a time hint parks the warp instead of spinning,
 // so eight idle epilogue warps do not compete with the producer / MMA warps
@@ -200,7 +213,7 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, u
       "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];" ::
           "r"(smem_u32(dst)),
       "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
-      : "memory");
+     );
 }
 
 // CTA-pair helpers (CFG_PAIR)
@@ -229,7 +242,7 @@ __device__ __forceinline__ uint32_t peer_addr(const void* p, uint32_t rank) {
   return r;
 }
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_bar) {
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_bar) : "memory");
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_bar));
 }
 // TMA load into this CTA's shared memory whose completion is signalled on an
 // mbarrier of either CTA of the pair (the leader's full barrier)
@@ -239,7 +252,7 @@ __device__ __forceinline__ void tma_load_3d_pair(void* dst, const CUtensorMap* m
       "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];" ::
           "r"(smem_u32(dst)),
       "l"(reinterpret_cast<uint64_t>(map)), "r"(cluster_bar), "r"(c0), "r"(c1), "r"(c2)
-      : "memory");
+     );
 }
 __device__ __forceinline__ void mma_bf16_pair(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
   asm volatile(
@@ -282,7 +295,7 @@ __device__ __forceinline__ void mma_commit_pair(uint64_t* bar) {
       "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n\t}" ::"r"(
           smem_u32(bar)),
       "h"((uint16_t)3)
-      : "memory");
+     );
 }
 
 // K-major, 128-byte swizzle smem descriptor (canonical ((8,m),(T,2)) : ((8T,SBO),(1,T))),
@@ -340,7 +353,7 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
       "{\n\t.reg .pred e;\n\t"
       "elect.sync _|e, 0xffffffff;\n\t"
       "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(smem_u32(bar))
-      : "memory");
+     );
 }
 
 __device__ __forceinline__ bool elect_one() {
@@ -665,7 +678,7 @@ __global__ void __launch_bounds__(THREADS, CFG == 1 ? 2 : 1) tc_gemm_kernel(cons
       if (lane == 0) ev(9, (int)tcount, 0);  // MMA warp: next tile decoded
       mbar_wait(&tempty[acc], ((tcount >> 1) & 1u) ^ 1u);  // epilogue drained this buffer
       if (lane == 0) ev(5, (int)tcount, 0);  // MMA warp: accumulator free
-      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      asm volatile("tcgen05.fence::after_thread_sync;");
       const uint32_t dst = tmem + acc * ACC_COLS;
       uint32_t accumulate = 0;
       if constexpr (!mn) {
@@ -678,12 +691,12 @@ __global__ void __launch_bounds__(THREADS, CFG == 1 ? 2 : 1) tc_gemm_kernel(cons
             mbar_wait(&a_full[ra.s], ra.ph);
             if (lane == 0) ev(3, (int)tcount, c * 64 + cb);  // MMA warp: A halo ready
             const uint32_t a_lo0 = desc_lo(sa_u + (uint32_t)(ra.s * a_stage_bytes)) - (uint32_t)pmin * 8u;
-            if (b_res) asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            if (b_res) asm volatile("tcgen05.fence::after_thread_sync;");
             for (int w = w0; w < w1; ++w) {
               if (!b_res) {
                 mbar_wait(&b_full[rb.s], rb.ph);
                 if (lane == 0) ev(4, (int)tcount, w);  // MMA warp: B window ready
-                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                asm volatile("tcgen05.fence::after_thread_sync;");
               }
               const uint32_t b_lo = desc_lo(sb_u + (uint32_t)((b_res ? w : rb.s) * B_BYTES));
               // profiling switch 32: every window reads the aligned halo start (wrong values, timing only)
@@ -723,7 +736,7 @@ __global__ void __launch_bounds__(THREADS, CFG == 1 ? 2 : 1) tc_gemm_kernel(cons
           const int as = ra.slot(AST), bs = rb.slot(BSTAGES);
           mbar_wait(&a_full[as], ra.phase(AST));
           mbar_wait(&b_full[bs], rb.phase(BSTAGES));
-          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          asm volatile("tcgen05.fence::after_thread_sync;");
           const uint64_t da = sw128_mn_desc(sa + as * p.a_stage_bytes, 8192);
           const uint64_t db = sw128_mn_desc(sb + bs * B_BYTES, 8192);
 #pragma unroll
@@ -797,6 +810,39 @@ __global__ void __launch_bounds__(THREADS, CFG == 1 ? 2 : 1) tc_gemm_kernel(cons
           tmem_ld32(tmem + acc * ACC_COLS + (uint32_t)(g * BN) + ((uint32_t)(q * 32) << 16) + (uint32_t)c, v);
           const int nlim = min(32, p.n_ext - n0);
           const int64_t os = p.o_n;
+          if constexpr (MODE == MODE_ROWS && CFG != 1) {
+            if (p.out_kind == OUT_BF16 && os == 1 && nlim == 32 && !(dbg & 1)) {
+              __nv_bfloat16* ob = reinterpret_cast<__nv_bfloat16*>(p.out) + n0;
+              const bool al = !ok || ((reinterpret_cast<uintptr_t>(ob + off) & 15) == 0);
+              if (__all_sync(0xffffffffu, al)) {
+                // staged: my row's 32 values -> smem row `lane`, then each
+                // store instruction covers 8 rows x 64 contiguous bytes
+                uint32_t* stg = reinterpret_cast<uint32_t*>(smem + ring_bytes<CFG>() + 512) +
+                                (warp - 2) * (32 * EPI_ROW_WORDS);
+                uint4* mine = reinterpret_cast<uint4*>(stg + lane * EPI_ROW_WORDS);
+#pragma unroll
+                for (int q4 = 0; q4 < 4; ++q4) {
+                  __align__(16) __nv_bfloat162 h2[4];
+#pragma unroll
+                  for (int e = 0; e < 4; ++e)
+                    h2[e] = __floats2bfloat162_rn(have ? v[q4 * 8 + 2 * e] * scale : 0.f,
+                                                  have ? v[q4 * 8 + 2 * e + 1] * scale : 0.f);
+                  mine[q4] = *reinterpret_cast<const uint4*>(h2);
+                }
+                __syncwarp();
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                  const int rr = i * 8 + (lane >> 2), seg = lane & 3;
+                  const uint4 val = reinterpret_cast<const uint4*>(stg + rr * EPI_ROW_WORDS)[seg];
+                  const int okr = __shfl_sync(0xffffffffu, ok ? 1 : 0, rr);
+                  const long long offr = __shfl_sync(0xffffffffu, (long long)off, rr);
+                  if (okr) reinterpret_cast<uint4*>(ob + offr)[seg] = val;
+                }
+                __syncwarp();
+                continue;
+              }
+            }
+          }
           if (!ok || (dbg & 1)) {
             // masked row (pad pixel / beyond the extent): nothing to store
           } else if (MODE == MODE_WGRAD || p.out_kind == OUT_F32_ATOMIC) {
@@ -904,7 +950,7 @@ __global__ void __launch_bounds__(THREADS, CFG == 1 ? 2 : 1) tc_gemm_kernel(cons
 
 template <int BN, int CFG = 0>
 constexpr int smem_bytes() {
-  return 1024 + ring_bytes<CFG>() + 512;
+  return 1024 + ring_bytes<CFG>() + 512 + (CFG != 1 ? EPI_STAGE_BYTES : 0);
 }
 
 }  // namespace tc
