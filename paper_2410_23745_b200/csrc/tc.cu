@@ -827,6 +827,10 @@ struct ChainNC {
   unsigned* counter;               // zero between calls
 };
 
+// KH / KW: compile-time window extents (0: runtime).  With them known the
+// per-thread window values stay in registers (the runtime-bounded version
+// spilled them to local memory: a 512 x 512 x 3 x 3 chain took 16 us).
+template <int KH, int KW>
 __global__ void __launch_bounds__(256) chain_nc_kernel(const __grid_constant__ ChainArgs c, const __grid_constant__ ChainNC h) {
   pdl_trigger();
   pdl_wait();
@@ -835,30 +839,34 @@ __global__ void __launch_bounds__(256) chain_nc_kernel(const __grid_constant__ C
   const bool live = i < (int64_t)h.N * h.C;
   const int n = live ? (int)(i / h.C) : 0, ci = live ? (int)(i - (int64_t)n * h.C) : 0;
   const int64_t plane = (int64_t)h.N * h.C;
-  const int KK = h.Kh * h.Kw;  // <= 16 (host-checked)
-  const int KKo_w = h.ow ? h.Kw : 1;
-  const int KKo = (h.oh ? h.Kh : 1) * KKo_w;
+  constexpr int KKT = KH * KW;
+  constexpr int VN = KKT ? KKT : 16;
+  const int Kw = KW ? KW : h.Kw;
+  const int KK = KKT ? KKT : h.Kh * h.Kw;  // <= 16 (host-checked)
+  const int KKo_w = h.ow ? Kw : 1;
+  const int KKo = (h.oh ? (KH ? KH : h.Kh) : 1) * KKo_w;
   float* my = stage + threadIdx.x * KKo;
   for (int q = 0; q < KKo; ++q) my[q] = 0.f;
   if (live) {
     // all windows' loads in flight together, then the zeroing stores
     float* __restrict__ src = c.dwf + i;
-    float v[16];
+    float v[VN];
 #pragma unroll
-    for (int k = 0; k < 16; ++k)
+    for (int k = 0; k < VN; ++k)
       if (k < KK) v[k] = src[k * plane];
     if (c.zero_dwf) {
 #pragma unroll
-      for (int k = 0; k < 16; ++k)
+      for (int k = 0; k < VN; ++k)
         if (k < KK) src[k * plane] = 0.f;
     }
     float* vs = stage + blockDim.x * KKo + threadIdx.x * 17;  // per-thread window values (odd stride)
 #pragma unroll
-    for (int k = 0; k < 16; ++k)
+    for (int k = 0; k < VN; ++k)
       if (k < KK) vs[k] = v[k];
-#pragma unroll 1
-    for (int k = 0; k < KK; ++k) {
-      const int kh = k / h.Kw, kw = k - kh * h.Kw;
+#pragma unroll
+    for (int k = 0; k < VN; ++k) {
+      if (k >= KK) break;
+      const int kh = k / Kw, kw = k - kh * Kw;
       const float d = vs[k];
       float x = d;
 #pragma unroll 1
@@ -2256,7 +2264,10 @@ static void chain_fast(const TcPlan& tp, const TcWs& w, const Bindings& b, DType
       h.counter = w.chain_counter;
     }
     const size_t sm = (size_t)256 * (kko + 17) * sizeof(float);
-    launch_k(chain_nc_kernel, (unsigned)((nthreads + 255) / 256), 256, sm, stream, c, h);
+    const unsigned grid = (unsigned)((nthreads + 255) / 256);
+    if (h.Kh == 3 && h.Kw == 3) launch_k(chain_nc_kernel<3, 3>, grid, 256, sm, stream, c, h);
+    else if (h.Kh == 1 && h.Kw == 1) launch_k(chain_nc_kernel<1, 1>, grid, 256, sm, stream, c, h);
+    else launch_k(chain_nc_kernel<0, 0>, grid, 256, sm, stream, c, h);
     cuda_check(cudaGetLastError(), "chain kernel");
     prof_end(id, stream);
     return;
