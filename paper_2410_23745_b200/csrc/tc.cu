@@ -1422,6 +1422,10 @@ static bool tc_log();
 static void gemm(TcGemmParams& p, int bn, int m_tiles, int n_tiles, int z_tiles, cudaStream_t stream,
                  const char* name, double flops) {
   if (skip_class("gemm")) return;
+  {
+    const int split = p.mode == MODE_ROWS ? std::max(1, p.rsplit) : std::max(1, p.ksplit);
+    p.k_per = (p.n_cblocks + split - 1) / split;
+  }
   const bool pair = p.cfg == CFG_PAIR;
   // pair: the kernel's M tiles are pairs of 128-row tiles
   p.m_tiles = pair ? (m_tiles + 1) / 2 : m_tiles;
@@ -1733,6 +1737,7 @@ static void rows_schedule(TcGemmParams& p, std::vector<std::vector<Win>> groups,
       p.chunk_w1[nc - 1] = n;
     }
     p.g_chunk1[g] = nc;
+    p.g_nwin[g] = (int32_t)ws.size();
   }
   p.n_win = n;
   p.G = G;

@@ -116,6 +116,8 @@ struct alignas(64) TcGemmParams {
   // MODE_ROWS chunks: windows [chunk_w0, chunk_w1) share A plane chunk_plane and min shift chunk_pmin
   int32_t chunk_plane[MAXCHUNK], chunk_w0[MAXCHUNK], chunk_w1[MAXCHUNK], chunk_pmin[MAXCHUNK];
   int32_t g_chunk0[8], g_chunk1[8];  // chunk range of each group (blockIdx-level z)
+  int32_t g_nwin[8];                 // windows of each group (host: sum of its chunks' windows)
+  int32_t k_per;                     // channel blocks (MODE_ROWS) / pixel blocks (MODE_WGRAD) per split
   // MODE_WGRAD pairs: M rows [64h, 64h+64) of tile mt are pair 2*mt+h = (window, channel block)
   int32_t n_pairs;
   int16_t pair_win[MAXPAIR], pair_cb[MAXPAIR];
@@ -386,28 +388,58 @@ struct TileInfo {
   int cb0, cb1;  // MODE_ROWS channel-block range of this split
 };
 
-__device__ __forceinline__ TileInfo tile_info(const TcGemmParams& p, int t) {
+// Persistent tile walk without per-tile integer division: the first tile
+// and the stride are decomposed once into (n, m, z) digits and each step
+// adds the stride's digits with carries.  The per-tile k-step count and the
+// split widths come precomputed from the host (g_nwin, k_per).
+struct TileWalk {
+  int nt, mt, z, dn, dm, dz;
+  __device__ __forceinline__ void init(const TcGemmParams& p, int t0, int step) {
+    nt = t0 % p.n_tiles;
+    int q = t0 / p.n_tiles;
+    mt = q % p.m_tiles;
+    z = q / p.m_tiles;
+    dn = step % p.n_tiles;
+    q = step / p.n_tiles;
+    dm = q % p.m_tiles;
+    dz = q / p.m_tiles;
+  }
+  __device__ __forceinline__ void next(const TcGemmParams& p) {
+    nt += dn;
+    int c = 0;
+    if (nt >= p.n_tiles) {
+      nt -= p.n_tiles;
+      c = 1;
+    }
+    mt += dm + c;
+    c = 0;
+    if (mt >= p.m_tiles) {
+      mt -= p.m_tiles;
+      c = 1;
+    }
+    z += dz + c;
+  }
+};
+
+__device__ __forceinline__ TileInfo tile_info(const TcGemmParams& p, const TileWalk& w) {
   TileInfo ti;
-  ti.nt = t % p.n_tiles;
-  int q = t / p.n_tiles;
-  ti.mt = q % p.m_tiles;
-  const int z = q / p.m_tiles;
+  ti.nt = w.nt;
+  ti.mt = w.mt;
+  const int z = w.z;
   if (p.mode == MODE_ROWS) {
     const int rs = p.rsplit > 1 ? p.rsplit : 1;
-    ti.g = z / rs;
+    ti.g = rs == 1 ? z : z / rs;
     ti.ks = z - ti.g * rs;
-    const int per = (p.n_cblocks + rs - 1) / rs;
+    const int per = p.k_per;
     ti.cb0 = ti.ks * per;
     ti.cb1 = min(p.n_cblocks, ti.cb0 + per);
     ti.kb0 = 0;
-    ti.nkb = 0;
-    for (int c = p.g_chunk0[ti.g]; c < p.g_chunk1[ti.g]; ++c) ti.nkb += p.chunk_w1[c] - p.chunk_w0[c];
-    ti.nkb *= max(0, ti.cb1 - ti.cb0);  // MMA k-steps (one per window x channel block)
+    ti.nkb = p.g_nwin[ti.g] * max(0, ti.cb1 - ti.cb0);  // MMA k-steps (one per window x channel block)
   } else {
     ti.cb0 = ti.cb1 = 0;
-    ti.ks = z % p.ksplit;
-    ti.g = z / p.ksplit;
-    const int per = (p.n_cblocks + p.ksplit - 1) / p.ksplit;
+    ti.g = p.ksplit == 1 ? z : z / p.ksplit;
+    ti.ks = z - ti.g * p.ksplit;
+    const int per = p.k_per;
     ti.kb0 = ti.ks * per;
     const int kb1 = min(p.n_cblocks, ti.kb0 + per);
     ti.nkb = kb1 > ti.kb0 ? kb1 - ti.kb0 : 0;
@@ -474,8 +506,8 @@ __global__ void __launch_bounds__(THREADS, CFG == 1 ? 2 : 1) tc_gemm_kernel(cons
   const uint32_t rank = PAIR ? cluster_rank() : 0u;
   const int t_first = PAIR ? (int)cluster_id_x() : (int)blockIdx.x;
   const int t_step = PAIR ? (int)n_clusters_x() : (int)gridDim.x;
-  auto tinfo = [&](int t) {
-    TileInfo ti = tile_info(p, t);
+  auto tinfo = [&](const TileWalk& w) {
+    TileInfo ti = tile_info(p, w);
     if (PAIR) ti.mt = 2 * ti.mt + (int)rank;
     return ti;
   };
@@ -576,8 +608,10 @@ __global__ void __launch_bounds__(THREADS, CFG == 1 ? 2 : 1) tc_gemm_kernel(cons
       }
       __syncwarp();
     }
-    for (int t = t_first; t < n_tiles_total; t += t_step, ++pcount) {
-      const TileInfo ti = tinfo(t);
+    TileWalk tw;
+    tw.init(p, t_first, t_step);
+    for (int t = t_first; t < n_tiles_total; t += t_step, ++pcount, tw.next(p)) {
+      const TileInfo ti = tinfo(tw);
       if constexpr (MODE == MODE_ROWS) {
         for (int c = p.g_chunk0[ti.g]; c < p.g_chunk1[ti.g]; ++c) {
           for (int cb = ti.cb0; cb < ti.cb1; ++cb) {
@@ -672,8 +706,10 @@ __global__ void __launch_bounds__(THREADS, CFG == 1 ? 2 : 1) tc_gemm_kernel(cons
     const uint32_t sa_u = smem_u32(sa), sb_u = smem_u32(sb);
     const int a_stage_bytes = p.a_stage_bytes, Gr = p.G;
     if (b_res && blockIdx.x < n_tiles_total) mbar_wait(&b_full[0], 0);  // resident B tiles landed
-    for (int t = t_first; t < n_tiles_total; t += t_step, ++tcount) {
-      const TileInfo ti = tinfo(t);
+    TileWalk tw;
+    tw.init(p, t_first, t_step);
+    for (int t = t_first; t < n_tiles_total; t += t_step, ++tcount, tw.next(p)) {
+      const TileInfo ti = tinfo(tw);
       const uint32_t acc = tcount & 1u;
       if (lane == 0) ev(9, (int)tcount, 0);  // MMA warp: next tile decoded
       mbar_wait(&tempty[acc], ((tcount >> 1) & 1u) ^ 1u);  // epilogue drained this buffer
@@ -771,8 +807,10 @@ __global__ void __launch_bounds__(THREADS, CFG == 1 ? 2 : 1) tc_gemm_kernel(cons
     const int half = (warp - 2) >> 2;
     const int r = q * 32 + lane;
     uint32_t tcount = 0;
-    for (int t = t_first; t < n_tiles_total; t += t_step, ++tcount) {
-      const TileInfo ti = tinfo(t);
+    TileWalk tw;
+    tw.init(p, t_first, t_step);
+    for (int t = t_first; t < n_tiles_total; t += t_step, ++tcount, tw.next(p)) {
+      const TileInfo ti = tinfo(tw);
       const uint32_t acc = tcount & 1u;
       if (dbg & 64) mbar_wait(&tfull[acc], (tcount >> 1) & 1u);
       else mbar_wait_sleep(&tfull[acc], (tcount >> 1) & 1u);
