@@ -1459,6 +1459,8 @@ static void gemm(TcGemmParams& p, int bn, int m_tiles, int n_tiles, int z_tiles,
     if (small) {
       if (bn == 64) launch_gemm<64, MODE_WGRAD, 1>(p, grid, stream);
       else launch_gemm<128, MODE_WGRAD, 1>(p, grid, stream);
+    } else if (pair) {
+      launch_gemm<256, MODE_WGRAD, CFG_PAIR>(p, grid, stream);
     } else if (bn == 64) launch_gemm<64, MODE_WGRAD, 0>(p, grid, stream);
     else if (bn == 128) launch_gemm<128, MODE_WGRAD, 0>(p, grid, stream);
     else launch_gemm<256, MODE_WGRAD, 0>(p, grid, stream);
@@ -1987,6 +1989,12 @@ static void build_ws(TcPlan& tp, TcWs& w, DType dt) {
     int ksplit = std::max(1, (waves * sm_count() * (p.cfg ? 2 : 1)) / std::max(1, m_tiles * n_tiles));
     ksplit = std::min(ksplit, std::max(1, p.n_cblocks / 4));
     p.ksplit = ksplit;
+    // CTA pair (BN = 256, two or more M tiles): each CTA stages half of the
+    // dy columns; SYNO_TC_PAIR=0 / SYNO_TC_WG_PAIR=0 disable
+    static const bool wg_pair = !(getenv("SYNO_TC_PAIR") && atoi(getenv("SYNO_TC_PAIR")) == 0) &&
+                                !(getenv("SYNO_TC_WG_PAIR") && atoi(getenv("SYNO_TC_WG_PAIR")) == 0);
+    const bool pair_wg = wg_pair && bn == 256 && m_tiles >= 2 && getenv("SYNO_TC_FIXUP") == nullptr;
+    if (pair_wg) p.cfg = CFG_PAIR;
     p.m_ext = tp.C;
     p.n_ext = tp.N;
     p.o_m = 1;
@@ -1998,7 +2006,7 @@ static void build_ws(TcPlan& tp, TcWs& w, DType dt) {
     p.a_rows = 64;
     p.a_tx = (uint32_t)BM * BK * 2;
     p.a_stage_bytes = BM * BK * 2;
-    p.b_tx = (uint32_t)bn * BK * 2;
+    p.b_tx = (uint32_t)(pair_wg ? bn / 2 : bn) * BK * 2;
     w.bn_wg = bn;
     w.t_wg[0] = m_tiles;
     w.t_wg[1] = n_tiles;

@@ -467,7 +467,7 @@ template <int BN, int MODE, int CFG>
 __global__ void __launch_bounds__(THREADS, CFG == 1 ? 2 : 1) tc_gemm_kernel(const __grid_constant__ TcGemmParams p) {
   pdl_trigger();
   constexpr bool PAIR = CFG == CFG_PAIR;
-  static_assert(!PAIR || (MODE == MODE_ROWS && BN == 256), "CTA pair: MODE_ROWS, BN = 256");
+  static_assert(!PAIR || BN == 256, "CTA pair: BN = 256");
   constexpr int BSTAGES = b_stages<BN, CFG>();
   constexpr int B_BYTES = b_rows<BN, CFG>() * BK * 2;
   constexpr int G = gmax<BN, CFG>();
@@ -670,14 +670,18 @@ __global__ void __launch_bounds__(THREADS, CFG == 1 ? 2 : 1) tc_gemm_kernel(cons
           const int as = ra.slot(AST);
           mbar_wait(&a_empty[as], ra.phase(AST) ^ 1u);
           if (elect_one()) {
-            mbar_expect_tx(&a_full[as], p.a_tx);
+            if (!PAIR || rank == 0) mbar_expect_tx(&a_full[as], PAIR ? 2 * p.a_tx : p.a_tx);
 #pragma unroll
             for (int h = 0; h < BM / 64; ++h) {
               int pr = ti.mt * 2 + h;
-              if (pr >= p.n_pairs) pr = ti.mt * 2;  // masked rows: reload a valid pair
+              if (pr >= p.n_pairs) pr = 0;  // masked rows (beyond the pairs): reload a valid pair
               const int w = p.pair_win[pr];
-              tma_load_3d(sa + as * p.a_stage_bytes + h * 8192, &p.tma_a, &a_full[as], p.pair_cb[pr] * 64,
-                          kb * BK + p.a_shift[w], p.a_plane[w]);
+              if constexpr (PAIR)
+                tma_load_3d_pair(sa + as * p.a_stage_bytes + h * 8192, &p.tma_a, peer_addr(&a_full[as], 0),
+                                 p.pair_cb[pr] * 64, kb * BK + p.a_shift[w], p.a_plane[w]);
+              else
+                tma_load_3d(sa + as * p.a_stage_bytes + h * 8192, &p.tma_a, &a_full[as], p.pair_cb[pr] * 64,
+                            kb * BK + p.a_shift[w], p.a_plane[w]);
             }
           }
           __syncwarp();
@@ -685,10 +689,19 @@ __global__ void __launch_bounds__(THREADS, CFG == 1 ? 2 : 1) tc_gemm_kernel(cons
           const int bs = rb.slot(BSTAGES);
           mbar_wait(&b_empty[bs], rb.phase(BSTAGES) ^ 1u);
           if (elect_one()) {
-            mbar_expect_tx(&b_full[bs], p.b_tx);
+            if constexpr (PAIR) {
+              // this CTA's half of the N columns
+              if (rank == 0) mbar_expect_tx(&b_full[bs], 2 * p.b_tx);
 #pragma unroll
-            for (int h = 0; h < BN / 64; ++h)
-              tma_load_3d(sb + bs * B_BYTES + h * 8192, &p.tma_b, &b_full[bs], ti.nt * BN + h * 64, kb * BK, 0);
+              for (int h = 0; h < BN / 128; ++h)
+                tma_load_3d_pair(sb + bs * B_BYTES + h * 8192, &p.tma_b, peer_addr(&b_full[bs], 0),
+                                 ti.nt * BN + (int)rank * (BN / 2) + h * 64, kb * BK, 0);
+            } else {
+              mbar_expect_tx(&b_full[bs], p.b_tx);
+#pragma unroll
+              for (int h = 0; h < BN / 64; ++h)
+                tma_load_3d(sb + bs * B_BYTES + h * 8192, &p.tma_b, &b_full[bs], ti.nt * BN + h * 64, kb * BK, 0);
+            }
           }
           __syncwarp();
           rb.next(BSTAGES);
@@ -700,7 +713,7 @@ __global__ void __launch_bounds__(THREADS, CFG == 1 ? 2 : 1) tc_gemm_kernel(cons
    if (!PAIR || rank == 0) {
     // ---------------- MMA issuer: warp-wide loop, elected-lane issue
     constexpr bool mn = MODE == MODE_WGRAD;
-    const uint32_t idesc = mn ? idesc_bf16(BM, BN, 1, 1) : idesc_bf16(PAIR ? 2 * BM : BM, BN);
+    const uint32_t idesc = mn ? idesc_bf16(PAIR ? 2 * BM : BM, BN, 1, 1) : idesc_bf16(PAIR ? 2 * BM : BM, BN);
     Ring ra, rb;
     uint32_t tcount = 0;
     const uint32_t sa_u = smem_u32(sa), sb_u = smem_u32(sb);
@@ -778,11 +791,19 @@ __global__ void __launch_bounds__(THREADS, CFG == 1 ? 2 : 1) tc_gemm_kernel(cons
 #pragma unroll
           for (int k = 0; k < BK / 16; ++k) {
             // MN-major K advance: two 8-row k groups (2 x 1024 B)
-            mma_bf16(dst, da + (uint64_t)(k * 128), db + (uint64_t)(k * 128), idesc, accumulate);
+            if constexpr (PAIR)
+              mma_bf16_pair(dst, da + (uint64_t)(k * 128), db + (uint64_t)(k * 128), idesc, accumulate);
+            else
+              mma_bf16(dst, da + (uint64_t)(k * 128), db + (uint64_t)(k * 128), idesc, accumulate);
             accumulate = 1;
           }
-          mma_commit(&a_empty[as]);
-          mma_commit(&b_empty[bs]);
+          if constexpr (PAIR) {
+            mma_commit_pair(&a_empty[as]);
+            mma_commit_pair(&b_empty[bs]);
+          } else {
+            mma_commit(&a_empty[as]);
+            mma_commit(&b_empty[bs]);
+          }
           ra.next(AST);
           rb.next(BSTAGES);
         }
