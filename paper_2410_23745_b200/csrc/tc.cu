@@ -1777,6 +1777,10 @@ struct TcWs {
   // zero-copy operands: a source already in the packed layout (channels-last,
   // unpadded, e.g. QKV activations) is read by TMA in place
   bool x_ident = false, xw_ident = false, dyg_ident = false, dyw_ident = false;
+  // the forward B operand IS the weight (one bf16 [N][C] weight, one window,
+  // no channel padding, QKV-like): TMA reads it in place, no fold launch
+  bool wf_ident = false;
+  MapSpec ms_fwd_b;
   const void* packed_x_src = nullptr;  // x whose packed operand xcl currently holds (last forward)
   std::vector<const void*> wt_src;      // weights the grad-input operand wt was folded from (last forward)
   MapSpec ms_fwd_a, ms_dg_a, ms_wg_a, ms_wg_b;
@@ -1861,7 +1865,10 @@ static void build_ws(TcPlan& tp, TcWs& w, DType dt) {
     const int b_box = set_pair(p, bn, rt);
     w.ms_fwd_a = map_spec(Ck, F, planes, Ck, F * Ck, 64);
     p.tma_a = make_map(w.xcl, w.ms_fwd_a);
-    p.tma_b = make_map(w.wf, Ck, tp.N, tp.nwin(), Ck, (int64_t)tp.N * Ck, b_box);
+    w.ms_fwd_b = map_spec(Ck, tp.N, tp.nwin(), Ck, (int64_t)tp.N * Ck, b_box);
+    p.tma_b = make_map(w.wf, w.ms_fwd_b);
+    w.wf_ident = !w.f32 && tp.fast_fold && tp.nw == 1 && tp.nwin() == 1 && tp.wstr[0][2] == tp.C &&
+                 tp.wstr[0][3] == 1 && Ck == tp.C && tp.C % 8 == 0 && getenv("SYNO_TC_NO_WZC") == nullptr;
     p.Hp = w.gx.Hp;
     p.Wp = w.gx.Wp;
     p.lo_h = w.gx.lo_h;
@@ -2389,17 +2396,19 @@ bool tc_forward(TcPlan& tp, DType dt, const Bindings& b, cudaStream_t stream) {
   TcGemmParams p = w.fwd;
   w.wt_src.clear();
   bool fused = false;
+  const bool w_zero = w.wf_ident && aligned16(b.w.at(0));
+  if (w_zero) p.tma_b = make_map(b.w[0], w.ms_fwd_b);
   if (w.x_ident && aligned16(b.x)) {
     p.tma_a = make_map(b.x, w.ms_fwd_a);
-  } else if (pack_and_fold(tp, b, dt, b.x, w.gx, w.xcl, false, w.f32, w.wf, stream)) {
+  } else if (!w_zero && pack_and_fold(tp, b, dt, b.x, w.gx, w.xcl, false, w.f32, w.wf, stream)) {
     w.packed_x_src = b.x;
     fused = true;
   } else {
     pack_cl(b.x, dt, w.gx, w.xcl, stream);
     w.packed_x_src = b.x;
   }
-  if (fused) {
-    // operand folded by the fused launch
+  if (fused || w_zero) {
+    // operand folded by the fused launch / read in place
   } else if (tp.fast_fold && tp.dgrad_ok && fold_dual(tp, b, dt, w.f32, w.wf, w.wt, stream)) {
     w.wt_src = b.w;
   } else if (tp.fast_fold) {
