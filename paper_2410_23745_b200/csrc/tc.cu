@@ -859,15 +859,15 @@ __global__ void __launch_bounds__(256) chain_nc_kernel(const __grid_constant__ C
       for (int k = 0; k < VN; ++k)
         if (k < KK) src[k * plane] = 0.f;
     }
-    float* vs = stage + blockDim.x * KKo + threadIdx.x * 17;  // per-thread window values (odd stride)
-#pragma unroll
-    for (int k = 0; k < VN; ++k)
-      if (k < KK) vs[k] = v[k];
+    // per-thread window values of the side output (odd stride); the smem
+    // region exists only when h.side_j >= 0 (a small block leaves room to
+    // co-reside with a concurrent persistent GEMM CTA)
+    float* vs = stage + blockDim.x * KKo + threadIdx.x * 17;
 #pragma unroll
     for (int k = 0; k < VN; ++k) {
       if (k >= KK) break;
       const int kh = k / Kw, kw = k - kh * Kw;
-      const float d = vs[k];
+      const float d = v[k];
       float x = d;
 #pragma unroll 1
       for (int q = 0; q < c.nw; ++q) {
@@ -2283,7 +2283,7 @@ static void chain_fast(const TcPlan& tp, const TcWs& w, const Bindings& b, DType
       h.partial = w.chain_partial;
       h.counter = w.chain_counter;
     }
-    const size_t sm = (size_t)256 * (kko + 17) * sizeof(float);
+    const size_t sm = (size_t)256 * (kko + (side >= 0 ? 17 : 0)) * sizeof(float);
     const unsigned grid = (unsigned)((nthreads + 255) / 256);
     if (h.Kh == 3 && h.Kw == 3) launch_k(chain_nc_kernel<3, 3>, grid, 256, sm, stream, c, h);
     else if (h.Kh == 1 && h.Kw == 1) launch_k(chain_nc_kernel<1, 1>, grid, 256, sm, stream, c, h);
