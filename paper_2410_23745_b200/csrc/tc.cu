@@ -968,6 +968,28 @@ __global__ void __launch_bounds__(256) chain_nc_kernel(const __grid_constant__ C
   }
 }
 
+// Single weight whose every window is an output (conv3x3, strided and 1x1
+// convolutions): dW_j[n][ci][kh][kw] = dWf[k][n][ci], one thread per dWf
+// element (coalesced reads and re-zeroing), grid.y over the windows, so even
+// a 64 x 64 layer launches 16 x 9 blocks instead of 16 latency-bound ones.
+__global__ void __launch_bounds__(256) chain_win_kernel(const __grid_constant__ ChainArgs c,
+                                                        const __grid_constant__ ChainNC h) {
+  pdl_trigger();
+  pdl_wait();
+  const int64_t plane = (int64_t)h.N * h.C;
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= plane) return;
+  const int k = blockIdx.y;
+  const int kh = k / h.Kw, kw = k - kh * h.Kw;
+  const int n = (int)(i / h.C), ci = (int)(i - (int64_t)n * h.C);
+  float* src = c.dwf + (int64_t)k * plane + i;
+  const float v = *src;
+  if (c.zero_dwf) *src = 0.f;
+  const int64_t o = (int64_t)n * h.so_n + (int64_t)ci * h.so_c + (int64_t)kh * h.so_h + (int64_t)kw * h.so_w;
+  if (c.f32) reinterpret_cast<float*>(c.out)[o] = v;
+  else reinterpret_cast<__nv_bfloat16*>(c.out)[o] = __float2bfloat16(v);
+}
+
 // Long reductions: block (o, split) reduces one chunk; the last block of an
 // output sums the partials in split order (deterministic) and stores.
 __global__ void __launch_bounds__(256) chain_block_kernel(const __grid_constant__ ChainArgs c) {
@@ -2285,7 +2307,10 @@ static void chain_fast(const TcPlan& tp, const TcWs& w, const Bindings& b, DType
     }
     const size_t sm = (size_t)256 * (kko + (side >= 0 ? 17 : 0)) * sizeof(float);
     const unsigned grid = (unsigned)((nthreads + 255) / 256);
-    if (h.Kh == 3 && h.Kw == 3) launch_k(chain_nc_kernel<3, 3>, grid, 256, sm, stream, c, h);
+    static const bool win_split = getenv("SYNO_TC_NO_CHAIN_WIN") == nullptr;
+    if (win_split && tp.nw == 1 && side < 0 && (h.oh || h.Kh == 1) && (h.ow || h.Kw == 1) && h.Kh * h.Kw > 1) {
+      launch_k(chain_win_kernel, dim3(grid, (unsigned)(h.Kh * h.Kw)), 256, 0, stream, c, h);
+    } else if (h.Kh == 3 && h.Kw == 3) launch_k(chain_nc_kernel<3, 3>, grid, 256, sm, stream, c, h);
     else if (h.Kh == 1 && h.Kw == 1) launch_k(chain_nc_kernel<1, 1>, grid, 256, sm, stream, c, h);
     else launch_k(chain_nc_kernel<0, 0>, grid, 256, sm, stream, c, h);
     cuda_check(cudaGetLastError(), "chain kernel");
