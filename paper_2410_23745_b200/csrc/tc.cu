@@ -1447,6 +1447,8 @@ static void gemm(TcGemmParams& p, int bn, int m_tiles, int n_tiles, int z_tiles,
   {
     const int split = p.mode == MODE_ROWS ? std::max(1, p.rsplit) : std::max(1, p.ksplit);
     p.k_per = (p.n_cblocks + split - 1) / split;
+    // pair grad-weight stages two K blocks: every split but the last covers an even count
+    if (p.mode == MODE_WGRAD && p.cfg == CFG_PAIR) p.k_per += p.k_per & 1;
   }
   const bool pair = p.cfg == CFG_PAIR;
   // pair: the kernel's M tiles are pairs of 128-row tiles
@@ -2033,9 +2035,9 @@ static void build_ws(TcPlan& tp, TcWs& w, DType dt) {
     p.scale = (float)tp.scale;
     p.out = w.dwf;
     p.a_rows = 64;
-    p.a_tx = (uint32_t)BM * BK * 2;
-    p.a_stage_bytes = BM * BK * 2;
-    p.b_tx = (uint32_t)(pair_wg ? bn / 2 : bn) * BK * 2;
+    p.a_tx = (uint32_t)BM * BK * 2 * (pair_wg ? 2 : 1);  // the pair kernel stages two K blocks
+    p.a_stage_bytes = (int)p.a_tx;
+    p.b_tx = (uint32_t)(pair_wg ? bn / 2 * 2 : bn) * BK * 2;
     w.bn_wg = bn;
     w.t_wg[0] = m_tiles;
     w.t_wg[1] = n_tiles;

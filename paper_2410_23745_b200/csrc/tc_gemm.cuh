@@ -468,8 +468,12 @@ __global__ void __launch_bounds__(THREADS, CFG == 1 ? 2 : 1) tc_gemm_kernel(cons
   pdl_trigger();
   constexpr bool PAIR = CFG == CFG_PAIR;
   static_assert(!PAIR || BN == 256, "CTA pair: BN = 256");
-  constexpr int BSTAGES = b_stages<BN, CFG>();
-  constexpr int B_BYTES = b_rows<BN, CFG>() * BK * 2;
+  // KM: 64-element K blocks per ring stage.  The pair grad-weight kernel
+  // stages two (3 x 64 KB per CTA), halving the barrier hand-offs per MAC.
+  constexpr int KM = PAIR && MODE == MODE_WGRAD ? 2 : 1;
+  constexpr int BSTAGES = KM == 2 ? 3 : b_stages<BN, CFG>();
+  constexpr int B_BYTES = b_rows<BN, CFG>() * BK * 2 * KM;
+  static_assert(BSTAGES * B_BYTES == b_stages<BN, CFG>() * b_rows<BN, CFG>() * BK * 2, "B ring size");
   constexpr int G = gmax<BN, CFG>();
   constexpr uint32_t ACC_COLS = G * BN;          // one accumulator buffer: G sub-tiles
   constexpr uint32_t TMEM_COLS = 2 * ACC_COLS;   // double-buffered (512 for CFG 0)
@@ -665,8 +669,8 @@ __global__ void __launch_bounds__(THREADS, CFG == 1 ? 2 : 1) tc_gemm_kernel(cons
           }
         }
       } else {
-        for (int i = 0; i < ti.nkb; ++i) {
-          const int kb = ti.kb0 + i;
+        for (int i = 0; i < (ti.nkb + KM - 1) / KM; ++i) {
+          const int kb = ti.kb0 + KM * i;
           const int as = ra.slot(AST);
           mbar_wait(&a_empty[as], ra.phase(AST) ^ 1u);
           if (elect_one()) {
@@ -676,12 +680,17 @@ __global__ void __launch_bounds__(THREADS, CFG == 1 ? 2 : 1) tc_gemm_kernel(cons
               int pr = ti.mt * 2 + h;
               if (pr >= p.n_pairs) pr = 0;  // masked rows (beyond the pairs): reload a valid pair
               const int w = p.pair_win[pr];
-              if constexpr (PAIR)
-                tma_load_3d_pair(sa + as * p.a_stage_bytes + h * 8192, &p.tma_a, peer_addr(&a_full[as], 0),
-                                 p.pair_cb[pr] * 64, kb * BK + p.a_shift[w], p.a_plane[w]);
-              else
-                tma_load_3d(sa + as * p.a_stage_bytes + h * 8192, &p.tma_a, &a_full[as], p.pair_cb[pr] * 64,
-                            kb * BK + p.a_shift[w], p.a_plane[w]);
+#pragma unroll
+              for (int kq = 0; kq < KM; ++kq) {
+                // K block kb + kq at +16 KB (the last split's odd tail reads zero dy rows)
+                if constexpr (PAIR)
+                  tma_load_3d_pair(sa + as * p.a_stage_bytes + kq * 16384 + h * 8192, &p.tma_a,
+                                   peer_addr(&a_full[as], 0), p.pair_cb[pr] * 64, (kb + kq) * BK + p.a_shift[w],
+                                   p.a_plane[w]);
+                else
+                  tma_load_3d(sa + as * p.a_stage_bytes + h * 8192, &p.tma_a, &a_full[as], p.pair_cb[pr] * 64,
+                              kb * BK + p.a_shift[w], p.a_plane[w]);
+              }
             }
           }
           __syncwarp();
@@ -693,9 +702,11 @@ __global__ void __launch_bounds__(THREADS, CFG == 1 ? 2 : 1) tc_gemm_kernel(cons
               // this CTA's half of the N columns
               if (rank == 0) mbar_expect_tx(&b_full[bs], 2 * p.b_tx);
 #pragma unroll
-              for (int h = 0; h < BN / 128; ++h)
-                tma_load_3d_pair(sb + bs * B_BYTES + h * 8192, &p.tma_b, peer_addr(&b_full[bs], 0),
-                                 ti.nt * BN + (int)rank * (BN / 2) + h * 64, kb * BK, 0);
+              for (int kq = 0; kq < KM; ++kq)
+#pragma unroll
+                for (int h = 0; h < BN / 128; ++h)
+                  tma_load_3d_pair(sb + bs * B_BYTES + kq * 16384 + h * 8192, &p.tma_b, peer_addr(&b_full[bs], 0),
+                                   ti.nt * BN + (int)rank * (BN / 2) + h * 64, (kb + kq) * BK, 0);
             } else {
               mbar_expect_tx(&b_full[bs], p.b_tx);
 #pragma unroll
@@ -781,7 +792,7 @@ __global__ void __launch_bounds__(THREADS, CFG == 1 ? 2 : 1) tc_gemm_kernel(cons
           }
         }
       } else {
-        for (int i = 0; i < ti.nkb; ++i) {
+        for (int i = 0; i < (ti.nkb + KM - 1) / KM; ++i) {
           const int as = ra.slot(AST), bs = rb.slot(BSTAGES);
           mbar_wait(&a_full[as], ra.phase(AST));
           mbar_wait(&b_full[bs], rb.phase(BSTAGES));
@@ -789,12 +800,14 @@ __global__ void __launch_bounds__(THREADS, CFG == 1 ? 2 : 1) tc_gemm_kernel(cons
           const uint64_t da = sw128_mn_desc(sa + as * p.a_stage_bytes, 8192);
           const uint64_t db = sw128_mn_desc(sb + bs * B_BYTES, 8192);
 #pragma unroll
-          for (int k = 0; k < BK / 16; ++k) {
-            // MN-major K advance: two 8-row k groups (2 x 1024 B)
+          for (int k = 0; k < KM * BK / 16; ++k) {
+            // MN-major K advance: two 8-row k groups (2 x 1024 B) per 16 K;
+            // the second 64-block of a KM = 2 stage starts 16 KB further
+            const uint64_t ko = (uint64_t)((k & 3) * 128 + (k >> 2) * (16384 >> 4));
             if constexpr (PAIR)
-              mma_bf16_pair(dst, da + (uint64_t)(k * 128), db + (uint64_t)(k * 128), idesc, accumulate);
+              mma_bf16_pair(dst, da + ko, db + ko, idesc, accumulate);
             else
-              mma_bf16(dst, da + (uint64_t)(k * 128), db + (uint64_t)(k * 128), idesc, accumulate);
+              mma_bf16(dst, da + ko, db + ko, idesc, accumulate);
             accumulate = 1;
           }
           if constexpr (PAIR) {
