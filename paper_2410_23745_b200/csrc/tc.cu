@@ -1876,6 +1876,7 @@ static void build_ws(TcPlan& tp, TcWs& w, DType dt) {
     memset(&p, 0, sizeof(p));
     p.mode = MODE_ROWS;
     p.n_cblocks = (Ck + BK - 1) / BK;
+    p.kq_last = (Ck - (p.n_cblocks - 1) * BK + 15) / 16;  // 16-wide MMA K steps of the last channel block
     std::vector<std::vector<Win>> groups(1);
     for (int rh = 0; rh < tp.dh.K; ++rh)
       for (int rw = 0; rw < tp.dw.K; ++rw)
@@ -1945,6 +1946,7 @@ static void build_ws(TcPlan& tp, TcWs& w, DType dt) {
     memset(&p, 0, sizeof(p));
     p.mode = MODE_ROWS;
     p.n_cblocks = (Nk + BK - 1) / BK;
+    p.kq_last = (Nk - (p.n_cblocks - 1) * BK + 15) / 16;
     const int Sh = tp.dh.S, Sw = tp.dw.S;
     std::vector<std::vector<Win>> groups(Sh * Sw);
     for (int ph = 0; ph < Sh; ++ph)

@@ -118,6 +118,8 @@ struct alignas(64) TcGemmParams {
   int32_t g_chunk0[8], g_chunk1[8];  // chunk range of each group (blockIdx-level z)
   int32_t g_nwin[8];                 // windows of each group (host: sum of its chunks' windows)
   int32_t k_per;                     // channel blocks (MODE_ROWS) / pixel blocks (MODE_WGRAD) per split
+  int32_t kq_last;                   // MODE_ROWS: 16-wide K steps holding data in the last channel block
+                                     // (a 3-channel stem padded to 8 issues 1 MMA per window, not 4)
   // MODE_WGRAD pairs: M rows [64h, 64h+64) of tile mt are pair 2*mt+h = (window, channel block)
   int32_t n_pairs;
   int16_t pair_win[MAXPAIR], pair_cb[MAXPAIR];
@@ -728,7 +730,8 @@ __global__ void __launch_bounds__(THREADS, CFG == 1 ? 2 : 1) tc_gemm_kernel(cons
     Ring ra, rb;
     uint32_t tcount = 0;
     const uint32_t sa_u = smem_u32(sa), sb_u = smem_u32(sb);
-    const int a_stage_bytes = p.a_stage_bytes, Gr = p.G;
+    const int a_stage_bytes = p.a_stage_bytes, Gr = p.G, n_cb = p.n_cblocks;
+    const int kq_last = p.kq_last > 0 ? p.kq_last : BK / 16;
     if (b_res && blockIdx.x < n_tiles_total) mbar_wait(&b_full[0], 0);  // resident B tiles landed
     TileWalk tw;
     tw.init(p, t_first, t_step);
@@ -748,6 +751,7 @@ __global__ void __launch_bounds__(THREADS, CFG == 1 ? 2 : 1) tc_gemm_kernel(cons
         for (int c = p.g_chunk0[ti.g]; c < c1; ++c) {
           const int w0 = p.chunk_w0[c], w1 = p.chunk_w1[c], pmin = p.chunk_pmin[c];
           for (int cb = ti.cb0; cb < ti.cb1; ++cb) {
+            const int nk = cb == n_cb - 1 ? kq_last : BK / 16;
             mbar_wait(&a_full[ra.s], ra.ph);
             if (lane == 0) ev(3, (int)tcount, c * 64 + cb);  // MMA warp: A halo ready
             const uint32_t a_lo0 = desc_lo(sa_u + (uint32_t)(ra.s * a_stage_bytes)) - (uint32_t)pmin * 8u;
@@ -767,8 +771,9 @@ __global__ void __launch_bounds__(THREADS, CFG == 1 ? 2 : 1) tc_gemm_kernel(cons
                   if (g >= Gr) break;
 #pragma unroll
                   for (int k = 0; k < BK / 16; ++k)
-                    mma_lo<PAIR>(dst + g * BN, a_lo + (uint32_t)(g * BM * 8 + k * 2), b_lo + (uint32_t)(k * 2), idesc,
-                                 (accumulate || k > 0) ? 1u : 0u);
+                    if (k < nk)
+                      mma_lo<PAIR>(dst + g * BN, a_lo + (uint32_t)(g * BM * 8 + k * 2), b_lo + (uint32_t)(k * 2),
+                                   idesc, (accumulate || k > 0) ? 1u : 0u);
                 }
               }
               accumulate = 1;
