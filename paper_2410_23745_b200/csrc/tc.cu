@@ -1450,6 +1450,8 @@ static void gemm(TcGemmParams& p, int bn, int m_tiles, int n_tiles, int z_tiles,
     // pair grad-weight stages two K blocks: every split but the last covers an even count
     if (p.mode == MODE_WGRAD && p.cfg == CFG_PAIR) p.k_per += p.k_per & 1;
   }
+  if (p.mode == MODE_ROWS && (int64_t)m_tiles * std::max(1, p.G) * BM >= INT32_MAX)
+    fail(SYNO_E_UNSUPPORTED, "tc: 2^31 or more rows in one operand plane");
   const bool pair = p.cfg == CFG_PAIR;
   // pair: the kernel's M tiles are pairs of 128-row tiles
   p.m_tiles = pair ? (m_tiles + 1) / 2 : m_tiles;

@@ -864,14 +864,16 @@ __global__ void __launch_bounds__(THREADS, CFG == 1 ? 2 : 1) tc_gemm_kernel(cons
         bool ok;
         int64_t off;
         if constexpr (MODE == MODE_ROWS) {
-          const int64_t flat = ((int64_t)ti.mt * p.G + g) * BM + r;
-          const int64_t wp = flat % p.Wp;
-          const int64_t tq = flat / p.Wp;
-          const int64_t hp = tq % p.Hp;
-          const int64_t img = tq / p.Hp;
-          const int64_t h = hp - p.lo_h, w = wp - p.lo_w;
-          ok = img < p.n_img && h >= 0 && h < p.H && w >= 0 && w < p.W;
-          off = p.g_out_off[ti.g] + img * p.o_img + h * p.o_h + w * p.o_w;
+          // 32-bit row decode (the padded grid has < 2^31 rows per plane,
+          // host-checked): 64-bit div / mod are subroutine calls
+          const uint32_t flat = (uint32_t)((ti.mt * p.G + g) * BM + r);
+          const uint32_t tq = flat / (uint32_t)p.Wp;
+          const int wp = (int)(flat - tq * (uint32_t)p.Wp);
+          const uint32_t img = tq / (uint32_t)p.Hp;
+          const int hp = (int)(tq - img * (uint32_t)p.Hp);
+          const int h = hp - p.lo_h, w = wp - p.lo_w;
+          ok = (int)img < p.n_img && h >= 0 && h < p.H && w >= 0 && w < p.W;
+          off = p.g_out_off[ti.g] + (int64_t)img * p.o_img + (int64_t)h * p.o_h + (int64_t)w * p.o_w;
         } else {
           const int pr = ti.mt * 2 + (r >> 6);
           const int ci = pr < p.n_pairs ? p.pair_cb[pr] * 64 + (r & 63) : p.m_ext;
