@@ -107,6 +107,31 @@ def test_tc_qkv_projection(cuda, batch, t):
     assert _rel(dw, wf.grad) < 2e-2
 
 
+def test_tc_qkv_projection_fp32_pair(cuda):
+    """fp32 through the split-bf16 path on the CTA-pair configuration
+    (forward, grad-input and grad-weight all BN = 256 with several M tiles),
+    against torch float64, tolerance 1e-4 rel."""
+    import torch
+    from paper_2410_23745_b200 import ops
+    from paper_2410_23745_b200 import pgraph as P
+    from paper_2410_23745_b200 import workloads as WL
+    L = WL.qkv(batch=4, t=512)
+    hd = P.handle_for(L.graph)
+    g = torch.Generator(device="cpu").manual_seed(5)
+    x = torch.randn(hd.x_shape, generator=g).to("cuda")
+    w = (torch.randn(hd.w_shapes[0], generator=g) * 0.05).to("cuda")
+    dy = torch.randn(hd.y_shape, generator=g).to("cuda")
+    y = ops.forward(hd, x, [w])
+    dx, (dw,) = ops.backward(hd, x, [w], dy)
+    xd = x.double().requires_grad_(True)
+    wd = w.double().requires_grad_(True)
+    yr = xd @ wd.t()
+    yr.backward(dy.double())
+    assert _rel(y, yr) < 1e-4
+    assert _rel(dx, xd.grad) < 1e-4
+    assert _rel(dw, wd.grad) < 1e-4
+
+
 @pytest.mark.parametrize("op,c_in,c_out,h,batch", [("conv3x3", 64, 64, 16, 2), ("sep_shared", 64, 64, 16, 2),
                                                    ("conv3x3_s2", 64, 128, 8, 2)])
 @pytest.mark.parametrize("dtype", ["bfloat16", "float32"])
