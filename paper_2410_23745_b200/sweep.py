@@ -91,10 +91,6 @@ def within_budget(flops: int, params: int, flops_cap: Optional[int], params_cap:
     return True
 
 
-def _inner(a, b) -> float:
-    return float((a.double() * b.double()).sum())
-
-
 def evaluate(graph, sample_id: int, seed: int, dtype=None, device=None,
              flops_cap: Optional[int] = None, params_cap: Optional[int] = None,
              tol: Optional[float] = None) -> EvalRecord:
@@ -112,10 +108,15 @@ def evaluate(graph, sample_id: int, seed: int, dtype=None, device=None,
     op = print_steps(graph)
     if not within_budget(h.flops_unstaged, h.params, flops_cap, params_cap):
         return EvalRecord(sample_id, seed, h.flops_unstaged, h.params, "over_budget", op)
+    # one seeded draw for every input (x, the weights, dy), split into views:
+    # a candidate is launch-bound, so fewer host-side ops matter
     gen = torch.Generator(device=device).manual_seed(seed)
-    x = torch.randn(h.x_shape, generator=gen, device=device, dtype=torch.float32).to(dtype)
-    ws = [torch.randn(s, generator=gen, device=device, dtype=torch.float32).to(dtype) for s in h.w_shapes]
-    dy = torch.randn(h.y_shape, generator=gen, device=device, dtype=torch.float32).to(dtype)
+    shapes = [tuple(h.x_shape)] + [tuple(s) for s in h.w_shapes] + [tuple(h.y_shape)]
+    sizes = [math.prod(s) for s in shapes]
+    slots = [(n + 7) // 8 * 8 for n in sizes]  # every part starts 16-byte aligned (bf16 and fp32)
+    flat = torch.randn(sum(slots), generator=gen, device=device, dtype=torch.float32).to(dtype)
+    parts = [p[:n].view(s) for p, n, s in zip(torch.split(flat, slots), sizes, shapes)]
+    x, ws, dy = parts[0], parts[1:-1], parts[-1]
     stream = torch.cuda.current_stream(device)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     try:
@@ -127,11 +128,14 @@ def evaluate(graph, sample_id: int, seed: int, dtype=None, device=None,
     except Exception as exc:  # a device-engine limit or launch failure: logged like a RewardFailure
         return EvalRecord(sample_id, seed, h.flops_unstaged, h.params, "failed", op,
                           error=f"{type(exc).__name__}: {str(exc).splitlines()[0] if str(exc) else ''}"[:200])
-    s = _inner(dy, y)
-    scale = max(1.0, math.sqrt(_inner(dy, dy) * max(_inner(y, y), 1e-30)))
-    err = abs(_inner(dx, x) - s) / scale
-    for w, g in zip(ws, dws):
-        err = max(err, abs(_inner(g, w) - s) / scale)
+    # every inner product in float64 on the device, one host read
+    ip = torch.stack([(a.double() * b.double()).sum() for a, b in
+                      [(dy, y), (dy, dy), (y, y), (dx, x)] + list(zip(dws, ws))]).tolist()
+    s = ip[0]
+    scale = max(1.0, math.sqrt(ip[1] * max(ip[2], 1e-30)))
+    err = abs(ip[3] - s) / scale
+    for v in ip[4:]:
+        err = max(err, abs(v - s) / scale)
     limit = tol if tol is not None else (1e-4 if dtype == torch.float32 else 2e-2 if dtype == torch.bfloat16 else 1e-10)
     status = "ok" if err <= limit and math.isfinite(err) else "failed"
     return EvalRecord(sample_id, seed, h.flops_unstaged, h.params, status, op,
