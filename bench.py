@@ -381,7 +381,9 @@ def run_layers(args, rank, world, device, peaks):
 def measure_e2e(state, phases, args, device, dtype, world):
     """The same step through the public API (ops.forward / ops.backward) with
     HOST buffers: pinned host -> device copies of every layer's x (and dy),
-    compute, device -> host copies of y (and dx, every dW), all timed."""
+    compute, device -> host copies of y (and dx, every dW), all timed.  The
+    copies run on two copy streams (the link is full duplex) and overlap the
+    compute layer by layer; the timed region ends after the last copy."""
     import torch
 
     from paper_2410_23745_b200 import ops
@@ -399,19 +401,50 @@ def measure_e2e(state, phases, args, device, dtype, world):
         h2d += hx.numel() * esz + (0 if fwd_only else hdy.numel() * esz)
         d2h += hy.numel() * esz + (0 if fwd_only else (hdx.numel() + sum(g.numel() for g in hdw)) * esz)
     stream = torch.cuda.current_stream(device)
+    # copies overlap compute: host->device on one copy stream (every layer's
+    # inputs as fast as the link allows), device->host on another (each
+    # layer's results as soon as they exist), compute waits per layer; the
+    # step ends when the last device->host copy lands on the compute stream
+    up, down = torch.cuda.Stream(device), torch.cuda.Stream(device)
+    n_l = len(state)
+    ev_in = [torch.cuda.Event() for _ in range(n_l)]
+    ev_y = [torch.cuda.Event() for _ in range(n_l)]
+    ev_b = [torch.cuda.Event() for _ in range(n_l)]
+    ev_start, ev_down = torch.cuda.Event(), torch.cuda.Event()
 
     def step():
-        for s, (hx, hdy, hy, hdx, hdw) in zip(state, host):
-            s["x"].copy_(hx, non_blocking=True)
-            if not fwd_only:
-                s["dy"].copy_(hdy, non_blocking=True)
+        ev_start.record(stream)  # the previous step is done with every buffer
+        up.wait_event(ev_start)
+        down.wait_event(ev_start)
+        with torch.cuda.stream(up):
+            for i, (s, (hx, hdy, hy, hdx, hdw)) in enumerate(zip(state, host)):
+                s["x"].copy_(hx, non_blocking=True)
+                if not fwd_only:
+                    s["dy"].copy_(hdy, non_blocking=True)
+                ev_in[i].record(up)
+        outs = []
+        for i, s in enumerate(state):
+            stream.wait_event(ev_in[i])
             ops.forward(s["h"], s["x"], s["ws"], out=s["y"])
-            hy.copy_(s["y"], non_blocking=True)
+            ev_y[i].record(stream)
             if not fwd_only:
                 dx, dws = ops.backward(s["h"], s["x"], s["ws"], s["dy"])
-                hdx.copy_(dx, non_blocking=True)
-                for a, b in zip(hdw, dws):
-                    a.copy_(b, non_blocking=True)
+                for t in [dx] + list(dws):
+                    t.record_stream(down)
+                outs.append((dx, dws))
+                ev_b[i].record(stream)
+        with torch.cuda.stream(down):
+            for i, (s, (hx, hdy, hy, hdx, hdw)) in enumerate(zip(state, host)):
+                down.wait_event(ev_y[i])
+                hy.copy_(s["y"], non_blocking=True)
+                if not fwd_only:
+                    down.wait_event(ev_b[i])
+                    dx, dws = outs[i]
+                    hdx.copy_(dx, non_blocking=True)
+                    for a, b in zip(hdw, dws):
+                        a.copy_(b, non_blocking=True)
+            ev_down.record(down)
+        stream.wait_event(ev_down)
 
     for _ in range(max(1, min(args.warmup, 3))):
         step()
