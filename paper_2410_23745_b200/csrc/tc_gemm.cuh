@@ -71,7 +71,7 @@ __host__ __device__ constexpr int gmax() {
 }
 template <int BN, int CFG = 0>
 __host__ __device__ constexpr int b_stages() {
-  return CFG == CFG_PAIR ? 6 : CFG && BN >= 128 ? 2 : 4;
+  return CFG == CFG_PAIR ? 6 : CFG && BN >= 128 ? 3 : 4;
 }
 // B rows one CTA stages per k-step (the pair splits N)
 template <int BN, int CFG = 0>
