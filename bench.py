@@ -214,6 +214,12 @@ def layer_work(h, esize):
             "fwd_bytes": esize * (nx + nw + ny), "bwd_bytes": esize * (nx + nw + ny + nx + nw)}
 
 
+def unit_of(workload):
+    """Throughput unit of a layer workload: one batch element (an image, or a
+    T-token sequence for the QKV projection)."""
+    return "sequences/s" if workload == "qkv" else "images/s"
+
+
 def run_layers(args, rank, world, device, peaks):
     import ctypes
 
@@ -374,7 +380,7 @@ def run_layers(args, rank, world, device, peaks):
         "step_roofline_frac": (t_roof * 1e3) / ms_max, "step_tflops": step_flops / (ms_max / 1e3) / 1e12,
         "gpu_launches": int(launches), "clocks": sampler.summary() if rank == 0 else None,
         "e2e": e2e, "breakdown_ms": {k: round(statistics.median(v), 4) for k, v in times.items()},
-        "dtype": "bf16" if dtype == torch.bfloat16 else "f32", "unit": "images/s",
+        "dtype": "bf16" if dtype == torch.bfloat16 else "f32", "unit": unit_of(args.workload),
     }
 
 
@@ -458,7 +464,7 @@ def measure_e2e(state, phases, args, device, dtype, world):
     torch.cuda.synchronize(device)
     ms = allreduce_max(t0.elapsed_time(t1) / n, world, device)
     units = state[0]["h"].x_shape[0]
-    return {"value": world * units / (ms / 1e3), "unit": "images/s", "ms_per_step": ms,
+    return {"value": world * units / (ms / 1e3), "unit": unit_of(args.workload), "ms_per_step": ms,
             "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h}
 
 
@@ -621,9 +627,10 @@ def cpu_sample_spec(args):
     mult = 1 if fwd_only else 3
     flops_one = mult * h1.flops_unstaged
     per_image = sum(mult * P.handle_for(lay.graph).flops_unstaged for lay in layers) / batch
-    desc = (f"1 image of layer {L.name} ({L.op}) " + ("forward" if fwd_only else "fwd+grad-input+grad-weight")
+    elem = "sequence" if args.workload == "qkv" else "image"
+    desc = (f"1 {elem} of layer {L.name} ({L.op}) " + ("forward" if fwd_only else "fwd+grad-input+grad-weight")
             + (" at T=128" if args.workload == "qkv" else "")
-            + " in float64; images/s extrapolated by the layer's FLOP share of the full step")
+            + f" in float64; {unit_of(args.workload)} extrapolated by the layer's FLOP share of the full step")
     return spec, flops_one, per_image, desc
 
 
@@ -638,7 +645,8 @@ def cpu_baseline_layers(args, processes=1):
         with mp.get_context("fork").Pool(processes) as pool:
             pool.map(_oracle_job, jobs)
     dt = time.perf_counter() - t0
-    return {"value": processes * flops_one / dt / per_image, "unit": "images/s", "cores": processes, "kind": "port",
+    return {"value": processes * flops_one / dt / per_image, "unit": unit_of(args.workload), "cores": processes,
+            "kind": "port",
             "sample": desc + f" ({processes} process(es), {dt:.1f} s)", "seconds": dt}
 
 
