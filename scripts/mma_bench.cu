@@ -162,7 +162,65 @@ static void run_fixed(int n, int iters, int commit_every, int per_sm, unsigned l
          per_sm, mean / ((double)iters * CHAIN) / per_sm);
 }
 
+// MN-major operands (both A and B, as the grad-weight GEMM uses): one warp
+// issues chains of 128 x N x 16 MMAs from 128-byte-swizzled MN-major tiles.
+__global__ void mma_mn_kernel(int n, int chain, int iters, int per_sm_div, unsigned long long* out) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  __shared__ uint32_t tslot;
+  __shared__ __align__(8) uint64_t bar;
+  const int warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tslot)), "r"(256));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = tslot;
+  unsigned long long c0 = 0, c1 = 0;
+  if (warp == 0) {
+    const uint32_t idesc = idesc_bf16(128, n, 1, 1);
+    const uint64_t da = sw128_mn_desc(smem, 8192), db = sw128_mn_desc(smem + 32768, 8192);
+    c0 = clock64();
+    uint32_t nc = 0;
+    for (int it = 0; it < iters; ++it) {
+      for (int k = 0; k < chain; ++k)
+        mma_bf16(tmem, da + (uint64_t)((k & 3) * 128), db + (uint64_t)((k & 3) * 128), idesc, 1u);
+      mma_commit(&bar);
+      ++nc;
+    }
+    mbar_wait(&bar, (nc - 1) & 1u);
+    c1 = clock64();
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) out[blockIdx.x] = c1 - c0;
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(256));
+}
+
 int main() {
+  {
+    unsigned long long* d_o;
+    cudaMalloc(&d_o, 4096 * sizeof(unsigned long long));
+    static unsigned long long hh[4096];
+    cudaFuncSetAttribute(mma_mn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+    for (int n : {64, 128, 256}) {
+      for (int rep = 0; rep < 2; ++rep) mma_mn_kernel<<<148, 128, 100 * 1024>>>(n, 16, 128, 1, d_o);
+      cudaDeviceSynchronize();
+      cudaMemcpy(hh, d_o, 148 * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+      double mean = 0;
+      for (int i = 0; i < 148; ++i) mean += (double)hh[i];
+      printf("MN-major A and B: N=%3d chain=16 | %8.1f cycles/MMA/SM (floor %d)\n", n, mean / 148 / (128.0 * 16),
+             128 * n / 256);
+    }
+    cudaFree(d_o);
+  }
   unsigned long long* d_out;
   cudaMalloc(&d_out, 4096 * sizeof(unsigned long long));
   unsigned long long h[4096];
