@@ -2019,10 +2019,17 @@ static void build_ws(TcPlan& tp, TcWs& w, DType dt) {
         }
       }
     const int m_tiles = (p.n_pairs + 1) / 2, n_tiles = (tp.N + bn - 1) / bn;
-    static const int waves = getenv("SYNO_TC_WG_WAVES") ? atoi(getenv("SYNO_TC_WG_WAVES")) : 1;
+    // split-K sized to fill the grid once; long contractions (>= 64 pixel
+    // blocks per split) fill it twice (measured: QKV 0.184 -> 0.178 ms,
+    // ResNet-18's short splits slower at two waves); SYNO_TC_WG_WAVES overrides
+    static const int waves_env = getenv("SYNO_TC_WG_WAVES") ? atoi(getenv("SYNO_TC_WG_WAVES")) : 0;
     p.cfg = use_small_cfg(bn) ? 1 : 0;
-    int ksplit = std::max(1, (waves * sm_count() * (p.cfg ? 2 : 1)) / std::max(1, m_tiles * n_tiles));
-    ksplit = std::min(ksplit, std::max(1, p.n_cblocks / 4));
+    auto split_for = [&](int waves) {
+      const int k = std::max(1, (waves * sm_count() * (p.cfg ? 2 : 1)) / std::max(1, m_tiles * n_tiles));
+      return std::min(k, std::max(1, p.n_cblocks / 4));
+    };
+    int ksplit = split_for(waves_env > 0 ? waves_env : 1);
+    if (waves_env <= 0 && p.n_cblocks / ksplit >= 64) ksplit = split_for(2);
     p.ksplit = ksplit;
     // CTA pair (BN = 256, two or more M tiles): each CTA stages half of the
     // dy columns; SYNO_TC_PAIR=0 / SYNO_TC_WG_PAIR=0 disable
