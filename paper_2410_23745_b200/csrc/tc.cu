@@ -990,6 +990,33 @@ __global__ void __launch_bounds__(256) chain_win_kernel(const __grid_constant__ 
   else reinterpret_cast<__nv_bfloat16*>(c.out)[o] = __float2bfloat16(v);
 }
 
+// Single weight, single window, dense [N][C] gradient (QKV-like): dW = dWf
+// cast, dWf re-zeroed; four elements per thread with 16-byte accesses.
+__global__ void __launch_bounds__(256) chain_cast_kernel(float* __restrict__ dwf, void* __restrict__ out, int64_t n,
+                                                         int f32, int zero) {
+  pdl_trigger();
+  pdl_wait();
+  const int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4;
+  if (i + 3 < n) {
+    const float4 v = *reinterpret_cast<const float4*>(dwf + i);
+    if (zero) *reinterpret_cast<float4*>(dwf + i) = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (f32) {
+      *reinterpret_cast<float4*>(reinterpret_cast<float*>(out) + i) = v;
+    } else {
+      __nv_bfloat162* o = reinterpret_cast<__nv_bfloat162*>(reinterpret_cast<__nv_bfloat16*>(out) + i);
+      o[0] = __floats2bfloat162_rn(v.x, v.y);
+      o[1] = __floats2bfloat162_rn(v.z, v.w);
+    }
+  } else {
+    for (int64_t k = i; k < n; ++k) {
+      const float v = dwf[k];
+      if (zero) dwf[k] = 0.f;
+      if (f32) reinterpret_cast<float*>(out)[k] = v;
+      else reinterpret_cast<__nv_bfloat16*>(out)[k] = __float2bfloat16(v);
+    }
+  }
+}
+
 // Long reductions: block (o, split) reduces one chunk; the last block of an
 // output sums the partials in split order (deterministic) and stores.
 __global__ void __launch_bounds__(256) chain_block_kernel(const __grid_constant__ ChainArgs c) {
@@ -2321,7 +2348,12 @@ static void chain_fast(const TcPlan& tp, const TcWs& w, const Bindings& b, DType
     const size_t sm = (size_t)256 * (kko + (side >= 0 ? 17 : 0)) * sizeof(float);
     const unsigned grid = (unsigned)((nthreads + 255) / 256);
     static const bool win_split = getenv("SYNO_TC_NO_CHAIN_WIN") == nullptr;
-    if (win_split && tp.nw == 1 && side < 0 && (h.oh || h.Kh == 1) && (h.ow || h.Kw == 1) && h.Kh * h.Kw > 1) {
+    const bool aligned = (reinterpret_cast<uintptr_t>(c.out) & 15) == 0 && (reinterpret_cast<uintptr_t>(c.dwf) & 15) == 0;
+    if (tp.nw == 1 && side < 0 && h.Kh * h.Kw == 1 && h.so_c == 1 && h.so_n == h.C && aligned) {
+      const int64_t n = (int64_t)h.N * h.C;
+      launch_k(chain_cast_kernel, (unsigned)((n / 4 + 256) / 256), 256, 0, stream, c.dwf, c.out, n, c.f32,
+               c.zero_dwf);
+    } else if (win_split && tp.nw == 1 && side < 0 && (h.oh || h.Kh == 1) && (h.ow || h.Kw == 1) && h.Kh * h.Kw > 1) {
       launch_k(chain_win_kernel, dim3(grid, (unsigned)(h.Kh * h.Kw)), 256, 0, stream, c, h);
     } else if (h.Kh == 3 && h.Kw == 3) launch_k(chain_nc_kernel<3, 3>, grid, 256, sm, stream, c, h);
     else if (h.Kh == 1 && h.Kw == 1) launch_k(chain_nc_kernel<1, 1>, grid, 256, sm, stream, c, h);
