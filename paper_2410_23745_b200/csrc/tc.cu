@@ -835,9 +835,10 @@ __global__ void __launch_bounds__(256) chain_nc_kernel(const __grid_constant__ C
   pdl_trigger();
   pdl_wait();
   extern __shared__ float stage[];  // [blockDim.x][KKo]: each thread's window outputs
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int i32 = blockIdx.x * blockDim.x + threadIdx.x;  // N * C < 2^31 (host-checked)
+  const int64_t i = i32;
   const bool live = i < (int64_t)h.N * h.C;
-  const int n = live ? (int)(i / h.C) : 0, ci = live ? (int)(i - (int64_t)n * h.C) : 0;
+  const int n = live ? i32 / h.C : 0, ci = live ? i32 - n * h.C : 0;
   const int64_t plane = (int64_t)h.N * h.C;
   constexpr int KKT = KH * KW;
   constexpr int VN = KKT ? KKT : 16;
@@ -976,12 +977,13 @@ __global__ void __launch_bounds__(256) chain_win_kernel(const __grid_constant__ 
                                                         const __grid_constant__ ChainNC h) {
   pdl_trigger();
   pdl_wait();
-  const int64_t plane = (int64_t)h.N * h.C;
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t plane = (int64_t)h.N * h.C;  // < 2^31 (host-checked)
+  const int i32 = blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t i = i32;
   if (i >= plane) return;
   const int k = blockIdx.y;
   const int kh = k / h.Kw, kw = k - kh * h.Kw;
-  const int n = (int)(i / h.C), ci = (int)(i - (int64_t)n * h.C);
+  const int n = i32 / h.C, ci = i32 - n * h.C;  // 32-bit: a 64-bit divide is a subroutine call
   float* src = c.dwf + (int64_t)k * plane + i;
   const float v = *src;
   if (c.zero_dwf) *src = 0.f;
