@@ -1836,6 +1836,9 @@ struct TcWs {
   // no channel padding, QKV-like): TMA reads it in place, no fold launch
   bool wf_ident = false;
   MapSpec ms_fwd_b;
+  // the same weight as the grad-input B operand, read MN-major in place
+  bool wt_ident = false;
+  MapSpec ms_dg_b_mn;
   const void* packed_x_src = nullptr;  // x whose packed operand xcl currently holds (last forward)
   std::vector<const void*> wt_src;      // weights the grad-input operand wt was folded from (last forward)
   MapSpec ms_fwd_a, ms_dg_a, ms_wg_a, ms_wg_b;
@@ -1996,6 +1999,10 @@ static void build_ws(TcPlan& tp, TcWs& w, DType dt) {
     p.rsplit = rt.rs;
     set_b_res(p, bn, (tp.C + bn - 1) / bn);
     const int b_box = set_pair(p, bn, rt);
+    // MN-major view of a [N][C] weight: dims (C, N), 64 K (= N) rows per box
+    w.wt_ident = !w.f32 && tp.fast_fold && tp.nw == 1 && tp.nwin() == 1 && tp.wstr[0][2] == tp.C &&
+                 tp.wstr[0][3] == 1 && tp.C % 8 == 0 && !p.b_res && getenv("SYNO_TC_NO_WZC") == nullptr;
+    w.ms_dg_b_mn = map_spec(tp.C, tp.N, 1, tp.C, (int64_t)tp.N * tp.C, 64);
     w.ms_dg_a = map_spec(Nk, Fg, 1, Nk, Fg * Nk, 64);
     p.tma_a = make_map(w.dycl_g, w.ms_dg_a);
     p.tma_b = make_map(w.wt, Nk, tp.C, tp.nwin(), Nk, (int64_t)tp.C * Nk, b_box);
@@ -2504,7 +2511,12 @@ bool tc_backward(TcPlan& tp, DType dt, const Bindings& b, cudaStream_t stream) {
   cudaStream_t wstream = stream;
   if (b.dx) {
     TcGemmParams p = w.dg;
-    const bool wt_ready = b.w_unchanged && !w.wt_src.empty() && w.wt_src == b.w;
+    const bool wt_zero = w.wt_ident && aligned16(b.w.at(0));
+    if (wt_zero) {
+      p.tma_b = make_map(b.w[0], w.ms_dg_b_mn);
+      p.b_mn = 1;
+    }
+    const bool wt_ready = wt_zero || (b.w_unchanged && !w.wt_src.empty() && w.wt_src == b.w);
     bool fused = false;
     if (w.dyg_ident && aligned16(b.dy)) {
       p.tma_a = make_map(b.dy, w.ms_dg_a);

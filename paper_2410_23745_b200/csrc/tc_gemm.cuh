@@ -110,6 +110,9 @@ struct alignas(64) TcGemmParams {
   // windows stay resident in shared memory (loaded once per CTA), so the
   // window loop issues no B loads and no per-window commits
   int32_t b_res;
+  // MODE_ROWS: B read MN-major (64-wide N atoms of 64 K rows, 8 KB apart):
+  // a QKV-like grad-input reads the [N_out][C] weight in place, no transpose
+  int32_t b_mn;
   int32_t a_shift[MAXWIN];   // MODE_ROWS: row shift of A per window; MODE_WGRAD: B row (pixel) shift
   int32_t a_plane[MAXWIN];   // MODE_WGRAD: plane (phase) of x per window
   int32_t b_plane[MAXWIN];   // MODE_ROWS: B plane (packed weight window) per window
@@ -656,13 +659,27 @@ __global__ void __launch_bounds__(THREADS, CFG == 1 ? 2 : 1) tc_gemm_kernel(cons
                 if constexpr (PAIR) {
                   // this CTA's half of the N rows
                   if (rank == 0) mbar_expect_tx(&b_full[bs], 2 * p.b_tx);
-                  tma_load_3d_pair(sb + bs * B_BYTES, &p.tma_b, peer_addr(&b_full[bs], 0), cb * BK,
-                                   ti.nt * BN + (int)rank * (BN / 2), p.b_plane[w]);
+                  if (p.b_mn) {
+#pragma unroll 1
+                    for (int h = 0; h < BN / 128; ++h)
+                      tma_load_3d_pair(sb + bs * B_BYTES + h * 8192, &p.tma_b, peer_addr(&b_full[bs], 0),
+                                       ti.nt * BN + (int)rank * (BN / 2) + h * 64, cb * BK, p.b_plane[w]);
+                  } else {
+                    tma_load_3d_pair(sb + bs * B_BYTES, &p.tma_b, peer_addr(&b_full[bs], 0), cb * BK,
+                                     ti.nt * BN + (int)rank * (BN / 2), p.b_plane[w]);
+                  }
                 } else if (dbg & 8) {
                   mbar_arrive(&b_full[bs]);
                 } else {
                   mbar_expect_tx(&b_full[bs], p.b_tx);
-                  tma_load_3d(sb + bs * B_BYTES, &p.tma_b, &b_full[bs], cb * BK, ti.nt * BN, p.b_plane[w]);
+                  if (p.b_mn) {
+#pragma unroll 1
+                    for (int h = 0; h < BN / 64; ++h)
+                      tma_load_3d(sb + bs * B_BYTES + h * 8192, &p.tma_b, &b_full[bs], ti.nt * BN + h * 64, cb * BK,
+                                  p.b_plane[w]);
+                  } else {
+                    tma_load_3d(sb + bs * B_BYTES, &p.tma_b, &b_full[bs], cb * BK, ti.nt * BN, p.b_plane[w]);
+                  }
                 }
               }
               __syncwarp();
@@ -726,7 +743,10 @@ __global__ void __launch_bounds__(THREADS, CFG == 1 ? 2 : 1) tc_gemm_kernel(cons
    if (!PAIR || rank == 0) {
     // ---------------- MMA issuer: warp-wide loop, elected-lane issue
     constexpr bool mn = MODE == MODE_WGRAD;
-    const uint32_t idesc = mn ? idesc_bf16(PAIR ? 2 * BM : BM, BN, 1, 1) : idesc_bf16(PAIR ? 2 * BM : BM, BN);
+    const int b_mn = MODE == MODE_ROWS ? p.b_mn : 0;
+    const uint32_t bk_step = b_mn ? 128u : 2u;
+    const uint32_t idesc =
+        mn ? idesc_bf16(PAIR ? 2 * BM : BM, BN, 1, 1) : idesc_bf16(PAIR ? 2 * BM : BM, BN, 0, b_mn);
     Ring ra, rb;
     uint32_t tcount = 0;
     const uint32_t sa_u = smem_u32(sa), sb_u = smem_u32(sb);
@@ -762,7 +782,9 @@ __global__ void __launch_bounds__(THREADS, CFG == 1 ? 2 : 1) tc_gemm_kernel(cons
                 if (lane == 0) ev(4, (int)tcount, w);  // MMA warp: B window ready
                 asm volatile("tcgen05.fence::after_thread_sync;");
               }
-              const uint32_t b_lo = desc_lo(sb_u + (uint32_t)((b_res ? w : rb.s) * B_BYTES));
+              const uint32_t b_addr = sb_u + (uint32_t)((b_res ? w : rb.s) * B_BYTES);
+              // MN-major: LBO = 8 KB between 64-wide N atoms, K step = two 8-row groups (2 KB)
+              const uint32_t b_lo = b_mn ? ((b_addr >> 4) | ((8192u >> 4) << 16)) : desc_lo(b_addr);
               // profiling switch 32: every window reads the aligned halo start (wrong values, timing only)
               const uint32_t a_lo = (dbg & 32) ? a_lo0 + (uint32_t)pmin * 8u : a_lo0 + (uint32_t)p.a_shift[w] * 8u;
               if (!(dbg & 2)) {
@@ -772,7 +794,7 @@ __global__ void __launch_bounds__(THREADS, CFG == 1 ? 2 : 1) tc_gemm_kernel(cons
 #pragma unroll
                   for (int k = 0; k < BK / 16; ++k)
                     if (k < nk)
-                      mma_lo<PAIR>(dst + g * BN, a_lo + (uint32_t)(g * BM * 8 + k * 2), b_lo + (uint32_t)(k * 2),
+                      mma_lo<PAIR>(dst + g * BN, a_lo + (uint32_t)(g * BM * 8 + k * 2), b_lo + (uint32_t)(k * bk_step),
                                    idesc, (accumulate || k > 0) ? 1u : 0u);
                 }
               }
