@@ -19,8 +19,10 @@ proxy training of 12 GPT-2-small QKV projections as synthesized operators
 with the NCCL gradient allreduce.
 
 --impl reference times the reference's CPU implementation of the same path
-on the host cores: the pinned numpy restatement in oracle/ (the reference
-is pure Python with no compiled artifact to build), rank 0 only.
+on the host cores: the unmodified reference package (opsmith, installed
+into baseline/_ref) through its own interpret / weight_gradient, with the
+pinned oracle restatement for grad-input (absent in the reference), rank 0
+only.  That arm never loads libsyno.so.
 """
 from __future__ import annotations
 
@@ -161,7 +163,9 @@ def roofline_from_profile(prof, steps, step_ms, peaks):
         return None, {}
     dom, s = max(pooled.items(), key=lambda kv: kv[1]["ms"])
     per_launch_ms = s["ms"] / max(1, s["launches"])
-    tpeak = peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"])
+    # the burst peak: a millisecond-scale step is far shorter than the 4 s
+    # back-to-back run the sustained figure is measured over
+    tpeak = peaks["bf16_tflops"]
     if s["flops"] > 0 and dom == "tc_gemm":
         achieved = s["flops"] / (s["ms"] / 1e3) / 1e12
         roof = {"bound": "tensor", "achieved": achieved, "peak": tpeak, "unit": "TFLOP/s",
@@ -203,11 +207,13 @@ def build_layers(name, batch):
 
 
 def layer_work(h, esize):
-    """Algorithmic work of one layer: forward = codegen.flops(staged=False) (the
-    contraction the kernel performs, 2 per MAC, batch included); grad-input and
-    grad-weight are one contraction each of the same volume.  Bytes: fwd reads x,
-    w and writes y; bwd reads x, w, dy and writes dx, dw."""
-    f = h.flops_unstaged
+    """Algorithmic work of one layer: forward =
+    codegen.flops(graph, staged=True) (2 per MAC, batch included -- for
+    sep_shared the rfactored nest's 0.34x of the dense 3x3, whatever the
+    kernel executes); grad-input and grad-weight are one contraction each of
+    the same volume.  Bytes: fwd reads x, w and writes y; bwd reads x, w, dy
+    and writes dx, dw."""
+    f = h.flops_staged
     nx, ny = math.prod(h.x_shape), math.prod(h.y_shape)
     nw = sum(math.prod(s) for s in h.w_shapes)
     return {"fwd_flops": f, "bwd_flops": 2 * f,
@@ -367,7 +373,7 @@ def run_layers(args, rank, world, device, peaks):
                 times.setdefault(f"{s['L'].name}:{p}", []).append(all_evs[k].elapsed_time(all_evs[k + 1]))
                 k += 1
 
-    tpeak = peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"])
+    tpeak = peaks["bf16_tflops"]
     t_roof = 0.0
     for s in state:
         for p, _ in phases:
@@ -476,6 +482,7 @@ def measure_e2e(state, phases, args, device, dtype, world):
 
 SWEEP_BATCH = 8
 CONV_FLOPS_PER_IMAGE = 2 * 64 * 32 * 32 * 64 * 9
+SWEEP_PARAMS_CAP = 64 * 64 * 9 * 16
 
 
 def sweep_setup(limit=None):
@@ -483,8 +490,48 @@ def sweep_setup(limit=None):
     from paper_2410_23745_b200.sweep import candidate_costs
     graphs = WL.corpus(SWEEP_BATCH, limit=limit)
     flops_cap = 10 * CONV_FLOPS_PER_IMAGE * SWEEP_BATCH      # make_corpus.py's cap, per batch
-    params_cap = 64 * 64 * 9 * 16
+    params_cap = SWEEP_PARAMS_CAP
     return graphs, candidate_costs(graphs), flops_cap, params_cap
+
+
+# nominal FP32 FFMA peak of a B200 (148 SMs x 128 lanes x 2 FLOP x 1965 MHz):
+# the universal engine's fp32 arithmetic runs on that pipe, MEASURED_PEAKS.json
+# has no FP32 figure
+FP32_FFMA_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12
+
+
+def sweep_roofline(graphs, records, wall_s, peaks):
+    """Roofline of the executed candidates: per candidate
+    t_roof = max(F / P_fp32, B / BW_hbm) with F = (2 + n_weights) x
+    codegen.flops(staged=True) (forward, grad-input, one grad per weight) and
+    B = compulsory fp32 bytes (x, weights, y, dy, dx, dW once each); the
+    sweep's achieved fraction = sum(t_roof) / measured wall time."""
+    from paper_2410_23745_b200 import pgraph as P
+    t_roof = t_fl = t_by = 0.0
+    fl = by = 0.0
+    dev_s = 0.0
+    for r in records:
+        if r.status == "over_budget":
+            continue
+        h = P.handle_for(graphs[r.sample_id], None, True)
+        f = (2 + len(h.w_shapes)) * h.flops_staged
+        b = 4 * (2 * math.prod(h.x_shape) + 2 * math.prod(h.y_shape) + 2 * sum(math.prod(s) for s in h.w_shapes))
+        a, c = f / (FP32_FFMA_TFLOPS * 1e12), b / (peaks["hbm_gbs"] * 1e9)
+        t_roof += max(a, c)
+        t_fl += a
+        t_by += c
+        fl += f
+        by += b
+        dev_s += r.seconds
+    bound = "hbm" if t_by >= t_fl else "fp32"
+    return {"bound": bound, "achieved": (by / wall_s / 1e9) if bound == "hbm" else fl / wall_s / 1e12,
+            "peak": peaks["hbm_gbs"] if bound == "hbm" else FP32_FFMA_TFLOPS,
+            "unit": "GB/s" if bound == "hbm" else "TFLOP/s", "frac": t_roof / wall_s, "traffic": None,
+            "t_roof_s": t_roof, "t_roof_flops_s": t_fl, "t_roof_bytes_s": t_by, "algorithmic_flops": fl,
+            "algorithmic_bytes": by, "sum_candidate_device_s": dev_s,
+            "note": ("whole-sweep roofline: sum over executed candidates of max(F/P_fp32, B/BW) over the measured "
+                     "wall time (compile + table build + fwd + bwd + checks); P_fp32 = nominal FFMA peak, BW = "
+                     "MEASURED_PEAKS hbm_gbs")}
 
 
 def run_sweep(args, rank, world, device, peaks):
@@ -492,14 +539,19 @@ def run_sweep(args, rank, world, device, peaks):
 
     from paper_2410_23745_b200 import _lib
     from paper_2410_23745_b200 import pgraph as P
-    from paper_2410_23745_b200.sweep import lpt_shard, run_shard
+    from paper_2410_23745_b200.sweep import LocalClaim, StoreClaim, lpt_order, lpt_shard, run_dynamic, run_shard
 
     graphs, costs, fcap, pcap = sweep_setup(args.limit)
-    mine = lpt_shard(costs, world)[rank]
+    order = lpt_order(costs)
+    store = None
+    if world > 1:
+        import torch.distributed as dist
+        store = dist.distributed_c10d._get_default_store()
     # warm-up: the CUDA context and every kernel variant on the same ops at a
     # different batch (distinct handles: the timed steps compile from scratch)
     from paper_2410_23745_b200 import workloads as WL
     warm_graphs = WL.corpus(2, limit=args.limit)
+    mine = lpt_shard(costs, world)[rank]
     for k in range(max(1, args.warmup)):
         run_shard(warm_graphs, mine[k::max(1, args.warmup)], dtype=torch.float32, flops_cap=fcap, params_cap=pcap,
                   workers=args.workers)
@@ -510,39 +562,52 @@ def run_sweep(args, rank, world, device, peaks):
         time.sleep(0.2)
     step_s, recs_all = [], None
     launches0 = _lib.lib.syno_launch_count()
-    for _ in range(args.steps):
+    for step in range(args.steps):
         with P._CACHE_LOCK:
             P._CACHE.clear()  # every step compiles every candidate afresh
+        claim = StoreClaim(store, len(order), f"syno_sweep_next_{step}") if store is not None else \
+            LocalClaim(len(order))
         barrier(world)
         torch.cuda.synchronize(device)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        recs, _ = run_shard(graphs, mine, dtype=torch.float32, flops_cap=fcap, params_cap=pcap,
-                            workers=args.workers)
+        recs, _ = run_dynamic(graphs, order, claim, dtype=torch.float32, flops_cap=fcap, params_cap=pcap,
+                              workers=args.workers)
         e1.record()
         torch.cuda.synchronize(device)
         step_s.append(e0.elapsed_time(e1) / 1e3)
         recs_all = recs
-    barrier(world)
+        barrier(world)  # every rank finished this step before the next one's counter is used
     launches = _lib.lib.syno_launch_count() - launches0
     if rank == 0:
         sampler.stop()
     s = allreduce_max(statistics.median(step_s), world, device)
-    n_total = len(graphs)
+    # host-side merge of the per-rank records (after the timed region)
+    if world > 1:
+        import torch.distributed as dist
+        gathered = [None] * world
+        dist.all_gather_object(gathered, recs_all)
+    else:
+        gathered = [recs_all]
+    from paper_2410_23745_b200.sweep import merge
+    merged = merge(gathered)
     status = {}
-    for r in recs_all:
+    for r in merged:
         status[r.status] = status.get(r.status, 0) + 1
-    evaluated = sum(1 for r in recs_all if r.status != "over_budget")
+    executed = sum(1 for r in merged if r.status != "over_budget")
     log_dir = os.path.join(ROOT, "gpurun_out")
-    if os.path.isdir(log_dir):
-        with open(os.path.join(log_dir, f"sweep_rank{rank}.log"), "w") as f:
-            for r in recs_all:
+    if rank == 0 and os.path.isdir(log_dir):
+        with open(os.path.join(log_dir, f"sweep_w{world}.log"), "w") as f:
+            for r in merged:
                 f.write(r.line() + "\n" + r.diag() + "\n")
-    return {"value": n_total / s, "unit": "candidates/s", "ms_per_step": s * 1e3, "roofline": None,
+    per_rank = [sum(1 for r in g if r.status != "over_budget") for g in gathered]
+    roof = sweep_roofline(graphs, merged, s, peaks) if rank == 0 else None
+    return {"value": executed / s, "unit": "candidates/s", "ms_per_step": s * 1e3, "roofline": roof,
             "gpu_launches": int(launches), "clocks": sampler.summary() if rank == 0 else None,
-            "dtype": "f32", "sweep": {"candidates": n_total, "this_rank": len(mine), "executed_this_rank": evaluated,
-                                      "workers_per_gpu": args.workers,
-                                      "status_this_rank": status, "flops_cap": fcap, "params_cap": pcap},
+            "dtype": "f32", "sweep": {"candidates": len(graphs), "executed": executed,
+                                      "executed_per_rank": per_rank, "workers_per_gpu": args.workers,
+                                      "status": status, "flops_cap": fcap, "params_cap": pcap,
+                                      "schedule": "dynamic claims from one shared LPT order (TCPStore counter)"},
             "e2e": None}
 
 
@@ -586,119 +651,183 @@ def run_qkv_train(args, rank, world, device, peaks):
 
 
 # ---------------------------------------------------------------------------
-# CPU baseline: the pinned oracle restatement of the reference path
+# CPU baseline / reference arm: the UNMODIFIED reference (opsmith) on the host
 # ---------------------------------------------------------------------------
+#
+# Nothing on this path loads libsyno.so or imports the product package: the
+# operators are built by the reference's own parse_steps from the plain-data
+# tables in paper_2410_23745_b200/configs.py (loaded by file path), and run
+# by the reference's own codegen.interpret / codegen.weight_gradient
+# (codegen.py:598-630, 664-743).  Grad-input has no reference function
+# (SURVEY §8(c)); it is timed as the oracle restatement (oracle/) on the
+# nest text the REFERENCE emits (codegen.emit_loop_nest(build_loop_nest(g))).
 
-def _oracle_job(args):
-    """One image of one layer (or one candidate), fwd [+ grad-input + grad-weight]."""
+def _ref_modules():
+    """opsmith from baseline/_ref (the pip --target install that travels to
+    the GPU box), else the read-only source tree in this container."""
+    for path in (os.path.join(ROOT, "baseline", "_ref"), "/root/reference/pkg/src"):
+        if os.path.isdir(os.path.join(path, "opsmith")):
+            if path not in sys.path:
+                sys.path.insert(0, path)
+            import opsmith.codegen as RC
+            import opsmith.pgraph as RP
+            import opsmith.symexpr as RS
+            return RC, RP, RS
+    return None
+
+
+def _configs():
+    """paper_2410_23745_b200/configs.py loaded by path: importing the package
+    would load libsyno.so."""
+    import importlib.util
+    name = "_syno_configs_plain"
+    if name in sys.modules:
+        return sys.modules[name]
+    spec = importlib.util.spec_from_file_location(name, os.path.join(ROOT, "paper_2410_23745_b200", "configs.py"))
+    mod = importlib.util.module_from_spec(spec)
+    sys.modules[name] = mod
+    spec.loader.exec_module(mod)
+    return mod
+
+
+def _ref_graph(spec_args, steps):
+    RC, RP, RS = _ref_modules()
+    name, prim, coeffs, ref, out, inp, batch = spec_args
+    variables = tuple(RS.Variable(n) for n in prim) + tuple(RS.Variable(n, primary=False) for n in coeffs)
+    vm = {v.name: v for v in variables}
+    spec = RP.ProblemSpec(name=name, variables=variables, reference=tuple(ref.items()),
+                          output_dims=tuple(RS.parse_size(t, vm) for t in out),
+                          input_dims=tuple(RS.parse_size(t, vm) for t in inp),
+                          batch_dims=tuple(RS.parse_size(t, vm) for t in batch))
+    return RP.parse_steps(steps, spec)
+
+
+def _ref_job(job):
+    """One batch element of one operator through the reference: interpret
+    [+ grad-input restatement + weight_gradient], float64.  Returns seconds."""
     import numpy as np
 
     from oracle import nest_oracle as O
-    text, env, xshape, wshapes, yshape, fwd_only, seed = args
+    spec_args, steps, fwd_only, seed = job
+    RC, RP, RS = _ref_modules()
+    g = _ref_graph(spec_args, steps)
+    env = dict(spec_args[3])
     rng = np.random.default_rng(seed)
-    x = rng.standard_normal(xshape)
-    ws = [rng.standard_normal(s) for s in wshapes]
-    up = rng.standard_normal(yshape)
+    x = rng.standard_normal(RC.input_shape(g.spec, env))
+    ws = RC.random_weights(g, rng, env)
+    up = rng.standard_normal(RC.output_shape(g.spec, env))
+    # shapes include the batch axis (N = 1 in the sample assignment)
     t0 = time.perf_counter()
-    O.interpret(text, env, x, ws)
+    RC.interpret(g, x, ws)
     if not fwd_only:
-        O.input_gradient(text, env, x, up, ws)
+        text = RC.emit_loop_nest(RC.build_loop_nest(g, env))
+        O.input_gradient(text, env, x, up, ws, (1,))
         if ws:
-            O.weight_gradient(text, env, x, up, ws)
+            RC.weight_gradient(g, x, up, ws)
     return time.perf_counter() - t0
 
 
+def _ref_flops(spec_args, steps):
+    RC, RP, RS = _ref_modules()
+    g = _ref_graph(spec_args, steps)
+    return RC.flops(g), len(g.weights)
+
+
+def _pool_map(fn, jobs, processes):
+    import multiprocessing as mp
+    if processes == 1:
+        return [fn(j) for j in jobs]
+    with mp.get_context("fork").Pool(processes) as pool:
+        return pool.map(fn, jobs)
+
+
 def cpu_sample_spec(args):
-    """The bounded CPU sample: one image through one representative layer,
-    extrapolated to the whole step by the layers' FLOP share."""
-    from paper_2410_23745_b200 import codegen as C
-    from paper_2410_23745_b200 import pgraph as P
-    layers = build_layers(args.workload, args.batch)
-    pick = {"resnet18": "l1b0c2", "resnet34": "l2b1c2", "cfg1": "cfg1_conv3x3", "qkv": "qkv"}[args.workload]
-    L = next(lay for lay in layers if lay.name == pick)
-    one = dict(L.assignment)
-    bkey = "N" if "N" in one else "B"
-    batch = one[bkey]
+    """The bounded CPU sample: one batch element of one representative layer,
+    extrapolated to the whole step by the layers' FLOP share (the reference's
+    batch loop is serial and per-element identical, codegen.py:626-630)."""
+    cf = _configs()
+    batch = args.batch or {"resnet18": 128, "resnet34": 256, "cfg1": 8, "qkv": 16}[args.workload]
     if args.workload == "qkv":
-        one["T"] = 128  # the reference's full-grid interpreter needs ~58 GB per T=1024 element
-    one[bkey] = 1
-    text = C.emit_loop_nest(L.graph, one)
-    h1 = P.handle_for(L.graph, one)
+        rows = [("qkv", "qkv", None, None, None)]
+    elif args.workload == "cfg1":
+        rows = [("cfg1_conv3x3", "conv3x3", 64, 64, 32)]
+    else:
+        rows = cf.resnet18_table() if args.workload == "resnet18" else cf.resnet34_table()
+    pick = {"resnet18": "l1b0c2", "resnet34": "l2b1c2", "cfg1": "cfg1_conv3x3", "qkv": "qkv"}[args.workload]
     fwd_only = args.workload == "cfg1"
-    spec = (text, one, h1.x_shape[1:], [tuple(s) for s in h1.w_shapes], h1.y_shape[1:], fwd_only)
     mult = 1 if fwd_only else 3
-    flops_one = mult * h1.flops_unstaged
-    per_image = sum(mult * P.handle_for(lay.graph).flops_unstaged for lay in layers) / batch
+    per_image = 0.0
+    sample = None
+    for name, op, ci, co, h in rows:
+        if op == "qkv":
+            full = cf.qkv_spec_args(1)
+            one = cf.qkv_spec_args(1, t=128)  # the full-grid interpreter needs ~58 GB per T=1024 element
+        else:
+            full = one = cf.conv_spec_args(name, op, ci, co, h, 1)
+        f_full, _ = _ref_flops(full, cf.STEPS[op])
+        per_image += mult * f_full
+        if name == pick:
+            f_one, _ = _ref_flops(one, cf.STEPS[op])
+            sample = (one, cf.STEPS[op], f_one)
+    one, steps, f_one = sample
     elem = "sequence" if args.workload == "qkv" else "image"
-    desc = (f"1 {elem} of layer {L.name} ({L.op}) " + ("forward" if fwd_only else "fwd+grad-input+grad-weight")
+    desc = (f"1 {elem} of layer {pick} through the unmodified reference (opsmith from baseline/_ref): "
+            + ("codegen.interpret" if fwd_only else
+               "codegen.interpret + codegen.weight_gradient + grad-input (oracle restatement on the reference's "
+               "emitted nest; the reference has no grad-input)")
             + (" at T=128" if args.workload == "qkv" else "")
-            + f" in float64; {unit_of(args.workload)} extrapolated by the layer's FLOP share of the full step")
-    return spec, flops_one, per_image, desc
+            + f", float64; {unit_of(args.workload)} extrapolated by the layer's FLOP share of the full step")
+    return (one, steps, fwd_only), mult * f_one, per_image, desc
 
 
 def cpu_baseline_layers(args, processes=1):
-    import multiprocessing as mp
     spec, flops_one, per_image, desc = cpu_sample_spec(args)
     jobs = [spec + (k,) for k in range(processes)]
     t0 = time.perf_counter()
-    if processes == 1:
-        _oracle_job(jobs[0])
-    else:
-        with mp.get_context("fork").Pool(processes) as pool:
-            pool.map(_oracle_job, jobs)
+    _pool_map(_ref_job, jobs, processes)
     dt = time.perf_counter() - t0
     return {"value": processes * flops_one / dt / per_image, "unit": unit_of(args.workload), "cores": processes,
-            "kind": "port",
+            "kind": "reference",
             "sample": desc + f" ({processes} process(es), {dt:.1f} s)", "seconds": dt}
 
 
-def cpu_baseline_sweep(args, processes=1, budget_s=20.0):
-    """Oracle evaluation (fwd + grad-input + grad-weights, float64, per
-    image) of corpus candidates in corpus order until ~budget_s; rate
-    extrapolated to the whole corpus by the candidates' FLOP share."""
-    import multiprocessing as mp
+def _ref_budget_job(job):
+    """(index, unstaged flops at N=1, params, within budget) by the reference."""
+    i, spec_args, steps, fcap, pcap = job
+    RC, RP, RS = _ref_modules()
+    g = _ref_graph(spec_args, steps)
+    f, p = RC.flops(g), RC.param_count(g)
+    return i, f, p, (fcap is None or f <= fcap) and (pcap is None or p <= pcap)
 
-    from paper_2410_23745_b200 import codegen as C
-    from paper_2410_23745_b200 import pgraph as P
-    from paper_2410_23745_b200.sweep import within_budget
-    graphs, costs, fcap, pcap = sweep_setup(args.limit)
-    one = {"C_out": 64, "C_in": 64, "H": 32, "W": 32, "K": 3, "s": 2, "N": 1}
-    fl_all = 0.0
-    items = []
-    for i, g in enumerate(graphs):
-        h = P.handle_for(g)
-        if not within_budget(h.flops_unstaged, h.params, fcap, pcap):
-            continue
-        fl_all += h.flops_unstaged
-        items.append((i, g, h))
-    done_fl, n_done = 0.0, 0
+
+def cpu_baseline_sweep(args, processes=1, budget_s=20.0):
+    """Reference evaluation (interpret + grad-input restatement +
+    weight_gradient, float64, one batch element) of the in-budget corpus
+    candidates in corpus order until ~budget_s; the rate is extrapolated to
+    the whole sweep (every in-budget candidate at N=8) by FLOP share."""
+    cf = _configs()
+    ops = cf.corpus_ops(args.limit)
+    one = cf.corpus_spec_args(1)
+    fcap = 10 * CONV_FLOPS_PER_IMAGE  # per image (the sweep's cap is per batch of 8)
+    pcap = SWEEP_PARAMS_CAP
+    info = _pool_map(_ref_budget_job, [(i, one, op, fcap, pcap) for i, op in enumerate(ops)], processes)
+    items = [(i, f) for i, f, p, ok in info if ok]
+    fl_all = float(sum(f for _, f in items))
+    done_fl, n_done, k = 0.0, 0, 0
     t0 = time.perf_counter()
-    pool = mp.get_context("fork").Pool(processes) if processes > 1 else None
-    k = 0
     while k < len(items) and time.perf_counter() - t0 < budget_s:
         chunk = items[k:k + processes]
         k += len(chunk)
-        jobs = []
-        for i, g, h in chunk:
-            h1 = P.handle_for(g, one)
-            jobs.append((C.emit_loop_nest(g, one), one, h1.x_shape[1:], [tuple(s) for s in h1.w_shapes],
-                         h1.y_shape[1:], False, i))
-        if pool:
-            pool.map(_oracle_job, jobs)
-        else:
-            for j in jobs:
-                _oracle_job(j)
-        done_fl += sum(h.flops_unstaged for _, _, h in chunk)
+        _pool_map(_ref_job, [(one, ops[i], False, i) for i, _ in chunk], processes)
+        done_fl += sum(f for _, f in chunk)
         n_done += len(chunk)
     dt = time.perf_counter() - t0
-    if pool:
-        pool.close()
-    # oracle time for the whole corpus = dt * (fl_all / done_fl) * SWEEP_BATCH (per-image sample)
     total_s = dt * (fl_all / max(done_fl, 1.0)) * SWEEP_BATCH
-    return {"value": len(graphs) / total_s, "unit": "candidates/s", "cores": processes, "kind": "port",
-            "sample": (f"{n_done} in-budget corpus candidates, 1 image each, fwd+grad-input+grad-weight in float64 "
-                       f"({dt:.1f} s, {processes} process(es)); extrapolated to the 1024-candidate sweep at N=8 "
-                       "by FLOP share"), "seconds": dt}
+    return {"value": len(items) / total_s, "unit": "candidates/s", "cores": processes, "kind": "reference",
+            "sample": (f"{n_done} of {len(items)} in-budget corpus candidates, 1 image each, through the unmodified "
+                       "reference (interpret + weight_gradient + grad-input restatement, float64; "
+                       f"{dt:.1f} s, {processes} process(es)); extrapolated to the sweep at N=8 by FLOP share"),
+            "seconds": dt}
 
 
 def run_reference(args, rank, world):
@@ -721,7 +850,7 @@ def run_reference(args, rank, world):
         "ms_per_step": 1e3 * statistics.mean(secs), "higher_is_better": True,
         "scaling": "strong" if args.workload == "sweep" else "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic", "config": workload_config(args),
-        "cpu_baseline": {"value": v, "unit": r["unit"], "cores": procs, "kind": "port", "sample": r["sample"]},
+        "cpu_baseline": {"value": v, "unit": r["unit"], "cores": procs, "kind": r["kind"], "sample": r["sample"]},
         "e2e": {"value": v, "unit": r["unit"], "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -737,7 +866,7 @@ def workload_config(args):
         "cfg1": "cfg1: conv3x3 in Syno primitives, N=8 C=64 H=W=32, forward",
         "qkv": "cfg4 layer: GPT-2 small QKV projection as a synthesized operator, fwd+bwd",
         "qkv_train": "cfg4: proxy training, 12 GPT-2-small QKV synthesized operators, DP with NCCL allreduce",
-        "sweep": "cfg5: 1024 sampled primitive graphs (conv64 spec, N=8), LPT-sharded across GPUs",
+        "sweep": "cfg5: 1024 sampled primitive graphs (conv64 spec, N=8; the in-budget ones executed), sharded across GPUs",
     }[args.workload]
     batch = args.batch or {"resnet18": 128, "resnet34": 256, "cfg1": 8, "qkv": 16, "qkv_train": 16,
                            "sweep": SWEEP_BATCH}[args.workload]
@@ -746,7 +875,7 @@ def workload_config(args):
         cfg["l2"] = "flushed between timed steps (256 MB write)"
         cfg["parallelism"] = "replicas (no data-path collective)"
     elif args.workload == "sweep":
-        cfg["parallelism"] = "LPT candidate sharding, no collective"
+        cfg["parallelism"] = "candidate sharding (dynamic claims of one LPT order), no data-path collective"
         cfg["l2"] = "not flushed (every candidate compiles and allocates afresh)"
     else:
         cfg["parallelism"] = "data parallel, bucketed NCCL allreduce"
@@ -771,9 +900,21 @@ def main():
     if args.workload == "sweep" and args.steps == 10:
         args.steps = 3
 
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        # `bench.py --gpus N` outside torchrun: launch the N ranks ourselves
+        import socket
+        sock = socket.socket()
+        sock.bind(("127.0.0.1", 0))
+        port = sock.getsockname()[1]
+        sock.close()
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+        sys.exit(subprocess.call(cmd))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}; launch one rank per GPU")
     if args.impl == "reference":
         run_reference(args, rank, world)
         return
@@ -788,7 +929,7 @@ def main():
     r = runner(args, rank, world, device, peaks)
     if rank == 0:
         cpu = None
-        if not args.no_cpu_baseline and args.workload != "qkv_train":
+        if not args.no_cpu_baseline and args.workload != "qkv_train" and world == 1:
             cpu = cpu_baseline_sweep(args, 1) if args.workload == "sweep" else cpu_baseline_layers(args, 1)
             cpu.pop("seconds", None)
         line = {

@@ -141,6 +141,9 @@ uint64_t syno_launch_count(void);
  * synchronises those events and returns one row per kernel class with the
  * launch count, summed device milliseconds and the summed ALGORITHMIC
  * FLOPs / bytes of the launches (codegen.flops per contraction GEMM).
+ * While profiling is active the library serialises its launches on the
+ * caller's stream (the concurrent grad-weight side stream is not used), so
+ * per-launch durations never overlap and their sum is at most the step.
  * Must not be active during CUDA-graph capture. */
 typedef struct {
   char name[48];

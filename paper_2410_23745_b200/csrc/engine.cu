@@ -99,6 +99,8 @@ void prof_enable(bool on) {
   g_prof_on = on;
 }
 
+bool prof_active() { return g_prof_on.load(std::memory_order_relaxed); }
+
 int prof_begin(const char* name, double flops, double bytes, cudaStream_t stream) {
   if (!g_prof_on.load(std::memory_order_relaxed)) return -1;
   ProfRec r;

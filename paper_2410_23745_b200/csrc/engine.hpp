@@ -174,6 +174,9 @@ struct ProfStat {
   double ms = 0, flops = 0, bytes = 0;
 };
 void prof_enable(bool on);
+// true between syno_profile_begin/end: launches are serialised on the caller's
+// stream (no side-stream fork) so per-launch durations never overlap
+bool prof_active();
 std::vector<ProfStat> prof_collect();
 
 }  // namespace syno

@@ -1091,7 +1091,7 @@ struct TcPlan {
   int C = 0, N = 0, Cp = 0, Np = 0;
   PixDim dh, dw;
   double scale = 1;
-  double flops = 0;  // algorithmic FLOPs of one GEMM (= codegen.flops, unstaged, batch included)
+  double flops = 0;  // algorithmic FLOPs of one GEMM (= codegen.flops(staged=True), batch included)
   bool dgrad_ok = false;
   DevStage fold_fwd, fold_dgrad;
   std::vector<DevStage> chain;    // dW_j from the folded gradient
@@ -1356,7 +1356,9 @@ TcPlanPtr tc_build(const Plan& plan, cudaStream_t stream) {
   TcPlan* raw = try_match(plan);
   if (!raw) return TcPlanPtr();
   TcPlanPtr tp(raw);
-  tp->flops = (double)plan.flops_unstaged;
+  // algorithmic FLOPs per GEMM = codegen.flops(staged=True):
+  // a folded sep_shared GEMM is credited only with the staged volume
+  tp->flops = (double)(plan.flops_staged ? plan.flops_staged : plan.flops_unstaged);
   setup_fast_fold(plan, *tp);
   build_dev_stage(fold_stage(plan, *tp, false, true), &tp->fold_fwd, stream);
   if (tp->dgrad_ok) build_dev_stage(fold_stage(plan, *tp, true, true), &tp->fold_dgrad, stream);
@@ -2507,7 +2509,7 @@ bool tc_backward(TcPlan& tp, DType dt, const Bindings& b, cudaStream_t stream) {
   for (auto* q : b.dw) any_w = any_w || q;
   bool dy_w_packed = false;
   static const bool concurrent = getenv("SYNO_TC_SERIAL_BWD") == nullptr;
-  const bool fork = concurrent && b.dx && any_w;
+  const bool fork = concurrent && !prof_active() && b.dx && any_w;
   cudaStream_t wstream = stream;
   if (b.dx) {
     TcGemmParams p = w.dg;

@@ -58,18 +58,25 @@ class GradBuckets:
         self.pending = [0] * len(self.buckets)
         self.works: List[Optional[object]] = [None] * len(self.buckets)
         self.hooks = []
+        # collectives are issued strictly in bucket-index order on every rank
+        # (a bucket that completes early waits for its predecessors), so the
+        # NCCL call sequence cannot diverge across ranks
+        self.next_launch = 0
 
     def _stage(self, p):
         bi, off = self.where[id(p)]
         self.flat[bi][off:off + p.numel()].copy_(p.grad.reshape(-1))
         self.pending[bi] += 1
-        if self.pending[bi] == len(self.buckets[bi]):
-            self._launch(bi)
+        self._launch_ready()
 
-    def _launch(self, bi):
-        if self.world > 1:
-            self.works[bi] = self.dist.all_reduce(self.flat[bi], op=self.dist.ReduceOp.SUM, group=self.group,
-                                                  async_op=True)
+    def _launch_ready(self):
+        while self.next_launch < len(self.buckets) and \
+                self.pending[self.next_launch] == len(self.buckets[self.next_launch]):
+            bi = self.next_launch
+            if self.world > 1:
+                self.works[bi] = self.dist.all_reduce(self.flat[bi], op=self.dist.ReduceOp.SUM, group=self.group,
+                                                      async_op=True)
+            self.next_launch += 1
 
     def attach(self):
         for p in self.params:
@@ -82,12 +89,17 @@ class GradBuckets:
         self.hooks = []
 
     def finish(self):
+        if not self.hooks and any(self.pending[bi] != len(b) for bi, b in enumerate(self.buckets)):
+            raise RuntimeError("GradBuckets.finish() without attach(): call reduce() for the synchronous path")
+        # unused parameters contribute zeros; their buckets then launch in index order
         for bi, b in enumerate(self.buckets):
-            if self.pending[bi] != len(b):  # some gradient was never produced (unused parameter)
+            if self.pending[bi] != len(b):
                 for p in b:
                     if p.grad is None:
                         p.grad = torch.zeros_like(p)
                         self._stage(p)
+        assert self.next_launch == len(self.buckets)
+        for bi, b in enumerate(self.buckets):
             w = self.works[bi]
             if w is not None:
                 w.wait()
@@ -99,14 +111,17 @@ class GradBuckets:
                 off += p.numel()
             self.pending[bi] = 0
             self.works[bi] = None
+        self.next_launch = 0
 
     def reduce(self):
         """Synchronous path: stage every gradient, allreduce, write back."""
         for p in self.params:
             if p.grad is None:
                 p.grad = torch.zeros_like(p)
+        self.next_launch = 0
         for bi, b in enumerate(self.buckets):
             self.pending[bi] = 0
+        for bi, b in enumerate(self.buckets):
             for p in b:
                 self._stage(p)
         self.finish()

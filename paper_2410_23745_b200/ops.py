@@ -115,9 +115,13 @@ class SynoFunction(torch.autograd.Function):
     def backward(ctx, dy):
         x, *weights = ctx.saved_tensors
         need = ctx.needs_input_grad
-        # autograd saved x and weights (version-checked): the forward's operands are reusable
-        dx, dws = backward(ctx.h, x, weights, dy, bool(need[1]), [bool(n) for n in need[2:]], x_unchanged=True,
-                           w_unchanged=True)
+        # autograd saved x and weights (version-checked), so the forward's
+        # packed operands are reusable -- but only when the forward read these
+        # very buffers: a non-contiguous operand was packed from a temporary
+        # copy that is gone now, and the library's reuse check compares
+        # pointers only (a new temporary may land at the freed address)
+        dx, dws = backward(ctx.h, x, weights, dy, bool(need[1]), [bool(n) for n in need[2:]],
+                           x_unchanged=x.is_contiguous(), w_unchanged=all(w.is_contiguous() for w in weights))
         return (None, dx, *dws)
 
 

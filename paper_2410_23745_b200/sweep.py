@@ -16,9 +16,12 @@ size-independent identities of a multilinear operator y = A(x; w_1..w_n):
     <dy, y> == <dw_j, w_j>      (y is homogeneous of degree 1 in each w_j)
 
 Candidates are independent, so multi-GPU evaluation shards them across
-ranks by LPT on a predicted roofline time with NO collective on the data
-path; each rank writes its own records and the host merges
-them by sample id.
+ranks with NO collective on the data path: statically by LPT
+on a predicted roofline time (``lpt_shard``), or dynamically -- every rank
+claims the next candidate of one shared LPT order from the process group's
+key-value store (``StoreClaim``; an atomic counter on the host, no device
+traffic).  Each rank writes its own records and the host merges them by
+sample id.
 """
 from __future__ import annotations
 
@@ -142,15 +145,84 @@ def evaluate(graph, sample_id: int, seed: int, dtype=None, device=None,
                       e0.elapsed_time(e1) / 1e3, err)
 
 
-def candidate_costs(graphs) -> List[float]:
-    """Predicted seconds per candidate from the native plan (CPU only)."""
+def candidate_costs(graphs, flops_cap: Optional[int] = None, params_cap: Optional[int] = None) -> List[float]:
+    """Predicted seconds per candidate from the native plan (CPU only).
+
+    An over-budget candidate is never executed (``evaluate`` returns before
+    any launch, search.py:430-437), so it costs nothing to schedule; pricing
+    it by its FLOPs made such phantoms 99% of the predicted total."""
     from .pgraph import handle_for
     out = []
     for g in graphs:
         h = handle_for(g, None, True)
+        if not within_budget(h.flops_unstaged, h.params, flops_cap, params_cap):
+            out.append(0.0)
+            continue
         nbytes = 4 * (2 * math.prod(h.x_shape) + 2 * math.prod(h.y_shape)
                       + 2 * sum(math.prod(s) for s in h.w_shapes))
         out.append(predicted_seconds(h.flops_staged, nbytes))
+    return out
+
+
+def lpt_order(costs: Sequence[float]) -> List[int]:
+    """Candidate indices by decreasing predicted cost (ties by index): the
+    order a dynamic schedule hands work out in (greedy list scheduling in
+    LPT order, within 4/3 of optimal and immune to a cost model that is off
+    by a constant factor per class)."""
+    return sorted(range(len(costs)), key=lambda k: (-float(costs[k]), k))
+
+
+class StoreClaim:
+    """Dynamic work claiming across ranks through a key-value store's
+    atomic counter (torch.distributed's TCPStore: host-side coordination,
+    no data-path collective).  ``next()`` returns the next position in the
+    shared order, or None when the order is exhausted."""
+
+    def __init__(self, store, n: int, key: str = "syno_sweep_next"):
+        self.store, self.n, self.key = store, n, key
+
+    def __call__(self):
+        k = int(self.store.add(self.key, 1)) - 1
+        return k if k < self.n else None
+
+
+class LocalClaim:
+    """Single-process counterpart of StoreClaim (thread-safe)."""
+
+    def __init__(self, n: int):
+        self.n, self.k, self.mu = n, 0, threading.Lock()
+
+    def __call__(self):
+        with self.mu:
+            if self.k >= self.n:
+                return None
+            self.k += 1
+            return self.k - 1
+
+
+def claim_loop(order: Sequence[int], claim, work, workers: int = 1) -> list:
+    """Run ``work(i)`` for candidates claimed one at a time from ``order``
+    by ``workers`` threads until the claim returns None; returns the
+    results this process produced (any order)."""
+    out, mu = [], threading.Lock()
+
+    def loop():
+        while True:
+            k = claim()
+            if k is None:
+                return
+            r = work(order[k])
+            with mu:
+                out.append(r)
+
+    if workers <= 1:
+        loop()
+        return out
+    threads = [threading.Thread(target=loop) for _ in range(workers)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
     return out
 
 
@@ -190,6 +262,17 @@ def run_shard(graphs, indices: Sequence[int], seed0: int = 0, dtype=None, flops_
         futs = [pool.submit(_evaluate_on_own_stream, graphs[i], i, seed0 + i, dtype, flops_cap, params_cap)
                 for i in indices]
         recs = [f.result() for f in futs]
+    return recs, time.perf_counter() - t0
+
+
+def run_dynamic(graphs, order: Sequence[int], claim, seed0: int = 0, dtype=None, flops_cap=None,
+                params_cap=None, workers: int = 1):
+    """Evaluate candidates claimed dynamically from ``order`` (shared by
+    every rank through ``claim``) on this rank's device; each worker thread
+    uses its own CUDA stream.  Returns (records, wall seconds)."""
+    t0 = time.perf_counter()
+    recs = claim_loop(order, claim, lambda i: _evaluate_on_own_stream(graphs[i], i, seed0 + i, dtype, flops_cap,
+                                                                      params_cap), workers)
     return recs, time.perf_counter() - t0
 
 

@@ -102,6 +102,80 @@ def test_gloo_sweep_shards_cover_corpus_once(tmp_path):
     assert sorted(got[0] + got[1]) == list(range(96))
 
 
+def _claim_worker(rank, world, port, out_dir):
+    """The bench's dynamic sweep schedule on gloo: both ranks claim from one
+    LPT order through the process group's store; the host merge sees every
+    in-budget candidate exactly once."""
+    _init(rank, world, port)
+    import time as _time
+
+    from paper_2410_23745_b200 import workloads as WL
+    from paper_2410_23745_b200.sweep import EvalRecord, StoreClaim, claim_loop, lpt_order, merge
+    from paper_2410_23745_b200.sweep import candidate_costs
+    graphs = WL.corpus(8, limit=64)
+    costs = candidate_costs(graphs, flops_cap=6039797760, params_cap=589824)
+    order = lpt_order(costs)
+    store = dist.distributed_c10d._get_default_store()
+    for step in range(2):
+        claim = StoreClaim(store, len(order), f"k{step}")
+        dist.barrier()
+
+        def work(i):
+            _time.sleep(0.002 * (1 + i % 3))  # stand-in for a device evaluation
+            return EvalRecord(i, i, 0, 0, "ok", f"op{i}")
+        recs = claim_loop(order, claim, work, workers=3)
+        gathered = [None] * world
+        dist.all_gather_object(gathered, recs)
+        merged = merge(gathered)  # raises on a candidate evaluated twice
+        assert [r.sample_id for r in merged] == list(range(len(graphs)))
+        assert all(gathered), "both ranks got work"
+    if rank == 0:
+        with open(os.path.join(out_dir, "ok"), "w") as f:
+            f.write("ok")
+    dist.destroy_process_group()
+
+
+def test_gloo_dynamic_claims_cover_corpus_once(tmp_path):
+    _spawn(_claim_worker, 2, str(tmp_path))
+    assert (tmp_path / "ok").exists()
+
+
+def test_candidate_costs_ignore_over_budget():
+    from paper_2410_23745_b200 import pgraph as P
+    from paper_2410_23745_b200 import workloads as WL
+    from paper_2410_23745_b200.sweep import candidate_costs, lpt_order, within_budget
+    graphs = WL.corpus(8, limit=200)
+    fcap, pcap = 6039797760, 589824
+    costs = candidate_costs(graphs, fcap, pcap)
+    n_over = 0
+    for g, c in zip(graphs, costs):
+        h = P.handle_for(g, None, True)
+        if within_budget(h.flops_unstaged, h.params, fcap, pcap):
+            assert c > 0
+        else:
+            assert c == 0.0
+            n_over += 1
+    assert n_over > 0
+    order = lpt_order(costs)
+    assert sorted(order) == list(range(len(graphs)))
+    assert all(costs[a] >= costs[b] for a, b in zip(order, order[1:]))
+
+
+def test_claim_loop_local_threads():
+    from paper_2410_23745_b200.sweep import LocalClaim, claim_loop
+    order = list(range(50))[::-1]
+    got = claim_loop(order, LocalClaim(len(order)), lambda i: i * 2, workers=4)
+    assert sorted(got) == [2 * i for i in range(50)]
+
+
+def test_bench_gpus_mismatch_fails_loudly():
+    import subprocess
+    env = dict(os.environ, WORLD_SIZE="1", RANK="0", LOCAL_RANK="0")
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--impl", "reference"],
+                       env=env, capture_output=True, text=True, timeout=120)
+    assert r.returncode != 0 and "WORLD_SIZE" in (r.stderr + r.stdout)
+
+
 def test_merge_rejects_duplicates():
     from paper_2410_23745_b200.sweep import EvalRecord, merge
     a = [EvalRecord(0, 0, 1, 1, "ok", "x"), EvalRecord(2, 0, 1, 1, "ok", "x")]
@@ -152,6 +226,49 @@ def _grad_worker(rank, world, port, mode):
 @pytest.mark.parametrize("mode", ["sync", "hooks"])
 def test_gloo_gradient_allreduce_mean(mode):
     _spawn(_grad_worker, 2, mode)
+
+
+def _order_worker(rank, world, port):
+    """Buckets whose gradients complete out of order (rank 1 produces them in
+    reverse) still issue their allreduces in bucket-index order on every rank,
+    so the collective sequences match and the means are right."""
+    _init(rank, world, port)
+    from paper_2410_23745_b200.dp import GradBuckets
+    params = [torch.nn.Parameter(torch.zeros(40)) for _ in range(4)]
+    gb = GradBuckets(params, bucket_bytes=160).attach()  # one parameter per bucket
+    assert len(gb.buckets) == 4
+    issued = []
+    real = dist.all_reduce
+
+    def spy(t, *a, **k):
+        issued.append(next(bi for bi, f in enumerate(gb.flat) if f.data_ptr() == t.data_ptr()))
+        return real(t, *a, **k)
+    dist.all_reduce = spy
+    gb.dist = dist
+    seq = params if rank == 0 else params[::-1]
+    for k, p in enumerate(seq):
+        if rank == 1 and k == 3:
+            break  # rank 1 never produces one gradient (an unused parameter)
+        p.grad = torch.full_like(p, float(rank + 1))
+        gb._stage(p)
+    gb.finish()
+    dist.all_reduce = real
+    assert issued == [0, 1, 2, 3]
+    for p in params:
+        assert p.grad is not None
+    dist.destroy_process_group()
+
+
+def test_gloo_buckets_issue_in_index_order():
+    _spawn(_order_worker, 2)
+
+
+def test_finish_without_attach_raises():
+    from paper_2410_23745_b200.dp import GradBuckets
+    lin = torch.nn.Linear(3, 2)
+    gb = GradBuckets(list(lin.parameters()))
+    with pytest.raises(RuntimeError):
+        gb.finish()
 
 
 def test_grad_buckets_single_process_is_identity():
