@@ -14,6 +14,7 @@
 #include <algorithm>
 #include <atomic>
 #include <cstring>
+#include <map>
 #include <mutex>
 #include <set>
 
@@ -352,12 +353,103 @@ static std::vector<int64_t> row_major_strides(const std::vector<int64_t>& ext) {
   return s;
 }
 
+static int64_t dep_product(const CStage& s, const std::vector<int>& deps) {
+  int64_t n = 1;
+  for (int l : deps) n *= s.ext(l);
+  return n;
+}
+
+// A mixed coordinate (depends on axes AND reduces) that is provably inside
+// [0, n) needs no bound check, so its top-level parts (c_sum_parts) can be
+// tabulated separately: axis-linear parts become lin coefficients,
+// axis-only parts one axis table, reduce-only parts the reduce table, and
+// the remaining mixed parts one table per dependency set.  Each part table
+// holds non-negative entries (biased by the part's minimum, folded into
+// `base`), so -1 stays the out-of-range sentinel.  Done only when it makes
+// the largest mixed table smaller; false leaves the coordinate whole.
+static void add_fix_table(const CStage& s, TabSpec&& tab, KTerm* k, bool axis_only, int A,
+                          std::vector<TabSpec>* tabs, std::vector<Fixup>* fix);
+
+static bool split_in_range(const CStage& s, const CE& c, int64_t n, int64_t st, int A, KTerm* k,
+                           std::vector<TabSpec>* tabs, std::vector<Fixup>* fix, std::vector<ProgSpec>* rprogs) {
+  static const bool off = getenv("SYNO_NO_SPLIT") != nullptr;  // A/B switch
+  if (off) return false;
+  std::vector<int64_t> ext;
+  for (int l = 0; l < s.nloops(); ++l) ext.push_back(s.ext(l));
+  int64_t lo, hi;
+  if (!c_range(c, ext, &lo, &hi) || lo < 0 || hi >= n) return false;
+  int64_t c0;
+  std::vector<std::pair<int64_t, CE>> parts;
+  c_sum_parts(c, &c0, &parts);
+  std::vector<int> whole;
+  c_loops(c, &whole);
+  struct Part { int64_t coef; CE atom; std::vector<int> deps; int64_t alo, ahi; };
+  std::vector<Part> ps;
+  std::map<std::vector<int>, int> mixed_groups;
+  std::vector<int> axis_deps;
+  int64_t biggest = 0;
+  for (auto& [coef, a] : parts) {
+    Part q{coef, a, {}, 0, 0};
+    c_loops(a, &q.deps);
+    if (!c_range(a, ext, &q.alo, &q.ahi)) return false;
+    const double span = (double)std::llabs(coef) * (double)st * (double)(q.ahi - q.alo);
+    if (span >= 2147483647.0) return false;
+    const bool ax = q.deps.back() < A, rd = q.deps.front() >= A;
+    if (!ax && !rd) {
+      mixed_groups.emplace(q.deps, 0);
+      biggest = std::max(biggest, dep_product(s, q.deps));
+    } else if (ax && a->op != COp::Loop) {
+      for (int l : q.deps) axis_deps.push_back(l);
+    }
+    ps.push_back(q);
+  }
+  if (biggest >= dep_product(s, whole)) return false;  // no smaller table than the whole coordinate
+  const int new_atab = axis_deps.empty() ? 0 : 1;
+  if (k->n_atab + new_atab > MAXTAB || k->n_mix + (int)mixed_groups.size() > MAXMIX) return false;
+  k->base += c0 * st;
+  // biased part: coef*st*(atom - b) >= 0 with b = alo (coef > 0) or ahi (coef < 0)
+  auto biased = [&](const Part& q, int64_t* bias) {
+    *bias = q.coef > 0 ? q.alo : q.ahi;
+    k->base += q.coef * st * *bias;
+    return *bias == 0 ? q.atom : c_bin(COp::Sub, q.atom, c_const(*bias));
+  };
+  TabSpec atab;
+  std::map<std::vector<int>, TabSpec> mtabs;
+  for (auto& q : ps) {
+    const bool ax = q.deps.back() < A, rd = q.deps.front() >= A;
+    if (ax && q.atom->op == COp::Loop) {
+      k->lin[q.atom->loop] += q.coef * st;
+      continue;
+    }
+    int64_t bias;
+    CE e = biased(q, &bias);
+    if (rd) {
+      rprogs->push_back({e, 0, q.coef * st});
+    } else if (ax) {
+      atab.progs.push_back({e, 0, q.coef * st});
+    } else {
+      TabSpec& t = mtabs[q.deps];
+      t.progs.push_back({e, 0, q.coef * st});
+    }
+  }
+  if (!atab.progs.empty()) {
+    std::set<int> u(axis_deps.begin(), axis_deps.end());
+    atab.deps.assign(u.begin(), u.end());
+    add_fix_table(s, std::move(atab), k, true, A, tabs, fix);
+  }
+  for (auto& [deps, t] : mtabs) {
+    t.deps = deps;
+    add_fix_table(s, std::move(t), k, false, A, tabs, fix);
+  }
+  return true;
+}
+
 static void build_kterm(const CStage& s, const CTerm& t, KTerm* k, std::vector<TabSpec>* tabs,
                         std::vector<Fixup>* fix, bool* dead) {
   memset(k, 0, sizeof(KTerm));
   const int A = (int)s.axis_ext.size();
   const int L = s.nloops();
-  k->kind = t.t.kind == TK_PHANTOM ? 2 : (t.t.kind == TK_STAGE || t.t.kind == TK_DSTAGE ? 1 : 0);
+  k->kind = t.t.kind == TK_PHANTOM ? 2 : (t.t.kind == TK_STAGE || t.t.kind == TK_DSTAGE || t.t.kind == TK_SCRATCH ? 1 : 0);
   if (t.t.numel() >= (int64_t)INT32_MAX) fail(SYNO_E_UNSUPPORTED, "tensor has 2^31 or more elements");
   auto strides = row_major_strides(t.t.extents);
   if (t.coords.size() != t.t.extents.size()) fail(SYNO_E_SHAPE, "access rank does not match tensor rank");
@@ -387,43 +479,15 @@ static void build_kterm(const CStage& s, const CTerm& t, KTerm* k, std::vector<T
       continue;
     }
     bool axis_only = deps.back() < A, red_only = deps.front() >= A;
+    if (!axis_only && !red_only && split_in_range(s, c, n, st, A, k, tabs, fix, &rprogs)) continue;
     if (red_only) {
       rprogs.push_back({c, n, st});
       continue;
     }
     TabSpec tab;
     tab.deps = deps;
-    for (int l : deps) {
-      tab.dep_ext.push_back(s.ext(l));
-      tab.count *= s.ext(l);
-    }
     tab.progs.push_back({c, n, st});
-    if (tab.count >= table_limit()) fail(SYNO_E_UNSUPPORTED, "index table too large");
-    auto tstr = row_major_strides(tab.dep_ext);
-    int tid = (int)tabs->size();
-    tabs->push_back(tab);
-    if (axis_only) {
-      if (k->n_atab >= MAXTAB) fail(SYNO_E_UNSUPPORTED, "too many axis tables in one term");
-      int m = k->n_atab++;
-      for (size_t q = 0; q < deps.size(); ++q) k->atab_s[m][deps[q]] = (int32_t)tstr[q];
-      fix->push_back({&k->atab[m], tid});
-    } else {
-      if (k->n_mix >= MAXMIX) fail(SYNO_E_UNSUPPORTED, "too many mixed tables in one term");
-      int m = k->n_mix++;
-      CE ri = c_const(0);
-      for (size_t q = 0; q < deps.size(); ++q) {
-        if (deps[q] < A) k->mtab_s[m][deps[q]] = (int32_t)tstr[q];
-        else ri = c_bin(COp::Add, ri, c_bin(COp::Mul, c_loop(deps[q]), c_const(tstr[q])));
-      }
-      fix->push_back({&k->mtab[m], tid});
-      TabSpec rt;
-      rt.deps = all_red;
-      rt.dep_ext = red_ext;
-      rt.count = R;
-      rt.progs.push_back({ri, 0, 1});
-      fix->push_back({&k->mri[m], (int)tabs->size()});
-      tabs->push_back(rt);
-    }
+    add_fix_table(s, std::move(tab), k, axis_only, A, tabs, fix);
   }
   if (!rprogs.empty()) {
     TabSpec rt;
@@ -436,8 +500,55 @@ static void build_kterm(const CStage& s, const CTerm& t, KTerm* k, std::vector<T
   }
 }
 
+static void add_fix_table(const CStage& s, TabSpec&& tab, KTerm* k, bool axis_only, int A,
+                          std::vector<TabSpec>* tabs, std::vector<Fixup>* fix) {
+  const std::vector<int> deps = tab.deps;
+  tab.dep_ext.clear();
+  tab.count = 1;
+  for (int l : deps) {
+    tab.dep_ext.push_back(s.ext(l));
+    tab.count *= s.ext(l);
+  }
+  if (tab.count >= table_limit()) fail(SYNO_E_UNSUPPORTED, "index table too large");
+  auto tstr = row_major_strides(tab.dep_ext);
+  int tid = (int)tabs->size();
+  tabs->push_back(tab);
+  if (axis_only) {
+    if (k->n_atab >= MAXTAB) fail(SYNO_E_UNSUPPORTED, "too many axis tables in one term");
+    int m = k->n_atab++;
+    for (size_t q = 0; q < deps.size(); ++q) k->atab_s[m][deps[q]] = (int32_t)tstr[q];
+    fix->push_back({&k->atab[m], tid});
+    return;
+  }
+  if (k->n_mix >= MAXMIX) fail(SYNO_E_UNSUPPORTED, "too many mixed tables in one term");
+  int m = k->n_mix++;
+  CE ri = c_const(0);
+  for (size_t q = 0; q < deps.size(); ++q) {
+    if (deps[q] < A) k->mtab_s[m][deps[q]] = (int32_t)tstr[q];
+    else ri = c_bin(COp::Add, ri, c_bin(COp::Mul, c_loop(deps[q]), c_const(tstr[q])));
+  }
+  fix->push_back({&k->mtab[m], tid});
+  std::vector<int> all_red;
+  std::vector<int64_t> red_ext;
+  int64_t R = 1;
+  for (int l = A; l < s.nloops(); ++l) {
+    all_red.push_back(l);
+    red_ext.push_back(s.ext(l));
+    R *= s.ext(l);
+  }
+  TabSpec rt;
+  rt.deps = all_red;
+  rt.dep_ext = red_ext;
+  rt.count = R;
+  rt.progs.push_back({ri, 0, 1});
+  fix->push_back({&k->mri[m], (int)tabs->size()});
+  tabs->push_back(rt);
+}
+
 void release_dev_stage(DevStage& ds) {
   // callers have synchronised the device (DevPlan / TcPlan teardown)
+  if (ds.tile && ds.tile->finish) release_dev_stage(*ds.tile->finish);
+  ds.tile.reset();
   if (ds.tables) cudaFreeAsync(ds.tables, nullptr);
   ds.tables = nullptr;
   if (ds.prog) cudaFree(ds.prog);
@@ -493,12 +604,107 @@ static void build_prog_stage(const CStage& cs, DevStage* ds) {
     KTerm& kt = k.terms[t];
     memset(&kt, 0, sizeof(KTerm));
     const int tk = cs.terms[t].t.kind;
-    kt.kind = tk == TK_PHANTOM ? 2 : (tk == TK_STAGE || tk == TK_DSTAGE ? 1 : 0);
+    kt.kind = tk == TK_PHANTOM ? 2 : (tk == TK_STAGE || tk == TK_DSTAGE || tk == TK_SCRATCH ? 1 : 0);
   }
   memset(&k.target, 0, sizeof(KTerm));
 }
 
+static void build_dev_stage_impl(const CStage& cs, DevStage* ds, cudaStream_t stream, bool allow_tile);
+
 void build_dev_stage(const CStage& cs, DevStage* ds, cudaStream_t stream) {
+  build_dev_stage_impl(cs, ds, stream, true);
+}
+
+// The tiled gather form of a gather stage (TileArgs, engine.hpp), decided
+// from the built terms: reduce-dependent terms are those with a reduce or
+// mixed table; F = axes their mixed tables read, I = other axes they read,
+// B = the rest.  The finish stage (axes = the stage's, one reduce over the
+// splits) reads the scratch sums as a TK_SCRATCH term and multiplies in the
+// reduce-invariant terms.
+static void build_tile(const CStage& cs, DevStage* ds, cudaStream_t stream) {
+  static const bool off = getenv("SYNO_NO_TILE") != nullptr;  // A/B switch
+  const KStage& k = ds->k;
+  if (off || cs.scatter || k.prog || ds->dead || k.R < 8 || k.out_count == 0) return;
+  const int A = k.n_axes;
+  std::vector<int> rt;
+  std::vector<bool> inF(A, false), inI(A, false);
+  for (int t = 0; t < k.n_terms; ++t) {
+    const KTerm& T = k.terms[t];
+    if (!T.rtab && T.n_mix == 0) continue;
+    rt.push_back(t);
+    for (int m = 0; m < T.n_mix; ++m)
+      for (int a = 0; a < A; ++a) inF[a] = inF[a] || T.mtab_s[m][a] != 0;
+  }
+  if (rt.empty()) return;
+  for (int t : rt) {
+    const KTerm& T = k.terms[t];
+    for (int a = 0; a < A; ++a) {
+      bool used = T.lin[a] != 0;
+      for (int m = 0; m < T.n_atab; ++m) used = used || T.atab_s[m][a] != 0;
+      inI[a] = inI[a] || (used && !inF[a]);
+    }
+  }
+  auto info = std::make_shared<TileInfo>();
+  TileArgs& a = info->a;
+  memset(&a, 0, sizeof(a));
+  int64_t NF = 1, NI = 1;
+  for (int x = 0; x < A; ++x) {
+    if (inF[x]) {
+      a.faxis[a.nF] = x;
+      a.fext[a.nF++] = (int32_t)k.axis_ext[x];
+      NF *= k.axis_ext[x];
+    } else if (inI[x]) {
+      a.iaxis[a.nI] = x;
+      a.iext[a.nI++] = (int32_t)k.axis_ext[x];
+      NI *= k.axis_ext[x];
+    }
+  }
+  if (NF * NI >= (int64_t)1 << 30) return;
+  a.NF = (int32_t)NF;
+  a.NI = (int32_t)NI;
+  a.n_rt = (int32_t)rt.size();
+  for (size_t q = 0; q < rt.size(); ++q) a.rterm[q] = rt[q];
+  a.TI = (int32_t)std::min<int64_t>(NI, 256);
+  a.TF = (int32_t)std::min<int64_t>(NF, 256 / a.TI);
+  a.TR = (int32_t)std::max<int64_t>(1, std::min<int64_t>({256 / (a.TI * a.TF), 64, k.R}));
+  a.nIb = (int32_t)((NI + a.TI - 1) / a.TI);
+  const int64_t budget = 40 * 1024 / 4;  // int32 row entries per chunk
+  a.RC = (int32_t)std::max<int64_t>(8, std::min<int64_t>({k.R, budget / ((int64_t)a.n_rt * a.TF) - 1, 1024}));
+  info->ctas = (int64_t)a.nIb * ((NF + a.TF - 1) / a.TF);
+  const int64_t want = 148 * 4;
+  int64_t S = std::max<int64_t>(1, (want + info->ctas - 1) / info->ctas);
+  S = std::min<int64_t>({S, std::max<int64_t>(1, k.R / std::max<int32_t>(a.RC, 32)), 65535});
+  const int64_t r_chunk = (k.R + S - 1) / S;
+  S = (k.R + r_chunk - 1) / r_chunk;
+  info->splits = S;
+  info->smem = std::max<size_t>((size_t)a.n_rt * a.TF * (a.RC + 1) * 4, 256 * 8);
+  // finish stage: out[axes] = scale * sum_s acc[s, F, I] * prod(reduce-invariant terms)
+  CStage fin;
+  fin.axis_ext = cs.axis_ext;
+  fin.red_ext = {S};
+  fin.scale = cs.scale;
+  fin.out = cs.out;
+  CTerm acc;
+  acc.t.kind = TK_SCRATCH;
+  acc.t.extents = {S};
+  acc.coords = {c_loop(A)};
+  for (int q = 0; q < a.nF; ++q) {
+    acc.t.extents.push_back(a.fext[q]);
+    acc.coords.push_back(c_loop(a.faxis[q]));
+  }
+  for (int q = 0; q < a.nI; ++q) {
+    acc.t.extents.push_back(a.iext[q]);
+    acc.coords.push_back(c_loop(a.iaxis[q]));
+  }
+  fin.terms.push_back(acc);
+  for (int t = 0; t < k.n_terms; ++t)
+    if (std::find(rt.begin(), rt.end(), t) == rt.end()) fin.terms.push_back(cs.terms[t]);
+  info->finish = std::make_shared<DevStage>();
+  build_dev_stage_impl(fin, info->finish.get(), stream, false);
+  ds->tile = info;
+}
+
+static void build_dev_stage_impl(const CStage& cs, DevStage* ds, cudaStream_t stream, bool allow_tile) {
   ds->cs = cs;
   KStage& k = ds->k;
   memset(&k, 0, sizeof(KStage));
@@ -544,6 +750,7 @@ void build_dev_stage(const CStage& cs, DevStage* ds, cudaStream_t stream) {
     for (auto& t : tabs) launch_k1(t, ds->tables + t.offset, nullptr, stream);
   }
   for (auto& f : fix) *f.field = ds->tables + tabs[f.table].offset;
+  if (allow_tile) build_tile(cs, ds, stream);
 }
 
 DevPlan::~DevPlan() {
@@ -923,6 +1130,124 @@ __global__ void __launch_bounds__(256) stage_block_kernel(const __grid_constant_
   }
 }
 
+// Tiled gather form (TileArgs in engine.hpp).  Thread (ti, tf, tr) of CTA
+// (ib, fb) owns output (F index fb*TF+tf, I index ib*TI+ti) and every TR-th
+// reduce index of each shared-memory chunk.  Per chunk, the CTA first builds
+// the offset row of every reduce-dependent term for its TF F-combinations
+// (reduce tables + mixed tables indexed by the F digits; -1 = out of range),
+// then every thread runs its products reading the rows (one shared load per
+// term) plus its own per-thread offset part.  The TR partial sums are added
+// in a fixed order: the result is deterministic.
+template <typename TI, typename TA, int NT>
+__global__ void __launch_bounds__(256) stage_tile_kernel(const __grid_constant__ KStage S,
+                                                         const __grid_constant__ TileArgs A) {
+  pdl_trigger();
+  pdl_wait();
+  extern __shared__ int32_t srow[];
+  const int tid = threadIdx.x;
+  const int ti = tid % A.TI, tf = (tid / A.TI) % A.TF, tr = tid / (A.TI * A.TF);
+  const int ib = blockIdx.x % A.nIb, fb = blockIdx.x / A.nIb;
+  const int i = ib * A.TI + ti, f = fb * A.TF + tf;
+  const bool live = i < A.NI && f < A.NF && tr < A.TR;
+  int32_t av[MAXA];
+#pragma unroll
+  for (int k = 0; k < MAXA; ++k) av[k] = 0;
+  {
+    int rem = live ? i : 0;
+    for (int q = A.nI - 1; q >= 0; --q) {
+      av[A.iaxis[q]] = rem % A.iext[q];
+      rem /= A.iext[q];
+    }
+    rem = live ? f : 0;
+    for (int q = A.nF - 1; q >= 0; --q) {
+      av[A.faxis[q]] = rem % A.fext[q];
+      rem /= A.fext[q];
+    }
+  }
+  int64_t base[NT];
+  bool aok[NT];
+#pragma unroll
+  for (int k = 0; k < NT; ++k) {
+    base[k] = 0;
+    aok[k] = false;
+    if (k < A.n_rt) {
+      int32_t ia[MAXMIX];
+      term_prep(S.terms[A.rterm[k]], S.n_axes, av, &base[k], &aok[k], ia);
+    }
+  }
+  const int64_t r0 = (int64_t)blockIdx.y * S.r_chunk;
+  const int64_t r1 = min(S.R, r0 + S.r_chunk);
+  const int pitch = A.RC + 1;
+  TA acc = 0;
+  for (int64_t c0 = r0; c0 < r1; c0 += A.RC) {
+    const int rc = (int)min((int64_t)A.RC, r1 - c0);
+    __syncthreads();
+    const int items = A.n_rt * A.TF * rc;
+    for (int it = tid; it < items; it += blockDim.x) {
+      const int rl = it % rc;
+      const int rest = it / rc;
+      const int fl = rest % A.TF, k = rest / A.TF;
+      const int fg = fb * A.TF + fl;
+      int32_t v = -1;
+      if (fg < A.NF) {
+        const KTerm& T = S.terms[A.rterm[k]];
+        const int64_t r = c0 + rl;
+        bool ok = true;
+        int64_t o = 0;
+        if (T.rtab) {
+          const int32_t x = __ldg(T.rtab + r);
+          ok = x >= 0;
+          o = x;
+        }
+        if (T.n_mix) {
+          int32_t fd[MAXA];
+          int rem = fg;
+          for (int q = A.nF - 1; q >= 0; --q) {
+            fd[q] = rem % A.fext[q];
+            rem /= A.fext[q];
+          }
+          for (int m = 0; m < T.n_mix && ok; ++m) {
+            int32_t idx = __ldg(T.mri[m] + r);
+            for (int q = 0; q < A.nF; ++q) idx += T.mtab_s[m][A.faxis[q]] * fd[q];
+            const int32_t x = __ldg(T.mtab[m] + idx);
+            ok = x >= 0;
+            o += x;
+          }
+        }
+        v = ok ? (int32_t)o : -1;
+      }
+      srow[(k * A.TF + fl) * pitch + rl] = v;
+    }
+    __syncthreads();
+    if (live) {
+      for (int rl = tr; rl < rc; rl += A.TR) {
+        TA prod = 1;
+        bool ok = true;
+#pragma unroll
+        for (int k = 0; k < NT; ++k) {
+          if (k < A.n_rt && ok) {
+            const int32_t o = srow[(k * A.TF + tf) * pitch + rl];
+            const KTerm& T = S.terms[A.rterm[k]];
+            if (o < 0 || !aok[k]) ok = false;
+            else if (T.kind != 2) prod *= load_term<TI, TA>(T, base[k] + o);
+          }
+        }
+        if (ok) acc += prod;
+      }
+    }
+  }
+  // fixed-order combination of the TR partial sums of each output
+  __syncthreads();
+  TA* red = reinterpret_cast<TA*>(srow);
+  red[tid] = acc;
+  __syncthreads();
+  if (tr == 0 && live) {
+    TA s = acc;
+    for (int q = 1; q < A.TR; ++q) s += red[tid + q * A.TI * A.TF];
+    ((TA*)A.acc)[((int64_t)blockIdx.y * A.NF + f) * A.NI + i] = s;
+  }
+}
+
 template <typename TO, typename TA>
 __global__ void sum_partials(const TA* part, int64_t count, int nsplit, TO* out) {
   pdl_trigger();
@@ -959,6 +1284,7 @@ static const void* bind_ptr(const CTensor& t, const Bindings& b) {
     case TK_DX: return b.dx;
     case TK_DW: return b.dw.at(t.index);
     case TK_DSTAGE: return b.dstages.at(t.index);
+    case TK_SCRATCH: return b.scratch;
     default: return nullptr;
   }
 }
@@ -1014,6 +1340,29 @@ static void launch_stage_impl(const DevStage& ds, const Bindings& b, void* out, 
     if (k.n_terms <= 2) launch_k(affine_kernel<TI, TA, 2>, blocks, 256, 0, stream, k);
     else launch_k(affine_kernel<TI, TA, MAXT>, blocks, 256, 0, stream, k);
     cuda_check(cudaGetLastError(), "affine_kernel");
+    return;
+  }
+  if (ds.tile && !ds.cs.scatter && !k.prog) {
+    *kind = "stage_tile";
+    const TileInfo& ti = *ds.tile;
+    TileArgs a = ti.a;
+    TA* acc = nullptr;
+    cuda_check(cudaMallocAsync((void**)&acc, (size_t)ti.splits * a.NF * a.NI * sizeof(TA), stream), "alloc tile sums");
+    a.acc = acc;
+    k.r_chunk = (k.R + ti.splits - 1) / ti.splits;
+    k.out = nullptr;
+    const dim3 grid((unsigned)ti.ctas, (unsigned)ti.splits);
+    const unsigned threads = (unsigned)(a.TI * a.TF * a.TR);
+    note_launch();
+    if (a.n_rt <= 2) launch_k(stage_tile_kernel<TI, TA, 2>, grid, threads, ti.smem, stream, k, a);
+    else if (a.n_rt <= 4) launch_k(stage_tile_kernel<TI, TA, 4>, grid, threads, ti.smem, stream, k, a);
+    else launch_k(stage_tile_kernel<TI, TA, MAXT>, grid, threads, ti.smem, stream, k, a);
+    cuda_check(cudaGetLastError(), "stage_tile_kernel");
+    Bindings b2 = b;
+    b2.scratch = acc;
+    const char* fk = nullptr;
+    launch_stage_impl<TI>(*ti.finish, b2, out, out_acc, stream, &fk);
+    cuda_check(cudaFreeAsync(acc, stream), "free tile sums");
     return;
   }
   const bool block_mode = !ds.cs.scatter && k.out_count <= 16384 && k.R >= 2048 && !k.prog;

@@ -61,9 +61,41 @@ struct KStage {
 
 // One device-resident stage: tables plus a descriptor with null pointers
 // for the run-time tensors (bound per launch).
+// Tiled gather form (engine.cu, stage_tile_kernel): the stage's axes split
+// into F (read together with reduces through mixed tables), I (read only
+// through per-thread axis parts) and B (not read by any reduce-dependent
+// term).  One CTA computes the reduce sum for a tile of F x I outputs,
+// staging the per-(F, r) offset rows of every reduce-dependent term in
+// shared memory once per CTA; a finish stage multiplies in the
+// reduce-invariant terms, sums the reduce splits in a fixed order and
+// broadcasts over B.
+struct TileArgs {
+  int32_t nF, nI;
+  int32_t faxis[MAXA], iaxis[MAXA];
+  int32_t fext[MAXA], iext[MAXA];
+  int32_t NF, NI;
+  int32_t TF, TI, TR;       // CTA tile: TI x TF outputs, TR threads per output along the reduce
+  int32_t RC;               // reduce chunk staged in shared memory
+  int32_t n_rt;             // reduce-dependent terms
+  int32_t rterm[MAXT];
+  int32_t nIb;              // CTAs along I
+  int32_t pad_;
+  void* acc;                // [S][NF][NI] accumulator scratch
+};
+
+struct DevStage;
+struct TileInfo {
+  TileArgs a;
+  int64_t splits = 1;
+  int64_t ctas = 1;
+  size_t smem = 0;
+  std::shared_ptr<DevStage> finish;
+};
+
 struct DevStage {
   CStage cs;
   KStage k;
+  std::shared_ptr<TileInfo> tile;  // tiled gather form, when it applies
   std::vector<int> term_slot;   // CTensor of each term, to bind pointers
   int32_t* tables = nullptr;    // owned device allocation
   int64_t* prog = nullptr;      // owned device allocation (program fallback)
@@ -100,6 +132,7 @@ struct Bindings {
   std::vector<void*> dw;
   std::vector<void*> stages;  // t_k buffers
   std::vector<void*> dstages; // gradients of t_k (staged backward)
+  const void* scratch = nullptr;  // tiled form: the reduce sums read by the finish stage
   bool x_unchanged = false;   // syno_backward_ex(SYNO_BWD_X_UNCHANGED)
   bool w_unchanged = false;   // syno_backward_ex(SYNO_BWD_W_UNCHANGED)
 };

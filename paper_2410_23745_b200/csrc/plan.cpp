@@ -81,7 +81,7 @@ double CStage::grid_points() const {
 
 std::string CStage::describe() const {
   std::ostringstream o;
-  static const char* kn[] = {"x", "w", "t", "y", "dy", "dx", "dw", "phantom", "dt"};
+  static const char* kn[] = {"x", "w", "t", "y", "dy", "dx", "dw", "phantom", "dt", "acc"};
   o << (scatter ? "scatter" : "gather") << " out=" << kn[out.kind] << out.index << " axes=[";
   for (size_t k = 0; k < axis_ext.size(); ++k) o << (k ? "," : "") << axis_ext[k];
   o << "] reduces=[";
@@ -446,6 +446,13 @@ Plan build_plan(const LoopNest& unstaged, const LoopNest& staged, const std::vec
       }
     }
   }
+  // the engine's stages get simplified coordinates (smaller index tables);
+  // `unstaged` keeps the reference's form for the tensor-core matcher
+  for (auto& st : p.forward) simplify_stage(&st);
+  for (auto& st : p.grad_x) simplify_stage(&st);
+  for (auto& gw : p.grad_w)
+    for (auto& st : gw) simplify_stage(&st);
+  for (auto& st : p.bwd_staged) simplify_stage(&st);
   return p;
 }
 

@@ -51,6 +51,7 @@ enum TensorKind : int {
   TK_DW = 6,      // weight gradient j
   TK_PHANTOM = 7, // validity-only term (value 1 when in range)
   TK_DSTAGE = 8,  // gradient of intermediate t_k (workspace, accumulator precision)
+  TK_SCRATCH = 9, // engine-internal partial sums (accumulator precision)
 };
 
 struct CTensor {
@@ -108,6 +109,16 @@ struct Plan {
 CStage derive_gradient(const CStage& S, int j, const CTensor& grad);
 // Same, with an explicit upstream tensor (dy, or the gradient of an intermediate).
 CStage derive_gradient(const CStage& S, int j, const CTensor& grad, const CTensor& upstream);
+
+// Quasi-affine simplification (csrc/simplify.cpp): the same values for every
+// loop assignment within `loop_ext`, with multiples pulled out of floor
+// divisions / modulos and range-resolved ones removed.
+CE c_simplify(const CE& e, const std::vector<int64_t>& loop_ext);
+// Interval bounds of e over the loop extents (false: unbounded / unknown).
+bool c_range(const CE& e, const std::vector<int64_t>& loop_ext, int64_t* lo, int64_t* hi);
+void simplify_stage(CStage* s);
+// e as c0 + sum coef * atom over its top-level + - and constant products.
+void c_sum_parts(const CE& e, int64_t* c0, std::vector<std::pair<int64_t, CE>>* parts);
 
 Plan build_plan(const LoopNest& unstaged, const LoopNest& staged_or_same, const std::vector<Size>& batch_dims,
                 const Assignment& env);

@@ -122,7 +122,18 @@ def operator_document(graph) -> str:
     if spec.batch_dims:
         lines.append("batch " + " ".join(str(s) for s in spec.batch_dims))
     lines.append("steps " + print_steps(graph))
-    return "\n".join(lines) + "\n"
+    text = "\n".join(lines) + "\n"
+    # the reference's print_operator ends with the match_input permutation
+    # (pgraph.py:724-726); the native replay computes it (csrc/graph.cpp)
+    with _CACHE_LOCK:
+        doc = _REF_DOCS.get(text)
+    if doc is None:
+        doc = Handle(text, None, False, replay_only=True).document()
+        with _CACHE_LOCK:
+            if len(_REF_DOCS) >= _CACHE_MAX:
+                _REF_DOCS.pop(next(iter(_REF_DOCS)))
+            _REF_DOCS[text] = doc
+    return doc
 
 
 # ---------------------------------------------------------------------------
@@ -174,6 +185,7 @@ class Handle:
 
 
 _CACHE: dict = {}
+_REF_DOCS: dict = {}
 _CACHE_LOCK = threading.Lock()
 _CACHE_MAX = 4096
 

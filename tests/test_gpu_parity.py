@@ -275,15 +275,16 @@ def test_staged_handles_forward_backward(cuda, case, dtype):
         assert O.rel_err(a, b) < tol
 
 
-@pytest.mark.parametrize("chunk", range(4))
+@pytest.mark.parametrize("chunk", range(8))
 def test_corpus_reduced_staged_fp32(cuda, chunk):
-    """Corpus operators through staged handles (rfactored forward, staged
-    backward where it applies) at reduced sizes, fp32, against the oracle."""
+    """Every corpus operator (all 1024 over the 8 chunks) through staged
+    handles (rfactored forward, staged backward where it applies) at reduced
+    sizes, fp32, against the oracle."""
     from paper_2410_23745_b200 import codegen as C
     from paper_2410_23745_b200 import ops
     from paper_2410_23745_b200 import pgraph as P
     torch = _torch()
-    ops_ = _corpus()[chunk::4][:96]
+    ops_ = _corpus()[chunk::8]
     checked = 0
     for op in ops_:
         g, red = reduced_case(op)
@@ -308,3 +309,160 @@ def test_corpus_reduced_staged_fp32(cuda, chunk):
             assert O.rel_err(f(a), b) < 1e-4, op
         checked += 1
     assert checked >= len(ops_) // 2
+
+
+@pytest.mark.parametrize("name", ["conv2d_8", "strided_conv1d", "sep_shared", "bpool", "corpus0003", "corpus0011"])
+def test_program_fallback_fp32(cuda, name, monkeypatch):
+    """The on-the-fly coordinate-program path (what a 2^28-entry table falls
+    back to at full size) in float32, tolerance 1e-4."""
+    from paper_2410_23745_b200 import ops
+    from paper_2410_23745_b200 import pgraph as P
+    torch = _torch()
+    case = next(c for c in CASES if c["name"] == name)
+    monkeypatch.setenv("SYNO_TABLE_LIMIT", "2")
+    h = P.Handle(case["document"], case["assignment"], False)
+    x, ws, up, _, _, _ = case_tensors(case)
+    env, bs = case["env"], case["batch_shape"]
+    x, up = _rounded(x, "float32"), _rounded(up, "float32")
+    ws = [_rounded(w, "float32") for w in ws]
+    xd, ud = ops.to_device(x, "float32"), ops.to_device(up, "float32")
+    wd = [ops.to_device(w, "float32") for w in ws]
+    gy = ops.forward(h, xd, wd)
+    gdx, gdw = ops.backward(h, xd, wd, ud)
+    torch.cuda.synchronize()
+    f = lambda t: t.double().cpu().numpy()  # noqa: E731
+    assert O.rel_err(f(gy), O.interpret(case["nest"], env, x, ws, bs)) < 1e-4
+    assert O.rel_err(f(gdx), O.input_gradient(case["nest"], env, x, up, ws, bs)) < 1e-4
+    for a, b in zip(gdw, O.weight_gradient(case["nest"], env, x, up, ws, bs) if ws else []):
+        assert O.rel_err(f(a), b) < 1e-4
+
+
+@pytest.mark.parametrize("chunk", range(4))
+def test_corpus_program_fallback_reduced_fp32(cuda, chunk, monkeypatch):
+    """Corpus operators with every index table forced onto the program path
+    (SYNO_TABLE_LIMIT=2), fp32 at reduced sizes, against the oracle."""
+    from paper_2410_23745_b200 import codegen as C
+    from paper_2410_23745_b200 import ops
+    from paper_2410_23745_b200 import pgraph as P
+    torch = _torch()
+    monkeypatch.setenv("SYNO_TABLE_LIMIT", "2")
+    checked = 0
+    for op in _corpus()[chunk::16]:
+        g, red = reduced_case(op)
+        if red is None:
+            continue
+        for staged in (False, True):
+            h = P.Handle(P.operator_document(g), red, staged)
+            text = C.emit_loop_nest(g, red)
+            rng = np.random.default_rng(2000 + checked)
+            xr = _rounded(rng.standard_normal(h.x_shape), "float32")
+            wr = [_rounded(rng.standard_normal(s), "float32") for s in h.w_shapes]
+            upr = _rounded(rng.standard_normal(h.y_shape), "float32")
+            xd, ud = ops.to_device(xr, "float32"), ops.to_device(upr, "float32")
+            wd = [ops.to_device(w, "float32") for w in wr]
+            gy = ops.forward(h, xd, wd)
+            gdx, gdw = ops.backward(h, xd, wd, ud)
+            torch.cuda.synchronize()
+            bs = h.x_shape[:1]
+            f = lambda t: t.double().cpu().numpy()  # noqa: E731
+            assert O.rel_err(f(gy), O.interpret(text, red, xr, wr, bs)) < 1e-4, op
+            assert O.rel_err(f(gdx), O.input_gradient(text, red, xr, upr, wr, bs)) < 1e-4, op
+            for a, b in zip(gdw, O.weight_gradient(text, red, xr, upr, wr, bs) if wr else []):
+                assert O.rel_err(f(a), b) < 1e-4, op
+        checked += 1
+    assert checked >= 10
+
+
+def _full_size_spot_ids(count=16, max_grid=1 << 24):
+    """Seeded choice of corpus candidates whose full-size (one image) grid the
+    oracle evaluates in seconds: half with weights, half pure gathers."""
+    from paper_2410_23745_b200 import codegen as C
+    from paper_2410_23745_b200 import pgraph as P
+    spec = P.build_spec(**dict(CORPUS_SPEC, reference=dict(CORPUS_SPEC["reference"], N=1)))
+    rng = np.random.default_rng(8)
+    weighted, plain = [], []
+    for i in rng.permutation(len(_corpus())):
+        g = P.parse_steps(_corpus()[i], spec)
+        try:
+            if C.flops(g) // 2 > max_grid:
+                continue
+        except Exception:
+            continue
+        bucket = weighted if g.n_weights else plain
+        if len(bucket) < count // 2:
+            bucket.append(int(i))
+        if len(weighted) + len(plain) == count:
+            break
+    return sorted(weighted + plain)
+
+
+@pytest.mark.parametrize("staged", [False, True], ids=["unstaged", "staged"])
+def test_corpus_full_size_oracle_spot_check(cuda, staged):
+    """a seeded subset of corpus candidates at FULL size
+    (C=64, H=W=32, one image), fp32, forward + grad-input + grad-weight
+    against the oracle (reference codegen.py:598-743)."""
+    from paper_2410_23745_b200 import codegen as C
+    from paper_2410_23745_b200 import ops
+    from paper_2410_23745_b200 import pgraph as P
+    torch = _torch()
+    spec = P.build_spec(**dict(CORPUS_SPEC, reference=dict(CORPUS_SPEC["reference"], N=1)))
+    ids = _full_size_spot_ids()
+    assert len(ids) == 16
+    for i in ids:
+        g = P.parse_steps(_corpus()[i], spec)
+        h = P.handle_for(g, None, staged)
+        env = dict(CORPUS_SPEC["reference"], N=1)
+        text = C.emit_loop_nest(g)
+        rng = np.random.default_rng(3000 + i)
+        xr = _rounded(rng.standard_normal(h.x_shape), "float32")
+        wr = [_rounded(rng.standard_normal(s), "float32") for s in h.w_shapes]
+        upr = _rounded(rng.standard_normal(h.y_shape), "float32")
+        xd, ud = ops.to_device(xr, "float32"), ops.to_device(upr, "float32")
+        wd = [ops.to_device(w, "float32") for w in wr]
+        gy = ops.forward(h, xd, wd)
+        gdx, gdw = ops.backward(h, xd, wd, ud)
+        torch.cuda.synchronize()
+        f = lambda t: t.double().cpu().numpy()  # noqa: E731
+        assert O.rel_err(f(gy), O.interpret(text, env, xr, wr, (1,))) < 1e-4, i
+        assert O.rel_err(f(gdx), O.input_gradient(text, env, xr, upr, wr, (1,))) < 1e-4, i
+        for a, b in zip(gdw, O.weight_gradient(text, env, xr, upr, wr, (1,)) if wr else []):
+            assert O.rel_err(f(a), b) < 1e-4, i
+
+
+# the heaviest sweep candidates (program fallback / 2^28-entry tables at
+# N=8), sample 828 among them
+HEAVY = [828, 170, 171, 172, 732, 736, 518, 7, 8, 319]
+
+
+@pytest.mark.parametrize("sid", HEAVY)
+def test_heavy_sweep_candidates_adjoint_f64(cuda, sid):
+    """Full sweep size (N=8): the float64 run must satisfy the adjoint
+    identities <dy, y> = <dx, x> = <dw_j, w_j> to 1e-10 (what the sweep
+    checks in fp32 to 1e-4), and the fp32 run must agree with the f64 run
+    to 1e-4 in y, dx and every dw."""
+    from paper_2410_23745_b200 import ops
+    from paper_2410_23745_b200 import workloads as WL
+    from paper_2410_23745_b200.sweep import evaluate
+    torch = _torch()
+    g = WL.corpus(8)[sid]
+    r = evaluate(g, sid, sid, dtype=torch.float64)
+    assert r.status == "ok" and r.adjoint_err < 1e-10, r
+    r32 = evaluate(g, sid, sid, dtype=torch.float32)
+    assert r32.status == "ok", r32
+    from paper_2410_23745_b200 import pgraph as P
+    h = P.handle_for(g, None, True)
+    gen = torch.Generator(device="cuda").manual_seed(sid)
+    x = torch.randn(h.x_shape, generator=gen, device="cuda", dtype=torch.float64)
+    ws = [torch.randn(s, generator=gen, device="cuda", dtype=torch.float64) for s in h.w_shapes]
+    dy = torch.randn(h.y_shape, generator=gen, device="cuda", dtype=torch.float64)
+    x, ws, dy = x.float().double(), [w.float().double() for w in ws], dy.float().double()
+    y64 = ops.forward(h, x, ws)
+    dx64, dw64 = ops.backward(h, x, ws, dy)
+    y32 = ops.forward(h, x.float(), [w.float() for w in ws])
+    dx32, dw32 = ops.backward(h, x.float(), [w.float() for w in ws], dy.float())
+    torch.cuda.synchronize()
+    f = lambda t: t.double().cpu().numpy()  # noqa: E731
+    assert O.rel_err(f(y32), f(y64)) < 1e-4
+    assert O.rel_err(f(dx32), f(dx64)) < 1e-4
+    for a, b in zip(dw32, dw64):
+        assert O.rel_err(f(a), f(b)) < 1e-4

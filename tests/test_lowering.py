@@ -78,3 +78,40 @@ def test_parse_errors_follow_the_reference():
         P.parse_operator(doc.replace("perm 0 1 2", "perm 2 1 0"))
     with pytest.raises(OperatorParseError):
         P.parse_operator(doc.replace("var K coefficient 3", "var K scalar 3"))
+
+
+_SIMPLIFY_CHECK = r"""
+import sys
+sys.path.insert(0, sys.argv[1])
+sys.path.insert(0, sys.argv[1] + '/tests')
+from conftest import CASES
+from paper_2410_23745_b200 import pgraph as P
+from paper_2410_23745_b200 import workloads as WL
+n = 0
+for staged in (False, True):
+    for g in WL.corpus(8) + WL.corpus(1):
+        P.Handle(P.operator_document(g), None, staged)
+        n += 1
+    for c in CASES:
+        P.Handle(c["document"], c["assignment"], staged)
+        n += 1
+print("checked", n)
+"""
+
+
+def test_coordinate_simplification_is_exact():
+    """The engine's quasi-affine rewrite of every coordinate (csrc/simplify.cpp)
+    leaves each value unchanged: SYNO_CHECK_SIMPLIFY compares rewritten and
+    original expressions at the loop-range corners and 4096 pseudo-random
+    grid points, for every stage (forward, staged forward, grad-input,
+    grad-weight, staged backward) of the whole corpus and the golden cases."""
+    import os
+    import subprocess
+    import sys
+
+    from conftest import ROOT
+    env = dict(os.environ, SYNO_CHECK_SIMPLIFY="1")
+    r = subprocess.run([sys.executable, "-c", _SIMPLIFY_CHECK, ROOT], env=env, capture_output=True, text=True,
+                       timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    assert "checked" in r.stdout
