@@ -13,6 +13,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <cmath>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -549,6 +550,8 @@ void release_dev_stage(DevStage& ds) {
   // callers have synchronised the device (DevPlan / TcPlan teardown)
   if (ds.tile && ds.tile->finish) release_dev_stage(*ds.tile->finish);
   ds.tile.reset();
+  if (ds.pre) release_dev_stage(*ds.pre);
+  ds.pre.reset();
   if (ds.tables) cudaFreeAsync(ds.tables, nullptr);
   ds.tables = nullptr;
   if (ds.prog) cudaFree(ds.prog);
@@ -624,48 +627,101 @@ void build_dev_stage(const CStage& cs, DevStage* ds, cudaStream_t stream) {
 static void build_tile(const CStage& cs, DevStage* ds, cudaStream_t stream) {
   static const bool off = getenv("SYNO_NO_TILE") != nullptr;  // A/B switch
   const KStage& k = ds->k;
-  if (off || cs.scatter || k.prog || ds->dead || k.R < 8 || k.out_count == 0) return;
+  if (off || k.prog || ds->dead || k.R < 8 || k.out_count == 0) return;
+  const bool scatter = cs.scatter;
   const int A = k.n_axes;
-  std::vector<int> rt;
+  std::vector<int> rt, inv;
   std::vector<bool> inF(A, false), inI(A, false);
-  for (int t = 0; t < k.n_terms; ++t) {
-    const KTerm& T = k.terms[t];
-    if (!T.rtab && T.n_mix == 0) continue;
-    rt.push_back(t);
+  auto mixed_axes = [&](const KTerm& T) {
     for (int m = 0; m < T.n_mix; ++m)
       for (int a = 0; a < A; ++a) inF[a] = inF[a] || T.mtab_s[m][a] != 0;
-  }
-  if (rt.empty()) return;
-  for (int t : rt) {
+  };
+  for (int t = 0; t < k.n_terms; ++t) {
     const KTerm& T = k.terms[t];
+    if (!T.rtab && T.n_mix == 0) {
+      inv.push_back(t);
+      continue;
+    }
+    rt.push_back(t);
+    mixed_axes(T);
+  }
+  if (scatter) {
+    // the target must move with the reduce (else the sum belongs in a gather)
+    if (!k.target.rtab && k.target.n_mix == 0) return;
+    mixed_axes(k.target);
+  } else if (rt.empty()) {
+    return;
+  }
+  auto thread_axes = [&](const KTerm& T) {
     for (int a = 0; a < A; ++a) {
       bool used = T.lin[a] != 0;
       for (int m = 0; m < T.n_atab; ++m) used = used || T.atab_s[m][a] != 0;
       inI[a] = inI[a] || (used && !inF[a]);
     }
+  };
+  for (int t : rt) thread_axes(k.terms[t]);
+  if (scatter) {
+    // every grid point contributes: all axes are enumerated (F or I)
+    for (int a = 0; a < A; ++a) inI[a] = !inF[a];
   }
   auto info = std::make_shared<TileInfo>();
   TileArgs& a = info->a;
   memset(&a, 0, sizeof(a));
-  int64_t NF = 1, NI = 1;
+  a.scatter = scatter ? 1 : 0;
+  // lanes should walk the axis the first loaded reduce-dependent term reads
+  // contiguously (its last coordinate) -- for a scatter the target's, so the
+  // atomics of a warp hit neighbouring words: that axis goes innermost of its
+  // group and, when it is an F axis, the lanes run along F
+  int contig = -1;
+  const CTerm* lead = scatter ? &cs.target : nullptr;
+  for (int t : rt) {
+    if (lead) break;
+    if (k.terms[t].kind != 2) lead = &cs.terms[t];
+  }
+  if (lead && !lead->coords.empty()) {
+    std::vector<int> d;
+    c_loops(lead->coords.back(), &d);
+    for (int l : d)
+      if (l < A && (inF[l] || inI[l])) contig = l;  // the highest such axis
+  }
+  std::vector<int> forder, iorder;
   for (int x = 0; x < A; ++x) {
-    if (inF[x]) {
-      a.faxis[a.nF] = x;
-      a.fext[a.nF++] = (int32_t)k.axis_ext[x];
-      NF *= k.axis_ext[x];
-    } else if (inI[x]) {
-      a.iaxis[a.nI] = x;
-      a.iext[a.nI++] = (int32_t)k.axis_ext[x];
-      NI *= k.axis_ext[x];
-    }
+    if (x == contig) continue;
+    if (inF[x]) forder.push_back(x);
+    else if (inI[x]) iorder.push_back(x);
+  }
+  if (contig >= 0) (inF[contig] ? forder : iorder).push_back(contig);
+  a.ffast = contig >= 0 && inF[contig] ? 1 : 0;
+  int64_t NF = 1, NI = 1;
+  for (int x : forder) {
+    a.faxis[a.nF] = x;
+    a.fext[a.nF++] = (int32_t)k.axis_ext[x];
+    NF *= k.axis_ext[x];
+  }
+  for (int x : iorder) {
+    a.iaxis[a.nI] = x;
+    a.iext[a.nI++] = (int32_t)k.axis_ext[x];
+    NI *= k.axis_ext[x];
   }
   if (NF * NI >= (int64_t)1 << 30) return;
   a.NF = (int32_t)NF;
   a.NI = (int32_t)NI;
+  if (scatter) rt.push_back(-1);  // the target's row comes last
+  if ((int)rt.size() > MAXT) return;
   a.n_rt = (int32_t)rt.size();
   for (size_t q = 0; q < rt.size(); ++q) a.rterm[q] = rt[q];
-  a.TI = (int32_t)std::min<int64_t>(NI, 256);
-  a.TF = (int32_t)std::min<int64_t>(NF, 256 / a.TI);
+  if (scatter) {
+    a.n_inv = (int32_t)inv.size();
+    for (size_t q = 0; q < inv.size(); ++q) a.inv[q] = inv[q];
+  }
+  if (a.ffast) {
+    // one warp of F combinations; the rest of the CTA along I reuses the rows
+    a.TF = (int32_t)std::min<int64_t>(NF, 32);
+    a.TI = (int32_t)std::min<int64_t>(NI, 256 / a.TF);
+  } else {
+    a.TI = (int32_t)std::min<int64_t>(NI, 256);
+    a.TF = (int32_t)std::min<int64_t>(NF, 256 / a.TI);
+  }
   a.TR = (int32_t)std::max<int64_t>(1, std::min<int64_t>({256 / (a.TI * a.TF), 64, k.R}));
   a.nIb = (int32_t)((NI + a.TI - 1) / a.TI);
   const int64_t budget = 40 * 1024 / 4;  // int32 row entries per chunk
@@ -678,6 +734,10 @@ static void build_tile(const CStage& cs, DevStage* ds, cudaStream_t stream) {
   S = (k.R + r_chunk - 1) / r_chunk;
   info->splits = S;
   info->smem = std::max<size_t>((size_t)a.n_rt * a.TF * (a.RC + 1) * 4, 256 * 8);
+  if (scatter) {  // contributions go straight to the fixed-point sums: no finish stage
+    ds->tile = info;
+    return;
+  }
   // finish stage: out[axes] = scale * sum_s acc[s, F, I] * prod(reduce-invariant terms)
   CStage fin;
   fin.axis_ext = cs.axis_ext;
@@ -704,7 +764,93 @@ static void build_tile(const CStage& cs, DevStage* ds, cudaStream_t stream) {
   ds->tile = info;
 }
 
-static void build_dev_stage_impl(const CStage& cs, DevStage* ds, cudaStream_t stream, bool allow_tile) {
+static CE remap_loops(const CE& e, const std::vector<int>& m) {
+  if (e->op == COp::Loop) return c_loop(m.at(e->loop));
+  if (e->op == COp::Const) return e;
+  return c_bin(e->op, remap_loops(e->lhs, m), remap_loops(e->rhs, m));
+}
+
+// Scatter pre-reduction (DevStage::pre): with U = axes read by the target or
+// by a reduce-dependent term and P = the other axes, the scatter
+//     dst[target(U, r)] += scale * prod_{dep}(U, r) * prod_{inv}(U, P)
+// summed over P first is
+//     g[U] = sum_P prod_{inv}(U, P);  dst[target(U, r)] += scale * g[U] * prod_{dep}(U, r)
+// which scatters |P| times fewer points (e.g. a grad-input whose upstream is
+// summed over output channels the input never sees).
+static bool split_scatter(const CStage& cs, CStage* pre, CStage* main) {
+  static const bool off = getenv("SYNO_NO_PREREDUCE") != nullptr;  // A/B switch
+  if (off || !cs.scatter) return false;
+  const int A = (int)cs.axis_ext.size(), L = cs.nloops();
+  std::vector<bool> used(A, false);
+  std::vector<bool> rdep(cs.terms.size(), false);
+  auto mark = [&](const CTerm& t) {
+    for (auto& c : t.coords) {
+      std::vector<int> d;
+      c_loops(c, &d);
+      for (int l : d)
+        if (l < A) used[l] = true;
+    }
+  };
+  mark(cs.target);
+  for (size_t t = 0; t < cs.terms.size(); ++t) {
+    for (auto& c : cs.terms[t].coords) {
+      std::vector<int> d;
+      c_loops(c, &d);
+      for (int l : d) rdep[t] = rdep[t] || l >= A;
+    }
+    if (rdep[t]) mark(cs.terms[t]);
+  }
+  std::vector<int> U, P;
+  for (int a = 0; a < A; ++a) (used[a] ? U : P).push_back(a);
+  if (P.empty()) return false;
+  bool any_inv = false;
+  for (size_t t = 0; t < cs.terms.size(); ++t) any_inv = any_inv || !rdep[t];
+  // loop maps: main = (U, reduces); pre = (U, P)
+  std::vector<int> mm(L, -1), pm(L, -1);
+  for (size_t q = 0; q < U.size(); ++q) mm[U[q]] = pm[U[q]] = (int)q;
+  for (size_t q = 0; q < P.size(); ++q) pm[P[q]] = (int)(U.size() + q);
+  for (int l = A; l < L; ++l) mm[l] = (int)U.size() + (l - A);
+  *main = CStage();
+  main->scatter = true;
+  main->out = cs.out;
+  main->scale = cs.scale;
+  main->red_ext = cs.red_ext;
+  for (int a : U) main->axis_ext.push_back(cs.axis_ext[a]);
+  auto remap_term = [](const CTerm& t, const std::vector<int>& m) {
+    CTerm r = t;
+    for (auto& c : r.coords) c = remap_loops(c, m);
+    return r;
+  };
+  if (any_inv) {
+    *pre = CStage();
+    pre->axis_ext = main->axis_ext;
+    for (int a : P) pre->red_ext.push_back(cs.axis_ext[a]);
+    for (size_t t = 0; t < cs.terms.size(); ++t)
+      if (!rdep[t]) pre->terms.push_back(remap_term(cs.terms[t], pm));
+    pre->out.kind = TK_SCRATCH;
+    pre->out.extents = main->axis_ext;
+    CTerm g;
+    g.t.kind = TK_SCRATCH;
+    g.t.extents = main->axis_ext;
+    for (size_t q = 0; q < U.size(); ++q) g.coords.push_back(c_loop((int)q));
+    main->terms.push_back(g);
+  } else {
+    for (int a : P) main->scale *= (double)cs.axis_ext[a];  // no term reads P: multiplicity
+  }
+  for (size_t t = 0; t < cs.terms.size(); ++t)
+    if (rdep[t]) main->terms.push_back(remap_term(cs.terms[t], mm));
+  main->target = remap_term(cs.target, mm);
+  return true;
+}
+
+static void build_dev_stage_impl(const CStage& cs_in, DevStage* ds, cudaStream_t stream, bool allow_tile) {
+  CStage pre_cs, main_cs;
+  const bool split = allow_tile && split_scatter(cs_in, &pre_cs, &main_cs);
+  const CStage& cs = split ? main_cs : cs_in;
+  if (split && !pre_cs.terms.empty()) {
+    ds->pre = std::make_shared<DevStage>();
+    build_dev_stage_impl(pre_cs, ds->pre.get(), stream, true);
+  }
   ds->cs = cs;
   KStage& k = ds->k;
   memset(&k, 0, sizeof(KStage));
@@ -905,7 +1051,92 @@ __device__ __forceinline__ bool term_offset(const KTerm& T, int64_t base, bool o
   return ok;
 }
 
-template <typename T> __device__ __forceinline__ void atomic_add(T* p, T v) { atomicAdd(p, v); }
+// ---------------------------------------------------------------------------
+// Deterministic scatter accumulation (reference np.add.at, codegen.py:740-742)
+// ---------------------------------------------------------------------------
+// Floating-point atomics make the sum's rounding depend on the arrival order,
+// so equal inputs could give different low bits run to run (and the search's
+// rewards with them).  Integer addition is associative: every contribution is
+// rounded ONCE to a fixed-point integer (2^shift units) and added with integer
+// atomics, so the result is the same for any order.  The shift is chosen so
+// that no partial sum can overflow: |partial| <= fx_mult * prod_t max|term_t|
+// (fx_mult = grid points x scale).  fp32 / bf16 use one signed 64-bit word
+// (sum < 2^61); f64 a 128-bit (lo, hi) word pair (sum < 2^124), whose carry
+// out of the low word is counted exactly once per wrap-around.
+
+template <typename TA> struct FxWide { static constexpr bool value = false; };
+template <> struct FxWide<double> { static constexpr bool value = true; };
+
+template <typename TA>
+__device__ __forceinline__ int fx_shift(const KStage& S) {
+  double b = S.fx_mult;
+  for (int i = 0; i < S.fx_n; ++i) b *= S.fx_max[i];
+  if (!(b > 0.0) || isinf(b)) return 0;
+  int e;
+  frexp(b, &e);  // b < 2^e
+  const int top = FxWide<TA>::value ? 124 : 61;
+  return max(-1000, min(1000, top - e));
+}
+
+template <typename TA>
+__device__ __forceinline__ void fx_add(unsigned long long* fx, int64_t off, double v, int sh) {
+  const double x = rint(ldexp(v, sh));
+  if (!FxWide<TA>::value) {
+    atomicAdd(fx + off, (unsigned long long)__double2ll_rn(x));
+    return;
+  }
+  const double hd = floor(ldexp(x, -64));
+  const unsigned long long lo = __double2ull_rn(x - ldexp(hd, 64));  // exact, in [0, 2^64)
+  const long long hi = __double2ll_rn(hd);
+  if (lo) {
+    const unsigned long long old = atomicAdd(fx + 2 * off, lo);
+    if (old + lo < old) atomicAdd(fx + 2 * off + 1, 1ull);
+  }
+  if (hi) atomicAdd(fx + 2 * off + 1, (unsigned long long)hi);
+}
+
+template <typename TA>
+__device__ __forceinline__ double fx_value(const unsigned long long* fx, int64_t i, int sh) {
+  if (!FxWide<TA>::value) return ldexp((double)(long long)fx[i], -sh);
+  return ldexp((double)(long long)fx[2 * i + 1], 64 - sh) + ldexp((double)fx[2 * i], -sh);
+}
+
+struct MaxAbsArgs {
+  const void* ptr[MAXT + 1];
+  int64_t count[MAXT + 1];
+  int32_t acc[MAXT + 1];  // element type: 1 = accumulator dtype, 0 = input dtype
+  double* out;            // one max |v| per tensor (zeroed before)
+};
+
+// max |v| of each loaded term (blockIdx.y = term): the overflow bound of the
+// fixed-point scatter.  atomicMax on the bits of a non-negative double is
+// order independent.
+template <typename TI, typename TA>
+__global__ void __launch_bounds__(256) maxabs_kernel(const __grid_constant__ MaxAbsArgs a) {
+  pdl_trigger();
+  pdl_wait();
+  const int t = blockIdx.y;
+  const int64_t n = a.count[t];
+  double m = 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const double v = a.acc[t] ? (double)((const TA*)a.ptr[t])[i] : (double)cvt(((const TI*)a.ptr[t])[i]);
+    m = fmax(m, fabs(v));
+  }
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, d));
+  if ((threadIdx.x & 31) == 0 && m > 0.0)
+    atomicMax((unsigned long long*)(a.out + t), (unsigned long long)__double_as_longlong(m));
+}
+
+// fixed-point sums -> the scatter's output (accumulator or input dtype)
+template <typename TO, typename TA>
+__global__ void fx_convert_kernel(const __grid_constant__ KStage S, int64_t count, TO* out) {
+  pdl_trigger();
+  pdl_wait();
+  const int sh = fx_shift<TA>(S);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = from_acc<TO, TA>((TA)fx_value<TA>(S.fx, i, sh));
+}
 
 // NT = compile-time bound on the number of terms: fewer live registers and
 // higher occupancy for the common 1-3 term stages.
@@ -945,6 +1176,7 @@ __global__ void __launch_bounds__(256, NT <= 2 ? 4 : 2) stage_kernel(const __gri
   int32_t tia[MAXMIX];
   if (SCATTER) term_prep(S.target, S.n_axes, av, &tbase, &tok, tia);
   const TA scale = (TA)S.scale;
+  const int sh = SCATTER ? fx_shift<TA>(S) : 0;
   TA acc = 0;
   for (int64_t r = r0; r < r1; ++r) {
     TA prod = 1;
@@ -960,7 +1192,7 @@ __global__ void __launch_bounds__(256, NT <= 2 ? 4 : 2) stage_kernel(const __gri
     }
     if (SCATTER) {
       int64_t off;
-      if (ok && term_offset(S.target, tbase, tok, tia, r, &off)) atomic_add((TA*)S.out + off, prod * scale);
+      if (ok && term_offset(S.target, tbase, tok, tia, r, &off)) fx_add<TA>(S.fx, off, (double)(prod * scale), sh);
     } else if (ok) {
       acc += prod;
     }
@@ -1004,6 +1236,7 @@ __global__ void __launch_bounds__(128) stage_prog_kernel(const __grid_constant__
     }
   }
   const TA scale = (TA)S.scale;
+  const int sh = SCATTER ? fx_shift<TA>(S) : 0;
   TA acc = 0;
   for (int64_t r = r0; r < r1; ++r) {
     int64_t rem = r;
@@ -1021,7 +1254,7 @@ __global__ void __launch_bounds__(128) stage_prog_kernel(const __grid_constant__
     if (!ok) continue;
     if (SCATTER) {
       int64_t off;
-      if (prog_offset(S.prog, S.prog_term_off[S.n_terms], vals, &off)) atomic_add((TA*)S.out + off, prod * scale);
+      if (prog_offset(S.prog, S.prog_term_off[S.n_terms], vals, &off)) fx_add<TA>(S.fx, off, (double)(prod * scale), sh);
     } else {
       acc += prod;
     }
@@ -1138,14 +1371,16 @@ __global__ void __launch_bounds__(256) stage_block_kernel(const __grid_constant_
 // then every thread runs its products reading the rows (one shared load per
 // term) plus its own per-thread offset part.  The TR partial sums are added
 // in a fixed order: the result is deterministic.
-template <typename TI, typename TA, int NT>
+template <typename TI, typename TA, int NT, bool SCATTER>
 __global__ void __launch_bounds__(256) stage_tile_kernel(const __grid_constant__ KStage S,
                                                          const __grid_constant__ TileArgs A) {
   pdl_trigger();
   pdl_wait();
   extern __shared__ int32_t srow[];
   const int tid = threadIdx.x;
-  const int ti = tid % A.TI, tf = (tid / A.TI) % A.TF, tr = tid / (A.TI * A.TF);
+  const int ti = A.ffast ? (tid / A.TF) % A.TI : tid % A.TI;
+  const int tf = A.ffast ? tid % A.TF : (tid / A.TI) % A.TF;
+  const int tr = tid / (A.TI * A.TF);
   const int ib = blockIdx.x % A.nIb, fb = blockIdx.x / A.nIb;
   const int i = ib * A.TI + ti, f = fb * A.TF + tf;
   const bool live = i < A.NI && f < A.NF && tr < A.TR;
@@ -1164,16 +1399,35 @@ __global__ void __launch_bounds__(256) stage_tile_kernel(const __grid_constant__
       rem /= A.fext[q];
     }
   }
+  // scatter: the last row is the target's; n_ld terms are loaded per point
+  const int n_ld = SCATTER ? A.n_rt - 1 : A.n_rt;
   int64_t base[NT];
   bool aok[NT];
 #pragma unroll
   for (int k = 0; k < NT; ++k) {
     base[k] = 0;
     aok[k] = false;
-    if (k < A.n_rt) {
+    if (k < n_ld) {
       int32_t ia[MAXMIX];
       term_prep(S.terms[A.rterm[k]], S.n_axes, av, &base[k], &aok[k], ia);
     }
+  }
+  int64_t tbase = 0;
+  bool tok = true;
+  TA pre = (TA)S.scale;
+  int sh = 0;
+  if (SCATTER) {
+    int32_t ia[MAXMIX];
+    term_prep(S.target, S.n_axes, av, &tbase, &tok, ia);
+    for (int q = 0; q < A.n_inv && tok; ++q) {
+      const KTerm& T = S.terms[A.inv[q]];
+      int64_t b0;
+      bool ok0;
+      term_prep(T, S.n_axes, av, &b0, &ok0, ia);
+      if (!ok0) tok = false;
+      else if (T.kind != 2) pre *= load_term<TI, TA>(T, b0);
+    }
+    sh = fx_shift<TA>(S);
   }
   const int64_t r0 = (int64_t)blockIdx.y * S.r_chunk;
   const int64_t r1 = min(S.R, r0 + S.r_chunk);
@@ -1190,7 +1444,7 @@ __global__ void __launch_bounds__(256) stage_tile_kernel(const __grid_constant__
       const int fg = fb * A.TF + fl;
       int32_t v = -1;
       if (fg < A.NF) {
-        const KTerm& T = S.terms[A.rterm[k]];
+        const KTerm& T = A.rterm[k] < 0 ? S.target : S.terms[A.rterm[k]];
         const int64_t r = c0 + rl;
         bool ok = true;
         int64_t o = 0;
@@ -1219,23 +1473,29 @@ __global__ void __launch_bounds__(256) stage_tile_kernel(const __grid_constant__
       srow[(k * A.TF + fl) * pitch + rl] = v;
     }
     __syncthreads();
-    if (live) {
+    if (live && tok) {
       for (int rl = tr; rl < rc; rl += A.TR) {
-        TA prod = 1;
+        TA prod = SCATTER ? pre : (TA)1;
         bool ok = true;
 #pragma unroll
         for (int k = 0; k < NT; ++k) {
-          if (k < A.n_rt && ok) {
+          if (k < n_ld && ok) {
             const int32_t o = srow[(k * A.TF + tf) * pitch + rl];
             const KTerm& T = S.terms[A.rterm[k]];
             if (o < 0 || !aok[k]) ok = false;
             else if (T.kind != 2) prod *= load_term<TI, TA>(T, base[k] + o);
           }
         }
-        if (ok) acc += prod;
+        if (SCATTER) {
+          const int32_t o = srow[(n_ld * A.TF + tf) * pitch + rl];
+          if (ok && o >= 0) fx_add<TA>(S.fx, tbase + o, (double)prod, sh);
+        } else if (ok) {
+          acc += prod;
+        }
       }
     }
   }
+  if (SCATTER) return;
   // fixed-order combination of the TR partial sums of each output
   __syncthreads();
   TA* red = reinterpret_cast<TA*>(srow);
@@ -1321,7 +1581,8 @@ static void launch_stage_impl(const DevStage& ds, const Bindings& b, void* out, 
   KStage k = ds.k;
   for (int t = 0; t < k.n_terms; ++t) {
     k.terms[t].ptr = bind_ptr(ds.cs.terms[t].t, b);
-    if (!k.terms[t].ptr && k.terms[t].kind != 2) fail(SYNO_E_INVALID, "stage input tensor is not bound");
+    if (!k.terms[t].ptr && k.terms[t].kind != 2 && !(ds.pre && ds.cs.terms[t].t.kind == TK_SCRATCH))
+      fail(SYNO_E_INVALID, "stage input tensor is not bound");
   }
   const int64_t out_bytes = k.out_count * (int64_t)(out_acc ? sizeof(TA) : sizeof(TI));
   if (ds.dead || k.out_count == 0) {
@@ -1354,9 +1615,9 @@ static void launch_stage_impl(const DevStage& ds, const Bindings& b, void* out, 
     const dim3 grid((unsigned)ti.ctas, (unsigned)ti.splits);
     const unsigned threads = (unsigned)(a.TI * a.TF * a.TR);
     note_launch();
-    if (a.n_rt <= 2) launch_k(stage_tile_kernel<TI, TA, 2>, grid, threads, ti.smem, stream, k, a);
-    else if (a.n_rt <= 4) launch_k(stage_tile_kernel<TI, TA, 4>, grid, threads, ti.smem, stream, k, a);
-    else launch_k(stage_tile_kernel<TI, TA, MAXT>, grid, threads, ti.smem, stream, k, a);
+    if (a.n_rt <= 2) launch_k(stage_tile_kernel<TI, TA, 2, false>, grid, threads, ti.smem, stream, k, a);
+    else if (a.n_rt <= 4) launch_k(stage_tile_kernel<TI, TA, 4, false>, grid, threads, ti.smem, stream, k, a);
+    else launch_k(stage_tile_kernel<TI, TA, MAXT, false>, grid, threads, ti.smem, stream, k, a);
     cuda_check(cudaGetLastError(), "stage_tile_kernel");
     Bindings b2 = b;
     b2.scratch = acc;
@@ -1402,11 +1663,69 @@ static void launch_stage_impl(const DevStage& ds, const Bindings& b, void* out, 
   }
   if (ds.cs.scatter) {
     *kind = "stage_scatter";
+    void* g = nullptr;
+    if (ds.pre) {
+      cuda_check(cudaMallocAsync(&g, (size_t)ds.pre->k.out_count * sizeof(TA), stream), "alloc pre-reduction");
+      const char* pk = nullptr;
+      launch_stage_impl<TI>(*ds.pre, b, g, true, stream, &pk);
+      for (int t = 0; t < k.n_terms; ++t)
+        if (ds.cs.terms[t].t.kind == TK_SCRATCH) k.terms[t].ptr = g;
+    }
+    // deterministic fixed-point accumulation (fx_add): zero the integer
+    // sums and the bound slots, bound every loaded term, scatter, convert
+    const bool wide = sizeof(TA) == 8;
+    const int64_t n_out = ds.cs.out.numel();
+    MaxAbsArgs ma;
+    memset(&ma, 0, sizeof(ma));
+    int nl = 0;
+    int64_t most = 0;
+    for (int t = 0; t < k.n_terms; ++t) {
+      if (k.terms[t].kind == 2) continue;
+      ma.ptr[nl] = k.terms[t].ptr;
+      ma.count[nl] = ds.cs.terms[t].t.numel();
+      ma.acc[nl] = k.terms[t].kind == 1;
+      most = std::max(most, ma.count[nl]);
+      ++nl;
+    }
+    const size_t fx_bytes = (size_t)n_out * (wide ? 16 : 8);
+    uint8_t* buf = nullptr;
+    cuda_check(cudaMallocAsync((void**)&buf, fx_bytes + 8 * (MAXT + 1), stream), "alloc scatter sums");
+    zero_fill(buf, fx_bytes + 8 * (MAXT + 1), stream);
+    ma.out = (double*)(buf + fx_bytes);
+    if (nl) {
+      note_launch();
+      const unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>((most + 255) / 256, 148 * 4));
+      launch_k(maxabs_kernel<TI, TA>, dim3(blocks, nl), 256, 0, stream, ma);
+      cuda_check(cudaGetLastError(), "maxabs_kernel");
+    }
     k.out = out;
     k.out_acc = 1;
+    k.fx = (unsigned long long*)buf;
+    k.fx_max = ma.out;
+    k.fx_n = nl;
+    k.fx_mult = (double)k.out_count * (double)k.R * std::fabs(k.scale);
     note_launch();
-    launch_nt<TI, TA, true>(k, grid, stream);
-    cuda_check(cudaGetLastError(), "stage_kernel<scatter>");
+    if (ds.tile) {
+      *kind = "stage_tile_scatter";
+      const TileInfo& ti = *ds.tile;
+      k.r_chunk = (k.R + ti.splits - 1) / ti.splits;
+      const dim3 tgrid((unsigned)ti.ctas, (unsigned)ti.splits);
+      const unsigned threads = (unsigned)(ti.a.TI * ti.a.TF * ti.a.TR);
+      if (ti.a.n_rt <= 3) launch_k(stage_tile_kernel<TI, TA, 2, true>, tgrid, threads, ti.smem, stream, k, ti.a);
+      else if (ti.a.n_rt <= 5) launch_k(stage_tile_kernel<TI, TA, 4, true>, tgrid, threads, ti.smem, stream, k, ti.a);
+      else launch_k(stage_tile_kernel<TI, TA, MAXT, true>, tgrid, threads, ti.smem, stream, k, ti.a);
+      cuda_check(cudaGetLastError(), "stage_tile_kernel<scatter>");
+    } else {
+      launch_nt<TI, TA, true>(k, grid, stream);
+      cuda_check(cudaGetLastError(), "stage_kernel<scatter>");
+    }
+    const unsigned cb = (unsigned)std::max<int64_t>(1, std::min<int64_t>((n_out + 255) / 256, 148 * 8));
+    note_launch();
+    if (out_acc) launch_k(fx_convert_kernel<TA, TA>, cb, 256, 0, stream, k, n_out, (TA*)out);
+    else launch_k(fx_convert_kernel<TI, TA>, cb, 256, 0, stream, k, n_out, (TI*)out);
+    cuda_check(cudaGetLastError(), "fx_convert_kernel");
+    cuda_check(cudaFreeAsync(buf, stream), "free scatter sums");
+    if (g) cuda_check(cudaFreeAsync(g, stream), "free pre-reduction");
     return;
   }
   *kind = "stage_gather_reduce";

@@ -57,6 +57,16 @@ struct KStage {
   int32_t n_red;
   int32_t pad2_;
   int64_t red_ext[16];
+  // Scatter form: deterministic fixed-point accumulation (engine.cu fx_add):
+  // per output element one signed 64-bit word (fp32/bf16) or a 128-bit
+  // (lo, hi) pair (f64), scaled by 2^shift with the shift derived from a
+  // bound on every partial sum: fx_mult * prod(fx_max[0..fx_n)) (the max |v|
+  // of each loaded term, computed on the device by maxabs_kernel).
+  unsigned long long* fx;
+  const double* fx_max;
+  int32_t fx_n;
+  int32_t pad3_;
+  double fx_mult;
 };
 
 // One device-resident stage: tables plus a descriptor with null pointers
@@ -79,7 +89,10 @@ struct TileArgs {
   int32_t n_rt;             // reduce-dependent terms
   int32_t rterm[MAXT];
   int32_t nIb;              // CTAs along I
-  int32_t pad_;
+  int32_t ffast;            // lanes run along F (else along I)
+  int32_t scatter;          // scatter form: rterm's last entry (-1) is the target
+  int32_t n_inv;            // scatter form: reduce-invariant terms (a per-thread factor)
+  int32_t inv[MAXT];
   void* acc;                // [S][NF][NI] accumulator scratch
 };
 
@@ -96,6 +109,10 @@ struct DevStage {
   CStage cs;
   KStage k;
   std::shared_ptr<TileInfo> tile;  // tiled gather form, when it applies
+  // Scatter form with axes that neither the target nor any reduce-dependent
+  // term reads: `pre` (a gather stage) first sums the reduce-invariant terms
+  // over those axes into a scratch tensor, which this stage then scatters.
+  std::shared_ptr<DevStage> pre;
   std::vector<int> term_slot;   // CTensor of each term, to bind pointers
   int32_t* tables = nullptr;    // owned device allocation
   int64_t* prog = nullptr;      // owned device allocation (program fallback)
