@@ -79,7 +79,7 @@ typedef struct {
   int64_t index_grid;     /* points of the unstaged batch-explicit loop grid */
   int32_t complete;       /* frontier matches the input (pgraph.match_input) */
   int32_t replay_only;    /* compiled with SYNO_REPLAY_ONLY: shapes/flops not filled */
-  int32_t tc_path;        /* 1: bf16 runs on the tcgen05 implicit-GEMM path */
+  int32_t tc_path;        /* tcgen05 path for fp32 / bf16: 1 conv-shaped implicit GEMM, 2 gathered GEMM, 0 none */
 } syno_info;
 
 /* Parse an operator document (pgraph.print_operator format), replay its

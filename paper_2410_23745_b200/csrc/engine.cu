@@ -264,9 +264,13 @@ __global__ void k1_build_table(const __grid_constant__ K1Args a) {
 // Largest index table (entries) a coordinate may get before the stage
 // falls back to on-the-fly programs.  SYNO_TABLE_LIMIT lowers it (tests use
 // it to drive the program path on small operators).
+// A table is built once per (operator, device) and read row by row by the
+// tiled kernels, so even a 2^29-entry (2 GB) table costs one K1 pass plus
+// one coalesced read -- far less than evaluating its program at every one of
+// the (larger) grid's points.
 static int64_t table_limit() {
   const char* e = getenv("SYNO_TABLE_LIMIT");
-  return e ? std::max<int64_t>(1, atoll(e)) : ((int64_t)1 << 28);
+  return e ? std::max<int64_t>(1, atoll(e)) : ((int64_t)1 << 29) + 1;
 }
 
 struct ProgSpec {
@@ -913,6 +917,7 @@ DevPlan::~DevPlan() {
   rel(bwd_staged);
   for (auto& g : grad_w) rel(g);
   tc.reset();
+  gg.reset();
   if (device >= 0 && device != cur && cur >= 0) cudaSetDevice(cur);
 }
 
@@ -955,6 +960,8 @@ static void ensure_backward(const Plan& plan, DevPlan& dp, cudaStream_t stream) 
   dp.have_backward = true;
 }
 
+static std::shared_ptr<GatherGemm> gg_build(const Plan& plan, cudaStream_t stream);
+
 DevPlan* build_dev_plan(const Plan& plan, cudaStream_t stream) {
   auto dp = std::make_unique<DevPlan>();
   cuda_check(cudaGetDevice(&dp->device), "cudaGetDevice");
@@ -971,6 +978,7 @@ DevPlan* build_dev_plan(const Plan& plan, cudaStream_t stream) {
     }
   }
   dp->tc = tc_build(plan, stream);
+  if (!dp->tc) dp->gg = gg_build(plan, stream);
   cuda_check(cudaStreamSynchronize(stream), "build_dev_plan");
   return dp.release();
 }
@@ -1544,7 +1552,8 @@ static const void* bind_ptr(const CTensor& t, const Bindings& b) {
     case TK_DX: return b.dx;
     case TK_DW: return b.dw.at(t.index);
     case TK_DSTAGE: return b.dstages.at(t.index);
-    case TK_SCRATCH: return b.scratch;
+    case TK_SCRATCH:
+    case TK_SCRATCH_IN: return b.scratch;
     default: return nullptr;
   }
 }
@@ -1769,10 +1778,307 @@ static void launch_cast(DType dt, const void* acc, int64_t count, void* out, cud
   cuda_check(cudaGetLastError(), "cast_kernel");
 }
 
+// ---------------------------------------------------------------------------
+// Gathered GEMM: a contraction whose operands are arbitrary gathers
+// ---------------------------------------------------------------------------
+// The reference's `contract` snapshots any target expressions as the weight
+// access (pgraph.py:335-352), so a sampled operator is often
+//     y[b, n.., m..] = scale * sum_r x[gx(b, m.., r)] * w[gw(n.., r)]
+// with windowed / merged / strided index maps that the conv matcher (tc.cu)
+// does not take.  Here the two operands are gathered into dense matrices
+//     X~[b][r][m] = x[gx(b, m, r)]   (0 out of range)     W~[n][r] = w[gw(n, r)]
+// by universal-engine stages (HBM-bound), and the contraction runs on the
+// tcgen05 path as a pointwise operator with C_in = |r|, C_out = |n|,
+// pixels = |m| -- the same kernels and the same fp32 split-bf16 scheme as the
+// config layers.  Backward: the pointwise grad-input / grad-weight give dX~
+// and dW~, which scatter back through the same index maps (deterministic
+// fixed-point scatter stages).  When w's access is the identity
+// (w[n.., r..] in order) W~ is w itself and dW~ is dw.
+struct GatherGemm {
+  Plan pw;                       // the synthetic pointwise operator
+  std::unique_ptr<DevPlan> pdev; // its device plan (tcgen05)
+  DevStage gx, gxs;              // X~ = gather(x); dx = scatter(dX~)
+  bool w_ident = true;
+  bool mr = false;               // QKV-like: X~ = [batch][m][r], y N-contiguous
+  DevStage gw, gws;              // W~ = gather(w); dw = scatter(dW~)
+  int64_t nx = 0, nw = 0, nxin = 0, nwin = 0;
+  ~GatherGemm() {
+    release_dev_stage(gx);
+    release_dev_stage(gxs);
+    release_dev_stage(gw);
+    release_dev_stage(gws);
+  }
+};
+
+static int64_t numel_of(const std::vector<int64_t>& e);
+static size_t dtype_size(DType dt);
+
+struct GGShape {
+  int tx = -1, tw = -1;
+  std::vector<int> Nax, Max;
+  int64_t NN = 1, MM = 1, RR = 1;
+  bool nfirst = true;
+};
+
+// Host-only structural match of the gathered-GEMM form (see GatherGemm).
+static bool gg_shape(const Plan& plan, GGShape* out) {
+  static const bool off = getenv("SYNO_NO_GATHER_GEMM") != nullptr;  // A/B switch
+  const CStage& S = plan.unstaged;
+  if (off || S.terms.size() != 2 || plan.w_ext.size() != 1 || S.scale != 1.0 || S.dead) return false;
+  GGShape g;
+  for (int t = 0; t < 2; ++t) {
+    if (S.terms[t].t.kind == TK_X) g.tx = t;
+    if (S.terms[t].t.kind == TK_W) g.tw = t;
+  }
+  if (g.tx < 0 || g.tw < 0) return false;
+  const int A = (int)S.axis_ext.size(), L = S.nloops();
+  const int B = (int)plan.batch_ext.size();
+  if (B != 1) return false;
+  auto uses = [&](const CTerm& t, std::vector<bool>* u) {
+    u->assign(L, false);
+    for (auto& c : t.coords) {
+      std::vector<int> d;
+      c_loops(c, &d);
+      for (int l : d) (*u)[l] = true;
+    }
+  };
+  std::vector<bool> ux, uw;
+  uses(S.terms[g.tx], &ux);
+  uses(S.terms[g.tw], &uw);
+  // x's leading coordinate is the bare batch loop; w never reads the batch
+  if (S.terms[g.tx].coords.empty() || S.terms[g.tx].coords[0]->op != COp::Loop ||
+      S.terms[g.tx].coords[0]->loop != 0 || uw[0])
+    return false;
+  for (int a = B; a < A; ++a) {
+    if (ux[a] && uw[a]) return false;
+    if (uw[a]) g.Nax.push_back(a);
+    else if (ux[a]) g.Max.push_back(a);
+    else return false;  // broadcast axis: not a GEMM output
+  }
+  if (g.Nax.empty() || g.Max.empty()) return false;
+  // y = [batch][N block][M block] (a pointwise operator, NCHW-like) or
+  // y = [batch][M block][N block] (a QKV-like projection, N contiguous)
+  bool nlast = true;
+  for (size_t q = 0; q < g.Nax.size(); ++q) {
+    g.nfirst = g.nfirst && g.Nax[q] == B + (int)q;
+    nlast = nlast && g.Nax[q] == A - (int)g.Nax.size() + (int)q;
+  }
+  if (!g.nfirst && !nlast) return false;
+  for (int a : g.Nax) g.NN *= S.axis_ext[a];
+  for (int a : g.Max) g.MM *= S.axis_ext[a];
+  for (auto r : S.red_ext) g.RR *= r;
+  // worth a GEMM, and the gathered operand fits comfortably
+  if (g.RR < 64 || g.NN < 16 || g.MM < 64 || (double)plan.batch * g.RR * g.MM > 6.0e8) return false;
+  *out = g;
+  return true;
+}
+
+bool gg_matches(const Plan& plan) {
+  GGShape g;
+  return gg_shape(plan, &g);
+}
+
+static std::shared_ptr<GatherGemm> gg_build(const Plan& plan, cudaStream_t stream) {
+  GGShape sh;
+  if (!gg_shape(plan, &sh)) return nullptr;
+  const CStage& S = plan.unstaged;
+  const int A = (int)S.axis_ext.size(), L = S.nloops();
+  const int tx = sh.tx, tw = sh.tw;
+  const std::vector<int>& Nax = sh.Nax;
+  const std::vector<int>& Max = sh.Max;
+  const int64_t NN = sh.NN, MM = sh.MM, RR = sh.RR;
+  const bool nfirst = sh.nfirst;
+  const int64_t batch = plan.batch;
+  const int nR = (int)S.red_ext.size();
+  auto gg = std::make_shared<GatherGemm>();
+  // the synthetic operator: pointwise (C_in = RR, C_out = NN, H x W = MM)
+  // or QKV-like (T = MM, E = RR, E3 = NN); W~ = [n][r] in both
+  const int64_t Wd = S.axis_ext[Max.back()], Hd = MM / Wd;
+  const bool mr = !nfirst;  // X~ = [batch][m][r] (QKV-like) instead of [batch][r][m]
+  gg->mr = mr;
+  std::string doc = mr ? "operator gathered_gemm\nvar T primary " + std::to_string(MM) + "\nvar E primary " +
+                             std::to_string(RR) + "\nvar E3 primary " + std::to_string(NN) + "\nvar B primary " +
+                             std::to_string(batch) +
+                             "\noutput T E3\ninput T E\nbatch B\nsteps op{reduce(E); contract[1:weight,2:both]}\n"
+                       : "operator gathered_gemm\nvar C_out primary " + std::to_string(NN) + "\nvar C_in primary " +
+                             std::to_string(RR) + "\nvar H primary " + std::to_string(Hd) + "\nvar W primary " +
+                             std::to_string(Wd) + "\nvar N primary " + std::to_string(batch) +
+                             "\noutput C_out H W\ninput C_in H W\nbatch N\nsteps op{reduce(C_in); contract[0:weight,3:both]}\n";
+  try {
+    Graph g = parse_operator(doc);
+    Assignment env = g.spec->assignment();
+    LoopNest un = build_loop_nest(g, env);
+    gg->pw = build_plan(un, un, g.spec->batch_dims, env);
+  } catch (const Error&) {
+    return nullptr;
+  }
+  gg->pdev.reset(build_dev_plan(gg->pw, stream));
+  if (!gg->pdev->tc) return nullptr;
+  auto remap = [](const CTerm& t, const std::vector<int>& m) {
+    CTerm r = t;
+    for (auto& c : r.coords) c = remap_loops(c, m);
+    return r;
+  };
+  // X~ = [batch][r..][m..] (or [batch][m..][r..]): a gather stage, no reduce
+  {
+    const int nM = (int)Max.size();
+    std::vector<int> m(L, -1);
+    m[0] = 0;
+    for (int j = 0; j < nR; ++j) m[A + j] = mr ? 1 + nM + j : 1 + j;
+    for (int q = 0; q < nM; ++q) m[Max[q]] = mr ? 1 + q : 1 + nR + q;
+    CStage g;
+    g.axis_ext.push_back(batch);
+    if (!mr)
+      for (auto r : S.red_ext) g.axis_ext.push_back(r);
+    for (int a : Max) g.axis_ext.push_back(S.axis_ext[a]);
+    if (mr)
+      for (auto r : S.red_ext) g.axis_ext.push_back(r);
+    g.terms.push_back(remap(S.terms[tx], m));
+    g.out.kind = TK_SCRATCH;
+    g.out.extents = g.axis_ext;
+    simplify_stage(&g);
+    build_dev_stage(g, &gg->gx, stream);
+    gg->nx = g.out.numel();
+    // dx[gx(b, m, r)] += dX~[b][r][m]: scatter over (batch, M) x reduces
+    std::vector<int> ms(L, -1);
+    ms[0] = 0;
+    for (size_t q = 0; q < Max.size(); ++q) ms[Max[q]] = 1 + (int)q;
+    for (int j = 0; j < nR; ++j) ms[A + j] = 1 + (int)Max.size() + j;
+    CStage sc;
+    sc.axis_ext.push_back(batch);
+    for (int a : Max) sc.axis_ext.push_back(S.axis_ext[a]);
+    sc.red_ext = S.red_ext;
+    CTerm d;
+    d.t.kind = TK_SCRATCH_IN;  // dX~ comes from the tensor-core path in the operator's dtype
+    d.t.extents = g.axis_ext;
+    d.coords.push_back(c_loop(0));
+    if (!mr)
+      for (int j = 0; j < nR; ++j) d.coords.push_back(c_loop(1 + nM + j));
+    for (int q = 0; q < nM; ++q) d.coords.push_back(c_loop(1 + q));
+    if (mr)
+      for (int j = 0; j < nR; ++j) d.coords.push_back(c_loop(1 + nM + j));
+    sc.terms.push_back(d);
+    sc.scatter = true;
+    sc.target = remap(S.terms[tx], ms);
+    sc.target.t.kind = TK_DX;
+    sc.out = sc.target.t;
+    simplify_stage(&sc);
+    build_dev_stage(sc, &gg->gxs, stream);
+    gg->nxin = numel_of(plan.x_ext);
+  }
+  // W~ = [n..][r..]
+  {
+    const CTerm& wt = S.terms[tw];
+    bool ident = wt.coords.size() == Nax.size() + (size_t)nR;
+    for (size_t q = 0; ident && q < wt.coords.size(); ++q) {
+      const int want = q < Nax.size() ? Nax[q] : A + (int)(q - Nax.size());
+      ident = wt.coords[q]->op == COp::Loop && wt.coords[q]->loop == want &&
+              wt.t.extents[q] == S.ext(want);
+    }
+    gg->w_ident = ident;
+    gg->nw = NN * RR;
+    gg->nwin = numel_of(plan.w_ext[0]);
+    if (!ident) {
+      std::vector<int> m(L, -1);
+      for (size_t q = 0; q < Nax.size(); ++q) m[Nax[q]] = (int)q;
+      for (int j = 0; j < nR; ++j) m[A + j] = (int)Nax.size() + j;
+      CStage g;
+      for (int a : Nax) g.axis_ext.push_back(S.axis_ext[a]);
+      for (auto r : S.red_ext) g.axis_ext.push_back(r);
+      g.terms.push_back(remap(wt, m));
+      g.out.kind = TK_SCRATCH;
+      g.out.extents = g.axis_ext;
+      simplify_stage(&g);
+      build_dev_stage(g, &gg->gw, stream);
+      std::vector<int> ms(L, -1);
+      for (size_t q = 0; q < Nax.size(); ++q) ms[Nax[q]] = (int)q;
+      for (int j = 0; j < nR; ++j) ms[A + j] = (int)Nax.size() + j;
+      CStage sc;
+      for (int a : Nax) sc.axis_ext.push_back(S.axis_ext[a]);
+      for (auto r : S.red_ext) sc.red_ext.push_back(r);
+      CTerm d;
+      d.t.kind = TK_SCRATCH_IN;
+      d.t.extents = g.axis_ext;
+      for (size_t q = 0; q < g.axis_ext.size(); ++q) d.coords.push_back(c_loop((int)q));
+      // as a scatter over (N) x reduces: dW~[n][r] -> dw[gw(n, r)]
+      sc.terms.push_back(d);
+      sc.scatter = true;
+      sc.target = remap(wt, ms);
+      sc.target.t.kind = TK_DW;
+      sc.target.t.index = 0;
+      sc.out = sc.target.t;
+      simplify_stage(&sc);
+      build_dev_stage(sc, &gg->gws, stream);
+    }
+  }
+  return gg;
+}
+
+static void run_grad(DType dt, const DevStage& ds, const Bindings& b, void* out, int64_t count, cudaStream_t stream);
+static int64_t numel_of(const std::vector<int64_t>& e);
+
+static bool gg_forward(GatherGemm& gg, DType dt, const Bindings& b, cudaStream_t stream) {
+  if (dt != DT_F32 && dt != DT_BF16) return false;
+  const size_t es = dtype_size(dt);
+  void *xt = nullptr, *wt = nullptr;
+  cuda_check(cudaMallocAsync(&xt, gg.nx * es, stream), "alloc gathered x");
+  run_stage(dt, gg.gx, b, xt, false, stream);
+  if (!gg.w_ident) {
+    cuda_check(cudaMallocAsync(&wt, gg.nw * es, stream), "alloc gathered w");
+    run_stage(dt, gg.gw, b, wt, false, stream);
+  }
+  Bindings pb;
+  pb.x = xt;
+  pb.w = {gg.w_ident ? b.w.at(0) : wt};
+  pb.y = b.y;
+  const bool ok = tc_forward(*gg.pdev->tc, dt, pb, stream);
+  cuda_check(cudaFreeAsync(xt, stream), "free gathered x");
+  if (wt) cuda_check(cudaFreeAsync(wt, stream), "free gathered w");
+  if (!ok) fail(SYNO_E_INVALID, "gathered GEMM: tensor-core forward refused its own plan");
+  return true;
+}
+
+static bool gg_backward(GatherGemm& gg, DType dt, const Bindings& b, cudaStream_t stream) {
+  if (dt != DT_F32 && dt != DT_BF16) return false;
+  const size_t es = dtype_size(dt);
+  const bool want_w = !b.dw.empty() && b.dw[0];
+  void *xt = nullptr, *wt = nullptr, *dxt = nullptr, *dwt = nullptr;
+  cuda_check(cudaMallocAsync(&xt, gg.nx * es, stream), "alloc gathered x");
+  run_stage(dt, gg.gx, b, xt, false, stream);
+  if (!gg.w_ident) {
+    cuda_check(cudaMallocAsync(&wt, gg.nw * es, stream), "alloc gathered w");
+    run_stage(dt, gg.gw, b, wt, false, stream);
+  }
+  if (b.dx) cuda_check(cudaMallocAsync(&dxt, gg.nx * es, stream), "alloc gathered dx");
+  if (want_w && !gg.w_ident) cuda_check(cudaMallocAsync(&dwt, gg.nw * es, stream), "alloc gathered dw");
+  Bindings pb;
+  pb.x = xt;
+  pb.w = {gg.w_ident ? b.w.at(0) : wt};
+  pb.dy = b.dy;
+  pb.dx = dxt;
+  pb.dw = {want_w ? (gg.w_ident ? b.dw[0] : dwt) : nullptr};
+  const bool ok = tc_backward(*gg.pdev->tc, dt, pb, stream);
+  if (!ok) fail(SYNO_E_INVALID, "gathered GEMM: tensor-core backward refused its own plan");
+  if (b.dx) {
+    Bindings sb = b;
+    sb.scratch = dxt;
+    run_grad(dt, gg.gxs, sb, b.dx, gg.nxin, stream);
+  }
+  if (dwt) {
+    Bindings sb = b;
+    sb.scratch = dwt;
+    run_grad(dt, gg.gws, sb, b.dw[0], gg.nwin, stream);
+  }
+  for (void* p : {xt, wt, dxt, dwt})
+    if (p) cuda_check(cudaFreeAsync(p, stream), "free gathered operand");
+  return true;
+}
+
 void run_forward(const Plan& plan, DevPlan& dp, DType dt, const Bindings& b_in, cudaStream_t stream) {
   // Tensor-core path first: it computes the unstaged contraction, which the
   // staged nest equals by construction (codegen.py:605-608).
   if (dp.tc && tc_forward(*dp.tc, dt, b_in, stream)) return;
+  if (dp.gg && gg_forward(*dp.gg, dt, b_in, stream)) return;
   ensure_forward(plan, dp, stream);
   Bindings b = b_in;
   b.stages.assign(plan.stage_ext.size(), nullptr);
@@ -1866,6 +2172,7 @@ static void run_backward_staged(const Plan& plan, DevPlan& dp, DType dt, const B
 
 void run_backward(const Plan& plan, DevPlan& dp, DType dt, const Bindings& b, cudaStream_t stream) {
   if (dp.tc && tc_backward(*dp.tc, dt, b, stream)) return;
+  if (dp.gg && gg_backward(*dp.gg, dt, b, stream)) return;
   if (!plan.bwd_staged.empty()) {
     run_backward_staged(plan, dp, dt, b, stream);
     return;

@@ -126,8 +126,11 @@ struct TcPlanDeleter {
 };
 using TcPlanPtr = std::unique_ptr<TcPlan, TcPlanDeleter>;
 
+struct GatherGemm;  // gathered-operand tensor-core path (engine.cu)
+
 struct DevPlan {
   int device = -1;
+  std::shared_ptr<GatherGemm> gg;  // null unless the operator is a gathered GEMM
   // Universal-engine stages are built on first use (the tensor-core path
   // usually makes them unnecessary); guarded by `mu`.
   std::mutex mu;
@@ -158,6 +161,10 @@ struct Bindings {
 void build_dev_stage(const CStage& cs, DevStage* ds, cudaStream_t stream);
 void release_dev_stage(DevStage& ds);
 void run_stage(DType dt, const DevStage& ds, const Bindings& b, void* out, bool out_acc, cudaStream_t stream);
+
+// Host-only: does the operator take the gathered-GEMM tensor-core path
+// (engine.cu GatherGemm) for fp32 / bf16?
+bool gg_matches(const Plan& plan);
 
 // Builds tables on `stream` (K1) for every stage of the plan.
 DevPlan* build_dev_plan(const Plan& plan, cudaStream_t stream);

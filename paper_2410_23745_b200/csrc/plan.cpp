@@ -81,7 +81,7 @@ double CStage::grid_points() const {
 
 std::string CStage::describe() const {
   std::ostringstream o;
-  static const char* kn[] = {"x", "w", "t", "y", "dy", "dx", "dw", "phantom", "dt", "acc"};
+  static const char* kn[] = {"x", "w", "t", "y", "dy", "dx", "dw", "phantom", "dt", "acc", "op"};
   o << (scatter ? "scatter" : "gather") << " out=" << kn[out.kind] << out.index << " axes=[";
   for (size_t k = 0; k < axis_ext.size(); ++k) o << (k ? "," : "") << axis_ext[k];
   o << "] reduces=[";

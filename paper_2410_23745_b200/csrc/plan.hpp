@@ -52,6 +52,7 @@ enum TensorKind : int {
   TK_PHANTOM = 7, // validity-only term (value 1 when in range)
   TK_DSTAGE = 8,  // gradient of intermediate t_k (workspace, accumulator precision)
   TK_SCRATCH = 9, // engine-internal partial sums (accumulator precision)
+  TK_SCRATCH_IN = 10, // engine-internal operand in the operator's dtype
 };
 
 struct CTensor {

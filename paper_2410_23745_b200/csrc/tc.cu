@@ -2436,6 +2436,10 @@ static TcWs& workspace(TcPlan& tp, DType dt, cudaStream_t stream) {
   if (it != tp.ws.end()) return *it->second;
   auto w = std::make_unique<TcWs>();
   build_ws(tp, *w, dt);
+  // the workspace's zero fills (cudaMemset) run on the legacy default stream,
+  // which does not order against non-blocking streams such as the caller's:
+  // finish them before any kernel on `stream` reads the buffers
+  cuda_check(cudaStreamSynchronize(0), "workspace zero fill");
   TcWs& ref = *w;
   tp.ws[key] = std::move(w);
   return ref;

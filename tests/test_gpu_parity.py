@@ -466,3 +466,43 @@ def test_heavy_sweep_candidates_adjoint_f64(cuda, sid):
     assert O.rel_err(f(dx32), f(dx64)) < 1e-4
     for a, b in zip(dw32, dw64):
         assert O.rel_err(f(a), f(b)) < 1e-4
+
+
+# weighted corpus candidates of the gathered-GEMM form
+# y[b, n, m] = sum_r x[gx(b, m, r)] * w[gw(n, r)] (engine.cu GatherGemm)
+GATHERED_GEMM = [171, 1016, 792, 179, 197, 319, 381, 688]
+
+
+@pytest.mark.parametrize("sid", GATHERED_GEMM)
+@pytest.mark.parametrize("dtype", ["float32", "bfloat16"])
+def test_gathered_gemm_candidates(cuda, sid, dtype):
+    """Sampled contractions with gathered operands run on the tcgen05 path
+    (the profile shows tensor-core GEMM launches) and match the float64
+    universal engine (itself pinned to the oracle) on the same inputs:
+    fp32 1e-4, bf16 2e-2 (inputs rounded to the dtype first)."""
+    from paper_2410_23745_b200 import _lib, ops
+    from paper_2410_23745_b200 import pgraph as P
+    from paper_2410_23745_b200 import workloads as WL
+    torch = _torch()
+    g = WL.corpus(2)[sid]
+    h = P.handle_for(g, None, True)
+    dt = getattr(torch, dtype)
+    gen = torch.Generator(device="cuda").manual_seed(sid)
+    x = torch.randn(h.x_shape, generator=gen, device="cuda").to(dt)
+    ws = [torch.randn(s, generator=gen, device="cuda").to(dt) for s in h.w_shapes]
+    dy = torch.randn(h.y_shape, generator=gen, device="cuda").to(dt)
+    _lib.profile_begin()
+    y = ops.forward(h, x, ws)
+    dx, dws = ops.backward(h, x, ws, dy)
+    torch.cuda.synchronize()
+    prof = _lib.profile_end()
+    if sid != 688:
+        assert any(k.startswith("tc_gemm") for k in prof), (sid, sorted(prof))
+    y64 = ops.forward(h, x.double(), [w.double() for w in ws])
+    dx64, dw64 = ops.backward(h, x.double(), [w.double() for w in ws], dy.double())
+    tol = TOL[dtype]
+    f = lambda t: t.double().cpu().numpy()  # noqa: E731
+    assert O.rel_err(f(y), f(y64)) < tol
+    assert O.rel_err(f(dx), f(dx64)) < tol
+    for a, b in zip(dws, dw64):
+        assert O.rel_err(f(a), f(b)) < tol
