@@ -918,46 +918,70 @@ DevPlan::~DevPlan() {
   for (auto& g : grad_w) rel(g);
   tc.reset();
   gg.reset();
+  for (cudaEvent_t e : {ev_plan, ev_fwd, ev_bwd})
+    if (e) cudaEventDestroy(e);
   if (device >= 0 && device != cur && cur >= 0) cudaSetDevice(cur);
 }
 
+void wait_built(cudaEvent_t ev, cudaStream_t stream) {
+  if (!ev) return;
+  cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(stream, &st);
+  if (st != cudaStreamCaptureStatusNone) return;  // built before the capture on this stream
+  cuda_check(cudaStreamWaitEvent(stream, ev, 0), "cudaStreamWaitEvent(plan built)");
+}
+
+static cudaEvent_t record_built(cudaStream_t stream) {
+  cudaEvent_t ev;
+  cuda_check(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "cudaEventCreate(built)");
+  cuda_check(cudaEventRecord(ev, stream), "cudaEventRecord(built)");
+  return ev;
+}
+
+// Tables are filled on the building stream; the readiness event orders any
+// other stream after them (wait_built) without a host synchronisation.
 static void ensure_forward(const Plan& plan, DevPlan& dp, cudaStream_t stream) {
-  std::lock_guard<std::mutex> lock(dp.mu);
-  if (dp.have_forward) return;
-  for (auto& s : plan.forward) {
-    dp.forward.emplace_back();
-    build_dev_stage(s, &dp.forward.back(), stream);
+  {
+    std::lock_guard<std::mutex> lock(dp.mu);
+    if (!dp.have_forward) {
+      for (auto& s : plan.forward) {
+        dp.forward.emplace_back();
+        build_dev_stage(s, &dp.forward.back(), stream);
+      }
+      dp.ev_fwd = record_built(stream);
+      dp.have_forward = true;
+    }
   }
-  // tables are filled on `stream`; other streams may use them next
-  cuda_check(cudaStreamSynchronize(stream), "ensure_forward");
-  dp.have_forward = true;
+  wait_built(dp.ev_fwd, stream);
 }
 
 static void ensure_backward(const Plan& plan, DevPlan& dp, cudaStream_t stream) {
-  std::lock_guard<std::mutex> lock(dp.mu);
-  if (dp.have_backward) return;
-  if (!plan.bwd_staged.empty()) {
-    for (auto& s : plan.bwd_staged) {
-      dp.bwd_staged.emplace_back();
-      build_dev_stage(s, &dp.bwd_staged.back(), stream);
+  {
+    std::lock_guard<std::mutex> lock(dp.mu);
+    if (!dp.have_backward) {
+      if (!plan.bwd_staged.empty()) {
+        for (auto& s : plan.bwd_staged) {
+          dp.bwd_staged.emplace_back();
+          build_dev_stage(s, &dp.bwd_staged.back(), stream);
+        }
+      } else {
+        for (auto& s : plan.grad_x) {
+          dp.grad_x.emplace_back();
+          build_dev_stage(s, &dp.grad_x.back(), stream);
+        }
+        for (auto& gw : plan.grad_w) {
+          dp.grad_w.emplace_back();
+          for (auto& s : gw) {
+            dp.grad_w.back().emplace_back();
+            build_dev_stage(s, &dp.grad_w.back().back(), stream);
+          }
+        }
+      }
+      dp.ev_bwd = record_built(stream);
+      dp.have_backward = true;
     }
-    cuda_check(cudaStreamSynchronize(stream), "ensure_backward");
-    dp.have_backward = true;
-    return;
   }
-  for (auto& s : plan.grad_x) {
-    dp.grad_x.emplace_back();
-    build_dev_stage(s, &dp.grad_x.back(), stream);
-  }
-  for (auto& gw : plan.grad_w) {
-    dp.grad_w.emplace_back();
-    for (auto& s : gw) {
-      dp.grad_w.back().emplace_back();
-      build_dev_stage(s, &dp.grad_w.back().back(), stream);
-    }
-  }
-  cuda_check(cudaStreamSynchronize(stream), "ensure_backward");
-  dp.have_backward = true;
+  wait_built(dp.ev_bwd, stream);
 }
 
 static std::shared_ptr<GatherGemm> gg_build(const Plan& plan, cudaStream_t stream);
@@ -979,7 +1003,7 @@ DevPlan* build_dev_plan(const Plan& plan, cudaStream_t stream) {
   }
   dp->tc = tc_build(plan, stream);
   if (!dp->tc) dp->gg = gg_build(plan, stream);
-  cuda_check(cudaStreamSynchronize(stream), "build_dev_plan");
+  dp->ev_plan = record_built(stream);
   return dp.release();
 }
 
@@ -2075,6 +2099,7 @@ static bool gg_backward(GatherGemm& gg, DType dt, const Bindings& b, cudaStream_
 }
 
 void run_forward(const Plan& plan, DevPlan& dp, DType dt, const Bindings& b_in, cudaStream_t stream) {
+  wait_built(dp.ev_plan, stream);
   // Tensor-core path first: it computes the unstaged contraction, which the
   // staged nest equals by construction (codegen.py:605-608).
   if (dp.tc && tc_forward(*dp.tc, dt, b_in, stream)) return;
@@ -2171,6 +2196,7 @@ static void run_backward_staged(const Plan& plan, DevPlan& dp, DType dt, const B
 }
 
 void run_backward(const Plan& plan, DevPlan& dp, DType dt, const Bindings& b, cudaStream_t stream) {
+  wait_built(dp.ev_plan, stream);
   if (dp.tc && tc_backward(*dp.tc, dt, b, stream)) return;
   if (dp.gg && gg_backward(*dp.gg, dt, b, stream)) return;
   if (!plan.bwd_staged.empty()) {

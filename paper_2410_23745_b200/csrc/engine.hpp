@@ -138,6 +138,10 @@ struct DevPlan {
   std::vector<DevStage> forward, grad_x, bwd_staged;
   std::vector<std::vector<DevStage>> grad_w;
   TcPlanPtr tc;  // null when the operator is not contraction-shaped
+  // Readiness of what the builds enqueued (index tables, folds) on the
+  // building stream: other streams wait on these instead of the host
+  // synchronising after every build.
+  cudaEvent_t ev_plan = nullptr, ev_fwd = nullptr, ev_bwd = nullptr;
   ~DevPlan();
 };
 
@@ -168,6 +172,9 @@ bool gg_matches(const Plan& plan);
 
 // Builds tables on `stream` (K1) for every stage of the plan.
 DevPlan* build_dev_plan(const Plan& plan, cudaStream_t stream);
+
+// Make `stream` wait for the plan's device-side builds (no-op while capturing).
+void wait_built(cudaEvent_t ev, cudaStream_t stream);
 
 // Launches. All pointers are device pointers; tensors are dense row-major.
 void run_forward(const Plan& plan, DevPlan& dp, DType dt, const Bindings& b, cudaStream_t stream);

@@ -123,8 +123,9 @@ static void fold_unread_reduces(CStage* s) {
     for (auto& c : t.coords) loops_into(c, &read);
   };
   for (auto& t : s->terms) scan(t);
+  // a reduce no term and no target coordinate reads repeats identical
+  // contributions: for a gather sum and for a scatter alike it is a factor
   if (s->scatter) scan(s->target);
-  if (s->scatter) return;  // scatter grids keep their shape; folding only applies to gather sums
   int A = (int)s->axis_ext.size();
   std::vector<int64_t> keep;
   std::map<int, int> remap;
@@ -146,6 +147,8 @@ static void fold_unread_reduces(CStage* s) {
   };
   for (auto& t : s->terms)
     for (auto& c : t.coords) c = rn(c);
+  if (s->scatter)
+    for (auto& c : s->target.coords) c = rn(c);
   s->red_ext = keep;
 }
 
@@ -448,11 +451,16 @@ Plan build_plan(const LoopNest& unstaged, const LoopNest& staged, const std::vec
   }
   // the engine's stages get simplified coordinates (smaller index tables);
   // `unstaged` keeps the reference's form for the tensor-core matcher
-  for (auto& st : p.forward) simplify_stage(&st);
-  for (auto& st : p.grad_x) simplify_stage(&st);
+  // (simplification can remove a reduce from every coordinate: fold it again)
+  auto simp = [](CStage& st) {
+    simplify_stage(&st);
+    fold_unread_reduces(&st);
+  };
+  for (auto& st : p.forward) simp(st);
+  for (auto& st : p.grad_x) simp(st);
   for (auto& gw : p.grad_w)
-    for (auto& st : gw) simplify_stage(&st);
-  for (auto& st : p.bwd_staged) simplify_stage(&st);
+    for (auto& st : gw) simp(st);
+  for (auto& st : p.bwd_staged) simp(st);
   return p;
 }
 

@@ -1871,13 +1871,17 @@ static bool same_grid(const PackGeom& a, const PackGeom& b) {
          (a.split == SPLIT_NONE || a.lo_mask == b.lo_mask);
 }
 
+// The stream a workspace is being built for (workspace() sets it): the zero
+// fills are ordered on it, ahead of the caller's first kernel.
+static thread_local cudaStream_t g_ws_stream = nullptr;
+
 template <typename T>
 static T* ws_alloc(TcWs& w, size_t count) {
   void* p = nullptr;
   cuda_check(cudaMalloc(&p, std::max<size_t>(count, 1) * sizeof(T)), "cudaMalloc(tc workspace)");
   w.owned.push_back(p);
   // packed operands rely on this: their padding is written once, here
-  cuda_check(cudaMemset(p, 0, std::max<size_t>(count, 1) * sizeof(T)), "cudaMemset(tc workspace)");
+  cuda_check(cudaMemsetAsync(p, 0, std::max<size_t>(count, 1) * sizeof(T), g_ws_stream), "cudaMemset(tc workspace)");
   return static_cast<T*>(p);
 }
 
@@ -2143,7 +2147,8 @@ static void build_ws(TcPlan& tp, TcWs& w, DType dt) {
     if (need) {
       w.chain_partial = ws_alloc<float>(w, (size_t)need);
       w.chain_counter = ws_alloc<unsigned>(w, (size_t)outs);
-      cuda_check(cudaMemset(w.chain_counter, 0, (size_t)outs * sizeof(unsigned)), "memset(chain counter)");
+      cuda_check(cudaMemsetAsync(w.chain_counter, 0, (size_t)outs * sizeof(unsigned), g_ws_stream),
+                 "memset(chain counter)");
     }
   }
 }
@@ -2435,11 +2440,11 @@ static TcWs& workspace(TcPlan& tp, DType dt, cudaStream_t stream) {
   auto it = tp.ws.find(key);
   if (it != tp.ws.end()) return *it->second;
   auto w = std::make_unique<TcWs>();
+  // the zero fills go on the caller's stream (cudaMemset would run on the
+  // legacy default stream, unordered against non-blocking streams)
+  g_ws_stream = stream;
   build_ws(tp, *w, dt);
-  // the workspace's zero fills (cudaMemset) run on the legacy default stream,
-  // which does not order against non-blocking streams such as the caller's:
-  // finish them before any kernel on `stream` reads the buffers
-  cuda_check(cudaStreamSynchronize(0), "workspace zero fill");
+  g_ws_stream = nullptr;
   TcWs& ref = *w;
   tp.ws[key] = std::move(w);
   return ref;

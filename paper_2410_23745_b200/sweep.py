@@ -94,10 +94,15 @@ def within_budget(flops: int, params: int, flops_cap: Optional[int], params_cap:
     return True
 
 
-def evaluate(graph, sample_id: int, seed: int, dtype=None, device=None,
-             flops_cap: Optional[int] = None, params_cap: Optional[int] = None,
-             tol: Optional[float] = None) -> EvalRecord:
-    """Evaluate one candidate on the current CUDA device."""
+def launch(graph, sample_id: int, seed: int, dtype=None, device=None,
+           flops_cap: Optional[int] = None, params_cap: Optional[int] = None,
+           tol: Optional[float] = None):
+    """Enqueue one candidate evaluation on the current CUDA stream without
+    waiting for it; returns ``finalize() -> EvalRecord`` (which waits).
+
+    Nothing here synchronises the host with the device: the inner products
+    of the adjoint check stay on the device until ``finalize`` reads them,
+    so a worker can enqueue the next candidate while this one runs."""
     import torch
 
     from . import ops
@@ -110,7 +115,8 @@ def evaluate(graph, sample_id: int, seed: int, dtype=None, device=None,
     h = handle_for(graph, None, True)
     op = print_steps(graph)
     if not within_budget(h.flops_unstaged, h.params, flops_cap, params_cap):
-        return EvalRecord(sample_id, seed, h.flops_unstaged, h.params, "over_budget", op)
+        rec = EvalRecord(sample_id, seed, h.flops_unstaged, h.params, "over_budget", op)
+        return lambda: rec
     # one seeded draw for every input (x, the weights, dy), split into views:
     # a candidate is launch-bound, so fewer host-side ops matter
     gen = torch.Generator(device=device).manual_seed(seed)
@@ -127,22 +133,33 @@ def evaluate(graph, sample_id: int, seed: int, dtype=None, device=None,
         y = ops.forward(h, x, ws)
         dx, dws = ops.backward(h, x, ws, dy)
         e1.record(stream)
-        e1.synchronize()
     except Exception as exc:  # a device-engine limit or launch failure: logged like a RewardFailure
-        return EvalRecord(sample_id, seed, h.flops_unstaged, h.params, "failed", op,
-                          error=f"{type(exc).__name__}: {str(exc).splitlines()[0] if str(exc) else ''}"[:200])
-    # every inner product in float64 on the device, one host read
+        rec = EvalRecord(sample_id, seed, h.flops_unstaged, h.params, "failed", op,
+                         error=f"{type(exc).__name__}: {str(exc).splitlines()[0] if str(exc) else ''}"[:200])
+        return lambda: rec
+    # every inner product in float64 on the device, read once in finalize
     ip = torch.stack([(a.double() * b.double()).sum() for a, b in
-                      [(dy, y), (dy, dy), (y, y), (dx, x)] + list(zip(dws, ws))]).tolist()
-    s = ip[0]
-    scale = max(1.0, math.sqrt(ip[1] * max(ip[2], 1e-30)))
-    err = abs(ip[3] - s) / scale
-    for v in ip[4:]:
-        err = max(err, abs(v - s) / scale)
+                      [(dy, y), (dy, dy), (y, y), (dx, x)] + list(zip(dws, ws))])
     limit = tol if tol is not None else (1e-4 if dtype == torch.float32 else 2e-2 if dtype == torch.bfloat16 else 1e-10)
-    status = "ok" if err <= limit and math.isfinite(err) else "failed"
-    return EvalRecord(sample_id, seed, h.flops_unstaged, h.params, status, op,
-                      e0.elapsed_time(e1) / 1e3, err)
+
+    def finalize() -> EvalRecord:
+        vals = ip.tolist()
+        s = vals[0]
+        scale = max(1.0, math.sqrt(vals[1] * max(vals[2], 1e-30)))
+        err = abs(vals[3] - s) / scale
+        for v in vals[4:]:
+            err = max(err, abs(v - s) / scale)
+        status = "ok" if err <= limit and math.isfinite(err) else "failed"
+        return EvalRecord(sample_id, seed, h.flops_unstaged, h.params, status, op, e0.elapsed_time(e1) / 1e3, err)
+
+    return finalize
+
+
+def evaluate(graph, sample_id: int, seed: int, dtype=None, device=None,
+             flops_cap: Optional[int] = None, params_cap: Optional[int] = None,
+             tol: Optional[float] = None) -> EvalRecord:
+    """Evaluate one candidate on the current CUDA device (and wait for it)."""
+    return launch(graph, sample_id, seed, dtype, device, flops_cap, params_cap, tol)()
 
 
 def candidate_costs(graphs, flops_cap: Optional[int] = None, params_cap: Optional[int] = None) -> List[float]:
@@ -243,6 +260,12 @@ def _evaluate_on_own_stream(graph, i, seed, dtype, flops_cap, params_cap):
         return evaluate(graph, i, seed, dtype=dtype, flops_cap=flops_cap, params_cap=params_cap)
 
 
+def _launch_on_own_stream(graph, i, seed, dtype, flops_cap, params_cap):
+    import torch
+    with torch.cuda.stream(_worker_stream()):
+        return launch(graph, i, seed, dtype=dtype, flops_cap=flops_cap, params_cap=params_cap)
+
+
 def run_shard(graphs, indices: Sequence[int], seed0: int = 0, dtype=None, flops_cap=None, params_cap=None,
               workers: int = 1):
     """Evaluate ``graphs[i]`` for i in ``indices`` on this rank's device.
@@ -271,8 +294,11 @@ def run_dynamic(graphs, order: Sequence[int], claim, seed0: int = 0, dtype=None,
     every rank through ``claim``) on this rank's device; each worker thread
     uses its own CUDA stream.  Returns (records, wall seconds)."""
     t0 = time.perf_counter()
-    recs = claim_loop(order, claim, lambda i: _evaluate_on_own_stream(graphs[i], i, seed0 + i, dtype, flops_cap,
-                                                                      params_cap), workers)
+    # workers only enqueue (sweep.launch); the records are read once every
+    # candidate of this rank is in flight
+    pending = claim_loop(order, claim, lambda i: _launch_on_own_stream(graphs[i], i, seed0 + i, dtype, flops_cap,
+                                                                       params_cap), workers)
+    recs = [f() for f in pending]
     return recs, time.perf_counter() - t0
 
 
