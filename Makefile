@@ -13,7 +13,7 @@ endif
 PKG := paper_2410_23745_b200
 SRC := $(PKG)/csrc
 OBJ := build/obj
-HOST_SRCS := symbolic graph nest plan simplify capi
+HOST_SRCS := symbolic graph nest plan simplify shapedist capi
 CUDA_SRCS := engine tc
 OBJS := $(addprefix $(OBJ)/,$(addsuffix .o,$(HOST_SRCS) $(CUDA_SRCS)))
 HDRS := $(wildcard $(SRC)/*.hpp) $(wildcard $(SRC)/*.cuh) include/syno.h

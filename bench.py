@@ -833,6 +833,9 @@ def cpu_baseline_sweep(args, processes=1, budget_s=20.0):
 def run_reference(args, rank, world):
     if rank != 0:
         return
+    if _ref_modules() is None:
+        print(json.dumps({"impl": "reference", "unavailable": "opsmith not installed in baseline/_ref"}), flush=True)
+        return
     cores = len(os.sched_getaffinity(0))
     procs = max(1, min(cores, 64))
     vals, secs, r = [], [], None
@@ -930,8 +933,11 @@ def main():
     if rank == 0:
         cpu = None
         if not args.no_cpu_baseline and args.workload != "qkv_train" and world == 1:
-            cpu = cpu_baseline_sweep(args, 1) if args.workload == "sweep" else cpu_baseline_layers(args, 1)
-            cpu.pop("seconds", None)
+            if _ref_modules() is None:
+                cpu = {"unavailable": "reference not installed in baseline/_ref (see DESIGN.md §5)"}
+            else:
+                cpu = cpu_baseline_sweep(args, 1) if args.workload == "sweep" else cpu_baseline_layers(args, 1)
+                cpu.pop("seconds", None)
         line = {
             "metric": SWEEP_METRIC if args.workload == "sweep" else METRIC, "value": r["value"], "unit": r["unit"],
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": r["ms_per_step"],

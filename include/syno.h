@@ -119,6 +119,27 @@ int syno_describe_plan(syno_op_t op, char* buf, size_t cap, size_t* len);
  * out_dev must hold info.index_grid int64 values. */
 int syno_index_map(syno_op_t op, int term, int coord, int64_t* out_dev, void* stream);
 
+/* Search-side shape distance (shapedist.py).
+ *
+ * syno_shape_distance   shapedist.shape_distance / explain_distance  shapedist.py:377-412
+ * syno_graph_distance   shapedist.graph_distance                     shapedist.py:415-420
+ * syno_shape_distance_clear_cache  shapedist.clear_cache             shapedist.py:423-433
+ *
+ * Sizes are monomials: frontier dim k has dim_nterms[k] (variable id,
+ * exponent) int32 pairs, consecutive in dim_terms (input dims likewise in
+ * in_terms); variable ids are any non-negative ints the caller chooses (the
+ * distance does not depend on the naming).  dim_flags[k]: bit 0 reduce_pure,
+ * bit 1 strided.  *out receives the distance (+inf when no grouping is
+ * valid).  When dim_group / in_group / n_groups are non-null they receive
+ * one optimal grouping (explain_distance's witness): the group index of
+ * every frontier dim and every input dim, and the group count.  The memo is
+ * process-wide and thread-safe. */
+int syno_shape_distance(int n_dims, const int32_t* dim_nterms, const int32_t* dim_terms, const uint8_t* dim_flags,
+                        int n_inputs, const int32_t* in_nterms, const int32_t* in_terms, int may_reduce,
+                        double* out, int32_t* dim_group, int32_t* in_group, int32_t* n_groups);
+int syno_graph_distance(syno_op_t op, double* out);
+void syno_shape_distance_clear_cache(void);
+
 void syno_destroy(syno_op_t op);
 const char* syno_last_error(void);
 const char* syno_version(void);

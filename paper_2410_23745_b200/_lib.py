@@ -39,6 +39,7 @@ EXPORTS = (
     "syno_emit_loop_nest", "syno_print_operator", "syno_describe_plan",
     "syno_index_map", "syno_destroy", "syno_last_error", "syno_version", "syno_launch_count",
     "syno_profile_begin", "syno_profile_end", "syno_backward_ex", "syno_tensor_write", "syno_tensor_read",
+    "syno_shape_distance", "syno_graph_distance", "syno_shape_distance_clear_cache",
 )
 
 
@@ -100,6 +101,11 @@ def _load():
     for name in ("syno_print_operator", "syno_describe_plan"):
         getattr(lib, name).argtypes = [vp, ctypes.c_char_p, ctypes.c_size_t, ctypes.POINTER(ctypes.c_size_t)]
     lib.syno_index_map.argtypes = [vp, ctypes.c_int, ctypes.c_int, vp, vp]
+    i32p = ctypes.POINTER(ctypes.c_int32)
+    lib.syno_shape_distance.argtypes = [ctypes.c_int, i32p, i32p, ctypes.POINTER(ctypes.c_uint8), ctypes.c_int,
+                                        i32p, i32p, ctypes.c_int, ctypes.POINTER(ctypes.c_double), i32p, i32p, i32p]
+    lib.syno_graph_distance.argtypes = [vp, ctypes.POINTER(ctypes.c_double)]
+    lib.syno_shape_distance_clear_cache.restype = None
     lib.syno_destroy.argtypes = [vp]
     lib.syno_destroy.restype = None
     lib.syno_last_error.restype = ctypes.c_char_p
@@ -109,7 +115,7 @@ def _load():
     lib.syno_profile_end.argtypes = [ctypes.POINTER(KernelStat), ctypes.c_int, ctypes.POINTER(ctypes.c_int)]
     for name in EXPORTS:
         if name not in ("syno_destroy", "syno_last_error", "syno_version", "syno_launch_count",
-                        "syno_profile_begin"):
+                        "syno_profile_begin", "syno_shape_distance_clear_cache"):
             getattr(lib, name).restype = ctypes.c_int
     return lib
 

@@ -266,6 +266,18 @@ int syno_index_map(syno_op_t op, int term, int coord, int64_t* out_dev, void* st
   });
 }
 
+int syno_graph_distance(syno_op_t op, double* out) {
+  return guarded([&] {
+    if (!op || !out) fail(SYNO_E_INVALID, "null argument");
+    *out = graph_distance(op->graph);
+  });
+}
+
+int syno_capi_set_error(const char* msg) {
+  g_last_error = msg ? msg : "";
+  return 0;
+}
+
 void syno_destroy(syno_op_t op) { delete op; }
 
 const char* syno_last_error(void) { return g_last_error.c_str(); }

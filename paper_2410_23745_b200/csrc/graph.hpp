@@ -64,5 +64,6 @@ Graph parse_steps(const std::string& text, std::shared_ptr<const Spec> spec);  /
 Graph parse_operator(const std::string& doc);                    // pgraph.py:730-790
 std::string print_steps(const Graph& g);                         // pgraph.py:659-672
 std::string print_operator(const Graph& g);                      // pgraph.py:712-727
+double graph_distance(const Graph& g);                             // shapedist.graph_distance (shapedist.py:415-420)
 
 }  // namespace syno
