@@ -6,6 +6,10 @@ CXXFLAGS := -O3 -std=c++17 -Xcompiler -fPIC -Xcompiler -Wall -lineinfo
 ifdef TRACE
 CXXFLAGS += -DSYNO_TC_TRACE_EVENTS
 endif
+# `make SUSPEND=1` (after touching csrc/tc.cu): every GEMM barrier wait uses the suspending try_wait
+ifdef SUSPEND
+CXXFLAGS += -DSYNO_MBAR_SUSPEND
+endif
 # `make DBG=1` (after touching csrc/tc.cu) compiles the SYNO_TC_DEBUG switches in
 ifdef DBG
 CXXFLAGS += -DSYNO_TC_DBG_SWITCHES

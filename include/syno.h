@@ -14,6 +14,7 @@
  *   syno_query           codegen.flops / param_count / input_shape /
  *                        output_shape / weight_shapes codegen.py:575-657
  *   syno_emit_loop_nest  codegen.emit_loop_nest     codegen.py:750-794
+ *   syno_compile_nest    codegen.parse_loop_nest    codegen.py:846-943
  *   syno_print_operator  pgraph.print_operator      pgraph.py:712-727
  *   syno_index_map       codegen._eval_array        codegen.py:153-176
  *
@@ -89,6 +90,16 @@ typedef struct {
 int syno_compile(const char* op_document, const char* assignment_kv, int flags, syno_op_t* out);
 
 /* y = interpret(graph, x, w).  n_w must equal the operator's weight count. */
+/* codegen.parse_loop_nest (codegen.py:846-943) + run_nest's operator:
+ * parse loop-nest text (emit_loop_nest's grammar) under the spec of an
+ * operator document (its operator/var/output/input/batch lines; a steps
+ * line is optional and ignored) into a handle.  The handle runs the nest as
+ * run_nest does: x without batch axes.  A single-stage nest is a complete
+ * operator (forward, backward, tensor cores); a multi-stage (rfactored) nest
+ * runs forward only.  Malformed text is SYNO_E_PARSE (LoopNestParseError). */
+int syno_compile_nest(const char* spec_document, const char* nest_text, const char* assignment_kv, int flags,
+                      syno_op_t* out);
+
 int syno_forward(syno_op_t op, int dtype, const void* x, const void* const* w, int n_w, void* y, void* stream);
 
 /* Gradients of <dy, interpret(graph, x, w)>.  dx may be NULL; dw may be

@@ -39,7 +39,7 @@ EXPORTS = (
     "syno_emit_loop_nest", "syno_print_operator", "syno_describe_plan",
     "syno_index_map", "syno_destroy", "syno_last_error", "syno_version", "syno_launch_count",
     "syno_profile_begin", "syno_profile_end", "syno_backward_ex", "syno_tensor_write", "syno_tensor_read",
-    "syno_shape_distance", "syno_graph_distance", "syno_shape_distance_clear_cache",
+    "syno_shape_distance", "syno_graph_distance", "syno_shape_distance_clear_cache", "syno_compile_nest",
 )
 
 
@@ -85,6 +85,8 @@ def _load():
     lib = ctypes.CDLL(LIB_PATH)
     vp = ctypes.c_void_p
     lib.syno_compile.argtypes = [ctypes.c_char_p, ctypes.c_char_p, ctypes.c_int, ctypes.POINTER(vp)]
+    lib.syno_compile_nest.argtypes = [ctypes.c_char_p, ctypes.c_char_p, ctypes.c_char_p, ctypes.c_int,
+                                      ctypes.POINTER(vp)]
     lib.syno_forward.argtypes = [vp, ctypes.c_int, vp, ctypes.POINTER(vp), ctypes.c_int, vp, vp]
     lib.syno_backward.argtypes = [vp, ctypes.c_int, vp, ctypes.POINTER(vp), ctypes.c_int, vp, vp,
                                   ctypes.POINTER(vp), vp]

@@ -7,6 +7,7 @@ Same names, argument meaning and error behaviour as the reference:
     flops(graph, assignment=None, staged=False)                        codegen.py:633-651
     param_count(graph, assignment=None)                                codegen.py:654-657
     input_shape / output_shape / weight_shapes / random_weights        codegen.py:575-595
+    emit_loop_nest / parse_loop_nest / run_nest                        codegen.py:750-794, 846-943, 549-572
 
 plus ``input_gradient`` (the adjoint of the x access),
 which the reference does not have.
@@ -23,12 +24,13 @@ from typing import Mapping, Optional, Sequence
 
 import numpy as np
 
-from .errors import ShapeMismatch
-from .pgraph import PGraph, handle_for, operator_document
+from .errors import LoopNestParseError, OperatorParseError, ShapeMismatch
+from .pgraph import Handle, PGraph, handle_for, operator_document, spec_header
 
 __all__ = [
     "ShapeMismatch", "interpret", "weight_gradient", "input_gradient", "flops", "param_count",
     "input_shape", "output_shape", "weight_shapes", "random_weights", "emit_loop_nest",
+    "LoopNest", "LoopNestParseError", "parse_loop_nest", "run_nest",
 ]
 
 
@@ -68,8 +70,74 @@ def param_count(graph, assignment: Optional[Mapping[str, int]] = None) -> int:
 
 
 def emit_loop_nest(graph, assignment: Optional[Mapping[str, int]] = None, staged: bool = False) -> str:
-    """codegen.emit_loop_nest(build_loop_nest(graph)) or of its rfactor staging."""
+    """codegen.emit_loop_nest(build_loop_nest(graph)) or of its rfactor staging;
+    of a parsed ``LoopNest``, its own text (the reference's round trip)."""
+    if isinstance(graph, LoopNest):
+        return graph.handle.emit(False)
     return handle_for(graph, assignment).emit(staged)
+
+
+class LoopNest:
+    """A loop nest parsed from text (codegen.LoopNest via parse_loop_nest), held
+    by the native library as an executable handle (``syno_compile_nest``)."""
+
+    def __init__(self, handle: Handle, assignment: tuple):
+        self.handle = handle
+        self.assignment = assignment
+
+    @property
+    def name(self) -> str:
+        return self.text.splitlines()[0][len("nest "):]
+
+    @property
+    def text(self) -> str:
+        return self.handle.emit(False)
+
+    @property
+    def n_stages(self) -> int:
+        return int(self.handle.info.n_forward_stages)
+
+    def __eq__(self, other) -> bool:
+        return isinstance(other, LoopNest) and (self.text, self.assignment) == (other.text, other.assignment)
+
+    def __hash__(self):
+        return hash((self.text, self.assignment))
+
+
+def parse_loop_nest(text: str, spec, assignment: Optional[Mapping[str, int]] = None) -> LoopNest:
+    """codegen.parse_loop_nest (codegen.py:846-943): the inverse of
+    emit_loop_nest under a spec's variables (ours or the reference's);
+    extents from the spec's reference assignment unless one is given.
+    Raises LoopNestParseError for malformed text."""
+    try:
+        h = Handle(spec_header(spec), assignment, False, nest_text=text)
+    except OperatorParseError as exc:
+        raise LoopNestParseError(str(exc)) from None
+    env = dict(assignment) if assignment is not None else dict(spec.reference)
+    return LoopNest(h, tuple(sorted((k, int(v)) for k, v in env.items())))
+
+
+def run_nest(nest: LoopNest, x, weights: Sequence = ()):
+    """codegen.run_nest (codegen.py:549-572): one element (no batch axes)
+    through a parsed nest's stages on the GPU.  numpy in -> float64 -> numpy
+    out; torch CUDA tensors in their own dtype."""
+    from . import ops
+    h = nest.handle
+    torch_in = _is_torch(x)
+    if not torch_in:
+        x = np.asarray(x, dtype=np.float64)
+        weights = [np.asarray(w, dtype=np.float64) for w in weights]
+    if len(weights) != h.n_weights:
+        raise ShapeMismatch(f"{nest.name}: expected {h.n_weights} weight tensors, got {len(weights)}")
+    if tuple(x.shape) != h.x_shape:
+        raise ShapeMismatch(f"{nest.name}: expected input shape {h.x_shape}, got {tuple(x.shape)}")
+    for j, (w, want) in enumerate(zip(weights, h.w_shapes)):
+        if tuple(w.shape) != tuple(want):
+            raise ShapeMismatch(f"w{j}: expected shape {tuple(want)}, got {tuple(w.shape)}")
+    if torch_in:
+        return ops.forward(h, x, list(weights))
+    xd, *wd = _to_device([x] + list(weights), "float64")
+    return ops.to_numpy(ops.forward(h, xd, wd))
 
 
 # ---------------------------------------------------------------------------

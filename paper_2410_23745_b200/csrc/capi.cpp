@@ -21,6 +21,7 @@ struct syno_op {
   Assignment env;
   bool staged = false;
   bool replay_only = false;
+  bool nest_handle = false;  // syno_compile_nest: built from loop-nest text, not from steps
   LoopNest unstaged, staged_nest;
   Plan plan;
   std::mutex mu;
@@ -106,6 +107,44 @@ int syno_compile(const char* doc, const char* assignment_kv, int flags, syno_op_
   });
 }
 
+int syno_compile_nest(const char* spec_document, const char* nest_text, const char* assignment_kv, int flags,
+                      syno_op_t* out) {
+  return guarded([&] {
+    if (!spec_document || !nest_text || !out) fail(SYNO_E_INVALID, "null argument");
+    if (flags) fail(SYNO_E_INVALID, "syno_compile_nest takes no flags");
+    std::string doc = spec_document;
+    if (doc.find("\nsteps ") == std::string::npos && doc.compare(0, 6, "steps ") != 0) {
+      if (!doc.empty() && doc.back() != '\n') doc += "\n";
+      doc += "steps op{}\n";
+    }
+    auto op = std::make_unique<syno_op>();
+    op->graph = parse_operator(doc);
+    op->env = assignment_kv ? parse_assignment(assignment_kv) : op->graph.spec->assignment();
+    LoopNest nest = parse_loop_nest(nest_text, *op->graph.spec, op->env);
+    if (nest.stages.empty()) fail(SYNO_E_PARSE, "loop nest has no stages");
+    // executable nests name declared tensors only (run_nest would fail later)
+    auto declared = [&](const std::string& name) {
+      for (auto& t : nest.tensors)
+        if (t.name == name) return true;
+      return false;
+    };
+    for (auto& st : nest.stages) {
+      if (!declared(st.tensor)) fail(SYNO_E_PARSE, "stage writes undeclared tensor '" + st.tensor + "'");
+      for (auto& t : st.terms)
+        if (!declared(t.tensor)) fail(SYNO_E_PARSE, "term reads undeclared tensor '" + t.tensor + "'");
+    }
+    if (!declared("x") || !declared("y")) fail(SYNO_E_PARSE, "loop nest declares no input x / output y");
+    op->nest_handle = true;
+    op->unstaged = nest;
+    op->staged_nest = nest;
+    // run_nest (codegen.py:549-572) has no batch; a single-stage nest is an
+    // unstaged operator and gets the full plan (backward, tensor cores)
+    const bool single = nest.stages.size() == 1;
+    op->plan = build_plan(nest, nest, {}, op->env, single);
+    *out = op.release();
+  });
+}
+
 static void check_weights(syno_op* op, const void* const* w, int n_w) {
   if (op->replay_only) fail(SYNO_E_INVALID, "handle was compiled with SYNO_REPLAY_ONLY");
   if (n_w != (int)op->plan.w_ext.size())
@@ -145,6 +184,8 @@ int syno_backward_ex(syno_op_t op, int dtype, const void* x, const void* const* 
     b.dy = dy;
     b.dx = dx;
     for (int j = 0; j < n_w; ++j) b.dw.push_back(dw ? dw[j] : nullptr);
+    if (op->plan.nest_only)
+      fail(SYNO_E_UNSUPPORTED, "a parsed loop nest with several stages runs forward only (codegen.run_nest)");
     b.x_unchanged = (flags & SYNO_BWD_X_UNCHANGED) != 0;
     b.w_unchanged = (flags & SYNO_BWD_W_UNCHANGED) != 0;
     run_backward(op->plan, dp, (DType)dtype, b, s);
@@ -161,7 +202,7 @@ int syno_query(syno_op_t op, syno_info* info) {
     if (!op || !info) fail(SYNO_E_INVALID, "null argument");
     memset(info, 0, sizeof(*info));
     std::vector<int> perm;
-    info->complete = match_input(op->graph, &perm);
+    info->complete = op->nest_handle ? 1 : match_input(op->graph, &perm);
     if (op->replay_only) {
       info->replay_only = 1;
       info->n_weights = (int)op->graph.weights.size();
@@ -186,18 +227,18 @@ int syno_query(syno_op_t op, syno_info* info) {
         n *= p.w_ext[j][k];
       }
       params += n;
-      info->grad_w_scatter[j] = p.grad_w.at(j).at(0).scatter;
+      info->grad_w_scatter[j] = p.nest_only ? 0 : p.grad_w.at(j).at(0).scatter;
     }
     info->params = params;
     info->flops_unstaged = p.flops_unstaged;
     info->flops_staged = p.flops_staged;
     info->n_forward_stages = (int)p.forward.size();
-    info->grad_x_scatter = p.grad_x.at(0).scatter;
+    info->grad_x_scatter = p.nest_only ? 0 : p.grad_x.at(0).scatter;
     double g = 1;
     for (auto e : p.unstaged.axis_ext) g *= (double)e;
     for (auto e : op->unstaged.stages[0].reduces) g *= (double)e.extent;
     info->index_grid = (int64_t)g;
-    info->tc_path = tc_matches(p) ? 1 : gg_matches(p) ? 2 : 0;
+    info->tc_path = p.nest_only ? 0 : tc_matches(p) ? 1 : gg_matches(p) ? 2 : 0;
   });
 }
 

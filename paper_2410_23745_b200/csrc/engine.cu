@@ -1001,8 +1001,10 @@ DevPlan* build_dev_plan(const Plan& plan, cudaStream_t stream) {
       }
     }
   }
-  dp->tc = tc_build(plan, stream);
-  if (!dp->tc) dp->gg = gg_build(plan, stream);
+  if (!plan.nest_only) {
+    dp->tc = tc_build(plan, stream);
+    if (!dp->tc) dp->gg = gg_build(plan, stream);
+  }
   dp->ev_plan = record_built(stream);
   return dp.release();
 }

@@ -2,6 +2,7 @@
 #include "nest.hpp"
 
 #include <algorithm>
+#include <cstring>
 
 namespace syno {
 
@@ -300,6 +301,347 @@ std::string emit_loop_nest(const LoopNest& nest) {
     }
   }
   return out;
+}
+
+
+
+// ---------------------------------------------------------------------------
+// parse_loop_nest (codegen.py:846-943) with the coordinate parser
+// symexpr.parse_expr (symexpr.py:421-485) and its tokenizer (symexpr.py:502-531).
+// Failures are SYNO_E_PARSE (LoopNestParseError / ExprParseError, both
+// ValueErrors in the reference).
+// ---------------------------------------------------------------------------
+
+namespace {
+
+[[noreturn]] void nest_error(const std::string& msg) { fail(SYNO_E_PARSE, msg); }
+
+bool is_word(char c) { return isalnum((unsigned char)c) || c == '_'; }
+
+bool all_digits(const std::string& s) {
+  if (s.empty()) return false;
+  for (char c : s)
+    if (!isdigit((unsigned char)c)) return false;
+  return true;
+}
+
+std::string strip(const std::string& s) {
+  size_t a = 0, b = s.size();
+  while (a < b && isspace((unsigned char)s[a])) ++a;
+  while (b > a && isspace((unsigned char)s[b - 1])) --b;
+  return s.substr(a, b - a);
+}
+
+std::vector<std::string> tokenize(const std::string& text) {  // symexpr._tokenize
+  std::vector<std::string> tokens;
+  size_t i = 0;
+  while (i < text.size()) {
+    const char c = text[i];
+    if (isspace((unsigned char)c)) {
+      ++i;
+    } else if (std::string("+-*/%()^#").find(c) != std::string::npos) {
+      if (c == '-' && !tokens.empty() && tokens.back() == "^") {
+        size_t j = i + 1;
+        while (j < text.size() && isdigit((unsigned char)text[j])) ++j;
+        tokens.push_back(text.substr(i, j - i));
+        i = j;
+      } else {
+        tokens.push_back(std::string(1, c));
+        ++i;
+      }
+    } else if (is_word(c)) {
+      size_t j = i;
+      while (j < text.size() && is_word(text[j])) ++j;
+      tokens.push_back(text.substr(i, j - i));
+      i = j;
+    } else {
+      nest_error(std::string("bad character '") + c + "' in '" + text + "'");
+    }
+  }
+  return tokens;
+}
+
+struct ExprParser {  // symexpr.parse_expr
+  const std::string& text;
+  std::vector<std::string> tokens;
+  size_t pos = 0;
+  const std::map<std::string, E>& iters;
+  const std::map<std::string, Var>& vars;
+
+  const std::string* peek() const { return pos < tokens.size() ? &tokens[pos] : nullptr; }
+  std::string take() {
+    if (pos >= tokens.size()) nest_error("unexpected end of input in '" + text + "'");
+    return tokens[pos++];
+  }
+  static bool is_size(const E& e) { return e->op == Op::SizeRef; }
+  E size_of(const std::string& name, int exp) {
+    const Var& v = vars.at(name);
+    std::map<std::string, std::pair<bool, int>> acc;
+    acc[name] = {v.primary, exp};
+    return mk_sizeref(size_from_powers(acc));
+  }
+  E atom() {
+    std::string tok = take();
+    if (tok == "(") {
+      E inner = sum();
+      if (take() != ")") nest_error("missing ')' in '" + text + "'");
+      return inner;
+    }
+    std::string digits = tok;
+    while (!digits.empty() && digits[0] == '-') digits.erase(0, 1);
+    if (all_digits(digits)) {
+      try {
+        return mk_const(std::stoll(tok));
+      } catch (const std::exception&) {
+        nest_error("bad integer '" + tok + "' in '" + text + "'");
+      }
+    }
+    int exp = 1;
+    if (peek() && *peek() == "^") {
+      take();
+      std::string e = take();
+      try {
+        size_t used = 0;
+        exp = std::stoi(e, &used);
+        if (used != e.size()) throw std::invalid_argument(e);
+      } catch (const std::exception&) {
+        nest_error("bad exponent '" + e + "' in '" + text + "'");
+      }
+    }
+    if (vars.count(tok) && exp != 1) return size_of(tok, exp);
+    auto it = iters.find(tok);
+    if (it != iters.end()) return it->second;
+    if (vars.count(tok)) return size_of(tok, 1);
+    nest_error("unknown name '" + tok + "' in '" + text + "'");
+  }
+  E product() {
+    E node = atom();
+    while (peek() && (*peek() == "*" || *peek() == "/" || *peek() == "%")) {
+      const std::string op = take();
+      E rhs = atom();
+      if (op == "*" && is_size(node) && is_size(rhs)) node = mk_sizeref(size_mul(node->size, rhs->size));
+      else if (op == "*") node = mk_bin(Op::Mul, node, rhs);
+      else if (op == "/") node = mk_bin(Op::FloorDiv, node, rhs);
+      else node = mk_bin(Op::Mod, node, rhs);
+    }
+    return node;
+  }
+  E sum() {
+    E node = product();
+    while (peek() && (*peek() == "+" || *peek() == "-")) {
+      const std::string op = take();
+      E rhs = product();
+      node = mk_bin(op == "+" ? Op::Add : Op::Sub, node, rhs);
+    }
+    return node;
+  }
+  E parse() {
+    tokens = tokenize(text);
+    E r = sum();
+    if (pos != tokens.size()) nest_error("trailing tokens in '" + text + "'");
+    return r;
+  }
+};
+
+SizeLike parse_sizelike(const std::string& raw, const std::map<std::string, Var>& vars) {
+  SizeLike s;
+  if (all_digits(raw)) {
+    s.is_int = true;
+    s.ival = std::stoll(raw);
+  } else {
+    try {
+      s.sym = parse_size(raw, vars);
+    } catch (const Error& e) {
+      nest_error(e.what());
+    }
+  }
+  return s;
+}
+
+int64_t extent_of(const SizeLike& s, const Assignment& env) { return s.is_int ? s.ival : eval_size(s.sym, env); }
+
+// codegen._parse_terms: split on " * " outside index brackets.
+std::vector<Access> parse_terms(const std::string& text, const std::map<std::string, E>& iters,
+                                const std::map<std::string, Var>& vars) {
+  std::vector<std::string> parts;
+  int depth = 0;
+  size_t start = 0;
+  for (size_t k = 0; k < text.size(); ++k) {
+    if (text[k] == '[') ++depth;
+    else if (text[k] == ']') --depth;
+    else if (depth == 0 && text.compare(k, 3, " * ") == 0) {
+      parts.push_back(text.substr(start, k - start));
+      start = k + 3;
+      k += 2;
+    }
+  }
+  parts.push_back(text.substr(start));
+  std::vector<Access> terms;
+  for (auto& raw : parts) {
+    const std::string part = strip(raw);
+    size_t name_end = 0;
+    while (name_end < part.size() && is_word(part[name_end])) ++name_end;
+    Access a;
+    a.tensor = part.substr(0, name_end);
+    if (name_end == 0) nest_error("bad term: '" + part + "'");
+    if (name_end == part.size()) {
+      terms.push_back(a);
+      continue;
+    }
+    if (part[name_end] != '[' || part.back() != ']' ||
+        part.find(']', name_end) != part.size() - 1)
+      nest_error("bad term: '" + part + "'");
+    const std::string inner = part.substr(name_end + 1, part.size() - name_end - 2);
+    size_t s0 = 0;
+    while (true) {
+      size_t comma = inner.find(',', s0);
+      std::string e = strip(inner.substr(s0, comma == std::string::npos ? std::string::npos : comma - s0));
+      if (!e.empty()) a.exprs.push_back(ExprParser{e, {}, 0, iters, vars}.parse());
+      if (comma == std::string::npos) break;
+      s0 = comma + 1;
+    }
+    terms.push_back(a);
+  }
+  return terms;
+}
+
+// "<tensor>" or "<tensor>[...]" followed by " = <rest>"; false when the line has another shape.
+bool split_target(const std::string& line, std::string* tensor, std::string* rest) {
+  size_t k = 0;
+  while (k < line.size() && is_word(line[k])) ++k;
+  if (k == 0) return false;
+  *tensor = line.substr(0, k);
+  if (k < line.size() && line[k] == '[') {
+    size_t close = line.find(']', k);
+    if (close == std::string::npos || line.find('[', k + 1) < close) return false;
+    k = close + 1;
+  }
+  if (line.compare(k, 3, " = ") != 0) return false;
+  *rest = line.substr(k + 3);
+  return !rest->empty();
+}
+
+}  // namespace
+
+LoopNest parse_loop_nest(const std::string& text, const Spec& spec, const Assignment& env) {
+  const auto vars = spec.var_map();
+  std::vector<std::string> lines;
+  {
+    size_t s0 = 0;
+    while (s0 <= text.size()) {
+      size_t nl = text.find('\n', s0);
+      std::string ln = text.substr(s0, nl == std::string::npos ? std::string::npos : nl - s0);
+      if (!ln.empty() && ln.back() == '\r') ln.pop_back();
+      if (!strip(ln).empty()) lines.push_back(ln);
+      if (nl == std::string::npos) break;
+      s0 = nl + 1;
+    }
+  }
+  if (lines.empty() || lines[0].compare(0, 5, "nest ") != 0) nest_error("missing nest header");
+  LoopNest nest;
+  nest.name = strip(lines[0].substr(5));
+  nest.env = env;
+  size_t pos = 1;
+  while (pos < lines.size() && lines[pos].compare(0, 7, "tensor ") == 0) {
+    // ^tensor (\w+) = (input|output|stage|weight)(?: (\d+))? ?\[([^\]]*)\]$
+    const std::string& ln = lines[pos];
+    size_t k = 7;
+    size_t n0 = k;
+    while (k < ln.size() && is_word(ln[k])) ++k;
+    TensorDecl t;
+    t.name = ln.substr(n0, k - n0);
+    bool ok = !t.name.empty() && ln.compare(k, 3, " = ") == 0;
+    k += 3;
+    if (ok) {
+      ok = false;
+      for (const char* role : {"input", "output", "stage", "weight"})
+        if (ln.compare(k, strlen(role), role) == 0) {
+          t.role = role;
+          k += strlen(role);
+          ok = true;
+          break;
+        }
+    }
+    if (ok && k < ln.size() && ln[k] == ' ' && k + 1 < ln.size() && isdigit((unsigned char)ln[k + 1])) {
+      ++k;
+      while (k < ln.size() && isdigit((unsigned char)ln[k])) ++k;
+    }
+    if (ok && k < ln.size() && ln[k] == ' ') ++k;
+    ok = ok && k < ln.size() && ln[k] == '[' && ln.back() == ']' && ln.find(']', k) == ln.size() - 1;
+    if (!ok) nest_error("bad tensor line: '" + ln + "'");
+    const std::string raw = ln.substr(k + 1, ln.size() - k - 2);
+    size_t s0 = 0;
+    while (true) {
+      size_t comma = raw.find(',', s0);
+      std::string piece = strip(raw.substr(s0, comma == std::string::npos ? std::string::npos : comma - s0));
+      if (!piece.empty()) {
+        t.sizes.push_back(parse_sizelike(piece, vars));
+        t.extents.push_back(extent_of(t.sizes.back(), env));
+      }
+      if (comma == std::string::npos) break;
+      s0 = comma + 1;
+    }
+    nest.tensors.push_back(t);
+    ++pos;
+  }
+
+  while (pos < lines.size()) {
+    Stage st;
+    std::map<std::string, E> iters;
+    // `for <name> in <size>:` (codegen._FOR_RE); false when the line is not one
+    auto read_for = [&](const std::string& line, Axis* axis) {
+      const std::string s = strip(line);
+      if (s.compare(0, 4, "for ") != 0 || s.back() != ':') return false;
+      size_t k = 4;
+      while (k < s.size() && is_word(s[k])) ++k;
+      if (k == 4 || s.compare(k, 4, " in ") != 0) return false;
+      const std::string name = s.substr(4, k - 4);
+      const std::string raw = strip(s.substr(k + 4, s.size() - k - 5));
+      if (raw.empty() || raw.find(':') != std::string::npos) return false;
+      axis->name = name;
+      axis->size = parse_sizelike(raw, vars);
+      axis->extent = extent_of(axis->size, env);
+      iters[name] = mk_iter(name, axis->size.is_int ? Size{} : axis->size.sym);
+      return true;
+    };
+    while (pos < lines.size()) {
+      Axis a;
+      if (!read_for(lines[pos], &a)) break;
+      const std::string body = pos + 1 < lines.size() ? strip(lines[pos + 1]) : "";
+      st.axes.push_back(a);
+      ++pos;
+      if (body == "acc = 0") break;
+    }
+    if (pos >= lines.size()) nest_error("unexpected end of loop nest");
+    std::string stripped = strip(lines[pos]);
+    std::string tensor, rest;
+    if (stripped == "acc = 0") {
+      ++pos;
+      while (pos < lines.size()) {
+        Axis a;
+        if (!read_for(lines[pos], &a)) break;
+        st.reduces.push_back(a);
+        ++pos;
+      }
+      if (pos >= lines.size()) nest_error("unexpected end of loop nest");
+      stripped = strip(lines[pos]);
+      if (stripped.compare(0, 7, "acc += ") != 0) nest_error("expected accumulation, got '" + stripped + "'");
+      st.terms = parse_terms(stripped.substr(7), iters, vars);
+      ++pos;
+      if (pos >= lines.size()) nest_error("unexpected end of loop nest");
+      stripped = strip(lines[pos]);
+      if (!split_target(stripped, &tensor, &rest) || rest != "acc")
+        nest_error("expected store, got '" + stripped + "'");
+      ++pos;
+    } else {
+      if (!split_target(stripped, &tensor, &rest)) nest_error("expected assignment, got '" + stripped + "'");
+      st.terms = parse_terms(rest, iters, vars);
+      ++pos;
+    }
+    st.tensor = tensor;
+    nest.stages.push_back(st);
+  }
+  return nest;
 }
 
 }  // namespace syno

@@ -314,7 +314,7 @@ CStage derive_gradient(const CStage& S, int j, const CTensor& grad, const CTenso
 }
 
 Plan build_plan(const LoopNest& unstaged, const LoopNest& staged, const std::vector<Size>& batch_dims,
-                const Assignment& env) {
+                const Assignment& env, bool derive_backward) {
   Plan p;
   for (auto& s : batch_dims) {
     p.batch_ext.push_back(eval_size(s, env));
@@ -395,6 +395,14 @@ Plan build_plan(const LoopNest& unstaged, const LoopNest& staged, const std::vec
   p.unstaged = un.at(0);
   convert(staged, &p.forward, &p.stage_ext);
 
+  if (!derive_backward) {
+    p.nest_only = true;
+    for (auto& st : p.forward) {
+      simplify_stage(&st);
+      fold_unread_reduces(&st);
+    }
+    return p;
+  }
   // Backward always differentiates the unstaged nest, as the reference does
   // (codegen.py:680-681).  Gradients of reduces folded into `scale` keep it.
   CStage S = un.at(0);

@@ -88,6 +88,7 @@ struct CStage {
 };
 
 struct Plan {
+  bool nest_only = false;  // from a parsed multi-stage loop nest: forward (run_nest) on the stage engine only
   int64_t batch = 1;
   std::vector<int64_t> batch_ext;
   std::vector<int64_t> x_ext, y_ext;              // including batch
@@ -122,6 +123,6 @@ void simplify_stage(CStage* s);
 void c_sum_parts(const CE& e, int64_t* c0, std::vector<std::pair<int64_t, CE>>* parts);
 
 Plan build_plan(const LoopNest& unstaged, const LoopNest& staged_or_same, const std::vector<Size>& batch_dims,
-                const Assignment& env);
+                const Assignment& env, bool derive_backward = true);
 
 }  // namespace syno

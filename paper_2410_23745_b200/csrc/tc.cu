@@ -921,12 +921,29 @@ __global__ void __launch_bounds__(256) chain_nc_kernel(const __grid_constant__ C
     __syncthreads();
     if (last) {
       __threadfence();
+      // every thread sums a strided set of the blocks' partials per window,
+      // then a fixed-shape tree adds the 256 thread sums: the result depends
+      // only on gridDim, not on which block finished last
+      // (in the side-product region of the dynamic stage: 256 x 17 floats,
+      // free again; no static buffer, so the block stays small enough to
+      // co-reside with a persistent GEMM CTA)
+      float* red = stage + blockDim.x * KKo;  // [KK][blockDim.x]
       __shared__ float tot[16];
-      if (threadIdx.x < KK) {
+      for (int k = 0; k < KK; ++k) {
         float t = 0.f;
-        for (unsigned b = 0; b < gridDim.x; ++b) t += *((volatile float*)h.partial + (size_t)b * KK + threadIdx.x);
-        tot[threadIdx.x] = t;
+        for (unsigned b = threadIdx.x; b < gridDim.x; b += blockDim.x)
+          t += *((volatile float*)h.partial + (size_t)b * KK + k);
+        red[k * blockDim.x + threadIdx.x] = t;
       }
+      __syncthreads();
+      for (int width = (int)blockDim.x >> 1; width > 0; width >>= 1) {
+        for (int e = threadIdx.x; e < KK * width; e += blockDim.x) {
+          const int k = e / width, q = e - k * width;
+          red[k * blockDim.x + q] += red[k * blockDim.x + q + width];
+        }
+        __syncthreads();
+      }
+      if (threadIdx.x < KK) tot[threadIdx.x] = red[threadIdx.x * blockDim.x];
       __syncthreads();
       if (threadIdx.x == 0) {
         const int ow2 = h.side_ow ? h.Kw : 1;
@@ -1850,8 +1867,17 @@ struct TcWs {
   int bn_fwd = 0, bn_dg = 0, bn_wg = 0;
   int t_fwd[3] = {0, 0, 0}, t_dg[3] = {0, 0, 0}, t_wg[3] = {0, 0, 0};
   std::vector<void*> owned;
+  bool pooled = false;  // owned blocks come from the stream-ordered pool (cudaMallocAsync)
   ~TcWs() {
-    for (void* q : owned) cudaFree(q);
+    if (pooled && !owned.empty()) {
+      // every use of a workspace is ordered on the stream it was built for
+      // (and its joined side stream); after a device-wide wait the blocks go
+      // back to the pool, which keeps them mapped for the next operator
+      cudaDeviceSynchronize();
+      for (void* q : owned) cudaFreeAsync(q, 0);
+    } else {
+      for (void* q : owned) cudaFree(q);
+    }
     if (ev_fork) cudaEventDestroy(ev_fork);
     if (ev_join) cudaEventDestroy(ev_join);
     if (side) cudaStreamDestroy(side);
@@ -1875,10 +1901,22 @@ static bool same_grid(const PackGeom& a, const PackGeom& b) {
 // fills are ordered on it, ahead of the caller's first kernel.
 static thread_local cudaStream_t g_ws_stream = nullptr;
 
+// Workspaces come from the device's stream-ordered pool (kept mapped by its
+// release threshold, engine.cu build_dev_plan): a fresh operator -- every
+// candidate of a sweep -- then costs no driver-level allocation, where
+// cudaMalloc mapped new memory with the device idle behind the host.
+// SYNO_TC_SYNC_ALLOC=1 restores cudaMalloc (A/B switch).
 template <typename T>
 static T* ws_alloc(TcWs& w, size_t count) {
+  static const bool sync_alloc = getenv("SYNO_TC_SYNC_ALLOC") != nullptr;
   void* p = nullptr;
-  cuda_check(cudaMalloc(&p, std::max<size_t>(count, 1) * sizeof(T)), "cudaMalloc(tc workspace)");
+  const size_t bytes = std::max<size_t>(count, 1) * sizeof(T);
+  if (sync_alloc) {
+    cuda_check(cudaMalloc(&p, bytes), "cudaMalloc(tc workspace)");
+  } else {
+    cuda_check(cudaMallocAsync(&p, bytes, g_ws_stream), "cudaMallocAsync(tc workspace)");
+    w.pooled = true;
+  }
   w.owned.push_back(p);
   // packed operands rely on this: their padding is written once, here
   cuda_check(cudaMemsetAsync(p, 0, std::max<size_t>(count, 1) * sizeof(T), g_ws_stream), "cudaMemset(tc workspace)");

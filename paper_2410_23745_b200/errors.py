@@ -4,6 +4,7 @@
     NonIntegralSize     symexpr.py:21
     GraphError          pgraph.py:66
     OperatorParseError  pgraph.py:655 (a ValueError, as in the reference)
+    LoopNestParseError  codegen.py:72 (a ValueError)
 """
 from __future__ import annotations
 
@@ -24,6 +25,10 @@ class GraphError(Exception):
 
 class OperatorParseError(ValueError):
     pass
+
+
+class LoopNestParseError(ValueError):
+    """Malformed loop-nest text (codegen.parse_loop_nest)."""
 
 
 class UnsupportedOperator(Exception):

@@ -108,11 +108,11 @@ def print_steps(graph) -> str:
     return "op{" + "; ".join(_ref_step_text(s) for s in graph.steps) + "}"
 
 
-def operator_document(graph) -> str:
-    """The operator document of our PGraph or of a reference PGraph."""
-    if isinstance(graph, PGraph):
-        return graph.document
-    spec = graph.spec
+def spec_header(spec) -> str:
+    """The operator/var/output/input/batch lines of our ProblemSpec or of a
+    reference ProblemSpec (pgraph.print_operator's header, pgraph.py:712-723)."""
+    if isinstance(spec, ProblemSpec):
+        return spec.header()
     ref = dict(spec.reference)
     lines = [f"operator {spec.name}"]
     for v in spec.variables:
@@ -121,8 +121,14 @@ def operator_document(graph) -> str:
     lines.append("input " + " ".join(str(s) for s in spec.input_dims))
     if spec.batch_dims:
         lines.append("batch " + " ".join(str(s) for s in spec.batch_dims))
-    lines.append("steps " + print_steps(graph))
-    text = "\n".join(lines) + "\n"
+    return "\n".join(lines) + "\n"
+
+
+def operator_document(graph) -> str:
+    """The operator document of our PGraph or of a reference PGraph."""
+    if isinstance(graph, PGraph):
+        return graph.document
+    text = spec_header(graph.spec) + "steps " + print_steps(graph) + "\n"
     # the reference's print_operator ends with the match_input permutation
     # (pgraph.py:724-726); the native replay computes it (csrc/graph.cpp)
     with _CACHE_LOCK:
@@ -144,13 +150,17 @@ class Handle:
     """Owns one native syno_op_t."""
 
     def __init__(self, document: str, assignment: Optional[Mapping[str, int]], staged: bool,
-                 replay_only: bool = False):
+                 replay_only: bool = False, nest_text: Optional[str] = None):
         kv = None
         if assignment is not None:
             kv = ",".join(f"{k}={int(v)}" for k, v in assignment.items()).encode()
         ptr = ctypes.c_void_p()
-        flags = (_lib.SYNO_STAGED if staged else 0) | (_lib.SYNO_REPLAY_ONLY if replay_only else 0)
-        rc = _lib.lib.syno_compile(document.encode(), kv, flags, ctypes.byref(ptr))
+        if nest_text is not None:
+            # codegen.parse_loop_nest: `document` only supplies the spec
+            rc = _lib.lib.syno_compile_nest(document.encode(), nest_text.encode(), kv, 0, ctypes.byref(ptr))
+        else:
+            flags = (_lib.SYNO_STAGED if staged else 0) | (_lib.SYNO_REPLAY_ONLY if replay_only else 0)
+            rc = _lib.lib.syno_compile(document.encode(), kv, flags, ctypes.byref(ptr))
         if rc:
             raise_status(rc, _lib.last_error())
         self.ptr = ptr
