@@ -20,9 +20,15 @@ using namespace syno::tc;
 // 16 a second warp spins mbarrier.test_wait on a barrier the MMAs never complete, 32 the same with try_wait,
 // 64 a producer warp streams 24 KB bulk copies global -> shared while the MMAs run,
 // 128 eight epilogue warps loop tcgen05.ld of the second accumulator + bf16 global stores,
-// 256 operands hold random bf16 values (else zeros)
+// 256 operands hold random bf16 values (else zeros), 512 window shifts read from a __grid_constant__
+// parameter array with a dynamic index (as tc_gemm_kernel reads p.a_shift[w])
+struct ShiftParams {
+  int pad[256];  // a large parameter block, as TcGemmParams is
+  int shift[16];
+};
+
 __global__ void win_kernel(int n, int tiles, int variant, int kq, unsigned long long* out, const uint8_t* gsrc,
-                           __nv_bfloat16* gdst) {
+                           __nv_bfloat16* gdst, const __grid_constant__ ShiftParams sp) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   __shared__ uint32_t tslot;
@@ -73,8 +79,10 @@ __global__ void win_kernel(int n, int tiles, int variant, int kq, unsigned long 
     c0 = clock64();
     for (int t = 0; t < tiles; ++t) {
       const uint32_t dst = tmem + ((variant & 8) ? (uint32_t)(t & 1) * 128u : 0u);
+#pragma unroll 1
       for (int w = 0; w < 9; ++w) {
-        const uint32_t a_lo = a_base + (uint32_t)((variant & 1) ? 0 : shifts[w]) * 8u;
+        const int sh = (variant & 512) ? sp.shift[w] : shifts[w];
+        const uint32_t a_lo = a_base + (uint32_t)((variant & 1) ? 0 : sh) * 8u;
         const uint32_t b_lo = b_base + (uint32_t)((variant & 2) ? 0 : w) * (uint32_t)(n * 128 >> 4);
         for (int k = 0; k < kq; ++k)
           mma_lo<false>(dst, a_lo + (uint32_t)(k * 2), b_lo + (uint32_t)(k * 2), idesc,
@@ -151,14 +159,17 @@ int main() {
   cudaMalloc(&d_src, (size_t)4096 * 24576 + 4096);
   cudaMalloc(&d_dst, (size_t)296 * 8 * 64 * 128 * 2);
   cudaFuncSetAttribute(win_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  ShiftParams sp{};
+  const int shv[9] = {0, 1, 2, 33, 34, 35, 66, 67, 68};
+  for (int i = 0; i < 9; ++i) sp.shift[i] = shv[i];
   printf("  N variant kq ctas/SM | cycles/MMA/SM (floor %s)\n", "128N/256");
   for (int n : {64, 128}) {
     for (int per_sm : {1}) {
-      for (int variant : {0, 256, 192, 448}) {
+      for (int variant : {0, 512, 448, 960}) {
         for (int kq : {4}) {
           if (n == 128 && (per_sm == 2 || !(variant & 2))) continue;  // 9 B tiles of 16 KB do not fit
           const int tiles = 64, grid = 148 * per_sm;
-          for (int rep = 0; rep < 2; ++rep) win_kernel<<<grid, 320, smem>>>(n, tiles, variant, kq, d_out, d_src, d_dst);
+          for (int rep = 0; rep < 2; ++rep) win_kernel<<<grid, 320, smem>>>(n, tiles, variant, kq, d_out, d_src, d_dst, sp);
           cudaError_t e = cudaDeviceSynchronize();
           if (e != cudaSuccess) {
             printf("error %s\n", cudaGetErrorString(e));
