@@ -21,7 +21,8 @@ using namespace syno::tc;
 // 64 a producer warp streams 24 KB bulk copies global -> shared while the MMAs run,
 // 128 eight epilogue warps loop tcgen05.ld of the second accumulator + bf16 global stores,
 // 256 operands hold random bf16 values (else zeros), 512 window shifts read from a __grid_constant__
-// parameter array with a dynamic index (as tc_gemm_kernel reads p.a_shift[w])
+// parameter array with a dynamic index (as tc_gemm_kernel reads p.a_shift[w]), 1024 all 512 TMEM columns
+// allocated and the accumulator at column 256, 2048 resident B at the top of a 200 KB allocation
 struct ShiftParams {
   int pad[256];  // a large parameter block, as TcGemmParams is
   int shift[16];
@@ -59,7 +60,7 @@ __global__ void win_kernel(int n, int tiles, int variant, int kq, unsigned long 
     mbar_init(&bar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  const uint32_t cols = 256u;
+  const uint32_t cols = (variant & 1024) ? 512u : 256u;
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tslot)),
                  "r"(cols));
@@ -74,11 +75,21 @@ __global__ void win_kernel(int n, int tiles, int variant, int kq, unsigned long 
   if (warp == 0) {
     const uint32_t idesc = idesc_bf16(128, n);
     const uint32_t a_base = desc_lo(smem_u32(smem));
-    const uint32_t b_base = desc_lo(smem_u32(smem + 32 * 1024));
+    const uint32_t b_base = desc_lo(smem_u32(smem + ((variant & 2048) ? 128 : 32) * 1024));
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g0));
     c0 = clock64();
     for (int t = 0; t < tiles; ++t) {
-      const uint32_t dst = tmem + ((variant & 8) ? (uint32_t)(t & 1) * 128u : 0u);
+      const uint32_t dst = tmem + ((variant & 8) ? (uint32_t)(t & 1) * 128u : 0u) + ((variant & 1024) ? 256u : 0u);
+      if (!(variant & 4096)) {
+#pragma unroll
+      for (int w = 0; w < 9; ++w) {
+        const uint32_t a_lo = a_base + (uint32_t)((variant & 1) ? 0 : shifts[w]) * 8u;
+        const uint32_t b_lo = b_base + (uint32_t)((variant & 2) ? 0 : w) * (uint32_t)(n * 128 >> 4);
+        for (int k = 0; k < kq; ++k)
+          mma_lo<false>(dst, a_lo + (uint32_t)(k * 2), b_lo + (uint32_t)(k * 2), idesc,
+                        ((variant & 4) || w > 0 || k > 0) ? 1u : 0u);
+      }
+      } else
 #pragma unroll 1
       for (int w = 0; w < 9; ++w) {
         const int sh = (variant & 512) ? sp.shift[w] : shifts[w];
@@ -153,7 +164,7 @@ int main() {
   unsigned long long* d_out;
   cudaMalloc(&d_out, 4096 * sizeof(unsigned long long));
   static unsigned long long h[4096];
-  const size_t smem = 129 * 1024;
+  const size_t smem = 201 * 1024;
   uint8_t* d_src;
   __nv_bfloat16* d_dst;
   cudaMalloc(&d_src, (size_t)4096 * 24576 + 4096);
@@ -165,7 +176,7 @@ int main() {
   printf("  N variant kq ctas/SM | cycles/MMA/SM (floor %s)\n", "128N/256");
   for (int n : {64, 128}) {
     for (int per_sm : {1}) {
-      for (int variant : {0, 512, 448, 960}) {
+      for (int variant : {0, 64, 128, 256, 448, 4096, 4096+64, 4096+128, 4096+256, 4096+448, 4096+192}) {
         for (int kq : {4}) {
           if (n == 128 && (per_sm == 2 || !(variant & 2))) continue;  // 9 B tiles of 16 KB do not fit
           const int tiles = 64, grid = 148 * per_sm;
