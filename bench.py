@@ -145,7 +145,7 @@ def load_traffic():
         return json.load(f)
 
 
-def roofline_from_profile(prof, steps, step_ms, peaks):
+def roofline_from_profile(prof, steps, step_ms, peaks, workload="resnet18"):
     """Dominant kernel class of the profiled steps and its roofline.
 
     prof: {class: {launches, ms, flops, bytes}} from the library's
@@ -174,7 +174,7 @@ def roofline_from_profile(prof, steps, step_ms, peaks):
         achieved = s["bytes"] / (s["ms"] / 1e3) / 1e9 if s["ms"] else 0.0
         roof = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                 "frac": achieved / peaks["hbm_gbs"], "bytes_per_launch": s["bytes"] / max(1, s["launches"])}
-    tr = load_traffic().get(dom)
+    tr = load_traffic().get(workload, {}).get(dom)
     roof.update({
         "kernel": dom, "launches_per_step": s["launches"] / steps, "avg_launch_us": per_launch_ms * 1e3,
         "share_of_step": (s["ms"] / steps) / step_ms if step_ms else None,
@@ -357,7 +357,7 @@ def run_layers(args, rank, world, device, peaks):
             for f in d:
                 d[f] += v[f]
         del pg
-    roof, kernels = roofline_from_profile(prof, prof_steps, ms, peaks)
+    roof, kernels = roofline_from_profile(prof, prof_steps, ms, peaks, args.workload)
     if roof is not None:
         roof["timing"] = "library CUDA events captured in the step's graph (per-launch, on the launch stream)"
     # per-layer breakdown (eager calls, events between them; includes host launch gaps)

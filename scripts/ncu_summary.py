@@ -1,7 +1,8 @@
-"""Summarise an `ncu --set full` raw CSV of tc_gemm launches into
-profiles/<name>.txt and profiles/traffic.json (mean DRAM bytes per launch).
+"""Summarise an `ncu --set full` raw CSV of one workload's dominant-kernel
+launches into profiles/<name>.txt and its entry of profiles/traffic.json
+(mean DRAM bytes per launch, keyed by bench workload and kernel class).
 
-    python scripts/ncu_summary.py gpurun_out/final/tc_full_raw.csv profiles/r01_ncu_tc_gemm_resnet18.txt
+    python scripts/ncu_summary.py raw.csv profiles/r02_ncu_tc_gemm_resnet18.txt resnet18 tc_gemm "first step"
 """
 import csv
 import json
@@ -11,7 +12,7 @@ import sys
 UNIT = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-3, "usecond": 1, "msecond": 1e3}
 
 
-def main(src, dst):
+def main(src, dst, workload="resnet18", kclass="tc_gemm", what="first step"):
     rows = list(csv.reader(open(src)))
     hdr, units, data = rows[0], rows[1], rows[2:]
     col = {h: i for i, h in enumerate(hdr)}
@@ -28,7 +29,7 @@ def main(src, dst):
                         dram=val(r, "dram__bytes_read.sum") + val(r, "dram__bytes_write.sum")))
     n = len(out)
     mean = lambda k: sum(o[k] for o in out) / n
-    lines = [f"ncu --set full of the {n} tc_gemm launches of one ResNet-18 step (cold L2 per replay)",
+    lines = [f"ncu --set full of {n} {kclass} launches of the {workload} bench ({what}; cold L2 per replay)",
              f"launches {n}; mean duration {mean('us'):.1f} us; mean tensor-pipe active {mean('tensor'):.1f} %; "
              f"mean SM throughput {mean('sm'):.1f} %; mean DRAM bytes/launch {mean('dram') / 1e6:.2f} MB", "",
              f"{'us':>8} {'tensor%':>8} {'sm%':>6} {'DRAM MB':>8}  kernel"]
@@ -36,12 +37,16 @@ def main(src, dst):
         lines.append(f"{o['us']:8.1f} {o['tensor']:8.1f} {o['sm']:6.1f} {o['dram'] / 1e6:8.2f}  {o['name'][:60]}")
     open(dst, "w").write("\n".join(lines) + "\n")
     tj = os.path.join(os.path.dirname(dst), "traffic.json")
-    json.dump({"tc_gemm": {"dram_bytes_per_launch": mean("dram"), "launches_captured": n,
-                           "note": f"ncu --set full (cache control on: cold L2 per replay), first ResNet-18 step, {n} "
-                                   "tc_gemm launches; mean dram__bytes_read.sum+dram__bytes_write.sum per launch"}},
-              open(tj, "w"), indent=1)
+    table = json.load(open(tj)) if os.path.exists(tj) else {}
+    if "tc_gemm" in table and "dram_bytes_per_launch" in table["tc_gemm"]:
+        table = {}  # round-1 flat format
+    table.setdefault(workload, {})[kclass] = {
+        "dram_bytes_per_launch": mean("dram"), "launches_captured": n, "tensor_active_pct": mean("tensor"),
+        "note": f"ncu --set full (cache control on: cold L2 per replay), {workload} {what}, {n} {kclass} launches; "
+                "mean dram__bytes_read.sum+dram__bytes_write.sum per launch"}
+    json.dump(table, open(tj, "w"), indent=1, sort_keys=True)
     print("\n".join(lines[:2]))
 
 
 if __name__ == "__main__":
-    main(*sys.argv[1:3])
+    main(*sys.argv[1:])

@@ -41,6 +41,7 @@ def _torch_ref(op, x, ws, c_in, c_out):
 CASES = [
     ("conv3x3", 64, 64, 32, 2),
     ("conv3x3", 3, 64, 32, 2),       # stem: C_in padded to 8, K tail zero-filled by TMA
+    ("conv3x3", 8, 64, 32, 2),       # one 16-wide K step per window (kq_last), no padding
     ("conv3x3", 64, 128, 16, 3),
     ("conv3x3", 128, 256, 8, 2),
     ("conv3x3", 256, 512, 4, 2),
