@@ -198,3 +198,36 @@ def test_live_against_reference_objects():
     for text in ("op{}", "op{reduce(C_in)}", "op{reduce(C_in); reduce(K)}", CONV_STEPS):
         g = ref_parse(text, spec)
         assert SD.graph_distance(g) == RSD.graph_distance(g)
+
+
+@pytest.mark.skipif(not os.path.isdir(REF_SRC), reason="reference tree absent (GPU box)")
+def test_reference_search_log_unchanged_with_native_distance(monkeypatch):
+    """INTEGRATION.md's search-side opt-in: the reference's own MCTS with
+    graph_distance swapped for the native one logs the same samples, byte
+    for byte, for the same seed (search.py:62, 166-171)."""
+    if REF_SRC not in sys.path:
+        sys.path.insert(0, REF_SRC)
+    import numpy as np
+    import opsmith.search as S
+    from opsmith.pgraph import ProblemSpec, print_steps
+    from opsmith.symexpr import Variable, parse_size
+
+    variables = (Variable("C_out"), Variable("C_in"), Variable("H"), Variable("W"), Variable("K", primary=False))
+    vm = {v.name: v for v in variables}
+    spec = ProblemSpec(name="conv2d", variables=variables,
+                       reference=(("C_out", 8), ("C_in", 8), ("H", 8), ("W", 8), ("K", 3)),
+                       output_dims=tuple(parse_size(t, vm) for t in ("C_out", "H", "W")),
+                       input_dims=tuple(parse_size(t, vm) for t in ("C_in", "H", "W")))
+
+    def reward(g):
+        return (sum(map(ord, print_steps(g))) % 97) / 97.0
+
+    def run():
+        tree = S.SearchTree(spec, S.Budget(d_max=7), seed=11)
+        rng = np.random.default_rng(11)
+        return [r.line() for r in (S.mcts_step(tree, reward, rng) for _ in range(300)) if r is not None]
+
+    want = run()
+    monkeypatch.setattr(S, "graph_distance", SD.graph_distance)
+    got = run()
+    assert want and got == want
