@@ -114,6 +114,14 @@ struct PackGeom {
   int32_t split;                 // Split
   uint32_t lo_mask;              // bit k: part k holds lo(v), else hi(v)
   int64_t Fpitch;                // channel-major row pitch (multiple of 8)
+  // pack blocks cover PK_PIX consecutive pixels of the flattened (image, h, w)
+  // grid instead of whole rows: rows are contiguous (s_h = Win, s_w = 1), so
+  // V-wide loads work whenever the image plane (Hin x Win) is a multiple of
+  // V, also for rows that are not (14 x 14 maps).  2 = plane blocks: one
+  // image x 64 channels per block (Hin x Win <= PK_PIX), read as one
+  // contiguous run of 64 channel planes (s_c = Hin x Win) with 16-byte loads
+  // whatever the plane size (7 x 7 maps)
+  int32_t flat = 0;
   __host__ __device__ int32_t parts() const { return split == SPLIT_NONE ? 1 : 3; }
   __host__ __device__ int32_t n_img_out() const { return split == SPLIT_IMG ? 3 * n_img : n_img; }
   __host__ __device__ int32_t Ct() const { return split == SPLIT_CH ? 3 * Cp : Cp; }  // dst channel pitch
@@ -230,9 +238,13 @@ __device__ __forceinline__ void pack_rows_body(const TI* __restrict__ src, __nv_
   const int cb = (int)by;
   const int n_out = g.n_img_out();
   // rows of <= PK_PIX pixels: rows_per_block whole rows; wider rows: one PK_PIX segment per block
-  int64_t row0;
-  int nrows, wbeg, Win;
-  if (g.Win <= PK_PIX) {
+  int64_t row0 = 0;
+  int nrows = 0, wbeg = 0, Win = g.Win;
+  const int64_t HW = (int64_t)g.Hin * g.Win;
+  const int64_t q0 = (int64_t)bx * PK_PIX;  // flat mode: first pixel of the block
+  if (g.flat) {
+    // (flat mode: SPLIT_NONE only, so output image = source image)
+  } else if (g.Win <= PK_PIX) {
     row0 = (int64_t)bx * rows_per_block;
     nrows = (int)min((int64_t)rows_per_block, total_rows - row0);
     wbeg = 0;
@@ -244,8 +256,20 @@ __device__ __forceinline__ void pack_rows_body(const TI* __restrict__ src, __nv_
     wbeg = (int)(bx % nseg) * PK_PIX;
     Win = min(PK_PIX, g.Win - wbeg);
   }
-  const int npix = nrows * Win;
-  if (t < nrows) {
+  const int npix = g.flat == 2 ? (int)HW : g.flat ? (int)min((int64_t)PK_PIX, (int64_t)n_out * HW - q0) : nrows * Win;
+  if (g.flat) {
+    if (t < npix) {
+      const int64_t q = g.flat == 2 ? (int64_t)bx * HW + t : q0 + t;
+      const int imgo = (int)(q / HW);
+      const int rem = (int)(q - (int64_t)imgo * HW);
+      const int hi = rem / g.Win, wi = rem - hi * g.Win;
+      const int ph = hi % g.Sh, hp = hi / g.Sh + g.lo_h;
+      const int pw = wi % g.Sw, wp = wi / g.Sw + g.lo_w;
+      s_dst[t] = (hp < g.Hp && wp < g.Wp)
+                     ? (((int64_t)(ph * g.Sw + pw) * n_out + imgo) * g.Hp + hp) * g.Wp + wp
+                     : -1;
+    }
+  } else if (t < nrows) {
     const int64_t row = row0 + t;  // (img', hi) flattened
     int img = (int)(row / g.Hin);
     const int hi = (int)(row - (int64_t)img * g.Hin);
@@ -257,7 +281,7 @@ __device__ __forceinline__ void pack_rows_body(const TI* __restrict__ src, __nv_
     s_part[t] = part;
     s_src[t] = img * g.s_img + (int64_t)hi * g.s_h + (int64_t)wbeg * g.s_w;
   }
-  if (t < npix) {
+  if (!g.flat && t < npix) {
     const int rr = t / Win, wi = wbeg + t - rr * Win;
     const int64_t row = row0 + rr;
     const int imgo = (int)(row / g.Hin);
@@ -269,20 +293,54 @@ __device__ __forceinline__ void pack_rows_body(const TI* __restrict__ src, __nv_
                    : -1;  // never read by any window
   }
   __syncthreads();
+  if (g.flat == 2) {
+    // plane blocks: the block's 64 channel planes of image bx are one
+    // contiguous run; 16-byte loads walk it and scatter into the tile
+    constexpr int VE = 16 / (int)sizeof(TI);
+    const int nval = max(0, min(64, g.C - cb * 64));
+    const TI* base = src + (int64_t)bx * g.s_img + (int64_t)cb * 64 * g.s_c;
+    const int n_el = nval * npix;  // multiple of VE: host-checked (HW * 64 and the tail)
+    for (int e = t * VE; e < n_el; e += 256 * VE) {
+      __align__(16) TI q[VE];
+      *reinterpret_cast<uint4*>(q) = __ldg(reinterpret_cast<const uint4*>(base + e));
+#pragma unroll
+      for (int j = 0; j < VE; ++j) {
+        const int cl = (e + j) / npix, px = (e + j) - cl * npix;
+        tile[cl][(px + 8 * (cl >> 3)) & (PK_PIX - 1)] = __float2bfloat16((float)q[j]);
+      }
+    }
+    // channels past C: zero rows
+    for (int e = nval * npix + t; e < 64 * npix; e += 256) {
+      const int cl = e / npix, px = e - cl * npix;
+      tile[cl][(px + 8 * (cl >> 3)) & (PK_PIX - 1)] = __float2bfloat16(0.f);
+    }
+  } else {
   // ---- read: each thread keeps one pixel vector and walks the channels
-  const int vpr = Win / V;       // vectors per row
-  const int nvec = nrows * vpr;  // <= PK_PIX / V
+  const int vpr = g.flat ? 1 : Win / V;  // vectors per row
+  const int nvec = g.flat ? npix / V : nrows * vpr;  // <= PK_PIX / V
   const int cstep = max(1, 256 / nvec);
   if (t < cstep * nvec) {
     const int vi = t % nvec;
-    const int rr = vi / vpr;
-    const int w0 = (vi - rr * vpr) * V;
-    const int px0 = rr * Win + w0;
-    const TI* rowp = src + s_src[rr] + (int64_t)w0 * g.s_w;
+    int px0;
+    const TI* rowp;
+    int part0 = 0;
+    if (g.flat) {
+      // a vector never straddles two images: HW and q0 are multiples of V
+      px0 = vi * V;
+      const int64_t q = q0 + px0;
+      const int64_t img = q / HW;
+      rowp = src + img * g.s_img + (q - img * HW);
+    } else {
+      const int rr = vi / vpr;
+      const int w0 = (vi - rr * vpr) * V;
+      px0 = rr * Win + w0;
+      rowp = src + s_src[rr] + (int64_t)w0 * g.s_w;
+      part0 = s_part[rr];
+    }
 #pragma unroll 2
     for (int cl = t / nvec; cl < 64; cl += cstep) {
       int c = cb * 64 + cl;
-      int part = s_part[rr];
+      int part = part0;
       if (g.split == SPLIT_CH) {
         part = c / g.Cp;
         c -= part * g.Cp;
@@ -359,6 +417,7 @@ __device__ __forceinline__ void pack_rows_body(const TI* __restrict__ src, __nv_
       }
     }
   }
+  }  // row / flat blocks
   __syncthreads();
   // ---- write: 8 threads per destination pixel, 16 bytes each
   const int Ct = g.Ct();
@@ -1506,7 +1565,7 @@ static void gemm(TcGemmParams& p, int bn, int m_tiles, int n_tiles, int z_tiles,
   p.n_tiles = n_tiles;
   p.z_tiles = z_tiles;
   const bool small = p.cfg == 1 && bn <= 128;
-  const int a_region = pair ? a_region_bytes<256, CFG_PAIR>()
+  const int a_region = pair ? (bn == 128 ? a_region_bytes<128, CFG_PAIR>() : a_region_bytes<256, CFG_PAIR>())
                        : small ? (bn == 64 ? a_region_bytes<64, 1>() : a_region_bytes<128, 1>())
                                : (bn == 64 ? a_region_bytes<64>() : bn == 128 ? a_region_bytes<128>() : a_region_bytes<256>());
   const int ring = small ? ring_bytes<1>() : ring_bytes<0>();
@@ -1522,7 +1581,8 @@ static void gemm(TcGemmParams& p, int bn, int m_tiles, int n_tiles, int z_tiles,
   const int id = prof_begin(name, flops, 0.0, stream);
   if (p.mode == MODE_ROWS) {
     if (pair) {
-      launch_gemm<256, MODE_ROWS, CFG_PAIR>(p, grid, stream);
+      if (bn == 128) launch_gemm<128, MODE_ROWS, CFG_PAIR>(p, grid, stream);
+      else launch_gemm<256, MODE_ROWS, CFG_PAIR>(p, grid, stream);
     } else if (small) {
       if (bn == 64) launch_gemm<64, MODE_ROWS, 1>(p, grid, stream);
       else launch_gemm<128, MODE_ROWS, 1>(p, grid, stream);
@@ -1573,7 +1633,11 @@ static void set_b_res(TcGemmParams& p, int bn, int n_tiles) {
 // tiles.  Returns the B box rows of one CTA.
 static int set_pair(TcGemmParams& p, int bn, const RowsTiling& rt) {
   static const bool on = !(getenv("SYNO_TC_PAIR") && atoi(getenv("SYNO_TC_PAIR")) == 0);
-  if (!on || bn != 256 || rt.G != 1 || rt.rs != 1 || p.b_res || rt.m_tiles < 2) return bn;
+  // BN = 128 in CTA pairs (M = 256 x N = 128 per MMA, 64 B rows per CTA):
+  // experiment switch SYNO_TC_PAIR128=1
+  static const bool on128 = getenv("SYNO_TC_PAIR128") && atoi(getenv("SYNO_TC_PAIR128")) == 1;
+  if (!on || !(bn == 256 || (bn == 128 && on128)) || rt.G != 1 || rt.rs != 1 || p.b_res || rt.m_tiles < 2)
+    return bn;
   p.cfg = CFG_PAIR;
   p.b_tx = (uint32_t)(bn / 2) * BK * 2;
   return bn / 2;
@@ -1661,6 +1725,7 @@ struct PackPlan {
   int rpb = 1;
   int64_t rows = 0;
   int V = 1;
+  int flat = 0;  // PackGeom::flat blocks
 };
 
 static PackPlan pack_plan(const void* src, DType dt, const PackGeom& g) {
@@ -1676,6 +1741,34 @@ static PackPlan pack_plan(const void* src, DType dt, const PackGeom& g) {
   };
   if (dt == DT_BF16) pp.V = aligned(8, 2) ? 8 : aligned(4, 2) ? 4 : 1;
   else pp.V = aligned(4, 4) ? 4 : 1;
+  // flat pixel blocks when rows are contiguous and the row width defeats the
+  // vector loads (SYNO_TC_NO_FLAT_PACK=1: row blocks, A/B switch)
+  static const bool no_flat = getenv("SYNO_TC_NO_FLAT_PACK") != nullptr;
+  const int64_t HW = (int64_t)g.Hin * g.Win;
+  auto flat_ok = [&](int v, int es) {
+    return g.split == SPLIT_NONE && g.s_w == 1 && g.s_h == g.Win && HW % v == 0 && g.s_c % v == 0 &&
+           g.s_img % v == 0 && base % (v * es) == 0;
+  };
+  const int vmax = dt == DT_BF16 ? 8 : 4, es = dt == DT_BF16 ? 2 : 4;
+  int vf = 0;
+  for (int v = vmax; v >= 4 && !vf; v /= 2)
+    if (flat_ok(v, es)) vf = v;
+  if (!no_flat && vf > pp.V) {
+    pp.V = vf;
+    pp.flat = 1;
+    pp.rows = 0;
+    pp.grid = dim3((unsigned)(((int64_t)g.n_img_out() * HW + PK_PIX - 1) / PK_PIX), (unsigned)((g.Ct() + 63) / 64));
+  }
+  // plane blocks: planes of <= PK_PIX pixels whose rows defeat both vector forms
+  const int ve = 16 / es;
+  const int tail = g.C % 64;
+  if (!no_flat && pp.V == 1 && g.split == SPLIT_NONE && HW <= PK_PIX && g.s_w == 1 && g.s_h == g.Win &&
+      g.s_c == HW && g.s_img % ve == 0 && (64 * HW) % ve == 0 && (tail * HW) % ve == 0 && base % 16 == 0) {
+    pp.flat = 2;
+    pp.V = 1;
+    pp.rows = 0;
+    pp.grid = dim3((unsigned)g.n_img_out(), (unsigned)((g.Ct() + 63) / 64));
+  }
   return pp;
 }
 
@@ -1698,27 +1791,25 @@ static void log_pack(const char* what, const void* src, const PackGeom& g) {
 static void pack_cl(const void* src, DType dt, const PackGeom& g, __nv_bfloat16* dst, cudaStream_t stream) {
   if (skip_class("pack")) return;
   log_pack("pack", src, g);
-  // one block = whole source rows (<= PK_PIX pixels) or one PK_PIX segment of a wider row
-  const int rpb = std::max(1, PK_PIX / g.Win);
-  const int64_t rows = (int64_t)g.n_img_out() * g.Hin;
-  const int64_t blocks = g.Win <= PK_PIX ? (rows + rpb - 1) / rpb : rows * ((g.Win + PK_PIX - 1) / PK_PIX);
-  dim3 grid((unsigned)blocks, (unsigned)((g.Ct() + 63) / 64));
+  // one block = whole source rows (<= PK_PIX pixels), one PK_PIX segment of a
+  // wider row, or PK_PIX consecutive pixels of contiguous rows (flat)
+  const PackPlan pp = pack_plan(src, dt, g);
+  PackGeom gf = g;
+  gf.flat = pp.flat;
+  const int rpb = pp.rpb;
+  const int64_t rows = pp.rows;
+  const dim3 grid = pp.grid;
   const double src_elems = (double)g.n_img_out() * g.C * g.Hin * g.Win;
   const int id = prof_begin("pack_cl", 0.0, src_elems * (dt == DT_BF16 ? 2 : 4) * (g.split == SPLIT_CH ? 1 : 1) +
                                                 src_elems * (g.split == SPLIT_CH ? 3 : 1) * 2, stream);
   note_launch();
-  const uintptr_t base = reinterpret_cast<uintptr_t>(src);
-  const bool unit_w = g.s_w == 1;
-  auto aligned = [&](int v, int es) {
-    return unit_w && g.Win % v == 0 && (g.Win <= PK_PIX || PK_PIX % v == 0) && g.s_h % v == 0 && g.s_c % v == 0 && g.s_img % v == 0 && base % (v * es) == 0;
-  };
   if (dt == DT_BF16) {
-    if (aligned(8, 2)) launch_pack_rows<__nv_bfloat16, 8>(src, g, dst, grid, rpb, rows, stream);
-    else if (aligned(4, 2)) launch_pack_rows<__nv_bfloat16, 4>(src, g, dst, grid, rpb, rows, stream);
-    else launch_pack_rows<__nv_bfloat16, 1>(src, g, dst, grid, rpb, rows, stream);
+    if (pp.V == 8) launch_pack_rows<__nv_bfloat16, 8>(src, gf, dst, grid, rpb, rows, stream);
+    else if (pp.V == 4) launch_pack_rows<__nv_bfloat16, 4>(src, gf, dst, grid, rpb, rows, stream);
+    else launch_pack_rows<__nv_bfloat16, 1>(src, gf, dst, grid, rpb, rows, stream);
   } else {
-    if (aligned(4, 4)) launch_pack_rows<float, 4>(src, g, dst, grid, rpb, rows, stream);
-    else launch_pack_rows<float, 1>(src, g, dst, grid, rpb, rows, stream);
+    if (pp.V == 4) launch_pack_rows<float, 4>(src, gf, dst, grid, rpb, rows, stream);
+    else launch_pack_rows<float, 1>(src, gf, dst, grid, rpb, rows, stream);
   }
   cuda_check(cudaGetLastError(), "pack_rows_kernel");
   prof_end(id, stream);
@@ -2230,18 +2321,20 @@ static bool pack_and_fold(const TcPlan& tp, const Bindings& b, DType dt, const v
   if (!tp.fast_fold || KK <= 1 || KK > 16 || getenv("SYNO_TC_NO_PREP_FUSE")) return false;
   if (skip_class("pack") || skip_class("fold")) return false;
   const PackPlan pp = pack_plan(src, dt, g);
+  PackGeom gf = g;
+  gf.flat = pp.flat;
   log_pack(dgrad ? "prep(dgrad)" : "prep(fwd)", src, g);
   const FoldArgs f = fold_args(tp, b, dt, dgrad, split, folded);
   const double fold_elems = (double)KK * f.ext[2] * f.Bp;
   const int id = prof_begin("pack_cl", 0.0, pack_bytes(dt, g) + fold_elems * (split ? 6 : 2), stream);
   note_launch();
   if (dt == DT_BF16) {
-    if (pp.V == 8) launch_prep<__nv_bfloat16, 8>(src, g, packed, pp, f, stream);
-    else if (pp.V == 4) launch_prep<__nv_bfloat16, 4>(src, g, packed, pp, f, stream);
-    else launch_prep<__nv_bfloat16, 1>(src, g, packed, pp, f, stream);
+    if (pp.V == 8) launch_prep<__nv_bfloat16, 8>(src, gf, packed, pp, f, stream);
+    else if (pp.V == 4) launch_prep<__nv_bfloat16, 4>(src, gf, packed, pp, f, stream);
+    else launch_prep<__nv_bfloat16, 1>(src, gf, packed, pp, f, stream);
   } else {
-    if (pp.V == 4) launch_prep<float, 4>(src, g, packed, pp, f, stream);
-    else launch_prep<float, 1>(src, g, packed, pp, f, stream);
+    if (pp.V == 4) launch_prep<float, 4>(src, gf, packed, pp, f, stream);
+    else launch_prep<float, 1>(src, gf, packed, pp, f, stream);
   }
   cuda_check(cudaGetLastError(), "prep_kernel");
   prof_end(id, stream);

@@ -472,7 +472,7 @@ template <int BN, int MODE, int CFG>
 __global__ void __launch_bounds__(THREADS, CFG == 1 ? 2 : 1) tc_gemm_kernel(const __grid_constant__ TcGemmParams p) {
   pdl_trigger();
   constexpr bool PAIR = CFG == CFG_PAIR;
-  static_assert(!PAIR || BN == 256, "CTA pair: BN = 256");
+  static_assert(!PAIR || BN == 256 || (BN == 128 && MODE == MODE_ROWS), "CTA pair: BN = 256, or 128 (rows mode)");
   // KM: 64-element K blocks per ring stage.  The pair grad-weight kernel
   // stages two (3 x 64 KB per CTA), halving the barrier hand-offs per MAC.
   constexpr int KM = PAIR && MODE == MODE_WGRAD ? 2 : 1;
