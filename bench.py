@@ -472,8 +472,40 @@ def measure_e2e(state, phases, args, device, dtype, world):
     # other processes on the box) does not decide the number
     ms = allreduce_max(statistics.median(evs[k].elapsed_time(evs[k + 1]) for k in range(n)), world, device)
     units = state[0]["h"].x_shape[0]
+    link = link_bandwidth(device)
+    floor_ms = max(h2d, d2h) / (link * 1e9) * 1e3
     return {"value": world * units / (ms / 1e3), "unit": unit_of(args.workload), "ms_per_step": ms,
-            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h}
+            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+            "link_gbs_each_way": link, "link_floor_ms": floor_ms, "link_frac": floor_ms / ms}
+
+
+def link_bandwidth(device, mb=256):
+    """Measured host<->device bandwidth with both directions busy at once
+    (pinned buffers, two copy streams, best of 3): the e2e step's floor is
+    max(bytes up, bytes down) over it."""
+    import torch
+    n = mb << 20
+    hu, hd = torch.empty(n, dtype=torch.uint8).pin_memory(), torch.empty(n, dtype=torch.uint8).pin_memory()
+    du, dd = torch.empty(n, dtype=torch.uint8, device=device), torch.empty(n, dtype=torch.uint8, device=device)
+    s1, s2 = torch.cuda.Stream(device), torch.cuda.Stream(device)
+    best = float("inf")
+    cur = torch.cuda.current_stream(device)
+    for _ in range(3):
+        torch.cuda.synchronize(device)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(cur)
+        s1.wait_stream(cur)
+        s2.wait_stream(cur)
+        with torch.cuda.stream(s1):
+            du.copy_(hu, non_blocking=True)
+        with torch.cuda.stream(s2):
+            hd.copy_(dd, non_blocking=True)
+        cur.wait_stream(s1)
+        cur.wait_stream(s2)
+        e1.record(cur)
+        torch.cuda.synchronize(device)
+        best = min(best, e0.elapsed_time(e1) / 1e3)
+    return n / best / 1e9
 
 
 # ---------------------------------------------------------------------------

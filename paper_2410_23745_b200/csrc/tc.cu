@@ -17,6 +17,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <type_traits>
 #include <cmath>
 #include <cstring>
 #include <functional>
@@ -337,6 +338,34 @@ __device__ __forceinline__ void pack_rows_body(const TI* __restrict__ src, __nv_
       rowp = src + s_src[rr] + (int64_t)w0 * g.s_w;
       part0 = s_part[rr];
     }
+    if constexpr (sizeof(TI) == 2 && V >= 4) {
+      // bf16, vector rows: every load of the thread in flight before any
+      // shared-memory store (<= 8 per thread: nvec <= PK_PIX / 4 so cstep
+      // >= 8); the block's run is one latency round instead of several
+      using VT = typename std::conditional<V == 8, uint4, uint2>::type;
+      VT qv[8];
+      const int cl0 = t / nvec;
+#pragma unroll
+      for (int it = 0; it < 8; ++it) {
+        const int cl = cl0 + it * cstep;
+        const int c = cb * 64 + cl;
+        qv[it] = VT{};
+        if (cl < 64 && c < g.C) qv[it] = __ldg(reinterpret_cast<const VT*>(rowp + (int64_t)c * g.s_c));
+      }
+#pragma unroll
+      for (int it = 0; it < 8; ++it) {
+        const int cl = cl0 + it * cstep;
+        if (cl >= 64) break;
+        __nv_bfloat16* trow = &tile[cl][0];
+        if constexpr (V == 8) {
+          *reinterpret_cast<uint4*>(trow + ((px0 + 8 * (cl >> 3)) & (PK_PIX - 1))) = qv[it];
+        } else {
+          const __nv_bfloat16* hq = reinterpret_cast<const __nv_bfloat16*>(&qv[it]);
+#pragma unroll
+          for (int e = 0; e < 4; ++e) trow[(px0 + e + 8 * (cl >> 3)) & (PK_PIX - 1)] = hq[e];
+        }
+      }
+    } else
 #pragma unroll 2
     for (int cl = t / nvec; cl < 64; cl += cstep) {
       int c = cb * 64 + cl;
