@@ -556,6 +556,10 @@ void release_dev_stage(DevStage& ds) {
   ds.tile.reset();
   if (ds.pre) release_dev_stage(*ds.pre);
   ds.pre.reset();
+  if (ds.perm_in) release_dev_stage(*ds.perm_in);
+  ds.perm_in.reset();
+  if (ds.perm_out) release_dev_stage(*ds.perm_out);
+  ds.perm_out.reset();
   if (ds.tables) cudaFreeAsync(ds.tables, nullptr);
   ds.tables = nullptr;
   if (ds.prog) cudaFree(ds.prog);
@@ -618,7 +622,151 @@ static void build_prog_stage(const CStage& cs, DevStage* ds) {
 
 static void build_dev_stage_impl(const CStage& cs, DevStage* ds, cudaStream_t stream, bool allow_tile);
 
+// Lane-contiguous layout for heavy gather stages.  The tile kernel's lanes
+// run along the stage axis the lead gathered term's LAST coordinate reads;
+// when that coordinate does not advance by one along any stage axis (e.g.
+// x[b, (32 co + h + r) % 64, ..., (s // 64 + 16) % 32]: lanes walk a 4 KB
+// channel stride), but another coordinate does, the input is copied once
+// with that dimension innermost and the stage reads the copy: a warp's
+// gathers then touch one or two 32-byte sectors instead of 32.
+// SYNO_NO_PERM=1 disables (A/B switch).
+static bool lane_contiguous_layout(const CStage& cs, CStage* main, CStage* perm, int64_t* count) {
+  static const bool off = getenv("SYNO_NO_PERM") != nullptr;
+  // heavy stages only (an extra copy launch); SYNO_PERM_MIN_POINTS lowers
+  // the threshold so the parity tests exercise the transform at small sizes
+  static const double min_points = getenv("SYNO_PERM_MIN_POINTS") ? atof(getenv("SYNO_PERM_MIN_POINTS")) : 4194304.0;
+  if (off || cs.grid_points() < min_points) return false;
+  const int A = (int)cs.axis_ext.size(), L = cs.nloops();
+  // lead term: for a scatter its target; else the first input (operator
+  // dtype) whose coordinates move with a reduce
+  int lead = -1;
+  if (cs.scatter) {
+    if (cs.target.t.kind != TK_DX && cs.target.t.kind != TK_DW) return false;
+    lead = 0;
+  }
+  for (size_t t = 0; t < cs.terms.size() && lead < 0; ++t) {
+    const CTerm& T = cs.terms[t];
+    if (T.t.kind != TK_X && T.t.kind != TK_W && T.t.kind != TK_DY) continue;
+    for (auto& c : T.coords) {
+      std::vector<int> d;
+      c_loops(c, &d);
+      for (int l : d)
+        if (l >= A) lead = (int)t;
+    }
+  }
+  if (lead < 0) return false;
+  const CTerm& T = cs.scatter ? cs.target : cs.terms[lead];
+  const int D = (int)T.coords.size();
+  if (D < 2 || T.t.numel() > ((int64_t)1 << 28)) return false;
+  // unit-stride score of coordinate d as the LAST coordinate: the tile
+  // planner's lanes then walk the highest stage axis l it reads, so the score
+  // is how often coord(l + 1) - coord(l) == 1 at random grid points
+  uint64_t seed = 0x9e3779b97f4a7c15ull;
+  auto rnd = [&](int64_t n) {
+    seed ^= seed << 13;
+    seed ^= seed >> 7;
+    seed ^= seed << 17;
+    return (int64_t)(seed % (uint64_t)n);
+  };
+  auto score = [&](int d) {
+    std::vector<int> dl;
+    c_loops(T.coords[d], &dl);
+    int lane = -1;
+    for (int l : dl)
+      if (l < A) lane = std::max(lane, l);
+    double best = 0;
+    for (int l : dl) {
+      if (l != lane || cs.ext(l) < 2) continue;
+      int hit = 0;
+      const int n = 128;
+      std::vector<int64_t> v(L);
+      for (int i = 0; i < n; ++i) {
+        for (int q = 0; q < L; ++q) v[q] = rnd(cs.ext(q));
+        v[l] = rnd(cs.ext(l) - 1);
+        const int64_t a = c_eval(T.coords[d], v.data());
+        ++v[l];
+        hit += c_eval(T.coords[d], v.data()) - a == 1;
+      }
+      best = std::max(best, (double)hit / n);
+    }
+    return best;
+  };
+  static const bool log = getenv("SYNO_PERM_LOG") != nullptr;
+  const double last = score(D - 1);
+  if (log) fprintf(stderr, "[perm] stage %s\n[perm] lead term %d, last-coordinate score %.2f\n", cs.describe().c_str(), lead, last);
+  if (last >= 0.5) return false;
+  int dstar = -1;
+  double bs = 0.75;
+  for (int d = 0; d + 1 < D; ++d) {
+    const double sc = score(d);
+    if (log) fprintf(stderr, "[perm]   coordinate %d score %.2f\n", d, sc);
+    if (sc >= bs) {
+      bs = sc;
+      dstar = d;
+    }
+  }
+  if (dstar < 0) return false;
+  std::vector<int> order;  // new dimension k holds old dimension order[k]
+  for (int d = 0; d < D; ++d)
+    if (d != dstar) order.push_back(d);
+  order.push_back(dstar);
+  CTensor P;
+  P.kind = TK_PERM;
+  for (int k = 0; k < D; ++k) P.extents.push_back(T.t.extents[order[k]]);
+  if (cs.scatter) {
+    // accumulate into P (permuted target, accumulator precision); restore:
+    // target[j] = P[i] with i_k = j[order[k]] (an affine stage over the target)
+    *main = cs;
+    P.kind = TK_SCRATCH;
+    std::vector<CE> c2;
+    for (int k = 0; k < D; ++k) c2.push_back(cs.target.coords[order[k]]);
+    main->target.coords = c2;
+    main->target.t = P;
+    // cs.out keeps the target tensor: callers dispatch on it (dx / dw_j /
+    // an intermediate's gradient); the sums have its element count
+    *perm = CStage();
+    perm->axis_ext = T.t.extents;
+    CTerm src;
+    src.t = P;
+    for (int k = 0; k < D; ++k) src.coords.push_back(c_loop(order[k]));
+    perm->terms.push_back(src);
+    perm->out = T.t;
+    *count = P.numel();
+    return true;
+  }
+  // the copy: P[i_0..i_{D-1}] = T[j] with j[order[k]] = i_k (an affine stage)
+  *perm = CStage();
+  perm->axis_ext = P.extents;
+  CTerm src;
+  src.t = T.t;
+  src.coords.resize(D);
+  for (int k = 0; k < D; ++k) src.coords[order[k]] = c_loop(k);
+  perm->terms.push_back(src);
+  perm->out = P;
+  // every term of the stage that reads the same tensor reads the copy
+  *main = cs;
+  for (auto& U : main->terms) {
+    if (!(U.t == T.t)) continue;
+    std::vector<CE> c2;
+    for (int k = 0; k < D; ++k) c2.push_back(U.coords[order[k]]);
+    U.coords = c2;
+    U.t = P;
+  }
+  *count = P.numel();
+  return true;
+}
+
 void build_dev_stage(const CStage& cs, DevStage* ds, cudaStream_t stream) {
+  CStage main_cs, perm_cs;
+  int64_t count = 0;
+  if (lane_contiguous_layout(cs, &main_cs, &perm_cs, &count)) {
+    auto pst = std::make_shared<DevStage>();
+    build_dev_stage_impl(perm_cs, pst.get(), stream, false);
+    (cs.scatter ? ds->perm_out : ds->perm_in) = pst;
+    ds->perm_count = count;
+    build_dev_stage_impl(main_cs, ds, stream, true);
+    return;
+  }
   build_dev_stage_impl(cs, ds, stream, true);
 }
 
@@ -1580,6 +1728,7 @@ static const void* bind_ptr(const CTensor& t, const Bindings& b) {
     case TK_DSTAGE: return b.dstages.at(t.index);
     case TK_SCRATCH:
     case TK_SCRATCH_IN: return b.scratch;
+    case TK_PERM: return b.perm;
     default: return nullptr;
   }
 }
@@ -1610,9 +1759,38 @@ static void launch_stage_t(const DevStage& ds, const Bindings& b, void* out, boo
 }
 
 template <typename TI>
-static void launch_stage_impl(const DevStage& ds, const Bindings& b, void* out, bool out_acc, cudaStream_t stream,
+static void launch_stage_impl(const DevStage& ds, const Bindings& b_in, void* out, bool out_acc, cudaStream_t stream,
                               const char** kind) {
   using TA = typename Acc<TI>::type;
+  if (ds.perm_out) {
+    // scatter into the permuted target (accumulator precision), then restore
+    void* tmp = nullptr;
+    cuda_check(cudaMallocAsync(&tmp, (size_t)ds.perm_count * sizeof(TA), stream), "alloc permuted target");
+    DevStage inner = ds;
+    inner.perm_out.reset();
+    launch_stage_impl<TI>(inner, b_in, tmp, true, stream, kind);
+    Bindings b2 = b_in;
+    b2.scratch = tmp;
+    const char* pk = nullptr;
+    launch_stage_impl<TI>(*ds.perm_out, b2, out, out_acc, stream, &pk);
+    cuda_check(cudaFreeAsync(tmp, stream), "free permuted target");
+    return;
+  }
+  Bindings b = b_in;
+  void* perm_buf = nullptr;
+  if (ds.perm_in) {
+    cuda_check(cudaMallocAsync(&perm_buf, (size_t)ds.perm_count * sizeof(TI), stream), "alloc permuted input");
+    const char* pk = nullptr;
+    launch_stage_impl<TI>(*ds.perm_in, b_in, perm_buf, false, stream, &pk);
+    b.perm = perm_buf;
+  }
+  struct PermFree {
+    void* p;
+    cudaStream_t s;
+    ~PermFree() {
+      if (p) cudaFreeAsync(p, s);
+    }
+  } perm_free{perm_buf, stream};
   KStage k = ds.k;
   for (int t = 0; t < k.n_terms; ++t) {
     k.terms[t].ptr = bind_ptr(ds.cs.terms[t].t, b);

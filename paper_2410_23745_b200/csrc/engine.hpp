@@ -113,6 +113,15 @@ struct DevStage {
   // term reads: `pre` (a gather stage) first sums the reduce-invariant terms
   // over those axes into a scratch tensor, which this stage then scatters.
   std::shared_ptr<DevStage> pre;
+  // Lane-contiguous layout: `perm_in` copies one input with a permuted axis
+  // order (TK_PERM, perm_count elements) so that the tile kernel's lanes read
+  // it with unit stride; this stage reads the copy instead of the input.
+  std::shared_ptr<DevStage> perm_in;
+  int64_t perm_count = 0;
+  // ... and for a scatter whose target is written along a strided axis: the
+  // scatter accumulates into a permuted copy of the target (accumulator
+  // precision) and `perm_out` restores the target's own layout.
+  std::shared_ptr<DevStage> perm_out;
   std::vector<int> term_slot;   // CTensor of each term, to bind pointers
   int32_t* tables = nullptr;    // owned device allocation
   int64_t* prog = nullptr;      // owned device allocation (program fallback)
@@ -157,6 +166,7 @@ struct Bindings {
   std::vector<void*> stages;  // t_k buffers
   std::vector<void*> dstages; // gradients of t_k (staged backward)
   const void* scratch = nullptr;  // tiled form: the reduce sums read by the finish stage
+  const void* perm = nullptr;     // DevStage::perm_in's copy (TK_PERM)
   bool x_unchanged = false;   // syno_backward_ex(SYNO_BWD_X_UNCHANGED)
   bool w_unchanged = false;   // syno_backward_ex(SYNO_BWD_W_UNCHANGED)
 };

@@ -53,6 +53,7 @@ enum TensorKind : int {
   TK_DSTAGE = 8,  // gradient of intermediate t_k (workspace, accumulator precision)
   TK_SCRATCH = 9, // engine-internal partial sums (accumulator precision)
   TK_SCRATCH_IN = 10, // engine-internal operand in the operator's dtype
+  TK_PERM = 11,       // engine-internal permuted copy of an input (operator's dtype; DevStage::perm_in)
 };
 
 struct CTensor {
