@@ -926,7 +926,7 @@ def main():
                     choices=["resnet18", "resnet34", "cfg1", "qkv", "sweep", "qkv_train"])
     ap.add_argument("--batch", type=int, default=0)
     ap.add_argument("--limit", type=int, default=None, help="sweep: first N corpus candidates only")
-    ap.add_argument("--workers", type=int, default=1, help="sweep: enqueueing threads per GPU (own streams)")
+    ap.add_argument("--workers", type=int, default=4, help="sweep: enqueueing threads per GPU (own streams)")
     ap.add_argument("--impl", default="syno", choices=["syno", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graph", dest="graph", action="store_false", help="eager launches instead of a CUDA graph")

@@ -9,7 +9,8 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libsyno.so")
+# SYNO_LIB_PATH: an alternative build of the same library (A/B measurements)
+LIB_PATH = os.environ.get("SYNO_LIB_PATH") or os.path.join(_HERE, "libsyno.so")
 
 SYNO_OK = 0
 SYNO_E_PARSE = 1

@@ -878,6 +878,10 @@ static void build_tile(const CStage& cs, DevStage* ds, cudaStream_t stream) {
   a.nIb = (int32_t)((NI + a.TI - 1) / a.TI);
   const int64_t budget = 40 * 1024 / 4;  // int32 row entries per chunk
   a.RC = (int32_t)std::max<int64_t>(8, std::min<int64_t>({k.R, budget / ((int64_t)a.n_rt * a.TF) - 1, 1024}));
+  // the rows' pitch (RC + 1) must be odd: with lanes along F a warp reads 32
+  // rows at one reduce index, and an even pitch such as 320 put all 32 reads
+  // in one shared-memory bank (ncu: ~31 conflicts per load)
+  if (a.RC % 2 == 1 && a.RC > 8) a.RC -= 1;
   info->ctas = (int64_t)a.nIb * ((NF + a.TF - 1) / a.TF);
   const int64_t want = 148 * 4;
   int64_t S = std::max<int64_t>(1, (want + info->ctas - 1) / info->ctas);
@@ -1614,6 +1618,23 @@ __global__ void __launch_bounds__(256) stage_tile_kernel(const __grid_constant__
   const int64_t r0 = (int64_t)blockIdx.y * S.r_chunk;
   const int64_t r1 = min(S.R, r0 + S.r_chunk);
   const int pitch = A.RC + 1;
+  // per-thread view of the loaded terms, hoisted out of the reduce loop:
+  // base pointer (term pointer + the thread's offset), dtype and validity
+  const void* tp[NT];
+  int tk[NT];
+  bool any_off = false;
+#pragma unroll
+  for (int k = 0; k < NT; ++k) {
+    tp[k] = nullptr;
+    tk[k] = 2;
+    if (k < n_ld) {
+      const KTerm& T = S.terms[A.rterm[k]];
+      tk[k] = T.kind;
+      any_off = any_off || !aok[k];
+      if (T.kind == 0) tp[k] = static_cast<const TI*>(T.ptr) + base[k];
+      else if (T.kind == 1) tp[k] = static_cast<const TA*>(T.ptr) + base[k];
+    }
+  }
   TA acc = 0;
   for (int64_t c0 = r0; c0 < r1; c0 += A.RC) {
     const int rc = (int)min((int64_t)A.RC, r1 - c0);
@@ -1655,7 +1676,7 @@ __global__ void __launch_bounds__(256) stage_tile_kernel(const __grid_constant__
       srow[(k * A.TF + fl) * pitch + rl] = v;
     }
     __syncthreads();
-    if (live && tok) {
+    if (live && tok && !any_off) {
       for (int rl = tr; rl < rc; rl += A.TR) {
         TA prod = SCATTER ? pre : (TA)1;
         bool ok = true;
@@ -1663,9 +1684,9 @@ __global__ void __launch_bounds__(256) stage_tile_kernel(const __grid_constant__
         for (int k = 0; k < NT; ++k) {
           if (k < n_ld && ok) {
             const int32_t o = srow[(k * A.TF + tf) * pitch + rl];
-            const KTerm& T = S.terms[A.rterm[k]];
-            if (o < 0 || !aok[k]) ok = false;
-            else if (T.kind != 2) prod *= load_term<TI, TA>(T, base[k] + o);
+            if (o < 0) ok = false;
+            else if (tk[k] == 0) prod *= (TA)cvt(__ldg(static_cast<const TI*>(tp[k]) + o));
+            else if (tk[k] == 1) prod *= static_cast<const TA*>(tp[k])[o];
           }
         }
         if (SCATTER) {
