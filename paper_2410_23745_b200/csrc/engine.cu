@@ -1264,15 +1264,20 @@ __device__ __forceinline__ int fx_shift(const KStage& S) {
   return max(-1000, min(1000, top - e));
 }
 
+// The unit 2^sh as a double, computed once per thread: multiplying by an
+// exact power of two is the same rounding as ldexp (a library call per
+// contribution that dominated the scatter's instruction count).
+__device__ __forceinline__ double fx_unit(int sh) { return ldexp(1.0, sh); }
+
 template <typename TA>
-__device__ __forceinline__ void fx_add(unsigned long long* fx, int64_t off, double v, int sh) {
-  const double x = rint(ldexp(v, sh));
+__device__ __forceinline__ void fx_add(unsigned long long* fx, int64_t off, double v, double unit) {
   if (!FxWide<TA>::value) {
-    atomicAdd(fx + off, (unsigned long long)__double2ll_rn(x));
+    atomicAdd(fx + off, (unsigned long long)__double2ll_rn(v * unit));  // round to nearest, as rint
     return;
   }
-  const double hd = floor(ldexp(x, -64));
-  const unsigned long long lo = __double2ull_rn(x - ldexp(hd, 64));  // exact, in [0, 2^64)
+  const double x = rint(v * unit);
+  const double hd = floor(x * 0x1p-64);
+  const unsigned long long lo = __double2ull_rn(x - hd * 0x1p64);  // exact, in [0, 2^64)
   const long long hi = __double2ll_rn(hd);
   if (lo) {
     const unsigned long long old = atomicAdd(fx + 2 * off, lo);
@@ -1362,7 +1367,7 @@ __global__ void __launch_bounds__(256, NT <= 2 ? 4 : 2) stage_kernel(const __gri
   int32_t tia[MAXMIX];
   if (SCATTER) term_prep(S.target, S.n_axes, av, &tbase, &tok, tia);
   const TA scale = (TA)S.scale;
-  const int sh = SCATTER ? fx_shift<TA>(S) : 0;
+  const double sh = SCATTER ? fx_unit(fx_shift<TA>(S)) : 1.0;
   TA acc = 0;
   for (int64_t r = r0; r < r1; ++r) {
     TA prod = 1;
@@ -1422,7 +1427,7 @@ __global__ void __launch_bounds__(128) stage_prog_kernel(const __grid_constant__
     }
   }
   const TA scale = (TA)S.scale;
-  const int sh = SCATTER ? fx_shift<TA>(S) : 0;
+  const double sh = SCATTER ? fx_unit(fx_shift<TA>(S)) : 1.0;
   TA acc = 0;
   for (int64_t r = r0; r < r1; ++r) {
     int64_t rem = r;
@@ -1601,7 +1606,7 @@ __global__ void __launch_bounds__(256) stage_tile_kernel(const __grid_constant__
   int64_t tbase = 0;
   bool tok = true;
   TA pre = (TA)S.scale;
-  int sh = 0;
+  double sh = 1.0;
   if (SCATTER) {
     int32_t ia[MAXMIX];
     term_prep(S.target, S.n_axes, av, &tbase, &tok, ia);
@@ -1613,7 +1618,7 @@ __global__ void __launch_bounds__(256) stage_tile_kernel(const __grid_constant__
       if (!ok0) tok = false;
       else if (T.kind != 2) pre *= load_term<TI, TA>(T, b0);
     }
-    sh = fx_shift<TA>(S);
+    sh = fx_unit(fx_shift<TA>(S));
   }
   const int64_t r0 = (int64_t)blockIdx.y * S.r_chunk;
   const int64_t r1 = min(S.R, r0 + S.r_chunk);
@@ -1636,11 +1641,60 @@ __global__ void __launch_bounds__(256) stage_tile_kernel(const __grid_constant__
     }
   }
   TA acc = 0;
+  // per (row term, F combination): the mixed tables' F-digit offsets, decoded
+  // once per CTA (the row loop then needs no divisions by runtime extents)
+  __shared__ int32_t fofs[MAXT][MAXMIX][32];
+  const bool fofs_ok = A.TF <= 32;
+  if (fofs_ok) {
+    for (int e = tid; e < A.n_rt * A.TF; e += blockDim.x) {
+      const int fl = e % A.TF, k = e / A.TF;
+      const KTerm& T = A.rterm[k] < 0 ? S.target : S.terms[A.rterm[k]];
+      int32_t fd[MAXA];
+      int rem = min(fb * A.TF + fl, A.NF - 1);
+      for (int q = A.nF - 1; q >= 0; --q) {
+        fd[q] = rem % A.fext[q];
+        rem /= A.fext[q];
+      }
+      for (int m = 0; m < MAXMIX; ++m) {
+        int32_t idx = 0;
+        if (m < T.n_mix)
+          for (int q = 0; q < A.nF; ++q) idx += T.mtab_s[m][A.faxis[q]] * fd[q];
+        fofs[k][m][fl] = idx;
+      }
+    }
+  }
   for (int64_t c0 = r0; c0 < r1; c0 += A.RC) {
     const int rc = (int)min((int64_t)A.RC, r1 - c0);
     __syncthreads();
-    const int items = A.n_rt * A.TF * rc;
-    for (int it = tid; it < items; it += blockDim.x) {
+    if (fofs_ok && rc >= 64) {
+      // row-major: one (term, F) row at a time, lanes along the reduce index
+      for (int row = 0; row < A.n_rt * A.TF; ++row) {
+        const int k = row / A.TF, fl = row - k * A.TF;
+        const KTerm& T = A.rterm[k] < 0 ? S.target : S.terms[A.rterm[k]];
+        const bool fin = fb * A.TF + fl < A.NF;
+        for (int rl = tid; rl < rc; rl += blockDim.x) {
+          int32_t v = -1;
+          if (fin) {
+            const int64_t r = c0 + rl;
+            bool ok = true;
+            int32_t o = 0;
+            if (T.rtab) {
+              const int32_t x = __ldg(T.rtab + r);
+              ok = x >= 0;
+              o = x;
+            }
+            for (int m = 0; m < T.n_mix && ok; ++m) {
+              const int32_t x = __ldg(T.mtab[m] + __ldg(T.mri[m] + r) + fofs[k][m][fl]);
+              ok = x >= 0;
+              o += x;
+            }
+            v = ok ? o : -1;
+          }
+          srow[row * pitch + rl] = v;
+        }
+      }
+    } else
+    for (int it = tid; it < A.n_rt * A.TF * rc; it += blockDim.x) {
       const int rl = it % rc;
       const int rest = it / rc;
       const int fl = rest % A.TF, k = rest / A.TF;
