@@ -874,6 +874,11 @@ static void build_tile(const CStage& cs, DevStage* ds, cudaStream_t stream) {
     a.TI = (int32_t)std::min<int64_t>(NI, 256);
     a.TF = (int32_t)std::min<int64_t>(NF, 256 / a.TI);
   }
+  // a gather whose rows no I axis shares (TI = 1: every row entry serves one
+  // product) gains nothing from staging rows: the per-thread / block forms
+  // compute the same offsets without the shared-memory round trip
+  static const bool tile_ti1 = getenv("SYNO_TILE_TI1") != nullptr;  // A/B switch
+  if (!scatter && a.TI == 1 && !tile_ti1) return;
   a.TR = (int32_t)std::max<int64_t>(1, std::min<int64_t>({256 / (a.TI * a.TF), 64, k.R}));
   a.nIb = (int32_t)((NI + a.TI - 1) / a.TI);
   const int64_t budget = 40 * 1024 / 4;  // int32 row entries per chunk
