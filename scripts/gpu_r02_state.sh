@@ -1,6 +1,6 @@
 #!/bin/bash
 # Round-2 state capture: smoke, GPU tests, every bench workload, reference arm, ncu launch list.
-OUT=gpurun_out/r02_state
+OUT=gpurun_out/${1:-r02_state}
 mkdir -p $OUT
 nvidia-smi -L > $OUT/gpu.txt
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke.log 2>&1; echo "smoke rc=$?" >> $OUT/smoke.log
@@ -13,4 +13,4 @@ timeout 600 python bench.py --workload qkv_train --no-cpu-baseline > $OUT/bench_
 timeout 600 python bench.py --impl reference > $OUT/bench_reference.log 2>&1
 #timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv --log-file $OUT/launches_resnet18.csv \
 #  python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-graph > $OUT/ncu_bench.log 2>&1
-#timeout 1800 python -m pytest tests -m gpu -q > $OUT/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> $OUT/pytest_gpu.log
+timeout 1800 python -m pytest tests -m gpu -q > $OUT/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> $OUT/pytest_gpu.log
