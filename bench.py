@@ -203,6 +203,8 @@ def build_layers(name, batch):
         return [WL.cfg1_conv(batch or 8)]
     if name == "qkv":
         return [WL.qkv(batch or 16)]
+    if name == "qkv_variants":
+        return WL.qkv_variants(batch or 16)
     raise ValueError(name)
 
 
@@ -223,7 +225,7 @@ def layer_work(h, esize):
 def unit_of(workload):
     """Throughput unit of a layer workload: one batch element (an image, or a
     T-token sequence for the QKV projection)."""
-    return "sequences/s" if workload == "qkv" else "images/s"
+    return "sequences/s" if workload.startswith("qkv") else "images/s"
 
 
 def run_layers(args, rank, world, device, peaks):
@@ -240,8 +242,11 @@ def run_layers(args, rank, world, device, peaks):
     layers = build_layers(args.workload, args.batch)
     gen = torch.Generator(device="cpu").manual_seed(1234 + rank)
     state = []
+    # sampled variants run as the search evaluates them: the rfactored nest
+    # (interpret(staged=True)), backward through the stages where it applies
+    staged = args.workload == "qkv_variants"
     for L in layers:
-        h = P.handle_for(L.graph)
+        h = P.handle_for(L.graph, None, staged)
         x = torch.randn(h.x_shape, generator=gen).to(device=device, dtype=dtype)
         ws = [(torch.randn(s, generator=gen) / math.sqrt(max(1, math.prod(s[1:])))).to(device=device, dtype=dtype)
               for s in h.w_shapes]
@@ -778,29 +783,33 @@ def cpu_sample_spec(args):
     extrapolated to the whole step by the layers' FLOP share (the reference's
     batch loop is serial and per-element identical, codegen.py:626-630)."""
     cf = _configs()
-    batch = args.batch or {"resnet18": 128, "resnet34": 256, "cfg1": 8, "qkv": 16}[args.workload]
+    batch = args.batch or {"resnet18": 128, "resnet34": 256, "cfg1": 8, "qkv": 16, "qkv_variants": 16}[args.workload]
     if args.workload == "qkv":
         rows = [("qkv", "qkv", None, None, None)]
+    elif args.workload == "qkv_variants":
+        rows = [(f"qkv_v{i}", op, None, None, None) for i, op in enumerate(cf.qkv_variant_ops())]
     elif args.workload == "cfg1":
         rows = [("cfg1_conv3x3", "conv3x3", 64, 64, 32)]
     else:
         rows = cf.resnet18_table() if args.workload == "resnet18" else cf.resnet34_table()
-    pick = {"resnet18": "l1b0c2", "resnet34": "l2b1c2", "cfg1": "cfg1_conv3x3", "qkv": "qkv"}[args.workload]
+    pick = {"resnet18": "l1b0c2", "resnet34": "l2b1c2", "cfg1": "cfg1_conv3x3", "qkv": "qkv",
+            "qkv_variants": "qkv_v0"}[args.workload]
     fwd_only = args.workload == "cfg1"
     mult = 1 if fwd_only else 3
     per_image = 0.0
     sample = None
     for name, op, ci, co, h in rows:
-        if op == "qkv":
+        steps = cf.STEPS.get(op, op)  # a sampled variant carries its step string
+        if op == "qkv" or ci is None:
             full = cf.qkv_spec_args(1)
             one = cf.qkv_spec_args(1, t=128)  # the full-grid interpreter needs ~58 GB per T=1024 element
         else:
             full = one = cf.conv_spec_args(name, op, ci, co, h, 1)
-        f_full, _ = _ref_flops(full, cf.STEPS[op])
+        f_full, _ = _ref_flops(full, steps)
         per_image += mult * f_full
         if name == pick:
-            f_one, _ = _ref_flops(one, cf.STEPS[op])
-            sample = (one, cf.STEPS[op], f_one)
+            f_one, _ = _ref_flops(one, steps)
+            sample = (one, steps, f_one)
     one, steps, f_one = sample
     elem = "sequence" if args.workload == "qkv" else "image"
     desc = (f"1 {elem} of layer {pick} through the unmodified reference (opsmith from baseline/_ref): "
@@ -900,13 +909,15 @@ def workload_config(args):
         "resnet34": "cfg3: ResNet-34 ImageNet-shape layers as synthesized operators, fwd+bwd",
         "cfg1": "cfg1: conv3x3 in Syno primitives, N=8 C=64 H=W=32, forward",
         "qkv": "cfg4 layer: GPT-2 small QKV projection as a synthesized operator, fwd+bwd",
+        "qkv_variants": ("cfg4 variants: the dense QKV projection and 15 operators the reference sampler drew on "
+                         "its spec (tests/golden/corpus_qkv.txt), each fwd+bwd, staged handles"),
         "qkv_train": "cfg4: proxy training, 12 GPT-2-small QKV synthesized operators, DP with NCCL allreduce",
         "sweep": "cfg5: 1024 sampled primitive graphs (conv64 spec, N=8; the in-budget ones executed), sharded across GPUs",
     }[args.workload]
-    batch = args.batch or {"resnet18": 128, "resnet34": 256, "cfg1": 8, "qkv": 16, "qkv_train": 16,
-                           "sweep": SWEEP_BATCH}[args.workload]
+    batch = args.batch or {"resnet18": 128, "resnet34": 256, "cfg1": 8, "qkv": 16, "qkv_variants": 16,
+                           "qkv_train": 16, "sweep": SWEEP_BATCH}[args.workload]
     cfg = {"workload": desc, "batch_per_gpu": batch, "inputs": "synthetic N(0,1), resident in HBM"}
-    if args.workload in ("resnet18", "resnet34", "cfg1", "qkv"):
+    if args.workload in ("resnet18", "resnet34", "cfg1", "qkv", "qkv_variants"):
         cfg["l2"] = "flushed between timed steps (256 MB write)"
         cfg["parallelism"] = "replicas (no data-path collective)"
     elif args.workload == "sweep":
@@ -923,7 +934,7 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--workload", default="resnet18",
-                    choices=["resnet18", "resnet34", "cfg1", "qkv", "sweep", "qkv_train"])
+                    choices=["resnet18", "resnet34", "cfg1", "qkv", "qkv_variants", "sweep", "qkv_train"])
     ap.add_argument("--batch", type=int, default=0)
     ap.add_argument("--limit", type=int, default=None, help="sweep: first N corpus candidates only")
     ap.add_argument("--workers", type=int, default=4, help="sweep: enqueueing threads per GPU (own streams)")

@@ -84,6 +84,17 @@ CORPUS_PATH = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__fil
 CORPUS_REF = {"C_out": 64, "C_in": 64, "H": 32, "W": 32, "K": 3, "s": 2}
 
 
+QKV_CORPUS_PATH = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests", "golden",
+                               "corpus_qkv.txt")
+
+
+def qkv_variant_ops():
+    """cfg4's sampled variants of the QKV projection: the dense
+    baseline first, then operators the reference sampler drew on the QKV spec
+    within 2x its FLOPs and parameters (tests/golden/make_qkv_corpus.py)."""
+    return [ln.strip() for ln in open(QKV_CORPUS_PATH) if ln.strip()]
+
+
 def corpus_ops(limit=None):
     ops = [ln.strip() for ln in open(CORPUS_PATH) if ln.strip()]
     return ops[:limit] if limit is not None else ops

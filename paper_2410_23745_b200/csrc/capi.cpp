@@ -238,7 +238,7 @@ int syno_query(syno_op_t op, syno_info* info) {
     for (auto e : p.unstaged.axis_ext) g *= (double)e;
     for (auto e : op->unstaged.stages[0].reduces) g *= (double)e.extent;
     info->index_grid = (int64_t)g;
-    info->tc_path = p.nest_only ? 0 : tc_matches(p) ? 1 : gg_matches(p) ? 2 : 0;
+    info->tc_path = p.nest_only || staged_cheaper(p) ? 0 : tc_matches(p) ? 1 : gg_matches(p) ? 2 : 0;
   });
 }
 

@@ -1143,6 +1143,12 @@ static void ensure_backward(const Plan& plan, DevPlan& dp, cudaStream_t stream) 
 
 static std::shared_ptr<GatherGemm> gg_build(const Plan& plan, cudaStream_t stream);
 
+bool staged_cheaper(const Plan& plan) {
+  static const bool tc_unstaged = getenv("SYNO_TC_UNSTAGED") != nullptr;
+  return !tc_unstaged && plan.forward.size() > 1 && !plan.bwd_staged.empty() &&
+         (double)plan.flops_staged * 4.0 < (double)plan.flops_unstaged;
+}
+
 DevPlan* build_dev_plan(const Plan& plan, cudaStream_t stream) {
   auto dp = std::make_unique<DevPlan>();
   cuda_check(cudaGetDevice(&dp->device), "cudaGetDevice");
@@ -1158,7 +1164,12 @@ DevPlan* build_dev_plan(const Plan& plan, cudaStream_t stream) {
       }
     }
   }
-  if (!plan.nest_only) {
+  // a staged (rfactored) nest with a staged backward that is much cheaper
+  // than the unstaged contraction stays on the stage engine: the tensor-core
+  // paths compute the unstaged form (e.g. a sampled QKV variant whose staged
+  // forward is 0.1 GFLOP against 58 for the dense GEMM).  SYNO_TC_UNSTAGED=1
+  // keeps the tensor-core paths for them (A/B switch).
+  if (!plan.nest_only && !staged_cheaper(plan)) {
     dp->tc = tc_build(plan, stream);
     if (!dp->tc) dp->gg = gg_build(plan, stream);
   }

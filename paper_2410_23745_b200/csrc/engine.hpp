@@ -179,6 +179,9 @@ void run_stage(DType dt, const DevStage& ds, const Bindings& b, void* out, bool 
 // Host-only: does the operator take the gathered-GEMM tensor-core path
 // (engine.cu GatherGemm) for fp32 / bf16?
 bool gg_matches(const Plan& plan);
+// the staged nest (forward and backward) is far cheaper than the unstaged
+// contraction the tensor-core paths compute: stay on the stage engine
+bool staged_cheaper(const Plan& plan);
 
 // Builds tables on `stream` (K1) for every stage of the plan.
 DevPlan* build_dev_plan(const Plan& plan, cudaStream_t stream);

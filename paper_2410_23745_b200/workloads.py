@@ -17,7 +17,7 @@ from typing import Optional
 
 from .configs import (  # noqa: F401  (re-exported names)
     CONV3X3, CONV3X3_S2, CORPUS_PATH, POINTWISE, QKV, SEP_SHARED, STEPS, SUMPOOL3X3, conv_spec_args,
-    corpus_ops, corpus_spec_args, qkv_spec_args, resnet18_table, resnet34_table,
+    corpus_ops, corpus_spec_args, qkv_spec_args, qkv_variant_ops, resnet18_table, resnet34_table,
 )
 from .pgraph import PGraph, build_spec, parse_steps
 
@@ -31,7 +31,7 @@ class Layer:
 
     @property
     def steps(self) -> str:
-        return STEPS[self.op]
+        return STEPS.get(self.op, self.op)
 
 
 def conv_layer(name: str, op: str, c_in: int, c_out: int, h: int, batch: int) -> Layer:
@@ -55,6 +55,14 @@ def cfg1_conv(batch: int = 8) -> Layer:
 def qkv(batch: int = 16, t: int = 1024, e: int = 768, e3: int = 2304) -> Layer:
     args = qkv_spec_args(batch, t, e, e3)
     return Layer("qkv", "qkv", parse_steps(QKV, build_spec(*args)), args[3])
+
+
+def qkv_variants(batch: int = 16, t: int = 1024) -> list:
+    """cfg4: the dense QKV projection and its sampled variants (one Layer each,
+    op = the step string)."""
+    args = qkv_spec_args(batch, t)
+    spec = build_spec(*args)
+    return [Layer(f"qkv_v{i}", op, parse_steps(op, spec), args[3]) for i, op in enumerate(qkv_variant_ops())]
 
 
 def corpus(batch: int = 8, limit: Optional[int] = None) -> list:
