@@ -505,14 +505,125 @@ static void build_kterm(const CStage& s, const CTerm& t, KTerm* k, std::vector<T
   }
 }
 
+// Linear-form compression of a mixed table.  A coordinate such as
+//     (L3 + ((L1 + L2) + 640) // 768) - 3          (L1, L2 axes, L3 a reduce)
+// reads its axis loops only through one linear form u = L1 + L2 + 640; its
+// table then needs one entry per (u, reduce) -- 3327 x 1024 -- instead of
+// one per (L1, L2, reduce) -- 1024 x 2304 x 1024, over the table budget.  The
+// table is built over a virtual loop V = u - u_min (loop id nloops()), and
+// the axes index it with strides c_a * stride(V).
+struct LinForm {
+  std::vector<std::pair<int, int64_t>> coef;  // (axis loop, coefficient of u)
+  int64_t k0 = 0, umin = 0, ext = 0;
+  CE expr;  // the coordinate with u replaced by (V + umin)
+};
+
+static bool linear_node(const CE& e) {
+  switch (e->op) {
+    case COp::Loop:
+    case COp::Const: return true;
+    case COp::Add:
+    case COp::Sub: return linear_node(e->lhs) && linear_node(e->rhs);
+    case COp::Mul:
+      return (e->lhs->op == COp::Const && linear_node(e->rhs)) || (e->rhs->op == COp::Const && linear_node(e->lhs));
+    default: return false;
+  }
+}
+
+static void all_nodes(const CE& e, std::vector<CE>* out) {
+  out->push_back(e);
+  if (e->lhs) all_nodes(e->lhs, out);
+  if (e->rhs) all_nodes(e->rhs, out);
+}
+
+static CE replace_node(const CE& e, const std::string& key, const CE& repl) {
+  if (c_render(e) == key) return repl;
+  if (!e->lhs) return e;
+  return c_bin(e->op, replace_node(e->lhs, key, repl), replace_node(e->rhs, key, repl));
+}
+
+static bool linear_form(const CStage& s, const CE& c, int A, LinForm* f) {
+  static const bool off = getenv("SYNO_NO_LINFORM") != nullptr;  // A/B switch
+  if (off) return false;
+  const int L = s.nloops();
+  std::vector<int> deps, axd;
+  c_loops(c, &deps);
+  for (int l : deps)
+    if (l < A) axd.push_back(l);
+  if (axd.size() < 2) return false;
+  std::vector<CE> nodes;
+  all_nodes(c, &nodes);
+  std::sort(nodes.begin(), nodes.end(),
+            [](const CE& a, const CE& b) { return c_render(a).size() > c_render(b).size(); });
+  for (const CE& n : nodes) {
+    std::vector<int> nl;
+    c_loops(n, &nl);
+    if (nl != axd || !linear_node(n)) continue;
+    const std::string key = c_render(n);
+    std::vector<int> rest;
+    c_loops(replace_node(c, key, c_const(0)), &rest);
+    bool clean = true;
+    for (int l : rest) clean = clean && l >= A;
+    if (!clean) continue;
+    std::vector<int64_t> v(L + 1, 0);
+    f->k0 = c_eval(n, v.data());
+    f->coef.clear();
+    int64_t lo = f->k0, hi = f->k0;
+    for (int a : axd) {
+      v.assign(L + 1, 0);
+      v[a] = 1;
+      const int64_t ca = c_eval(n, v.data()) - f->k0;
+      f->coef.push_back({a, ca});
+      lo += std::min<int64_t>(0, ca * (s.ext(a) - 1));
+      hi += std::max<int64_t>(0, ca * (s.ext(a) - 1));
+    }
+    // linear check at the corners of the axis ranges
+    v.assign(L + 1, 0);
+    int64_t want = f->k0;
+    for (auto& p : f->coef) {
+      v[p.first] = s.ext(p.first) - 1;
+      want += p.second * (s.ext(p.first) - 1);
+    }
+    if (c_eval(n, v.data()) != want) continue;
+    f->umin = lo;
+    f->ext = hi - lo + 1;
+    f->expr = replace_node(c, key, c_bin(COp::Add, c_loop(L), c_const(lo)));
+    return true;
+  }
+  return false;
+}
+
 static void add_fix_table(const CStage& s, TabSpec&& tab, KTerm* k, bool axis_only, int A,
                           std::vector<TabSpec>* tabs, std::vector<Fixup>* fix) {
-  const std::vector<int> deps = tab.deps;
+  std::vector<int> deps = tab.deps;
   tab.dep_ext.clear();
   tab.count = 1;
   for (int l : deps) {
     tab.dep_ext.push_back(s.ext(l));
     tab.count *= s.ext(l);
+  }
+  LinForm lf;
+  bool lin = false;
+  // tables of 2^24 entries or more (SYNO_LINFORM_MIN lowers it for the parity tests)
+  static const double lin_min = getenv("SYNO_LINFORM_MIN") ? atof(getenv("SYNO_LINFORM_MIN")) : 16777216.0;
+  if (!axis_only && (double)tab.count >= lin_min && tab.progs.size() == 1 && linear_form(s, tab.progs[0].e, A, &lf)) {
+    std::vector<int> d2{s.nloops()};
+    std::vector<int64_t> e2{lf.ext};
+    int64_t n2 = lf.ext;
+    for (int l : deps)
+      if (l >= A) {
+        d2.push_back(l);
+        e2.push_back(s.ext(l));
+        n2 *= s.ext(l);
+      }
+    if (n2 * 4 <= tab.count || lin_min < 16777216.0) {
+      lin = true;
+      deps = d2;
+      tab.deps = d2;
+      tab.dep_ext = e2;
+      tab.count = n2;
+      tab.progs[0].e = lf.expr;
+    }
   }
   if (tab.count >= table_limit()) fail(SYNO_E_UNSUPPORTED, "index table too large");
   auto tstr = row_major_strides(tab.dep_ext);
@@ -529,8 +640,15 @@ static void add_fix_table(const CStage& s, TabSpec&& tab, KTerm* k, bool axis_on
   int m = k->n_mix++;
   CE ri = c_const(0);
   for (size_t q = 0; q < deps.size(); ++q) {
-    if (deps[q] < A) k->mtab_s[m][deps[q]] = (int32_t)tstr[q];
-    else ri = c_bin(COp::Add, ri, c_bin(COp::Mul, c_loop(deps[q]), c_const(tstr[q])));
+    if (lin && q == 0) {
+      // the virtual loop V = u - umin: axes index it through u's coefficients
+      for (auto& p : lf.coef) k->mtab_s[m][p.first] += (int32_t)(p.second * tstr[0]);
+      ri = c_bin(COp::Add, ri, c_const((lf.k0 - lf.umin) * tstr[0]));
+    } else if (deps[q] < A) {
+      k->mtab_s[m][deps[q]] = (int32_t)tstr[q];
+    } else {
+      ri = c_bin(COp::Add, ri, c_bin(COp::Mul, c_loop(deps[q]), c_const(tstr[q])));
+    }
   }
   fix->push_back({&k->mtab[m], tid});
   std::vector<int> all_red;
@@ -1041,6 +1159,8 @@ static void build_dev_stage_impl(const CStage& cs_in, DevStage* ds, cudaStream_t
   } catch (const Error& e) {
     if (e.code != SYNO_E_UNSUPPORTED) throw;
     // table budget exceeded: evaluate the coordinate programs on the fly
+    static const bool log = getenv("SYNO_PROG_LOG") != nullptr;
+    if (log) fprintf(stderr, "[prog] %s (%s)\n", cs.describe().c_str(), e.what());
     ds->dead = cs.dead;
     build_prog_stage(cs, ds);
     return;

@@ -1,4 +1,5 @@
-"""Lane-contiguous permuted layouts (engine.cu lane_contiguous_layout).
+"""Lane-contiguous permuted layouts (engine.cu lane_contiguous_layout) and
+linear-form table compression (engine.cu linear_form).
 
 Heavy gather stages read a copy of their lead input with the unit-stride
 dimension innermost, and heavy scatters accumulate into a permuted target
@@ -52,6 +53,18 @@ for staged in (False, True):
         checked += 1
 print("checked", checked)
 """
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("start", [0, 1])
+def test_forced_linear_form_tables_match_oracle(cuda, start):
+    """Every mixed table whose coordinate reads its axes through one linear
+    form is built over that form (threshold forced to 1)."""
+    env = dict(os.environ, SYNO_LINFORM_MIN="1")
+    code = CHILD.format(root=ROOT, tests=os.path.join(ROOT, "tests"), start=start, step=2)
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stderr[-3000:]
+    assert "checked" in r.stdout
 
 
 @pytest.mark.gpu
