@@ -454,7 +454,7 @@ static void build_kterm(const CStage& s, const CTerm& t, KTerm* k, std::vector<T
   memset(k, 0, sizeof(KTerm));
   const int A = (int)s.axis_ext.size();
   const int L = s.nloops();
-  k->kind = t.t.kind == TK_PHANTOM ? 2 : (t.t.kind == TK_STAGE || t.t.kind == TK_DSTAGE || t.t.kind == TK_SCRATCH ? 1 : 0);
+  k->kind = t.t.kind == TK_PHANTOM ? 2 : (t.t.kind == TK_STAGE || t.t.kind == TK_DSTAGE || t.t.kind == TK_SCRATCH || t.t.kind == TK_PRE ? 1 : 0);
   if (t.t.numel() >= (int64_t)INT32_MAX) fail(SYNO_E_UNSUPPORTED, "tensor has 2^31 or more elements");
   auto strides = row_major_strides(t.t.extents);
   if (t.coords.size() != t.t.extents.size()) fail(SYNO_E_SHAPE, "access rank does not match tensor rank");
@@ -678,6 +678,8 @@ void release_dev_stage(DevStage& ds) {
   ds.perm_in.reset();
   if (ds.perm_out) release_dev_stage(*ds.perm_out);
   ds.perm_out.reset();
+  if (ds.gpre) release_dev_stage(*ds.gpre);
+  ds.gpre.reset();
   if (ds.tables) cudaFreeAsync(ds.tables, nullptr);
   ds.tables = nullptr;
   if (ds.prog) cudaFree(ds.prog);
@@ -733,7 +735,7 @@ static void build_prog_stage(const CStage& cs, DevStage* ds) {
     KTerm& kt = k.terms[t];
     memset(&kt, 0, sizeof(KTerm));
     const int tk = cs.terms[t].t.kind;
-    kt.kind = tk == TK_PHANTOM ? 2 : (tk == TK_STAGE || tk == TK_DSTAGE || tk == TK_SCRATCH ? 1 : 0);
+    kt.kind = tk == TK_PHANTOM ? 2 : (tk == TK_STAGE || tk == TK_DSTAGE || tk == TK_SCRATCH || tk == TK_PRE ? 1 : 0);
   }
   memset(&k.target, 0, sizeof(KTerm));
 }
@@ -1122,8 +1124,106 @@ static bool split_scatter(const CStage& cs, CStage* pre, CStage* main) {
   return true;
 }
 
+// Gather pre-reduction (the reference's rfactor, codegen.py:433-508, applied
+// to any gather stage -- gradient stages included): with M a set of terms
+// and Q the reduce loops only terms of M read,
+//     out[A] = scale * sum_{R \ Q} prod_{t not in M} t * P[loops(M) \ Q],
+//     P = sum_Q prod_{t in M} t
+// which visits |loops(M) \ Q| * |Q| + |A| * |R \ Q| points instead of
+// |A| * |R| (e.g. a weight gradient whose upstream alone reads the output
+// channels: 29 G -> 50 M).  Taken when it saves 4x or more.
+static bool split_gather(const CStage& cs, CStage* pre, CStage* main) {
+  static const bool off = getenv("SYNO_NO_GATHER_PREREDUCE") != nullptr;  // A/B switch
+  const int A = (int)cs.axis_ext.size(), L = cs.nloops();
+  const int nT = (int)cs.terms.size();
+  if (off || cs.scatter || nT < 2 || nT > 30 || L == A) return false;
+  // one factored level per stage (a main stage already reads TK_PRE; its own
+  // pre stage may factor again)
+  for (auto& t : cs.terms)
+    if (t.t.kind == TK_PRE) return false;
+  std::vector<uint32_t> reads(L, 0);  // terms reading each loop
+  for (int t = 0; t < nT; ++t)
+    for (auto& c : cs.terms[t].coords) {
+      std::vector<int> d;
+      c_loops(c, &d);
+      for (int l : d) reads[l] |= 1u << t;
+    }
+  const uint32_t all = (1u << nT) - 1;
+  double grid = 1;
+  for (int l = 0; l < L; ++l) grid *= (double)cs.ext(l);
+  double best = grid / 4.0;
+  uint32_t bestM = 0;
+  for (int q = A; q < L; ++q) {
+    const uint32_t M = reads[q];
+    if (!M || M == all) continue;
+    double pre_pts = 1, main_pts = 1, psize = 1;
+    for (int l = 0; l < L; ++l) {
+      const bool inQ = l >= A && reads[l] && (reads[l] & ~M) == 0;
+      const bool readM = (reads[l] & M) != 0;
+      if (inQ) pre_pts *= (double)cs.ext(l);
+      else {
+        main_pts *= (double)cs.ext(l);
+        if (readM) psize *= (double)cs.ext(l);
+      }
+    }
+    const double cost = psize * pre_pts + main_pts;
+    if (cost < best && psize < (double)(1 << 28)) {
+      best = cost;
+      bestM = M;
+    }
+  }
+  if (!bestM) return false;
+  std::vector<int> Ploops, Q, Rrest;
+  for (int l = 0; l < L; ++l) {
+    const bool inQ = l >= A && reads[l] && (reads[l] & ~bestM) == 0;
+    if (inQ) Q.push_back(l);
+    else {
+      if (reads[l] & bestM) Ploops.push_back(l);
+      if (l >= A) Rrest.push_back(l);
+    }
+  }
+  std::vector<int> pm(L, -1), mm(L, -1);
+  for (size_t i = 0; i < Ploops.size(); ++i) pm[Ploops[i]] = (int)i;
+  for (size_t j = 0; j < Q.size(); ++j) pm[Q[j]] = (int)(Ploops.size() + j);
+  for (int a = 0; a < A; ++a) mm[a] = a;
+  for (size_t j = 0; j < Rrest.size(); ++j) mm[Rrest[j]] = A + (int)j;
+  auto remap_term = [](const CTerm& t, const std::vector<int>& m) {
+    CTerm r = t;
+    for (auto& c : r.coords) c = remap_loops(c, m);
+    return r;
+  };
+  *pre = CStage();
+  for (int l : Ploops) pre->axis_ext.push_back(cs.ext(l));
+  for (int l : Q) pre->red_ext.push_back(cs.ext(l));
+  for (int t = 0; t < nT; ++t)
+    if (bestM >> t & 1) pre->terms.push_back(remap_term(cs.terms[t], pm));
+  pre->out.kind = TK_PRE;
+  pre->out.extents = pre->axis_ext;
+  *main = CStage();
+  main->axis_ext = cs.axis_ext;
+  for (int l : Rrest) main->red_ext.push_back(cs.ext(l));
+  main->out = cs.out;
+  main->scale = cs.scale;
+  main->dead = cs.dead;
+  for (int t = 0; t < nT; ++t)
+    if (!(bestM >> t & 1)) main->terms.push_back(remap_term(cs.terms[t], mm));
+  CTerm P;
+  P.t.kind = TK_PRE;
+  P.t.extents = pre->axis_ext;
+  for (int l : Ploops) P.coords.push_back(c_loop(mm[l]));
+  main->terms.push_back(P);
+  return true;
+}
+
 static void build_dev_stage_impl(const CStage& cs_in, DevStage* ds, cudaStream_t stream, bool allow_tile) {
   CStage pre_cs, main_cs;
+  if (allow_tile && split_gather(cs_in, &pre_cs, &main_cs)) {
+    ds->gpre = std::make_shared<DevStage>();
+    build_dev_stage_impl(pre_cs, ds->gpre.get(), stream, true);
+    ds->gpre_count = pre_cs.out.numel();
+    build_dev_stage_impl(main_cs, ds, stream, true);
+    return;
+  }
   const bool split = allow_tile && split_scatter(cs_in, &pre_cs, &main_cs);
   const CStage& cs = split ? main_cs : cs_in;
   if (split && !pre_cs.terms.empty()) {
@@ -1940,6 +2040,7 @@ static const void* bind_ptr(const CTensor& t, const Bindings& b) {
     case TK_SCRATCH:
     case TK_SCRATCH_IN: return b.scratch;
     case TK_PERM: return b.perm;
+    case TK_PRE: return b.pre;
     default: return nullptr;
   }
 }
@@ -2002,11 +2103,27 @@ static void launch_stage_impl(const DevStage& ds, const Bindings& b_in, void* ou
       if (p) cudaFreeAsync(p, s);
     }
   } perm_free{perm_buf, stream};
+  void* gpre_buf = nullptr;
+  if (ds.gpre) {
+    cuda_check(cudaMallocAsync(&gpre_buf, (size_t)std::max<int64_t>(ds.gpre_count, 1) * sizeof(TA), stream),
+               "alloc factored partial sums");
+    const char* pk = nullptr;
+    launch_stage_impl<TI>(*ds.gpre, b, gpre_buf, true, stream, &pk);
+    b.pre = gpre_buf;
+  }
+  struct PreFree {
+    void* p;
+    cudaStream_t s;
+    ~PreFree() {
+      if (p) cudaFreeAsync(p, s);
+    }
+  } pre_free{gpre_buf, stream};
   KStage k = ds.k;
   for (int t = 0; t < k.n_terms; ++t) {
     k.terms[t].ptr = bind_ptr(ds.cs.terms[t].t, b);
     if (!k.terms[t].ptr && k.terms[t].kind != 2 && !(ds.pre && ds.cs.terms[t].t.kind == TK_SCRATCH))
-      fail(SYNO_E_INVALID, "stage input tensor is not bound");
+      fail(SYNO_E_INVALID, "stage input tensor is not bound (kind " + std::to_string(ds.cs.terms[t].t.kind) +
+                               ", stage " + ds.cs.describe() + ")");
   }
   const int64_t out_bytes = k.out_count * (int64_t)(out_acc ? sizeof(TA) : sizeof(TI));
   if (ds.dead || k.out_count == 0) {

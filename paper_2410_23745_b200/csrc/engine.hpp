@@ -122,6 +122,11 @@ struct DevStage {
   // scatter accumulates into a permuted copy of the target (accumulator
   // precision) and `perm_out` restores the target's own layout.
   std::shared_ptr<DevStage> perm_out;
+  // Factored gather: `gpre` sums the product of the terms that alone read
+  // some reduce loops over those loops (TK_PRE, gpre_count elements); this
+  // stage then reduces the rest (the reference's rfactor, for any stage).
+  std::shared_ptr<DevStage> gpre;
+  int64_t gpre_count = 0;
   std::vector<int> term_slot;   // CTensor of each term, to bind pointers
   int32_t* tables = nullptr;    // owned device allocation
   int64_t* prog = nullptr;      // owned device allocation (program fallback)
@@ -167,6 +172,7 @@ struct Bindings {
   std::vector<void*> dstages; // gradients of t_k (staged backward)
   const void* scratch = nullptr;  // tiled form: the reduce sums read by the finish stage
   const void* perm = nullptr;     // DevStage::perm_in's copy (TK_PERM)
+  const void* pre = nullptr;      // DevStage::gpre's partial sums (TK_PRE)
   bool x_unchanged = false;   // syno_backward_ex(SYNO_BWD_X_UNCHANGED)
   bool w_unchanged = false;   // syno_backward_ex(SYNO_BWD_W_UNCHANGED)
 };

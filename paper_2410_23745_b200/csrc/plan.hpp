@@ -54,6 +54,7 @@ enum TensorKind : int {
   TK_SCRATCH = 9, // engine-internal partial sums (accumulator precision)
   TK_SCRATCH_IN = 10, // engine-internal operand in the operator's dtype
   TK_PERM = 11,       // engine-internal permuted copy of an input (operator's dtype; DevStage::perm_in)
+  TK_PRE = 12,        // engine-internal partial sums of a factored gather (accumulator precision; DevStage::gpre)
 };
 
 struct CTensor {
