@@ -596,7 +596,11 @@ __global__ void __launch_bounds__(THREADS, CFG == 1 ? 2 : 1) tc_gemm_kernel(cons
     tr_n = 0;
   }
 
-  if (warp == 0) {
+  // profiling switches 1024 (MMA warp ignores every barrier) + 2048 (the other
+  // roles do nothing): the bare MMA issue stream over the kernel's tiles
+  const bool bare = (dbg & 1024) && (dbg & 2048);
+  if (bare && warp != 1) {
+  } else if (warp == 0) {
     // ---------------- TMA producer: the whole warp walks the schedule, one
     // elected lane issues (operands stay warp-uniform).
     if (elect_one()) {
@@ -752,14 +756,14 @@ __global__ void __launch_bounds__(THREADS, CFG == 1 ? 2 : 1) tc_gemm_kernel(cons
     const uint32_t sa_u = smem_u32(sa), sb_u = smem_u32(sb);
     const int a_stage_bytes = p.a_stage_bytes, Gr = p.G, n_cb = p.n_cblocks;
     const int kq_last = p.kq_last > 0 ? p.kq_last : BK / 16;
-    if (b_res && blockIdx.x < n_tiles_total) mbar_wait(&b_full[0], 0);  // resident B tiles landed
+    if (b_res && blockIdx.x < n_tiles_total && !(dbg & 1024)) mbar_wait(&b_full[0], 0);  // resident B tiles landed
     TileWalk tw;
     tw.init(p, t_first, t_step);
     for (int t = t_first; t < n_tiles_total; t += t_step, ++tcount, tw.next(p)) {
       const TileInfo ti = tinfo(tw);
       const uint32_t acc = tcount & 1u;
       if (lane == 0) ev(9, (int)tcount, 0);  // MMA warp: next tile decoded
-      mbar_wait(&tempty[acc], ((tcount >> 1) & 1u) ^ 1u);  // epilogue drained this buffer
+      if (!(dbg & 1024)) mbar_wait(&tempty[acc], ((tcount >> 1) & 1u) ^ 1u);  // epilogue drained this buffer
       if (lane == 0) ev(5, (int)tcount, 0);  // MMA warp: accumulator free
       asm volatile("tcgen05.fence::after_thread_sync;");
       const uint32_t dst = tmem + acc * ACC_COLS;
@@ -772,13 +776,13 @@ __global__ void __launch_bounds__(THREADS, CFG == 1 ? 2 : 1) tc_gemm_kernel(cons
           const int w0 = p.chunk_w0[c], w1 = p.chunk_w1[c], pmin = p.chunk_pmin[c];
           for (int cb = ti.cb0; cb < ti.cb1; ++cb) {
             const int nk = cb == n_cb - 1 ? kq_last : BK / 16;
-            mbar_wait(&a_full[ra.s], ra.ph);
+            if (!(dbg & 1024)) mbar_wait(&a_full[ra.s], ra.ph);
             if (lane == 0) ev(3, (int)tcount, c * 64 + cb);  // MMA warp: A halo ready
             const uint32_t a_lo0 = desc_lo(sa_u + (uint32_t)(ra.s * a_stage_bytes)) - (uint32_t)pmin * 8u;
             if (b_res) asm volatile("tcgen05.fence::after_thread_sync;");
             for (int w = w0; w < w1; ++w) {
               if (!b_res) {
-                mbar_wait(&b_full[rb.s], rb.ph);
+                if (!(dbg & 1024)) mbar_wait(&b_full[rb.s], rb.ph);
                 if (lane == 0) ev(4, (int)tcount, w);  // MMA warp: B window ready
                 asm volatile("tcgen05.fence::after_thread_sync;");
               }
@@ -821,8 +825,10 @@ __global__ void __launch_bounds__(THREADS, CFG == 1 ? 2 : 1) tc_gemm_kernel(cons
       } else {
         for (int i = 0; i < (ti.nkb + KM - 1) / KM; ++i) {
           const int as = ra.slot(AST), bs = rb.slot(BSTAGES);
-          mbar_wait(&a_full[as], ra.phase(AST));
-          mbar_wait(&b_full[bs], rb.phase(BSTAGES));
+          if (!(dbg & 1024)) {
+            mbar_wait(&a_full[as], ra.phase(AST));
+            mbar_wait(&b_full[bs], rb.phase(BSTAGES));
+          }
           asm volatile("tcgen05.fence::after_thread_sync;");
           const uint64_t da = sw128_mn_desc(sa + as * p.a_stage_bytes, 8192);
           const uint64_t db = sw128_mn_desc(sb + bs * B_BYTES, 8192);
