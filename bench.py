@@ -928,6 +928,40 @@ def workload_config(args):
     return cfg
 
 
+OTHER_CONFIGS = (("cfg1", 10), ("resnet34", 5), ("qkv", 10), ("sweep", 2))
+
+
+def run_other_configs(args, rank, world, device, peaks):
+    """The default (ResNet-18) run also measures BASELINE.json's other
+    single-GPU configs in the same process, after the headline measurement
+    is complete, so that every config has a number from the driver's own run.
+    Each keeps its own timing rules (warm-up, L2 flush, device events); no
+    CPU baseline here (their `--workload` lines carry one)."""
+    import copy
+    out = {}
+    for name, steps in OTHER_CONFIGS:
+        a = copy.copy(args)
+        a.workload, a.steps, a.batch, a.limit = name, steps, 0, None
+        t0 = time.time()
+        try:
+            r = (run_sweep if name == "sweep" else run_layers)(a, rank, world, device, peaks)
+        except Exception as e:  # recorded, never masks the headline line
+            out[name] = {"error": f"{type(e).__name__}: {e}"[:300]}
+            continue
+        roof = r.get("roofline") or {}
+        e2e = r.get("e2e") or {}
+        out[name] = {
+            "config": workload_config(a)["workload"], "metric": SWEEP_METRIC if name == "sweep" else METRIC,
+            "value": r["value"], "unit": r["unit"], "steps": steps, "ms_per_step": r["ms_per_step"],
+            "dtype": r["dtype"], "roofline_frac": roof.get("frac"), "roofline_kernel": roof.get("kernel"),
+            "roofline_bound": roof.get("bound"), "e2e": e2e.get("value"), "gpu_launches": r["gpu_launches"],
+            "clocks": r.get("clocks"), "wall_s": round(time.time() - t0, 1),
+        }
+        if "sweep" in r:
+            out[name]["sweep"] = {k: r["sweep"].get(k) for k in ("candidates", "executed", "status")}
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -941,6 +975,8 @@ def main():
     ap.add_argument("--impl", default="syno", choices=["syno", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graph", dest="graph", action="store_false", help="eager launches instead of a CUDA graph")
+    ap.add_argument("--no-others", dest="others", action="store_false",
+                    help="default run: skip the other configs' in-run measurement (other_configs key)")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     if args.workload == "sweep" and args.steps == 10:
@@ -973,6 +1009,9 @@ def main():
     peaks = load_peaks()
     runner = {"sweep": run_sweep, "qkv_train": run_qkv_train}.get(args.workload, run_layers)
     r = runner(args, rank, world, device, peaks)
+    others = None
+    if args.others and args.workload == "resnet18" and world == 1:
+        others = run_other_configs(args, rank, world, device, peaks)
     if rank == 0:
         cpu = None
         if not args.no_cpu_baseline and args.workload != "qkv_train" and world == 1:
@@ -992,6 +1031,8 @@ def main():
         for k in ("step_roofline_frac", "step_tflops", "kernels", "breakdown_ms", "sweep", "loss", "allreduce"):
             if k in r:
                 line[k] = r[k]
+        if others is not None:
+            line["other_configs"] = others
         print(json.dumps(line), flush=True)
     if world > 1:
         import torch.distributed as dist
