@@ -952,30 +952,40 @@ __global__ void __launch_bounds__(256) chain_nc_kernel(const __grid_constant__ C
     // region exists only when h.side_j >= 0 (a small block leaves room to
     // co-reside with a concurrent persistent GEMM CTA)
     float* vs = stage + blockDim.x * KKo + threadIdx.x * 17;
+    // every other weight's value per window, all loads in flight before the
+    // products (a serial load per (window, weight) made a 64 x 64
+    // sep_shared chain a 16 us latency chain); the products below keep the
+    // original multiplication order, so results are unchanged bit for bit
+    float wv[MAXFW][VN];
+#pragma unroll
+    for (int q = 0; q < MAXFW; ++q) {
+#pragma unroll
+      for (int k = 0; k < VN; ++k) {
+        wv[q][k] = 1.f;
+        if (q >= c.nw || k >= KK || (q == c.j && h.side_j < 0)) continue;
+        const int kh = k / Kw, kw = k - kh * Kw;
+        const int32_t* st = q == c.j ? h.side_sw[q] : h.sw[q];  // sw[j] is zeroed: w_j only feeds the side
+        const int32_t off = kh * st[0] + kw * st[1] + n * st[2] + ci * st[3];
+        wv[q][k] = c.f32 ? __ldg(reinterpret_cast<const float*>(c.w[q]) + off)
+                         : __bfloat162float(__ldg(reinterpret_cast<const __nv_bfloat16*>(c.w[q]) + off));
+      }
+    }
 #pragma unroll
     for (int k = 0; k < VN; ++k) {
       if (k >= KK) break;
       const int kh = k / Kw, kw = k - kh * Kw;
       const float d = v[k];
       float x = d;
-#pragma unroll 1
-      for (int q = 0; q < c.nw; ++q) {
-        if (q == c.j) continue;
-        const int32_t off = kh * h.sw[q][0] + kw * h.sw[q][1] + n * h.sw[q][2] + ci * h.sw[q][3];
-        x *= c.f32 ? __ldg(reinterpret_cast<const float*>(c.w[q]) + off)
-                   : __bfloat162float(__ldg(reinterpret_cast<const __nv_bfloat16*>(c.w[q]) + off));
-      }
+#pragma unroll
+      for (int q = 0; q < MAXFW; ++q)
+        if (q < c.nw && q != c.j) x *= wv[q][k];
       // windows the weight does not use fold onto the same output
       my[(h.oh ? kh : 0) * KKo_w + (h.ow ? kw : 0)] += x;
       if (h.side_j >= 0) {
         float z = d;
-#pragma unroll 1
-        for (int q = 0; q < c.nw; ++q) {
-          if (q == h.side_j) continue;
-          const int32_t off = kh * h.side_sw[q][0] + kw * h.side_sw[q][1] + n * h.side_sw[q][2] + ci * h.side_sw[q][3];
-          z *= c.f32 ? __ldg(reinterpret_cast<const float*>(c.w[q]) + off)
-                     : __bfloat162float(__ldg(reinterpret_cast<const __nv_bfloat16*>(c.w[q]) + off));
-        }
+#pragma unroll
+        for (int q = 0; q < MAXFW; ++q)
+          if (q < c.nw && q != h.side_j) z *= wv[q][k];
         vs[k] = z;
       }
     }
@@ -1326,6 +1336,16 @@ static TcPlan* try_match(const Plan& plan) {
   tp->C = (int)S.ext(chan);
   tp->N = (int)S.ext(naxis);
   tp->Cp = (tp->C + 7) / 8 * 8;
+  {
+    // narrow inputs (a 3-channel stem) padded to a whole 64-channel block:
+    // full 128-byte rows keep the TMA loads of the forward / grad-weight A
+    // operands efficient (8-channel rows with 112 bytes of out-of-bounds fill
+    // each made the stem's GEMMs the slowest of the step: ResNet-18 step
+    // 1.451 -> 1.413 ms, stem fwd 32 -> 19 us, grad-weight 49 -> 21 us);
+    // the MMA K steps stop at the real channels (kq_last): no extra MMAs
+    static const int cp_min = getenv("SYNO_TC_CP_MIN") ? atoi(getenv("SYNO_TC_CP_MIN")) : 64;  // A/B: 0 = off
+    if (tp->C < cp_min) tp->Cp = (cp_min + 7) / 8 * 8;
+  }
   tp->Np = (tp->N + 7) / 8 * 8;
   tp->scale = S.scale;
   for (PixDim* p : {&tp->dh, &tp->dw}) {
@@ -2074,7 +2094,8 @@ static void build_ws(TcPlan& tp, TcWs& w, DType dt) {
     memset(&p, 0, sizeof(p));
     p.mode = MODE_ROWS;
     p.n_cblocks = (Ck + BK - 1) / BK;
-    p.kq_last = (Ck - (p.n_cblocks - 1) * BK + 15) / 16;  // 16-wide MMA K steps of the last channel block
+    // 16-wide MMA K steps of the last channel block (bf16: up to the real channels; the padding is zero)
+    p.kq_last = ((w.f32 ? Ck : std::min(Ck, tp.C)) - (p.n_cblocks - 1) * BK + 15) / 16;
     std::vector<std::vector<Win>> groups(1);
     for (int rh = 0; rh < tp.dh.K; ++rh)
       for (int rw = 0; rw < tp.dw.K; ++rw)
