@@ -222,7 +222,11 @@ __global__ void __launch_bounds__(256) split_rows_kernel(const float* __restrict
 // 64 channels go out as 128 contiguous bytes.  Only data positions are
 // written: the padding of the flat grid is zeroed once when the workspace
 // is built and never changes.
-constexpr int PK_PIX = 128;
+#ifndef SYNO_PK_PIX
+#define SYNO_PK_PIX 128
+#endif
+constexpr int PK_PIX = SYNO_PK_PIX;  // <= 256 (one thread per pixel in the index phase)
+constexpr int PK_NQ = PK_PIX / 16;   // vector loads per thread of the bf16 read phase (cstep >= 1024 / PK_PIX)
 
 template <typename TI, int V>
 __device__ __forceinline__ void pack_rows_body(const TI* __restrict__ src, __nv_bfloat16* __restrict__ dst,
@@ -340,20 +344,20 @@ __device__ __forceinline__ void pack_rows_body(const TI* __restrict__ src, __nv_
     }
     if constexpr (sizeof(TI) == 2 && V >= 4) {
       // bf16, vector rows: every load of the thread in flight before any
-      // shared-memory store (<= 8 per thread: nvec <= PK_PIX / 4 so cstep
-      // >= 8); the block's run is one latency round instead of several
+      // shared-memory store (<= PK_NQ per thread: nvec <= PK_PIX / 4 so
+      // cstep >= 1024 / PK_PIX); the block's run is one latency round
       using VT = typename std::conditional<V == 8, uint4, uint2>::type;
-      VT qv[8];
+      VT qv[PK_NQ];
       const int cl0 = t / nvec;
 #pragma unroll
-      for (int it = 0; it < 8; ++it) {
+      for (int it = 0; it < PK_NQ; ++it) {
         const int cl = cl0 + it * cstep;
         const int c = cb * 64 + cl;
         qv[it] = VT{};
         if (cl < 64 && c < g.C) qv[it] = __ldg(reinterpret_cast<const VT*>(rowp + (int64_t)c * g.s_c));
       }
 #pragma unroll
-      for (int it = 0; it < 8; ++it) {
+      for (int it = 0; it < PK_NQ; ++it) {
         const int cl = cl0 + it * cstep;
         if (cl >= 64) break;
         __nv_bfloat16* trow = &tile[cl][0];
