@@ -1123,91 +1123,97 @@ __global__ void __launch_bounds__(256) chain_win_kernel(const __grid_constant__ 
 // chain_nc's multiplication order; the side output reduces per window in
 // blocks and the last block combines the block partials in a fixed tree
 // (deterministic: the result depends on gridDim only).
-template <int KH, int KW, bool OH, bool OW>
+template <int KH, int KW, bool OH, bool OW, bool SIDE>
 __global__ void __launch_bounds__(256) chain_v4_kernel(const __grid_constant__ ChainArgs c,
                                                        const __grid_constant__ ChainNC h) {
   pdl_trigger();
   pdl_wait();
   constexpr int KK = KH * KW;
   const int plane4 = h.N * h.C / 4;  // N * C < 2^31, C % 4 == 0 (host-checked)
-  const int i4 = blockIdx.x * blockDim.x + threadIdx.x;
-  const bool live = i4 < plane4;
-  const int q0 = live ? i4 * 4 : 0;  // flat (n, ci) of the thread's first element
-  const int n = q0 / h.C, ci = q0 - n * h.C;
   const int other = h.side_j >= 0 ? h.side_j : -1;
-  float4 v[KK];
-  float wj[KK][4], wo[KK];
-  if (live) {
-    float4* src = reinterpret_cast<float4*>(c.dwf) + i4;
+  float vs[KK];  // side products per window, summed over the thread's (n, ci) elements
 #pragma unroll
-    for (int k = 0; k < KK; ++k) v[k] = __ldcg(src + (int64_t)k * plane4);
-#pragma unroll
+  for (int k = 0; k < KK; ++k) vs[k] = 0.f;
+  // grid-stride: one block may walk a small problem (SYNO_TC_V4_ONE)
+#pragma unroll 1
+  for (int i4 = blockIdx.x * blockDim.x + threadIdx.x, it = 0; it == 0 || i4 < plane4;
+       i4 += gridDim.x * blockDim.x, ++it) {
+    const bool live = i4 < plane4;
+    const int q0 = live ? i4 * 4 : 0;  // flat (n, ci) of the thread's first element
+    const int n = q0 / h.C, ci = q0 - n * h.C;
+    float4 v[KK];
+    float wj[KK][4], wo[KK];
+    if (live) {
+      float4* src = reinterpret_cast<float4*>(c.dwf) + i4;
+  #pragma unroll
+      for (int k = 0; k < KK; ++k) v[k] = __ldcg(src + (int64_t)k * plane4);
+  #pragma unroll
+      for (int k = 0; k < KK; ++k) {
+        const int kh = k / KW, kw = k - kh * KW;
+        wo[k] = 1.f;
+        if (other >= 0) {
+          // the side weight's value at this window (window loops only)
+          const int32_t off = kh * h.sw[other][0] + kw * h.sw[other][1];
+          wo[k] = c.f32 ? __ldg(reinterpret_cast<const float*>(c.w[other]) + off)
+                        : __bfloat162float(__ldg(reinterpret_cast<const __nv_bfloat16*>(c.w[other]) + off));
+  #pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const int32_t offj = kh * h.side_sw[c.j][0] + kw * h.side_sw[c.j][1] + n * h.side_sw[c.j][2] +
+                                 (ci + e) * h.side_sw[c.j][3];
+            wj[k][e] = c.f32 ? __ldg(reinterpret_cast<const float*>(c.w[c.j]) + offj)
+                             : __bfloat162float(__ldg(reinterpret_cast<const __nv_bfloat16*>(c.w[c.j]) + offj));
+          }
+        }
+      }
+      if (c.zero_dwf) {
+  #pragma unroll
+        for (int k = 0; k < KK; ++k) src[(int64_t)k * plane4] = make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+    }
+    // main output: o[e][a] over the weight's window outputs (windows it does not use fold in)
+    constexpr int KKo_w = OW ? KW : 1;
+    constexpr int KKo = (OH ? KH : 1) * KKo_w;  // the weight's window outputs (compile-time: register arrays)
+    float o[4][KKo];
+  #pragma unroll
+    for (int e = 0; e < 4; ++e)
+  #pragma unroll
+      for (int a = 0; a < KKo; ++a) o[e][a] = 0.f;
+  #pragma unroll
     for (int k = 0; k < KK; ++k) {
       const int kh = k / KW, kw = k - kh * KW;
-      wo[k] = 1.f;
-      if (other >= 0) {
-        // the side weight's value at this window (window loops only)
-        const int32_t off = kh * h.sw[other][0] + kw * h.sw[other][1];
-        wo[k] = c.f32 ? __ldg(reinterpret_cast<const float*>(c.w[other]) + off)
-                      : __bfloat162float(__ldg(reinterpret_cast<const __nv_bfloat16*>(c.w[other]) + off));
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const int32_t offj = kh * h.side_sw[c.j][0] + kw * h.side_sw[c.j][1] + n * h.side_sw[c.j][2] +
-                               (ci + e) * h.side_sw[c.j][3];
-          wj[k][e] = c.f32 ? __ldg(reinterpret_cast<const float*>(c.w[c.j]) + offj)
-                           : __bfloat162float(__ldg(reinterpret_cast<const __nv_bfloat16*>(c.w[c.j]) + offj));
+      const int a = (OH ? kh : 0) * KKo_w + (OW ? kw : 0);
+      const float d[4] = {v[k].x, v[k].y, v[k].z, v[k].w};
+  #pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        if (!live) break;
+        o[e][a] += other >= 0 ? d[e] * wo[k] : d[e];
+        if (other >= 0) vs[k] += d[e] * wj[k][e];
+      }
+    }
+    if (live) {
+      // the thread's outputs: 4 * KKo contiguous elements at flat (n, ci) * KKo
+      const int64_t base = (int64_t)q0 * KKo;
+      if (c.f32) {
+        float* ob = reinterpret_cast<float*>(c.out) + base;
+  #pragma unroll
+        for (int e = 0; e < 4; ++e)
+  #pragma unroll
+          for (int a = 0; a < KKo; ++a) ob[e * KKo + a] = o[e][a];
+      } else {
+        // 8 * KKo bytes per thread at an 8-byte aligned offset: 2 * KKo 4-byte words
+        uint32_t* ob = reinterpret_cast<uint32_t*>(reinterpret_cast<__nv_bfloat16*>(c.out) + base);
+  #pragma unroll
+        for (int t = 0; t < 2 * KKo; ++t) {
+          const int i0 = 2 * t, i1 = 2 * t + 1;
+          const float f0 = o[i0 / KKo][i0 % KKo];
+          const float f1 = o[i1 / KKo][i1 % KKo];
+          const __nv_bfloat162 p2 = __floats2bfloat162_rn(f0, f1);
+          ob[t] = *reinterpret_cast<const uint32_t*>(&p2);
         }
       }
     }
-    if (c.zero_dwf) {
-#pragma unroll
-      for (int k = 0; k < KK; ++k) src[(int64_t)k * plane4] = make_float4(0.f, 0.f, 0.f, 0.f);
-    }
   }
-  // main output: o[e][a] over the weight's window outputs (windows it does not use fold in)
-  constexpr int KKo_w = OW ? KW : 1;
-  constexpr int KKo = (OH ? KH : 1) * KKo_w;  // the weight's window outputs (compile-time: register arrays)
-  float o[4][KKo];
-#pragma unroll
-  for (int e = 0; e < 4; ++e)
-#pragma unroll
-    for (int a = 0; a < KKo; ++a) o[e][a] = 0.f;
-  float vs[KK];  // side products per window, summed over the thread's 4 ci
-#pragma unroll
-  for (int k = 0; k < KK; ++k) {
-    const int kh = k / KW, kw = k - kh * KW;
-    const int a = (OH ? kh : 0) * KKo_w + (OW ? kw : 0);
-    const float d[4] = {v[k].x, v[k].y, v[k].z, v[k].w};
-    vs[k] = 0.f;
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      if (!live) break;
-      o[e][a] += other >= 0 ? d[e] * wo[k] : d[e];
-      if (other >= 0) vs[k] += d[e] * wj[k][e];
-    }
-  }
-  if (live) {
-    // the thread's outputs: 4 * KKo contiguous elements at flat (n, ci) * KKo
-    const int64_t base = (int64_t)q0 * KKo;
-    if (c.f32) {
-      float* ob = reinterpret_cast<float*>(c.out) + base;
-#pragma unroll
-      for (int e = 0; e < 4; ++e)
-#pragma unroll
-        for (int a = 0; a < KKo; ++a) ob[e * KKo + a] = o[e][a];
-    } else {
-      // 8 * KKo bytes per thread at an 8-byte aligned offset: 2 * KKo 4-byte words
-      uint32_t* ob = reinterpret_cast<uint32_t*>(reinterpret_cast<__nv_bfloat16*>(c.out) + base);
-#pragma unroll
-      for (int t = 0; t < 2 * KKo; ++t) {
-        const int i0 = 2 * t, i1 = 2 * t + 1;
-        const float f0 = o[i0 / KKo][i0 % KKo];
-        const float f1 = o[i1 / KKo][i1 % KKo];
-        const __nv_bfloat162 p2 = __floats2bfloat162_rn(f0, f1);
-        ob[t] = *reinterpret_cast<const uint32_t*>(&p2);
-      }
-    }
-  }
+  if constexpr (SIDE) {
   if (other < 0) return;
   // side output: block sums per window, then the last block combines
   __shared__ float wsum[8][KK];
@@ -1222,30 +1228,40 @@ __global__ void __launch_bounds__(256) chain_v4_kernel(const __grid_constant__ C
     if (lane == 0) wsum[warp][k] = t;
   }
   __syncthreads();
-  if (threadIdx.x < KK) {
-    float t = 0.f;
-    for (int q = 0; q < (int)(blockDim.x >> 5); ++q) t += wsum[q][threadIdx.x];
-    h.partial[(size_t)blockIdx.x * KK + threadIdx.x] = t;
-    __threadfence();
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) last = atomicAdd(h.counter, 1u) == gridDim.x - 1;
-  __syncthreads();
-  if (!last) return;
-  __threadfence();
-#pragma unroll
-  for (int k = 0; k < KK; ++k) {
-    float t = 0.f;
-    for (unsigned b = threadIdx.x; b < gridDim.x; b += blockDim.x) t += __ldcg(h.partial + (size_t)b * KK + k);
-    red[k][threadIdx.x] = t;
-  }
-  __syncthreads();
-  for (int width = (int)blockDim.x >> 1; width > 0; width >>= 1) {
-    if ((int)threadIdx.x < width) {
-#pragma unroll
-      for (int k = 0; k < KK; ++k) red[k][threadIdx.x] += red[k][threadIdx.x + width];
+  if (gridDim.x == 1) {
+    // one block: its warp sums are the totals (fixed order)
+    if (threadIdx.x < KK) {
+      float t = 0.f;
+      for (int q = 0; q < (int)(blockDim.x >> 5); ++q) t += wsum[q][threadIdx.x];
+      red[threadIdx.x][0] = t;
     }
     __syncthreads();
+  } else {
+    if (threadIdx.x < KK) {
+      float t = 0.f;
+      for (int q = 0; q < (int)(blockDim.x >> 5); ++q) t += wsum[q][threadIdx.x];
+      h.partial[(size_t)blockIdx.x * KK + threadIdx.x] = t;
+      __threadfence();
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) last = atomicAdd(h.counter, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+#pragma unroll
+    for (int k = 0; k < KK; ++k) {
+      float t = 0.f;
+      for (unsigned b = threadIdx.x; b < gridDim.x; b += blockDim.x) t += __ldcg(h.partial + (size_t)b * KK + k);
+      red[k][threadIdx.x] = t;
+    }
+    __syncthreads();
+    for (int width = (int)blockDim.x >> 1; width > 0; width >>= 1) {
+      if ((int)threadIdx.x < width) {
+#pragma unroll
+        for (int k = 0; k < KK; ++k) red[k][threadIdx.x] += red[k][threadIdx.x + width];
+      }
+      __syncthreads();
+    }
   }
   if (threadIdx.x == 0) {
     const int ow2 = h.side_ow ? KW : 1;
@@ -1262,8 +1278,9 @@ __global__ void __launch_bounds__(256) chain_v4_kernel(const __grid_constant__ C
       if (c.f32) reinterpret_cast<float*>(h.side_out)[off] = acc[q];
       else reinterpret_cast<__nv_bfloat16*>(h.side_out)[off] = __float2bfloat16(acc[q]);
     }
-    *h.counter = 0;  // ready for the next call (stream order)
+    if (gridDim.x > 1) *h.counter = 0;  // ready for the next call (stream order)
   }
+  }  // SIDE: no shared memory in the single-weight instances
 }
 
 // Single weight, single window, dense [N][C] gradient (QKV-like): dW = dWf
@@ -2709,16 +2726,20 @@ static void chain_fast(const TcPlan& tp, const TcWs& w, const Bindings& b, DType
     static const bool v4_on = getenv("SYNO_TC_NO_CHAIN_V4") == nullptr;  // A/B switch
     const bool v4 = v4_on && h.Kh == 3 && h.Kw == 3 && h.dense && h.C % 4 == 0 &&
                     // single-weight convolutions: only where one thread per element would need
-                    // many waves (64 x 64: chain_win 6.5 us vs 9.5 us; 512 x 512: 17.1 vs 14.7 us)
+                    // many waves (64 x 64: chain_win 6.6 us vs 8.8 us; 512 x 512: 17.0 vs 14.2 us)
                     ((tp.nw == 1 && side < 0 && h.oh && h.ow && nthreads >= 65536) ||
                      (tp.nw == 2 && side >= 0 && h.oh != h.ow)) &&
                     (reinterpret_cast<uintptr_t>(c.dwf) & 15) == 0 &&
                     (reinterpret_cast<uintptr_t>(c.out) & (c.f32 ? 3 : 7)) == 0;
     if (v4) {
-      const unsigned g4 = (unsigned)((nthreads / 4 + 255) / 256);
-      if (h.oh && h.ow) launch_k(chain_v4_kernel<3, 3, true, true>, g4, 256, 0, stream, c, h);
-      else if (h.oh) launch_k(chain_v4_kernel<3, 3, true, false>, g4, 256, 0, stream, c, h);
-      else launch_k(chain_v4_kernel<3, 3, false, true>, g4, 256, 0, stream, c, h);
+      // SYNO_TC_V4_ONE=<pairs>: problems that small run as one block walking its
+      // elements (no cross-block side reduction) -- measured slower (64 x 64
+      // conv3x3 18.4 vs 8.8 us, sep_shared 16.3 vs 14.8 us), so off by default
+      static const int64_t one_max = getenv("SYNO_TC_V4_ONE") ? atoll(getenv("SYNO_TC_V4_ONE")) : 0;
+      const unsigned g4 = nthreads <= one_max ? 1u : (unsigned)((nthreads / 4 + 255) / 256);
+      if (side < 0) launch_k(chain_v4_kernel<3, 3, true, true, false>, g4, 256, 0, stream, c, h);
+      else if (h.oh) launch_k(chain_v4_kernel<3, 3, true, false, true>, g4, 256, 0, stream, c, h);
+      else launch_k(chain_v4_kernel<3, 3, false, true, true>, g4, 256, 0, stream, c, h);
     } else if (tp.nw == 1 && side < 0 && h.Kh * h.Kw == 1 && h.so_c == 1 && h.so_n == h.C && aligned) {
       const int64_t n = (int64_t)h.N * h.C;
       launch_k(chain_cast_kernel, (unsigned)((n / 4 + 256) / 256), 256, 0, stream, c.dwf, c.out, n, c.f32,

@@ -1,8 +1,8 @@
 #!/bin/bash
 # Vectorised chain rule (chain_v4) A/B against the previous kernels (SYNO_TC_NO_CHAIN_V4) + full GPU suite.
-OUT=gpurun_out/r02_v4
+OUT=gpurun_out/${1:-r02_v4}
 mkdir -p $OUT
-for L in "sep_shared 64 64 32 128" "sep_shared 512 512 4 128" "conv3x3 64 64 32 128" "conv3x3 512 512 4 128"; do
+for L in "sep_shared 64 64 32 128" "sep_shared 128 128 16 128" "sep_shared 512 512 4 128" "conv3x3 64 64 32 128" "conv3x3 512 512 4 128"; do
   n=${L// /_}
   timeout 300 python scripts/gemm_probe.py $L > $OUT/probe_$n.log 2>&1
   SYNO_TC_NO_CHAIN_V4=1 timeout 300 python scripts/gemm_probe.py $L > $OUT/probe_old_$n.log 2>&1
