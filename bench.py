@@ -928,7 +928,7 @@ def workload_config(args):
     return cfg
 
 
-OTHER_CONFIGS = (("cfg1", 10), ("resnet34", 5), ("qkv", 10), ("sweep", 2))
+OTHER_CONFIGS = (("cfg1", 10), ("resnet34", 5), ("qkv", 10), ("sweep", 3))
 
 
 def run_other_configs(args, rank, world, device, peaks):

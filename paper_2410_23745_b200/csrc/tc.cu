@@ -1123,7 +1123,7 @@ __global__ void __launch_bounds__(256) chain_win_kernel(const __grid_constant__ 
 // chain_nc's multiplication order; the side output reduces per window in
 // blocks and the last block combines the block partials in a fixed tree
 // (deterministic: the result depends on gridDim only).
-template <int KH, int KW, bool OH, bool OW, bool SIDE>
+template <int KH, int KW, bool OH, bool OW, bool SIDE, bool WRED = false>
 __global__ void __launch_bounds__(256) chain_v4_kernel(const __grid_constant__ ChainArgs c,
                                                        const __grid_constant__ ChainNC h) {
   pdl_trigger();
@@ -1213,7 +1213,58 @@ __global__ void __launch_bounds__(256) chain_v4_kernel(const __grid_constant__ C
       }
     }
   }
-  if constexpr (SIDE) {
+  if constexpr (SIDE && WRED) {
+    // side output without shared memory (a block that needs none can start
+    // beside the concurrent grad-input GEMM's CTAs): warp sums per window to
+    // global partials, then the last warp to arrive reduces all of them in a
+    // fixed order (lane-strided sums + a fixed xor tree: deterministic)
+    const int lane = threadIdx.x & 31;
+    const unsigned gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;  // global warp
+    const unsigned nwarps = (gridDim.x * blockDim.x) >> 5;
+#pragma unroll
+    for (int k = 0; k < KK; ++k) {
+      float t = vs[k];
+#pragma unroll
+      for (int s = 16; s > 0; s >>= 1) t += __shfl_xor_sync(0xffffffffu, t, s);
+      vs[k] = t;
+    }
+    unsigned prev = 0;
+    if (lane == 0) {
+#pragma unroll
+      for (int k = 0; k < KK; ++k) h.partial[(size_t)gw * KK + k] = vs[k];
+      __threadfence();
+      prev = atomicAdd(h.counter, 1u);
+    }
+    prev = __shfl_sync(0xffffffffu, prev, 0);
+    if (prev != nwarps - 1) return;
+    __threadfence();
+    float tot[KK];
+#pragma unroll
+    for (int k = 0; k < KK; ++k) {
+      float t = 0.f;
+      for (unsigned w = lane; w < nwarps; w += 32) t += __ldcg(h.partial + (size_t)w * KK + k);
+#pragma unroll
+      for (int s = 16; s > 0; s >>= 1) t += __shfl_xor_sync(0xffffffffu, t, s);
+      tot[k] = t;
+    }
+    if (lane == 0) {
+      const int ow2 = h.side_ow ? KW : 1;
+      const int no = (h.side_oh ? KH : 1) * ow2;
+      for (int q = 0; q < no; ++q) {
+        const int ah = q / ow2, aw = q - ah * ow2;
+        float acc = 0.f;
+#pragma unroll
+        for (int k = 0; k < KK; ++k) {
+          const int kh = k / KW, kw = k - kh * KW;
+          if ((h.side_oh ? kh : 0) == ah && (h.side_ow ? kw : 0) == aw) acc += tot[k];
+        }
+        const int64_t off = (int64_t)ah * h.side_so_h + (int64_t)aw * h.side_so_w;
+        if (c.f32) reinterpret_cast<float*>(h.side_out)[off] = acc;
+        else reinterpret_cast<__nv_bfloat16*>(h.side_out)[off] = __float2bfloat16(acc);
+      }
+      *h.counter = 0;  // ready for the next call (stream order)
+    }
+  } else if constexpr (SIDE) {
   if (other < 0) return;
   // side output: block sums per window, then the last block combines
   __shared__ float wsum[8][KK];
@@ -2498,6 +2549,7 @@ static void build_ws(TcPlan& tp, TcWs& w, DType dt) {
     }
     // fused side chains (chain_side_ok): one partial per (block, window)
     need = std::max(need, ((int64_t)tp.N * tp.C + 255) / 256 * 16);
+    need = std::max(need, ((int64_t)tp.N * tp.C / 4 + 31) / 32 * 16);  // chain_v4 warp partials
     outs = std::max<int64_t>(outs, 1);
     if (need) {
       w.chain_partial = ws_alloc<float>(w, (size_t)need);
@@ -2735,11 +2787,18 @@ static void chain_fast(const TcPlan& tp, const TcWs& w, const Bindings& b, DType
       // SYNO_TC_V4_ONE=<pairs>: problems that small run as one block walking its
       // elements (no cross-block side reduction) -- measured slower (64 x 64
       // conv3x3 18.4 vs 8.8 us, sep_shared 16.3 vs 14.8 us), so off by default
+      // SYNO_TC_V4_WRED=1: side output reduced through global warp partials (no shared memory)
+      static const bool v4_wred = getenv("SYNO_TC_V4_WRED") && atoi(getenv("SYNO_TC_V4_WRED")) != 0;
       static const int64_t one_max = getenv("SYNO_TC_V4_ONE") ? atoll(getenv("SYNO_TC_V4_ONE")) : 0;
-      const unsigned g4 = nthreads <= one_max ? 1u : (unsigned)((nthreads / 4 + 255) / 256);
-      if (side < 0) launch_k(chain_v4_kernel<3, 3, true, true, false>, g4, 256, 0, stream, c, h);
-      else if (h.oh) launch_k(chain_v4_kernel<3, 3, true, false, true>, g4, 256, 0, stream, c, h);
-      else launch_k(chain_v4_kernel<3, 3, false, true, true>, g4, 256, 0, stream, c, h);
+      // SYNO_TC_V4_BLOCK: threads per block (A/B: a smaller block can co-reside with the
+      // concurrent grad-input GEMM's CTAs, whose registers fill most of each SM)
+      static const int v4_block = getenv("SYNO_TC_V4_BLOCK") ? atoi(getenv("SYNO_TC_V4_BLOCK")) : 256;
+      const unsigned g4 = nthreads <= one_max ? 1u : (unsigned)((nthreads / 4 + v4_block - 1) / v4_block);
+      if (side < 0) launch_k(chain_v4_kernel<3, 3, true, true, false>, g4, v4_block, 0, stream, c, h);
+      else if (v4_wred && g4 > 1 && h.oh) launch_k(chain_v4_kernel<3, 3, true, false, true, true>, g4, v4_block, 0, stream, c, h);
+      else if (v4_wred && g4 > 1) launch_k(chain_v4_kernel<3, 3, false, true, true, true>, g4, v4_block, 0, stream, c, h);
+      else if (h.oh) launch_k(chain_v4_kernel<3, 3, true, false, true>, g4, v4_block, 0, stream, c, h);
+      else launch_k(chain_v4_kernel<3, 3, false, true, true>, g4, v4_block, 0, stream, c, h);
     } else if (tp.nw == 1 && side < 0 && h.Kh * h.Kw == 1 && h.so_c == 1 && h.so_n == h.C && aligned) {
       const int64_t n = (int64_t)h.N * h.C;
       launch_k(chain_cast_kernel, (unsigned)((n / 4 + 256) / 256), 256, 0, stream, c.dwf, c.out, n, c.f32,
