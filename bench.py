@@ -938,8 +938,20 @@ def run_other_configs(args, rank, world, device, peaks):
     Each keeps its own timing rules (warm-up, L2 flush, device events); no
     CPU baseline here (their `--workload` lines carry one)."""
     import copy
+    import gc
+
+    import torch
+
+    from paper_2410_23745_b200 import pgraph as P
     out = {}
     for name, steps in OTHER_CONFIGS:
+        # each config starts from an empty handle cache (the previous one's
+        # workspaces released), as its own `--workload` run would
+        with P._CACHE_LOCK:
+            P._CACHE.clear()
+        gc.collect()
+        torch.cuda.synchronize(device)
+        torch.cuda.empty_cache()
         a = copy.copy(args)
         a.workload, a.steps, a.batch, a.limit = name, steps, 0, None
         t0 = time.time()
