@@ -528,7 +528,8 @@ def sweep_setup(limit=None):
     graphs = WL.corpus(SWEEP_BATCH, limit=limit)
     flops_cap = 10 * CONV_FLOPS_PER_IMAGE * SWEEP_BATCH      # make_corpus.py's cap, per batch
     params_cap = SWEEP_PARAMS_CAP
-    return graphs, candidate_costs(graphs), flops_cap, params_cap
+    # over-budget candidates are never executed: zero cost in the LPT order
+    return graphs, candidate_costs(graphs, flops_cap, params_cap), flops_cap, params_cap
 
 
 # nominal FP32 FFMA peak of a B200 (148 SMs x 128 lanes x 2 FLOP x 1965 MHz):
