@@ -279,3 +279,31 @@ def test_grad_buckets_single_process_is_identity():
     GradBuckets(list(lin.parameters())).reduce()
     for p, w in zip(lin.parameters(), g):
         assert torch.equal(p.grad, w)
+
+
+def test_bench_sweep_setup_prices_only_executed_candidates():
+    """bench.py's cfg5 setup hands the LPT order budget-aware costs: an
+    over-budget candidate (never executed, search.py:430-437) costs 0."""
+    sys.path.insert(0, ROOT)
+    import bench
+    from paper_2410_23745_b200 import pgraph as P
+    from paper_2410_23745_b200.sweep import within_budget
+    graphs, costs, fcap, pcap = bench.sweep_setup(limit=120)
+    assert len(costs) == len(graphs) == 120
+    for g, c in zip(graphs, costs):
+        h = P.handle_for(g, None, True)
+        assert (c > 0) == within_budget(h.flops_unstaged, h.params, fcap, pcap)
+
+
+def test_bench_other_configs_are_bench_workloads():
+    """The default run's other_configs measure BASELINE's other single-GPU
+    configs through the same runners and config descriptions."""
+    import argparse
+    sys.path.insert(0, ROOT)
+    import bench
+    names = [n for n, _ in bench.OTHER_CONFIGS]
+    assert names == ["cfg1", "resnet34", "qkv", "sweep"]
+    for n, steps in bench.OTHER_CONFIGS:
+        assert steps >= 1
+        cfg = bench.workload_config(argparse.Namespace(workload=n, batch=0))
+        assert cfg["workload"].startswith(("cfg1", "cfg3", "cfg4", "cfg5"))
