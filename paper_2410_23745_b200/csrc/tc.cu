@@ -369,6 +369,39 @@ __device__ __forceinline__ void pack_rows_body(const TI* __restrict__ src, __nv_
           for (int e = 0; e < 4; ++e) trow[(px0 + e + 8 * (cl >> 3)) & (PK_PIX - 1)] = hq[e];
         }
       }
+    } else if constexpr (sizeof(TI) == 4 && V == 4) {
+      // fp32, 4-pixel vectors (cfg1's split operands): as the bf16 form, every
+      // load of the thread in flight before any conversion (<= PK_NQ: cstep
+      // >= 1024 / PK_PIX); the serial two-at-a-time loop took 13 us for 2 MB
+      float4 qf[PK_NQ];
+      int partv[PK_NQ];
+      const int cl0 = t / nvec;
+#pragma unroll
+      for (int it = 0; it < PK_NQ; ++it) {
+        const int cl = cl0 + it * cstep;
+        int c = cb * 64 + cl, part = part0;
+        if (g.split == SPLIT_CH) {
+          part = c / g.Cp;
+          c -= part * g.Cp;
+        }
+        partv[it] = part;
+        qf[it] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (cl < 64 && c < g.C && part < g.parts()) qf[it] = __ldg(reinterpret_cast<const float4*>(rowp + (int64_t)c * g.s_c));
+      }
+#pragma unroll
+      for (int it = 0; it < PK_NQ; ++it) {
+        const int cl = cl0 + it * cstep;
+        if (cl >= 64) break;
+        const float v[4] = {qf[it].x, qf[it].y, qf[it].z, qf[it].w};
+        const bool lo = g.split != SPLIT_NONE && ((g.lo_mask >> partv[it]) & 1u);
+        __nv_bfloat16* trow = &tile[cl][0];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          __nv_bfloat16 hv = __float2bfloat16(v[e]);
+          if (lo) hv = __float2bfloat16(v[e] - __bfloat162float(hv));
+          trow[(px0 + e + 8 * (cl >> 3)) & (PK_PIX - 1)] = hv;
+        }
+      }
     } else
 #pragma unroll 2
     for (int cl = t / nvec; cl < 64; cl += cstep) {
