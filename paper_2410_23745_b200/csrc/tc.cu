@@ -1273,9 +1273,17 @@ __global__ void __launch_bounds__(256) chain_v4_kernel(const __grid_constant__ C
     __threadfence();
     float tot[KK];
 #pragma unroll
+    for (int k = 0; k < KK; ++k) tot[k] = 0.f;
+    for (unsigned w = lane; w < nwarps; w += 32) {
+      float pv[KK];
+#pragma unroll
+      for (int k = 0; k < KK; ++k) pv[k] = __ldcg(h.partial + (size_t)w * KK + k);
+#pragma unroll
+      for (int k = 0; k < KK; ++k) tot[k] += pv[k];
+    }
+#pragma unroll
     for (int k = 0; k < KK; ++k) {
-      float t = 0.f;
-      for (unsigned w = lane; w < nwarps; w += 32) t += __ldcg(h.partial + (size_t)w * KK + k);
+      float t = tot[k];
 #pragma unroll
       for (int s = 16; s > 0; s >>= 1) t += __shfl_xor_sync(0xffffffffu, t, s);
       tot[k] = t;
@@ -1332,12 +1340,21 @@ __global__ void __launch_bounds__(256) chain_v4_kernel(const __grid_constant__ C
     __syncthreads();
     if (!last) return;
     __threadfence();
+    // each thread sums a strided set of the blocks' partials, every window's
+    // load of one block in flight together (a loop per window serialised
+    // KK L2 round trips: ~6 us of a 64 x 64 layer's chain)
+    float tk[KK];
 #pragma unroll
-    for (int k = 0; k < KK; ++k) {
-      float t = 0.f;
-      for (unsigned b = threadIdx.x; b < gridDim.x; b += blockDim.x) t += __ldcg(h.partial + (size_t)b * KK + k);
-      red[k][threadIdx.x] = t;
+    for (int k = 0; k < KK; ++k) tk[k] = 0.f;
+    for (unsigned b = threadIdx.x; b < gridDim.x; b += blockDim.x) {
+      float pv[KK];
+#pragma unroll
+      for (int k = 0; k < KK; ++k) pv[k] = __ldcg(h.partial + (size_t)b * KK + k);
+#pragma unroll
+      for (int k = 0; k < KK; ++k) tk[k] += pv[k];
     }
+#pragma unroll
+    for (int k = 0; k < KK; ++k) red[k][threadIdx.x] = tk[k];
     __syncthreads();
     for (int width = (int)blockDim.x >> 1; width > 0; width >>= 1) {
       if ((int)threadIdx.x < width) {
