@@ -2838,8 +2838,12 @@ static void chain_fast(const TcPlan& tp, const TcWs& w, const Bindings& b, DType
         // SYNO_TC_V4_ONE=<pairs>: problems that small run as one block walking its
         // elements (no cross-block side reduction) -- measured slower (64 x 64
         // conv3x3 18.4 vs 8.8 us, sep_shared 16.3 vs 14.8 us), so off by default
-        // SYNO_TC_V4_WRED=1: side output reduced through global warp partials (no shared memory)
-        static const bool v4_wred = getenv("SYNO_TC_V4_WRED") && atoi(getenv("SYNO_TC_V4_WRED")) != 0;
+        // side output reduced through global warp partials (no shared memory, no
+        // block-level tree) where the last warp has few partials to sum: up to 128
+        // warps (64 x 64 sep_shared chain 12.7 -> 10.6 us, 128 x 128 12.7 -> 10.9;
+        // 512 x 512 would sum 2048: 14.9 -> 21 us); SYNO_TC_V4_WRED=0/1 forces it
+        static const int wred_env = getenv("SYNO_TC_V4_WRED") ? atoi(getenv("SYNO_TC_V4_WRED")) : -1;
+        const bool v4_wred = wred_env >= 0 ? wred_env != 0 : nthreads / 4 / 32 <= 128;
         static const int64_t one_max = getenv("SYNO_TC_V4_ONE") ? atoll(getenv("SYNO_TC_V4_ONE")) : 0;
         // SYNO_TC_V4_BLOCK: threads per block (A/B: a smaller block can co-reside with the
         // concurrent grad-input GEMM's CTAs, whose registers fill most of each SM)
