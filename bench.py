@@ -681,7 +681,13 @@ def run_qkv_train(args, rank, world, device, peaks):
     ms = allreduce_max(e0.elapsed_time(e1) / args.steps, world, device)
     tokens = world * batch * 1024
     flops = 12 * 3 * 2 * batch * 1024 * 768 * 2304  # 12 layers x (fwd + dgrad + wgrad)
-    return {"value": tokens / (ms / 1e3), "unit": "tokens/s", "ms_per_step": ms, "roofline": None,
+    achieved = flops / (ms / 1e3) / 1e12
+    # step-level roofline: the 12 layers' three contractions over the whole
+    # step time (loss, optimizer update and allreduce included, not counted)
+    roof = {"bound": "tensor", "achieved": achieved, "peak": peaks["bf16_tflops"], "unit": "TFLOP/s",
+            "frac": achieved / peaks["bf16_tflops"], "kernel": "whole training step (12 x fwd + dgrad + wgrad)",
+            "traffic": None, "peak_source": peaks["source"]}
+    return {"value": tokens / (ms / 1e3), "unit": "tokens/s", "ms_per_step": ms, "roofline": roof,
             "gpu_launches": int(_lib.lib.syno_launch_count() - launches0), "clocks": None, "dtype": "bf16",
             "step_tflops": flops / (ms / 1e3) / 1e12, "loss": float(loss), "e2e": None,
             "allreduce": {"buckets": len(buckets.buckets), "bytes": sum(f.numel() * f.element_size()
