@@ -670,12 +670,43 @@ def run_qkv_train(args, rank, world, device, peaks):
     for _ in range(args.warmup):
         train_step(model, buckets, x, target)
     torch.cuda.synchronize(device)
+    # one process, no collective on the path: the whole step (12 x fwd + bwd
+    # through the device kernels, gradient staging, SGD) is captured into a
+    # CUDA graph and replayed -- eager, the Python/autograd launch path and
+    # not the GPU bounds the step (3.5-7 ms eager depending on the host).
+    # With ranks the NCCL allreduces stay eager.
+    graph, static_loss, graph_note = None, None, "eager (ranks > 1)" if world > 1 else "eager (--no-graph)"
+    if args.graph and world == 1:
+        try:
+            side = torch.cuda.Stream(device)
+            side.wait_stream(torch.cuda.current_stream(device))
+            with torch.cuda.stream(side):
+                for _ in range(2):
+                    train_step(model, buckets, x, target)
+            torch.cuda.current_stream(device).wait_stream(side)
+            torch.cuda.synchronize(device)
+            c0 = _lib.lib.syno_launch_count()
+            graph = torch.cuda.CUDAGraph()
+            # capture on the warm-up stream: the library keeps its workspaces per (device, stream)
+            with torch.cuda.graph(graph, stream=side):
+                static_loss = train_step(model, buckets, x, target)
+            launches_per_step = _lib.lib.syno_launch_count() - c0
+            graph.replay()
+            torch.cuda.synchronize(device)
+            graph_note = "CUDA graph of the whole step"
+        except Exception as e:  # recorded; the eager step is measured instead
+            graph, graph_note = None, f"eager (graph capture failed: {type(e).__name__}: {e})"[:200]
+            torch.cuda.synchronize(device)
     barrier(world)
     launches0 = _lib.lib.syno_launch_count()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     for _ in range(args.steps):
-        loss = train_step(model, buckets, x, target)
+        if graph is not None:
+            graph.replay()
+            loss = static_loss
+        else:
+            loss = train_step(model, buckets, x, target)
     e1.record()
     torch.cuda.synchronize(device)
     ms = allreduce_max(e0.elapsed_time(e1) / args.steps, world, device)
@@ -687,8 +718,9 @@ def run_qkv_train(args, rank, world, device, peaks):
     roof = {"bound": "tensor", "achieved": achieved, "peak": peaks["bf16_tflops"], "unit": "TFLOP/s",
             "frac": achieved / peaks["bf16_tflops"], "kernel": "whole training step (12 x fwd + dgrad + wgrad)",
             "traffic": None, "peak_source": peaks["source"]}
+    launches = _lib.lib.syno_launch_count() - launches0 if graph is None else launches_per_step * args.steps
     return {"value": tokens / (ms / 1e3), "unit": "tokens/s", "ms_per_step": ms, "roofline": roof,
-            "gpu_launches": int(_lib.lib.syno_launch_count() - launches0), "clocks": None, "dtype": "bf16",
+            "gpu_launches": int(launches), "clocks": None, "dtype": "bf16", "execution": graph_note,
             "step_tflops": flops / (ms / 1e3) / 1e12, "loss": float(loss), "e2e": None,
             "allreduce": {"buckets": len(buckets.buckets), "bytes": sum(f.numel() * f.element_size()
                                                                        for f in buckets.flat)}}
@@ -1047,7 +1079,8 @@ def main():
             "roofline": r.get("roofline"), "cpu_baseline": cpu, "e2e": r.get("e2e"),
             "gpu_launches": r["gpu_launches"], "clocks": r.get("clocks"),
         }
-        for k in ("step_roofline_frac", "step_tflops", "kernels", "breakdown_ms", "sweep", "loss", "allreduce"):
+        for k in ("step_roofline_frac", "step_tflops", "kernels", "breakdown_ms", "sweep", "loss", "allreduce",
+                  "execution"):
             if k in r:
                 line[k] = r[k]
         if others is not None:
