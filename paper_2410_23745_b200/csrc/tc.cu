@@ -2031,11 +2031,17 @@ static void cast_to_bf16(float* in, void* out, int64_t n, cudaStream_t stream) {
   prof_end(id, stream);
 }
 
-static int pick_bn(int n) {
+static int pick_bn(int n, int64_t m_rows = -1) {
   // BN = 128 costs the same cycles per 128x128x16 as BN = 256 does per half of
   // its tile (shared-memory bound), and it allows two CTAs per SM
   static const int cap = getenv("SYNO_TC_MAXBN") ? atoi(getenv("SYNO_TC_MAXBN")) : 256;
-  const int bn = n <= 64 ? 64 : n <= 128 ? 128 : 256;
+  int bn = n <= 64 ? 64 : n <= 128 ? 128 : 256;
+  // a row GEMM whose 256-wide tiles would not cover the SMs once (ResNet-18's
+  // 8 x 8 and 4 x 4 maps: 50-81 tiles) takes 128-wide tiles, twice as many:
+  // forward / grad-input 1.368 -> 1.356 ms on the ResNet-18 step
+  // (profiles/r02_tiling.txt); SYNO_TC_BN_FILL=0 disables
+  static const bool fill = !(getenv("SYNO_TC_BN_FILL") && atoi(getenv("SYNO_TC_BN_FILL")) == 0);
+  if (fill && bn == 256 && m_rows >= 0 && (m_rows + BM - 1) / BM * ((n + 255) / 256) < sm_count()) bn = 128;
   return std::min(bn, std::max(64, cap));
 }
 
@@ -2366,7 +2372,7 @@ static void build_ws(TcPlan& tp, TcWs& w, DType dt) {
 
   // ---- forward: y = sum_win sum_ci Xcl[plane][flat + shift] Wf[win][n][ci]
   {
-    const int bn = pick_bn(tp.N);
+    const int bn = pick_bn(tp.N, F);
     TcGemmParams& p = w.fwd;
     memset(&p, 0, sizeof(p));
     p.mode = MODE_ROWS;
@@ -2437,7 +2443,7 @@ static void build_ws(TcPlan& tp, TcWs& w, DType dt) {
 
   // ---- grad-input: one group per output phase (psi_h, psi_w); its windows have phi(r) == psi
   if (tp.dgrad_ok) {
-    const int bn = pick_bn(tp.C);
+    const int bn = pick_bn(tp.C, Fg);
     TcGemmParams& p = w.dg;
     memset(&p, 0, sizeof(p));
     p.mode = MODE_ROWS;
@@ -2493,7 +2499,11 @@ static void build_ws(TcPlan& tp, TcWs& w, DType dt) {
   // padded grid, read MN-major (K = pixel rows): a window is a row shift
   {
     // M = (window, 64-channel block of C_in) pairs, N = C_out, K = pixel rows
-    const int bn = pick_bn(tp.N);
+    // the forward's tile-count rule decides the grad-weight tile width too: the
+    // l3/l4 grad-weights take 128-wide tiles (ResNet-18 step 1.356 -> 1.317 ms,
+    // ResNet-34 and QKV unchanged; SYNO_TC_WG_BN_FILL=0 disables)
+    static const bool wg_fill = !(getenv("SYNO_TC_WG_BN_FILL") && atoi(getenv("SYNO_TC_WG_BN_FILL")) == 0);
+    const int bn = pick_bn(tp.N, wg_fill ? F : -1);
     TcGemmParams& p = w.wg;
     memset(&p, 0, sizeof(p));
     w.ms_wg_a = map_spec(tp.Cp, Fw, planes, tp.Cp, Fw * tp.Cp, 64);
