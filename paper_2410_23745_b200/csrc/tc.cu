@@ -2041,7 +2041,9 @@ static int pick_bn(int n, int64_t m_rows = -1) {
   // forward / grad-input 1.368 -> 1.356 ms on the ResNet-18 step
   // (profiles/r02_tiling.txt); SYNO_TC_BN_FILL=0 disables
   static const bool fill = !(getenv("SYNO_TC_BN_FILL") && atoi(getenv("SYNO_TC_BN_FILL")) == 0);
-  if (fill && bn == 256 && m_rows >= 0 && (m_rows + BM - 1) / BM * ((n + 255) / 256) < sm_count()) bn = 128;
+  static const int fill_waves = getenv("SYNO_TC_BN_FILL_WAVES") ? atoi(getenv("SYNO_TC_BN_FILL_WAVES")) : 1;
+  if (fill && bn == 256 && m_rows >= 0 && (m_rows + BM - 1) / BM * ((n + 255) / 256) < fill_waves * sm_count())
+    bn = 128;
   return std::min(bn, std::max(64, cap));
 }
 
